@@ -1,0 +1,198 @@
+"""ctypes wrapper of oracle.c (TEST INFRASTRUCTURE ONLY; see oracle/__init__.py)."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+__all__ = ["build", "lib", "schedule", "keyframes", "bary_textbook", "fast_coeffs", "fast_eval",
+           "render_fwd", "render_bwd", "num_threads"]
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with gcc (plain IEEE fp64: no -ffast-math, no FMA contraction)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + ".tmp%d" % os.getpid()
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared",
+                               "-std=c99", "-Wall", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+class _Scene(C.Structure):
+    _fields_ = [("V", C.c_int), ("F", C.c_int), ("B", C.c_int), ("H", C.c_int), ("W", C.c_int),
+                ("verts", C.c_void_p), ("faces", C.c_void_p), ("colors", C.c_void_p),
+                ("cams", C.c_void_p), ("kind", C.c_void_p), ("vec", C.c_void_p),
+                ("angle", C.c_void_p), ("pivot", C.c_void_p), ("n_sub", C.c_void_p),
+                ("n_seg", C.c_void_p), ("rule", C.c_void_p), ("sub_range", C.c_void_p)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("mode", C.c_int), ("threads", C.c_int), ("check_fast", C.c_int),
+                ("eps_amb", C.c_double), ("amb_val_tol", C.c_double), ("amb_z_rel", C.c_double),
+                ("npix", C.c_int), ("pix", C.c_void_p)]
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            _lib = C.CDLL(build())
+            P = C.c_void_p
+            _lib.om_schedule.argtypes = [C.c_int, C.c_int, C.c_int, P, P]
+            _lib.om_keyframes.argtypes = [P, C.c_int, P, P, P]
+            _lib.om_bary_textbook.argtypes = [P, P, C.c_double, C.c_double, P, P]
+            _lib.om_fast_coeffs.argtypes = [P, P, P, P, C.c_double, C.c_double, P, P, P, P]
+            _lib.om_fast_coeffs.restype = None
+            _lib.om_fast_eval.argtypes = [P, P, P, P, C.c_double, C.c_double, C.c_double, P, P]
+            _lib.om_render_fwd.argtypes = [P, P, P, P, C.c_int, P, P, P, P]
+            _lib.om_render_bwd.argtypes = [P, P, P, P, P, P]
+            _lib.om_num_threads.argtypes = [C.c_int]
+        return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _d(a, shape=None):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    return a if shape is None else a.reshape(shape)
+
+
+def _i(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+class _Pack:
+    """Holds the fp64/int32 copies alive while a call runs."""
+
+    def __init__(self, sc, sub_range=None):
+        self.verts = _d(sc.verts)
+        self.faces = _i(sc.faces)
+        self.colors = _d(sc.colors)
+        self.cams = _d(sc.cams)
+        m = sc.motion
+        self.kind, self.vec, self.angle = _i(m["kind"]), _d(m["vec"]), _d(m["angle"])
+        self.pivot, self.n_sub, self.n_seg, self.rule = _d(m["pivot"]), _i(m["n_sub"]), _i(m["n_seg"]), _i(m["rule"])
+        self.sub_range = None if sub_range is None else _i(sub_range)
+        self.s = _Scene(self.verts.shape[0], self.faces.shape[0], self.cams.shape[0], sc.H, sc.W,
+                        _p(self.verts), _p(self.faces), _p(self.colors), _p(self.cams), _p(self.kind),
+                        _p(self.vec), _p(self.angle), _p(self.pivot), _p(self.n_sub), _p(self.n_seg),
+                        _p(self.rule), _p(self.sub_range))
+
+
+def _opts(mode="binned", threads=0, check_fast=False, eps_amb=0.0, amb_val_tol=1e-5, amb_z_rel=1e-6,
+          pixels=None):
+    pix = None if pixels is None else _i(pixels).reshape(-1, 3)
+    o = _Opts(1 if mode == "binned" else 0, threads, int(check_fast), eps_amb, amb_val_tol, amb_z_rel,
+              0 if pix is None else pix.shape[0], _p(pix))
+    return o, pix
+
+
+def num_threads(req: int = 0) -> int:
+    return lib().om_num_threads(req)
+
+
+def schedule(N: int, S: int, rule: int = 0):
+    s = np.zeros(N, np.int32)
+    t = np.zeros(N, np.float64)
+    if lib().om_schedule(N, S, rule, _p(s), _p(t)):
+        raise ValueError("invalid schedule (N=%d, S=%d, rule=%d)" % (N, S, rule))
+    return s, t
+
+
+def keyframes(sc, b: int = 0):
+    """(S+1, V, 3) NDC x, y and view z; (S+1, V) valid; (S+1, V, 3) view coordinates."""
+    pk = _Pack(sc)
+    S = int(sc.motion["n_seg"][b])
+    key = np.zeros((S + 1, sc.V, 3))
+    valid = np.zeros((S + 1, sc.V), np.uint8)
+    Q = np.zeros((S + 1, sc.V, 3))
+    lib().om_keyframes(C.byref(pk.s), b, _p(key), _p(valid), _p(Q))
+    return key, valid.astype(bool), Q
+
+
+def bary_textbook(x, y, u, v):
+    w = np.zeros(3)
+    det = np.zeros(1)
+    ok = lib().om_bary_textbook(_p(_d(x)), _p(_d(y)), float(u), float(v), _p(w), _p(det))
+    return (w if ok else None), float(det[0])
+
+
+def fast_coeffs(X0, Y0, X1, Y1, u, v):
+    A1, A2, A3, a = np.zeros(3), np.zeros(3), np.zeros(3), np.zeros(3)
+    lib().om_fast_coeffs(_p(_d(X0)), _p(_d(Y0)), _p(_d(X1)), _p(_d(Y1)), float(u), float(v),
+                         _p(A1), _p(A2), _p(A3), _p(a))
+    return A1, A2, A3, a
+
+
+def fast_eval(X0, Y0, X1, Y1, u, v, t):
+    w = np.zeros(3)
+    den = np.zeros(1)
+    ok = lib().om_fast_eval(_p(_d(X0)), _p(_d(Y0)), _p(_d(X1)), _p(_d(Y1)), float(u), float(v), float(t),
+                            _p(w), _p(den))
+    return (w if ok else None), float(den[0])
+
+
+def render_fwd(sc, mode="binned", threads=0, ids_k=-1, eps_amb=0.0, check_fast=False, sub_range=None,
+               frozen=None, pixels=None, colors=None, verts=None):
+    """Blurred RGBA (B,H,W,4) fp64 (or (npix,4) in pixel-list mode).
+    Returns dict(rgba, ids, amb_img, amb_ids, stats, behind)."""
+    import dataclasses
+    if colors is not None or verts is not None:
+        sc = dataclasses.replace(sc, colors=sc.colors if colors is None else colors,
+                                 verts=sc.verts if verts is None else verts)
+    pk = _Pack(sc, sub_range)
+    o, pix = _opts(mode, threads, check_fast, eps_amb, pixels=pixels)
+    shape = (pix.shape[0],) if pix is not None else (sc.B, sc.H, sc.W)
+    rgba = np.zeros(shape + (4,))
+    ids = np.full(shape, -1, np.int32)
+    amb_i = np.zeros(shape, np.uint8)
+    amb_d = np.zeros(shape, np.uint8)
+    stats = np.zeros(4)
+    fz = None if frozen is None else _i(frozen)
+    r = lib().om_render_fwd(C.byref(pk.s), C.byref(o), _p(rgba), _p(ids), int(ids_k),
+                            _p(amb_i) if eps_amb > 0 else None, _p(amb_d) if eps_amb > 0 else None,
+                            _p(fz), _p(stats))
+    if r < 0:
+        raise ValueError("oracle: invalid input")
+    return dict(rgba=rgba, ids=ids, amb_img=amb_i.astype(bool), amb_ids=amb_d.astype(bool),
+                stats=dict(max_fast_dev=stats[0], n_checked=stats[1], necessary_pairs=stats[2],
+                           covered=stats[3]), behind=bool(r == 1))
+
+
+def render_bwd(sc, grad_rgba, mode="binned", threads=0, sub_range=None, pixels=None, want_dkey=False,
+               colors=None, verts=None):
+    """(dverts (V,3), dcolors (V,3)[, dkey list per image (S+1,V,2)]) in fp64."""
+    import dataclasses
+    if colors is not None or verts is not None:
+        sc = dataclasses.replace(sc, colors=sc.colors if colors is None else colors,
+                                 verts=sc.verts if verts is None else verts)
+    pk = _Pack(sc, sub_range)
+    o, pix = _opts(mode, threads, pixels=pixels)
+    g = _d(grad_rgba)
+    dv = np.zeros((sc.V, 3))
+    dc = np.zeros((sc.V, 3))
+    nkey = int(sum((int(S) + 1) * sc.V * 2 for S in sc.motion["n_seg"]))
+    dk = np.zeros(nkey) if want_dkey else None
+    r = lib().om_render_bwd(C.byref(pk.s), C.byref(o), _p(g), _p(dv), _p(dc), _p(dk))
+    if r < 0:
+        raise ValueError("oracle: invalid input")
+    if not want_dkey:
+        return dv, dc
+    out, off = [], 0
+    for S in sc.motion["n_seg"]:
+        n = (int(S) + 1) * sc.V * 2
+        out.append(dk[off:off + n].reshape(int(S) + 1, sc.V, 2))
+        off += n
+    return dv, dc, out
