@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: one inverse-rendering step (fwd -> L2 loss -> bwd -> all-reduce) of
+the motion-blur rasterizer on N GPUs of one node; prints ONE JSON line (rank 0).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config C4] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU, NCCL)
+
+Workload (BASELINE.json configs[3], "C4"): 10,242-vertex / 20,480-face genus-0 mesh (icosphere
+level 5 template; targets = renders of its seeded SH-displaced version), 16 observed 512x512
+images (8 translational, 8 rotational views), N = 100 sub-frames, S = 1 / 12 segments; images
+sharded over ranks, NCCL all-reduce of [dV || dC].  Synthetic, seeded (scenes/).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "blurred images/s (fwd+bwd)"
+UNIT = "images/s"
+# FP32 SIMT peak derived from the profiling guide's unit counts and clock:
+# 148 SMs x 128 FP32 lanes x 2 flop (FFMA) x 1.965 GHz
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+# algorithmic work per unit: flop per covered (pixel, face, sub-frame) pair,
+# per covered (pixel, sub-frame) shade, per (face, sub-frame) coefficient evaluation, and the
+# backward's extra work per covered (pixel, sub-frame)
+FLOP_PAIR, FLOP_SHADE, FLOP_SETUP, FLOP_BWD = 18.0, 25.0, 30.0, 100.0
+LAUNCHES_FWD, LAUNCHES_LOSS, LAUNCHES_BWD = 9, 1, 2
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="C4")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--split", type=int, default=0, help="sub-frame ranges per image (0 = auto)")
+    p.add_argument("--max-chunk", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the oracle sample")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", "bench_clocks_%d_%d.csv" % (os.getpid(), gpu_index))
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], [], set()
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_target(sc, dev):
+    """Loss targets: renders of the displaced mesh (C4/C5 inverse-rendering step) or the seeded
+    uniform targets (C1-C3).  Built before timing."""
+    import torch
+    if "displaced_verts" not in sc.meta:
+        return torch.tensor(sc.target, device=dev)
+    from paper_2602_07860_b200 import BlurRenderer
+    out = torch.empty((sc.B, sc.H, sc.W, 4), dtype=torch.float32, device=dev)
+    for b0 in range(0, sc.B, 8):
+        sub = sc.subset(list(range(b0, min(sc.B, b0 + 8))))
+        r = BlurRenderer(sub.faces, sub.motion, sub.cams, sub.H, sub.W, sub.V, device=dev)
+        r.forward(torch.tensor(sc.meta["displaced_verts"], device=dev), torch.tensor(sc.colors, device=dev),
+                  out=out[b0:b0 + sub.B])
+        del r
+    torch.cuda.synchronize()
+    return out
+
+
+def cpu_baseline(sc, target_seconds: float):
+    """Time the fp64 oracle (as it stands) fwd + bwd on a bounded sample of the same workload:
+    image 0 (and image B-1, the other motion kind) over a leading sub-frame range sized for about
+    `target_seconds` of CPU time, all host cores.  Returns images/s and the sample description."""
+    import oracle
+    cores = oracle.num_threads(0)
+    imgs = sorted({0, sc.B - 1})
+    sub = sc.subset(imgs)
+    N = int(sub.motion["n_sub"][0])
+    G = np.zeros((sub.B, sub.H, sub.W, 4))
+
+    def run(ks):
+        rng = [[0, ks]] * sub.B
+        t0 = time.perf_counter()
+        fw = oracle.render_fwd(sub, sub_range=rng)
+        G[:] = 2.0 * (fw["rgba"] - (sub.target if sub.target is not None else 0.0)) / fw["rgba"].size
+        oracle.render_bwd(sub, G, sub_range=rng)
+        return time.perf_counter() - t0
+
+    t_probe = run(min(2, N))
+    ks = max(1, min(N, int(min(2, N) * target_seconds / max(t_probe, 1e-3))))
+    t = run(ks) if ks != min(2, N) else t_probe
+    images = sub.B * ks / N
+    return {"value": images / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": "fp64 oracle (binned) fwd+bwd of images %s of %s, sub-frames [0,%d) of %d, %.1f s on %d "
+                      "threads = %.4f images" % (imgs, sc.name, ks, N, t, cores, images),
+            "seconds": t}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import scenes
+    sc = scenes.make(args.config)
+    vals = []
+    for _ in range(args.warmup + args.steps):
+        vals.append(cpu_baseline(sc, max(2.0, args.cpu_seconds / max(1, args.steps))))
+    cb = vals[-1]
+    timed = vals[args.warmup:]
+    v = len(timed) / sum(1.0 / x["value"] for x in timed)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v * sc.B,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": sc.name, "images": sc.B, "H": sc.H, "W": sc.W,
+                                            "faces": sc.F, "subframes": int(sc.motion["n_sub"][0])},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "oracle",
+                             "sample": cb["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main (ours)
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import scenes
+    from paper_2602_07860_b200 import BlurRenderer, _lib
+    from paper_2602_07860_b200.dist import ShardedStep
+
+    assert torch.cuda.is_available(), "bench.py needs CUDA"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    sc = scenes.make(args.config)
+    target = make_target(sc, dev)
+    verts = torch.tensor(sc.verts, device=dev)
+    colors = torch.tensor(sc.colors, device=dev)
+
+    def make_renderer(images, sub_range):
+        s = sc.subset(images)
+        return BlurRenderer(s.faces, s.motion, s.cams, s.H, s.W, s.V, device=dev, sub_range=sub_range,
+                            max_chunk=args.max_chunk)
+
+    step = ShardedStep(sc.motion["n_sub"], target, make_renderer, rank, world, split=args.split, device=dev)
+    rend = step.renderer
+    stream = torch.cuda.current_stream()
+
+    # census (outside timing): algorithmic unit counts of this rank's forward
+    census = torch.zeros(4, dtype=torch.int64, device=dev)
+    units = np.zeros(4)
+    if rend is not None:
+        rend.forward(verts, colors, census=census)
+        units = census.cpu().numpy().astype(np.float64)
+    n_fsub = float(sum(u.k1 - u.k0 for u in step.mine)) * sc.F      # (face, sub-frame) evaluations
+
+    # raster-kernel timing events (recorded inside the C-ABI calls on this stream)
+    def evpair():
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        b.record(stream)
+        return a, b
+
+    flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
+
+    def one_step(ev_f=None, ev_b=None):
+        if rend is None:
+            return step(verts, colors)
+        out = rend.forward(verts, colors, events=ev_f)
+        for slot, g in step.groups:
+            part = out[slot].contiguous()
+            dist.all_reduce(part, group=g)
+            out[slot].copy_(part)
+        if all(u.k0 == 0 for u in step.mine):
+            loss, grads = rend.l2_loss_grad(out, step.targets, n_norm=step.n_norm)
+        else:
+            loss = torch.zeros(1, device=dev)
+            grads = torch.empty_like(out)
+            for i in range(len(step.images)):
+                li, gi = rend.l2_loss_grad(out[i:i + 1].contiguous(), step.targets[i:i + 1].contiguous(),
+                                           n_norm=step.n_norm)
+                loss += li * step.loss_mask[i]
+                grads[i].copy_(gi[0])
+        dv, dc = rend.backward(verts, colors, grads, reuse_setup=True, events=ev_b)
+        flat = torch.cat([dv.reshape(-1), dc.reshape(-1), loss])
+        if world > 1:
+            dist.all_reduce(flat)
+        return flat
+
+    for _ in range(max(3, args.warmup)):
+        one_step()
+    torch.cuda.synchronize()
+    if rend is not None:
+        st = rend.status()
+        if st & 3:
+            raise RuntimeError("device status %d after warm-up" % st)
+
+    K = args.steps
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    evf = [evpair() for _ in range(K)]
+    evb = [evpair() for _ in range(K)]
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    for i in range(K):
+        flush_buf.zero_()                                       # L2 flush between timed steps
+        ev_s[i].record(stream)
+        one_step(evf[i], evb[i])
+        ev_e[i].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [ev_s[i].elapsed_time(ev_e[i]) for i in range(K)]
+    tot_ms = float(sum(step_ms))
+    fwd_ms = [evf[i][0].elapsed_time(evf[i][1]) for i in range(K)] if rend is not None else [0.0]
+    bwd_ms = [evb[i][0].elapsed_time(evb[i][1]) for i in range(K)] if rend is not None else [0.0]
+    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_max = float(t.item())
+    ms_per_step = tot_max / K
+    value = sc.B / (ms_per_step / 1000.0)
+
+    # roofline of the dominant kernel (raster fwd K4 or raster bwd K6), this rank's launches
+    nec, cov, cand, staged = units
+    fw_flop = FLOP_PAIR * nec + FLOP_SHADE * cov + FLOP_SETUP * n_fsub
+    bw_flop = fw_flop + FLOP_BWD * cov
+    f_avg, b_avg = float(np.mean(fwd_ms)), float(np.mean(bwd_ms))
+    if b_avg >= f_avg:
+        kname, flop, dur = "k6_raster_bwd", bw_flop, b_avg
+    else:
+        kname, flop, dur = "k4_raster_fwd", fw_flop, f_avg
+    achieved = flop / (dur / 1000.0) / 1e12 if dur > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(sc.name, {}).get(kname)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "kernel": kname, "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md nominal "
+                               "SM count and clocks.max.sm)",
+                "fwd_raster_ms": f_avg, "bwd_raster_ms": b_avg,
+                "executed_pair_tests_per_launch": cand, "necessary_pairs_per_launch": nec}
+
+    # measured FFMA throughput (context for the derived peak)
+    ffma = None
+    if rank == 0:
+        sink = torch.empty(148 * 8 * 256, dtype=torch.float32, device=dev)
+        _lib.blur_ffma_probe(148 * 8, 64, sink)
+        torch.cuda.synchronize()
+        best = 0.0
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fl = _lib.blur_ffma_probe(148 * 8, 512, sink)
+            b.record(stream)
+            torch.cuda.synchronize()
+            best = max(best, fl / (a.elapsed_time(b) / 1000.0) / 1e12)
+        ffma = best
+
+    # end-to-end through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e and rend is not None:
+        h_verts = torch.tensor(sc.verts).pin_memory()
+        h_cols = torch.tensor(sc.colors).pin_memory()
+        h_tgt = step.targets.cpu().pin_memory()
+        d_verts, d_cols, d_tgt = torch.empty_like(verts), torch.empty_like(colors), torch.empty_like(step.targets)
+        h_out = torch.empty(6 * sc.V + 1, dtype=torch.float32).pin_memory()
+        saved = step.targets
+
+        def e2e_step():
+            d_verts.copy_(h_verts, non_blocking=True)
+            d_cols.copy_(h_cols, non_blocking=True)
+            d_tgt.copy_(h_tgt, non_blocking=True)
+            step.targets = d_tgt
+            flat = one_step_public(d_verts, d_cols)
+            h_out.copy_(flat, non_blocking=True)
+
+        def one_step_public(v, c):
+            loss, dv, dc = step(v, c)
+            return torch.cat([dv.reshape(-1), dc.reshape(-1), loss])
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(K):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        step.targets = saved
+        e2e = {"value": sc.B / (float(te.item()) / K / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(h_verts.numel() * 4 + h_cols.numel() * 4 + h_tgt.numel() * 4),
+               "d2h_bytes_per_step": int(h_out.numel() * 4)}
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(sc, args.cpu_seconds)
+        cb.pop("seconds", None)
+
+    if rank == 0:
+        n_sub = int(sc.motion["n_sub"][0])
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+                "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": sc.name, "images": sc.B, "H": sc.H, "W": sc.W, "faces": sc.F,
+                           "vertices": sc.V, "subframes": n_sub,
+                           "segments": sorted({int(x) for x in sc.motion["n_seg"]}),
+                           "parallelism": "image-sharded x%d" % world + ("" if not step.groups else " + subframe split"),
+                           "l2": "flushed (256 MB write) before every timed step"},
+                "barycentric_evals_per_s": {"executed": cand * world / (ms_per_step / 1000.0),
+                                            "necessary": nec * world / (ms_per_step / 1000.0),
+                                            "note": "per-rank census x ranks (rank 0's counts)"},
+                "roofline": roofline, "ffma_measured_tflops": ffma, "clocks": clk,
+                "gpu_launches": (LAUNCHES_FWD + LAUNCHES_LOSS + LAUNCHES_BWD) * K,
+                "e2e": e2e, "cpu_baseline": cb}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,166 @@
+/*
+ * blurrast.h -- C ABI of the B200 (sm_100a) motion-blur rasterizer: the hot path of
+ * arxiv 2602.07860 ("fast barycentric coordinate solver", section 3).
+ *
+ * Citations: P:L### = line of the paper's LaTeX source; Eq.n numbered in
+ * \begin{equation} order; A# = appendix equation; S:L### = SPEC.md; Q# = a reading of a
+ * silent/ambiguous passage, listed in DESIGN.md.
+ *
+ * What one call computes: for B observed images of one triangle mesh under a
+ * known rigid motion, the blurred RGBA image
+ *     I_b(p) = (1/N) sum_k [ covered_k(p) ? (sum_i w_i(tau_k) c_i, 1) : (0,0,0,0) ]
+ * where sub-frame k lies in segment s_k at segment time tau_k (Q1), the keyframes of segment s are
+ * the exact rigid pose at t = s/S projected with A34, vertices move linearly in
+ * screen space inside a segment (Eq.4-6), the barycentric weights are evaluated with
+ * the paper's fast solver w(tau) = (A1 tau^2 + A2 tau + A3)/(a1 tau^2 + a2 tau + a3) (Eq.8,
+ * P:L264; A11-A16) from coefficients computed once per (face, segment), a pixel is
+ * covered by a face iff all w_i >= 0 (Q7), the nearest covering face by interpolated view
+ * depth wins (Z-buffer, Q6; lower face index on exact ties), and shading is Eq.9
+ * with background (0,0,0,0) (Q10).  blur_render_bwd scatters dL/dI into per-vertex
+ * world-position and colour gradients through the same weights, frozen winners (Q11).
+ *
+ * Conventions for every entry point:
+ *  - Pointers are DEVICE pointers unless the comment says "host".  The caller owns every buffer;
+ *    the library keeps no allocation and no global state except a thread-local error string.
+ *  - Work is enqueued asynchronously on `stream` (a cudaStream_t; 0 = legacy default stream).
+ *    Argument errors are detected synchronously and returned before anything is enqueued.
+ *    Data-dependent errors (face index >= V, a vertex behind the near plane, bin overflow) are
+ *    recorded in a status word inside the workspace; read it with blur_read_status().  Faces with
+ *    an invalid index or a vertex behind the near plane are skipped, never clipped.
+ *    Bin overflow is not an error for the result: the affected tiles take a slower exact path.
+ *  - Layouts: verts [V,3] f32 world positions; faces [F,3] i32; colors [V,3] f32; images
+ *    [B,H,W,4] f32 RGBA, row 0 at the top, pixel (i,j) centre at NDC
+ *    (-1 + (2i+1)/W, 1 - (2j+1)/H) (Q9).
+ *  - Return value: a blur_status.  blur_last_error() gives a message for the last non-OK return
+ *    on the calling thread.
+ *  - Re-entrant on distinct workspaces/streams.  Setting BLURRAST_CHECK=1 in the environment makes
+ *    every render call synchronise and return the device status word.
+ */
+#ifndef BLURRAST_H
+#define BLURRAST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *blur_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    BLUR_OK = 0,
+    BLUR_EINVAL = 1,    /* invalid argument (sync) or face index out of range (status word) */
+    BLUR_EBEHIND = 2,   /* a vertex at or behind the near plane at some keyframe (status word) */
+    BLUR_ENOMEM = 3,    /* workspace smaller than blur_workspace_bytes() */
+    BLUR_ECUDA = 4,     /* a CUDA launch or copy failed */
+    BLUR_EOVERFLOW = 5  /* bin capacity exceeded: result exact, some tiles took the slow path */
+} blur_status;
+
+/* status-word bits (blur_read_status) */
+#define BLUR_ST_EINVAL 1
+#define BLUR_ST_EBEHIND 2
+#define BLUR_ST_EOVERFLOW 4
+#define BLUR_ST_EINTERNAL 8   /* internal consistency check failed (a bug: please report) */
+
+typedef enum { BLUR_STATIC = 0, BLUR_TRANSLATE = 1, BLUR_ROTATE = 2 } blur_motion_kind;
+typedef enum { BLUR_SCHED_GLOBAL_INCLUSIVE = 0, BLUR_SCHED_PAPER_SEGMENTED = 1 } blur_sched_rule;
+
+/* Motion over the exposure t in [0,1] (host struct, one per image).
+ *  BLUR_TRANSLATE: P(t) = P0 + (t - 0.5) vec          (A30, generalised; Q2)
+ *  BLUR_ROTATE:    P(t) = c + R(vec, angle t)(P0 - c)  (A31, generalised; Q3, Q4:
+ *                  right-handed Rodrigues rotation about the unit axis vec through c = pivot)
+ *  n_subframes N >= 1; n_segments S >= 1 (linear segments); sched_rule as Q1:
+ *   GLOBAL_INCLUSIVE: t_k = k/(N-1) (N=1: 0.5), s_k = min(floor(t_k S), S-1), tau_k = t_k S - s_k;
+ *   PAPER_SEGMENTED:  S | N, K = N/S, s_k = k div K, tau_k = (k mod K)/(K-1) (K=1: 0.5). */
+typedef struct {
+    int32_t kind;
+    float vec[3];
+    float angle;
+    float pivot[3];
+    int32_t n_subframes;
+    int32_t n_segments;
+    int32_t sched_rule;
+} blur_motion;
+
+/* Pinhole camera (host struct, one per image): looks from eye at target; right = normalize(f x up),
+ * up' = right x f; view coords Q = (right.(P-E), up'.(P-E), f.(P-E)); NDC x = Qx/(Qz tan(half_fov)),
+ * y = Qy/(Qz tan(half_fov)) (A34; Q5).  A vertex with Qz <= z_near is invalid. */
+typedef struct {
+    float eye[3];
+    float target[3];
+    float up[3];
+    float half_fov;   /* radians, in (0, pi/2) */
+    float z_near;     /* > 0 */
+} blur_camera;
+
+/* Tuning / instrumentation (host struct; NULL = defaults). */
+#define BLUR_REUSE_SETUP 1   /* bwd: reuse keyframes, coefficients and bins that the preceding fwd
+                                call with identical arguments left in the same workspace */
+typedef struct {
+    int32_t max_chunk;             /* G: max sub-frames sharing one tile bin (0 = automatic) */
+    int32_t flags;                 /* BLUR_REUSE_SETUP */
+    float bin_factor;              /* bin-entry capacity per (chunk, face) (0 = default 3.0) */
+    unsigned long long *census;    /* device u64[4] or NULL: fwd adds [covered (pixel,face,subframe)
+                                      pairs, covered (pixel,subframe), candidate pair tests,
+                                      staged (face,subframe,tile) records] */
+    void *raster_events[2];        /* host cudaEvent_t pair or NULLs: recorded on `stream` right
+                                      before / after the raster kernel (K4 in fwd, K6 in bwd), for
+                                      timing the dominant kernel inside a step */
+} blur_config;
+
+/* Bytes of device workspace the render calls need for these arguments (0 + blur_last_error() on
+ * invalid arguments).  `motions`, `cams` and `sub_range` are host arrays as in blur_render_fwd. */
+size_t blur_workspace_bytes(int V, int F, int B, int H, int W, const blur_motion *motions,
+                            const blur_camera *cams, const int32_t *sub_range, const blur_config *cfg);
+
+/* Forward: blurred images.
+ *  verts [V,3], faces [F,3], colors [V,3]: device, read-only.
+ *  motions [B], cams [B]: host.
+ *  sub_range: host [B][2] half-open sub-frame ranges [k0,k1) per image, or NULL for [0,N).
+ *  out_rgba [B,H,W,4]: overwritten with (1/N) sum over k in [k0,k1) of the sub-frame values, so
+ *    partial ranges add up (sub-frame sharding).
+ *  ids [B,H,W] or NULL: winning face index at sub-frame ids_subframe (-1 = background); pixels of
+ *    images whose [k0,k1) does not contain ids_subframe are left untouched.
+ *  ws / ws_bytes: device workspace of at least blur_workspace_bytes(...). */
+int blur_render_fwd(const float *verts, int V, const int32_t *faces, int F, const float *colors,
+                    const blur_motion *motions, const blur_camera *cams, int B, int H, int W,
+                    const int32_t *sub_range, float *out_rgba, int32_t *ids, int ids_subframe,
+                    const blur_config *cfg, void *ws, size_t ws_bytes, blur_stream_t stream);
+
+/* Backward: grad_rgba [B,H,W,4] = dL/d out_rgba (device).  grad_verts [V,3] and grad_colors [V,3]
+ * are OVERWRITTEN with dL/dverts (world) and dL/dcolors summed over the B images and the sub-frame
+ * ranges.  The alpha channel carries no position gradient in the hard-coverage path.
+ * With cfg->flags & BLUR_REUSE_SETUP the setup stages of the preceding blur_render_fwd on the same
+ * workspace with identical arguments are reused. */
+int blur_render_bwd(const float *verts, int V, const int32_t *faces, int F, const float *colors,
+                    const blur_motion *motions, const blur_camera *cams, int B, int H, int W,
+                    const int32_t *sub_range, const float *grad_rgba, float *grad_verts,
+                    float *grad_colors, const blur_config *cfg, void *ws, size_t ws_bytes,
+                    blur_stream_t stream);
+
+/* L2 image loss (BASELINE C1 "L2 loss"; Q14): loss[0] = sum((out - target)^2) / n_norm and
+ * grad = 2 (out - target) / n_norm over n elements (n_norm <= 0 -> n).  loss is a device float,
+ * overwritten; grad may alias nothing else. */
+int blur_l2_loss_grad(const float *out, const float *target, int64_t n, int64_t n_norm, float *loss,
+                      float *grad, blur_stream_t stream);
+
+/* Synchronises `stream`, reads the status word of `ws` (BLUR_ST_* bits) into *status_out (host) and
+ * clears it. */
+int blur_read_status(void *ws, blur_stream_t stream, int32_t *status_out);
+
+/* FP32 FFMA throughput microbenchmark (roofline denominator): runs `iters` iterations of 8
+ * independent FMA chains per thread on ctas x 256 threads; writes 2 * flops-per-launch into
+ * *flops (host) and sinks results into sink (device, >= ctas*256 floats). */
+int blur_ffma_probe(int ctas, int iters, float *sink, double *flops, blur_stream_t stream);
+
+/* Message for the last non-OK return on this thread ("" if none). */
+const char *blur_last_error(void);
+
+/* ABI version (increments on incompatible change). */
+int blur_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLURRAST_H */

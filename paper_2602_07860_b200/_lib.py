@@ -1,0 +1,219 @@
+"""Thin ctypes binding of libblurrast (include/blurrast.h): argument marshalling only.
+
+Every function has the name of the C entry point it calls.  Device buffers are passed as torch
+CUDA tensors (checked for device, dtype and contiguity), host structs are built from numpy arrays.
+There is no CPU fallback: if libblurrast.so is missing or CUDA is unavailable the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libblurrast.so")
+_lock = threading.Lock()
+_lib = None
+
+BLUR_OK, BLUR_EINVAL, BLUR_EBEHIND, BLUR_ENOMEM, BLUR_ECUDA, BLUR_EOVERFLOW = range(6)
+BLUR_ST_EINVAL, BLUR_ST_EBEHIND, BLUR_ST_EOVERFLOW, BLUR_ST_EINTERNAL = 1, 2, 4, 8
+BLUR_REUSE_SETUP = 1
+STATUS_NAMES = {0: "BLUR_OK", 1: "BLUR_EINVAL", 2: "BLUR_EBEHIND", 3: "BLUR_ENOMEM", 4: "BLUR_ECUDA",
+                5: "BLUR_EOVERFLOW"}
+
+EXPORTED = ["blur_workspace_bytes", "blur_render_fwd", "blur_render_bwd", "blur_l2_loss_grad",
+            "blur_read_status", "blur_ffma_probe", "blur_last_error", "blur_abi_version"]
+
+
+class BlurError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("%s: %s" % (STATUS_NAMES.get(code, str(code)), msg))
+        self.code = code
+
+
+class blur_motion(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("vec", C.c_float * 3), ("angle", C.c_float), ("pivot", C.c_float * 3),
+                ("n_subframes", C.c_int32), ("n_segments", C.c_int32), ("sched_rule", C.c_int32)]
+
+
+class blur_camera(C.Structure):
+    _fields_ = [("eye", C.c_float * 3), ("target", C.c_float * 3), ("up", C.c_float * 3),
+                ("half_fov", C.c_float), ("z_near", C.c_float)]
+
+
+class blur_config(C.Structure):
+    _fields_ = [("max_chunk", C.c_int32), ("flags", C.c_int32), ("bin_factor", C.c_float),
+                ("census", C.c_void_p), ("raster_events", C.c_void_p * 2)]
+
+
+def load():
+    """Load libblurrast.so (fails loudly if it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libblurrast.so not built (%s); run __graft_entry__.build()" % LIB_PATH)
+        lib = C.CDLL(LIB_PATH)
+        P, I, SZ = C.c_void_p, C.c_int, C.c_size_t
+        lib.blur_workspace_bytes.argtypes = [I, I, I, I, I, P, P, P, P]
+        lib.blur_workspace_bytes.restype = SZ
+        lib.blur_render_fwd.argtypes = [P, I, P, I, P, P, P, I, I, I, P, P, P, I, P, P, SZ, P]
+        lib.blur_render_bwd.argtypes = [P, I, P, I, P, P, P, I, I, I, P, P, P, P, P, P, SZ, P]
+        lib.blur_l2_loss_grad.argtypes = [P, P, C.c_int64, C.c_int64, P, P, P]
+        lib.blur_read_status.argtypes = [P, P, P]
+        lib.blur_ffma_probe.argtypes = [I, I, P, P, P]
+        lib.blur_last_error.restype = C.c_char_p
+        lib.blur_abi_version.restype = I
+        _lib = lib
+        return lib
+
+
+def _check(code):
+    if code != BLUR_OK:
+        raise BlurError(code, load().blur_last_error().decode())
+    return code
+
+
+def _dev(t, dtype, name):
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("%s must be a CUDA tensor" % name)
+    if t.dtype != dtype:
+        raise TypeError("%s must be %s, got %s" % (name, dtype, t.dtype))
+    if not t.is_contiguous():
+        raise ValueError("%s must be contiguous" % name)
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+# ------------------------------------------------------------------------- host structs
+
+def make_motions(motion: dict):
+    """motion dict of arrays (see scenes/) -> ctypes blur_motion[B]."""
+    B = len(motion["kind"])
+    arr = (blur_motion * max(B, 1))()
+    for b in range(B):
+        m = arr[b]
+        m.kind = int(motion["kind"][b])
+        m.vec[:] = [float(x) for x in motion["vec"][b]]
+        m.angle = float(motion["angle"][b])
+        m.pivot[:] = [float(x) for x in motion["pivot"][b]]
+        m.n_subframes = int(motion["n_sub"][b])
+        m.n_segments = int(motion["n_seg"][b])
+        m.sched_rule = int(motion["rule"][b])
+    return arr
+
+
+def make_cams(cams: np.ndarray):
+    """float [B,11] (eye, target, up, half_fov, z_near) -> ctypes blur_camera[B]."""
+    cams = np.asarray(cams, dtype=np.float64)
+    B = cams.shape[0]
+    arr = (blur_camera * max(B, 1))()
+    for b in range(B):
+        c = arr[b]
+        c.eye[:] = list(cams[b, 0:3])
+        c.target[:] = list(cams[b, 3:6])
+        c.up[:] = list(cams[b, 6:9])
+        c.half_fov = float(cams[b, 9])
+        c.z_near = float(cams[b, 10])
+    return arr
+
+
+def make_sub_range(sub_range):
+    if sub_range is None:
+        return None
+    a = np.ascontiguousarray(np.asarray(sub_range, dtype=np.int32).reshape(-1, 2))
+    return a
+
+
+def make_config(max_chunk=0, flags=0, bin_factor=0.0, census=None, events=None):
+    """events: optional (torch.cuda.Event, torch.cuda.Event) recorded around the raster kernel."""
+    cfg = blur_config(int(max_chunk), int(flags), float(bin_factor),
+                      None if census is None else C.c_void_p(census.data_ptr()))
+    if events is not None:
+        cfg.raster_events[0] = events[0].cuda_event
+        cfg.raster_events[1] = events[1].cuda_event
+    return cfg
+
+
+def _np_ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _ref(x):
+    return None if x is None else C.byref(x)
+
+
+# ------------------------------------------------------------------------- entry points
+
+def blur_workspace_bytes(V, F, B, H, W, motions, cams, sub_range=None, cfg=None) -> int:
+    n = load().blur_workspace_bytes(V, F, B, H, W, motions, cams, _np_ptr(sub_range), _ref(cfg))
+    if n == 0:
+        raise BlurError(BLUR_EINVAL, load().blur_last_error().decode())
+    return int(n)
+
+
+def blur_render_fwd(verts, faces, colors, motions, cams, B, H, W, out_rgba, ws, sub_range=None, ids=None,
+                    ids_subframe=-1, cfg=None, stream=None):
+    import torch
+    V = verts.shape[0]
+    F = faces.shape[0]
+    return _check(load().blur_render_fwd(
+        _dev(verts, torch.float32, "verts"), V, _dev(faces, torch.int32, "faces"), F,
+        _dev(colors, torch.float32, "colors"), motions, cams, B, H, W, _np_ptr(sub_range),
+        _dev(out_rgba, torch.float32, "out_rgba"), _dev(ids, torch.int32, "ids"), int(ids_subframe),
+        _ref(cfg), _dev(ws, torch.uint8, "ws"), ws.numel(), _stream(stream)))
+
+
+def blur_render_bwd(verts, faces, colors, motions, cams, B, H, W, grad_rgba, grad_verts, grad_colors, ws,
+                    sub_range=None, cfg=None, stream=None):
+    import torch
+    V = verts.shape[0]
+    F = faces.shape[0]
+    return _check(load().blur_render_bwd(
+        _dev(verts, torch.float32, "verts"), V, _dev(faces, torch.int32, "faces"), F,
+        _dev(colors, torch.float32, "colors"), motions, cams, B, H, W, _np_ptr(sub_range),
+        _dev(grad_rgba, torch.float32, "grad_rgba"), _dev(grad_verts, torch.float32, "grad_verts"),
+        _dev(grad_colors, torch.float32, "grad_colors"), _ref(cfg), _dev(ws, torch.uint8, "ws"), ws.numel(),
+        _stream(stream)))
+
+
+def blur_l2_loss_grad(out, target, loss, grad, n_norm=0, stream=None):
+    import torch
+    return _check(load().blur_l2_loss_grad(
+        _dev(out, torch.float32, "out"), _dev(target, torch.float32, "target"), out.numel(), int(n_norm),
+        _dev(loss, torch.float32, "loss"), _dev(grad, torch.float32, "grad"), _stream(stream)))
+
+
+def blur_read_status(ws, stream=None) -> int:
+    import torch
+    st = C.c_int32(0)
+    _check(load().blur_read_status(_dev(ws, torch.uint8, "ws"), _stream(stream), C.byref(st)))
+    return int(st.value)
+
+
+def blur_ffma_probe(ctas, iters, sink, stream=None) -> float:
+    import torch
+    fl = C.c_double(0)
+    _check(load().blur_ffma_probe(int(ctas), int(iters), _dev(sink, torch.float32, "sink"), C.byref(fl),
+                                  _stream(stream)))
+    return float(fl.value)
+
+
+def blur_last_error() -> str:
+    return load().blur_last_error().decode()
+
+
+def blur_abi_version() -> int:
+    return int(load().blur_abi_version())

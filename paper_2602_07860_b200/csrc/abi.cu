@@ -1,0 +1,435 @@
+// abi.cu -- the C ABI of libblurrast (include/blurrast.h): argument validation, the host-side
+// schedule/pose/chunk plan (L0), workspace carving and the launch sequence K1..K7.
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+#include "../../include/blurrast.h"
+
+using namespace br;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Q1 schedule (same reading as DESIGN.md; integer arithmetic for GLOBAL_INCLUSIVE)
+bool schedule(int N, int S, int rule, std::vector<int> &s_out, std::vector<float> &tau_out)
+{
+    s_out.resize(N);
+    tau_out.resize(N);
+    if (rule == BLUR_SCHED_PAPER_SEGMENTED) {
+        if (N % S) return false;
+        const int K = N / S;
+        for (int k = 0; k < N; ++k) {
+            s_out[k] = k / K;
+            tau_out[k] = K == 1 ? 0.5f : (float)((double)(k % K) / (double)(K - 1));
+        }
+        return true;
+    }
+    if (rule != BLUR_SCHED_GLOBAL_INCLUSIVE) return false;
+    if (N == 1) {
+        int s = S / 2;
+        if (s > S - 1) s = S - 1;
+        s_out[0] = s;
+        tau_out[0] = (float)(0.5 * S - s);
+        return true;
+    }
+    for (int k = 0; k < N; ++k) {
+        const long long num = (long long)k * S;
+        long long s = num / (N - 1);
+        if (s > S - 1) s = S - 1;
+        s_out[k] = (int)s;
+        tau_out[k] = (float)((double)(num - s * (N - 1)) / (double)(N - 1));
+    }
+    return true;
+}
+
+void rodrigues(const double ax_in[3], double th, double R[9])
+{
+    double a[3] = {ax_in[0], ax_in[1], ax_in[2]};
+    const double n = std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    for (double &x : a) x /= n;
+    const double K[9] = {0, -a[2], a[1], a[2], 0, -a[0], -a[1], a[0], 0};
+    const double sn = std::sin(th), cs = 1.0 - std::cos(th);
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double k2 = 0;
+            for (int l = 0; l < 3; ++l) k2 += K[i * 3 + l] * K[l * 3 + j];
+            R[i * 3 + j] = (i == j ? 1.0 : 0.0) + sn * K[i * 3 + j] + cs * k2;
+        }
+}
+
+struct Plan {
+    int B = 0, V = 0, F = 0, H = 0, W = 0, TX = 0, TY = 0, T = 0, NC = 0, maxS = 1;
+    std::vector<ImgInfo> imgs;
+    std::vector<Chunk> chunks;
+    std::vector<int> sched_s;
+    std::vector<float> sched_tau;
+    std::vector<PoseRec> poses;
+    long long n_key = 0, n_rec = 0, cap = 0;
+    size_t nbins = 0;
+    size_t o_status = 0, o_imgs = 0, o_chunks = 0, o_ss = 0, o_st = 0, o_poses = 0, o_tables_end = 0;
+    size_t o_key = 0, o_rec = 0, o_fcol = 0, o_cnt = 0, o_off = 0, o_bsum = 0, o_ent = 0, o_dkey = 0, total = 0;
+};
+
+int auto_chunk(const blur_motion &m, const blur_camera &c, int H, int W)
+{
+    const double dx = c.eye[0] - c.target[0], dy = c.eye[1] - c.target[1], dz = c.eye[2] - c.target[2];
+    const double dist = std::sqrt(dx * dx + dy * dy + dz * dz);
+    const double ndc_per_world = 1.0 / (dist * std::tan((double)c.half_fov));
+    const double px_per_ndc = 0.5 * (H > W ? H : W);
+    const int N = m.n_subframes;
+    if (N <= 1) return 16;
+    double world = 0.0;
+    if (m.kind == BLUR_TRANSLATE)
+        world = std::sqrt((double)m.vec[0] * m.vec[0] + (double)m.vec[1] * m.vec[1] + (double)m.vec[2] * m.vec[2]);
+    else if (m.kind == BLUR_ROTATE)
+        world = std::fabs((double)m.angle);   // unit-size object
+    const double disp = world * ndc_per_world * px_per_ndc / (N - 1);
+    if (disp <= 1e-6) return 16;
+    int g = (int)std::floor(TW / disp);
+    if (g < 2) g = 2;
+    if (g > 16) g = 16;
+    return g;
+}
+
+int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blur_camera *cams,
+              const int32_t *sub_range, const blur_config *cfg, Plan &P)
+{
+    if (V < 0 || F < 0 || B < 0) return fail(BLUR_EINVAL, "V, F, B must be >= 0");
+    if (F > 0 && V == 0) return fail(BLUR_EINVAL, "faces given but V == 0");
+    if (H < 1 || W < 1 || H > 32768 || W > 32768) return fail(BLUR_EINVAL, "H, W must be in [1, 32768]");
+    if (B > 0 && !m) return fail(BLUR_EINVAL, "motions is NULL");
+    P.B = B; P.V = V; P.F = F; P.H = H; P.W = W;
+    P.TX = (W + TW - 1) / TW;
+    P.TY = (H + TH - 1) / TH;
+    P.T = P.TX * P.TY;
+    P.imgs.resize(B);
+    int key_off = 0;
+    long long rec_off = 0;
+    for (int b = 0; b < B; ++b) {
+        const blur_motion &mo = m[b];
+        const int N = mo.n_subframes, S = mo.n_segments;
+        if (mo.kind < 0 || mo.kind > 2) return fail(BLUR_EINVAL, "motion kind must be 0, 1 or 2");
+        if (N < 1) return fail(BLUR_EINVAL, "n_subframes must be >= 1");
+        if (S < 1) return fail(BLUR_EINVAL, "n_segments must be >= 1");
+        if (mo.sched_rule == BLUR_SCHED_PAPER_SEGMENTED && N % S)
+            return fail(BLUR_EINVAL, "PAPER_SEGMENTED needs n_segments | n_subframes");
+        if (mo.sched_rule != 0 && mo.sched_rule != 1) return fail(BLUR_EINVAL, "bad sched_rule");
+        if (mo.kind == BLUR_ROTATE) {
+            const double n = std::sqrt((double)mo.vec[0] * mo.vec[0] + (double)mo.vec[1] * mo.vec[1] +
+                                       (double)mo.vec[2] * mo.vec[2]);
+            if (!(n > 0)) return fail(BLUR_EINVAL, "rotation axis is zero");
+        }
+        if (!std::isfinite(mo.angle) || !std::isfinite(mo.vec[0]) || !std::isfinite(mo.vec[1]) ||
+            !std::isfinite(mo.vec[2]))
+            return fail(BLUR_EINVAL, "non-finite motion parameter");
+        if (S > P.maxS) P.maxS = S;
+        ImgInfo &im = P.imgs[b];
+        std::memset(&im, 0, sizeof(im));
+        im.N = N;
+        im.S = S;
+        im.k0 = sub_range ? sub_range[2 * b] : 0;
+        im.k1 = sub_range ? sub_range[2 * b + 1] : N;
+        if (im.k0 < 0 || im.k1 > N || im.k0 > im.k1) return fail(BLUR_EINVAL, "sub_range out of [0, N]");
+        im.sched_off = (int)P.sched_s.size();
+        std::vector<int> ss;
+        std::vector<float> tt;
+        if (!schedule(N, S, mo.sched_rule, ss, tt)) return fail(BLUR_EINVAL, "invalid schedule");
+        P.sched_s.insert(P.sched_s.end(), ss.begin(), ss.end());
+        P.sched_tau.insert(P.sched_tau.end(), tt.begin(), tt.end());
+        im.key_off = key_off;
+        key_off += (S + 1) * V;
+        im.rec_off = rec_off;
+        rec_off += (long long)S * F;
+        // camera
+        const blur_camera &c = cams[b];
+        if (!(c.half_fov > 0.f && c.half_fov < 1.5707963f)) return fail(BLUR_EINVAL, "half_fov not in (0, pi/2)");
+        if (!(c.z_near > 0.f)) return fail(BLUR_EINVAL, "z_near must be > 0");
+        double f[3] = {(double)c.target[0] - c.eye[0], (double)c.target[1] - c.eye[1], (double)c.target[2] - c.eye[2]};
+        double fn = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+        if (!(fn > 0)) return fail(BLUR_EINVAL, "eye == target");
+        for (double &x : f) x /= fn;
+        double r[3] = {f[1] * c.up[2] - f[2] * c.up[1], f[2] * c.up[0] - f[0] * c.up[2], f[0] * c.up[1] - f[1] * c.up[0]};
+        double rn = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+        double upn = std::sqrt((double)c.up[0] * c.up[0] + (double)c.up[1] * c.up[1] + (double)c.up[2] * c.up[2]);
+        if (!(rn > 1e-9 * upn) || !(upn > 0)) return fail(BLUR_EINVAL, "up parallel to the view direction");
+        for (double &x : r) x /= rn;
+        const double u[3] = {r[1] * f[2] - r[2] * f[1], r[2] * f[0] - r[0] * f[2], r[0] * f[1] - r[1] * f[0]};
+        for (int i = 0; i < 3; ++i) { im.Rc[i] = r[i]; im.Rc[3 + i] = u[i]; im.Rc[6 + i] = f[i]; im.eye[i] = c.eye[i]; }
+        im.tan_half = std::tan((double)c.half_fov);
+        im.z_near = c.z_near;
+        // keyframe poses t = s/S
+        im.pose_off = (int)P.poses.size();
+        for (int s = 0; s <= S; ++s) {
+            PoseRec pr;
+            std::memset(&pr, 0, sizeof(pr));
+            const double t = (double)s / (double)S;
+            for (int i = 0; i < 3; ++i) pr.R[4 * i] = 1.0;
+            if (mo.kind == BLUR_TRANSLATE) {
+                for (int i = 0; i < 3; ++i) pr.T[i] = (t - 0.5) * (double)mo.vec[i];
+            } else if (mo.kind == BLUR_ROTATE) {
+                const double ax[3] = {mo.vec[0], mo.vec[1], mo.vec[2]};
+                rodrigues(ax, (double)mo.angle * t, pr.R);
+                for (int i = 0; i < 3; ++i) pr.c[i] = mo.pivot[i];
+            }
+            P.poses.push_back(pr);
+        }
+        // chunks: runs of consecutive sub-frames in one segment, at most G long
+        const int G = (cfg && cfg->max_chunk > 0) ? cfg->max_chunk : auto_chunk(mo, c, H, W);
+        im.chunk_begin = (int)P.chunks.size();
+        int k = im.k0;
+        while (k < im.k1) {
+            const int s = ss[k];
+            int e = k + 1;
+            while (e < im.k1 && ss[e] == s && e - k < G) ++e;
+            Chunk ch;
+            ch.b = b; ch.s = s; ch.k0 = k; ch.k1 = e;
+            ch.tmin = tt[k];
+            ch.tmax = tt[e - 1];
+            P.chunks.push_back(ch);
+            k = e;
+        }
+        im.chunk_end = (int)P.chunks.size();
+    }
+    P.NC = (int)P.chunks.size();
+    P.n_key = key_off;
+    P.n_rec = rec_off;
+    P.nbins = (size_t)P.NC * P.T;
+    if (P.nbins > (size_t)0x7fffffff) return fail(BLUR_EINVAL, "too many (chunk, tile) bins");
+    const double factor = (cfg && cfg->bin_factor > 0.f) ? cfg->bin_factor : 3.0;
+    double cap = factor * (double)P.NC * (double)F + 1024.0;
+    if (cap > 2.0e9) cap = 2.0e9;
+    P.cap = (long long)cap;
+    // workspace layout
+    size_t o = 0;
+    P.o_status = o; o = align256(o + 256);
+    P.o_imgs = o; o = align256(o + sizeof(ImgInfo) * (size_t)B);
+    P.o_chunks = o; o = align256(o + sizeof(Chunk) * P.chunks.size());
+    P.o_ss = o; o = align256(o + sizeof(int) * P.sched_s.size());
+    P.o_st = o; o = align256(o + sizeof(float) * P.sched_tau.size());
+    P.o_poses = o; o = align256(o + sizeof(PoseRec) * P.poses.size());
+    P.o_tables_end = o;
+    P.o_key = o; o = align256(o + 16 * (size_t)P.n_key);
+    P.o_rec = o; o = align256(o + 16 * REC_F4 * (size_t)P.n_rec);
+    P.o_fcol = o; o = align256(o + 48 * (size_t)F);
+    P.o_cnt = o; o = align256(o + 4 * P.nbins);
+    P.o_off = o; o = align256(o + 4 * (P.nbins + 1));
+    P.o_bsum = o; o = align256(o + 4 * ((P.nbins + 1023) / 1024 + 1));
+    P.o_ent = o; o = align256(o + 4 * (size_t)P.cap);
+    P.o_dkey = o; o = align256(o + 8 * (size_t)P.n_key);
+    P.total = o;
+    return BLUR_OK;
+}
+
+Tables make_tables(const Plan &P, void *ws)
+{
+    char *w = (char *)ws;
+    Tables t;
+    std::memset(&t, 0, sizeof(t));
+    t.status = (int *)(w + P.o_status);
+    t.imgs = (const ImgInfo *)(w + P.o_imgs);
+    t.chunks = (const Chunk *)(w + P.o_chunks);
+    t.sched_s = (const int *)(w + P.o_ss);
+    t.sched_tau = (const float *)(w + P.o_st);
+    t.poses = (const PoseRec *)(w + P.o_poses);
+    t.key = (float4 *)(w + P.o_key);
+    t.rec = (float4 *)(w + P.o_rec);
+    t.fcol = (float4 *)(w + P.o_fcol);
+    t.cnt = (int *)(w + P.o_cnt);
+    t.off = (int *)(w + P.o_off);
+    t.bsum = (int *)(w + P.o_bsum);
+    t.entries = (int *)(w + P.o_ent);
+    t.cap = P.cap;
+    t.dkey = (float2 *)(w + P.o_dkey);
+    t.NC = P.NC; t.T = P.T; t.TX = P.TX; t.TY = P.TY;
+    t.B = P.B; t.V = P.V; t.F = P.F; t.H = P.H; t.W = P.W;
+    return t;
+}
+
+int upload_tables(const Plan &P, void *ws, cudaStream_t st)
+{
+    std::vector<char> h(P.o_tables_end - P.o_imgs, 0);
+    auto put = [&](size_t off, const void *src, size_t n) {
+        if (n) std::memcpy(h.data() + (off - P.o_imgs), src, n);
+    };
+    put(P.o_imgs, P.imgs.data(), sizeof(ImgInfo) * P.imgs.size());
+    put(P.o_chunks, P.chunks.data(), sizeof(Chunk) * P.chunks.size());
+    put(P.o_ss, P.sched_s.data(), sizeof(int) * P.sched_s.size());
+    put(P.o_st, P.sched_tau.data(), sizeof(float) * P.sched_tau.size());
+    put(P.o_poses, P.poses.data(), sizeof(PoseRec) * P.poses.size());
+    cudaError_t e = cudaMemcpyAsync((char *)ws + P.o_imgs, h.data(), h.size(), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return fail(BLUR_ECUDA, std::string("table upload: ") + cudaGetErrorString(e));
+    return BLUR_OK;
+}
+
+int cuda_check(cudaError_t e, const char *what)
+{
+    if (e != cudaSuccess) return fail(BLUR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return BLUR_OK;
+}
+
+bool check_env()
+{
+    const char *s = std::getenv("BLURRAST_CHECK");
+    return s && s[0] == '1';
+}
+
+int status_to_code(int st)
+{
+    if (st & BLUR_ST_EINTERNAL) return fail(BLUR_ECUDA, "internal consistency check failed");
+    if (st & BLUR_ST_EINVAL) return fail(BLUR_EINVAL, "a face index is out of range [0, V)");
+    if (st & BLUR_ST_EBEHIND) return fail(BLUR_EBEHIND, "a vertex is at or behind the near plane");
+    if (st & BLUR_ST_EOVERFLOW) return fail(BLUR_EOVERFLOW, "bin capacity exceeded (exact slow path used)");
+    return BLUR_OK;
+}
+
+int sync_status(void *ws, const Plan &P, cudaStream_t st)
+{
+    int h = 0;
+    int r = cuda_check(cudaMemcpyAsync(&h, (char *)ws + P.o_status, sizeof(int), cudaMemcpyDeviceToHost, st), "status read");
+    if (r) return r;
+    r = cuda_check(cudaStreamSynchronize(st), "stream sync");
+    if (r) return r;
+    return status_to_code(h);
+}
+
+int prepare(const float *verts, int V, const int32_t *faces, int F, const float *colors, const blur_motion *m,
+            const blur_camera *cams, int B, int H, int W, const int32_t *sub_range, const blur_config *cfg,
+            void *ws, size_t ws_bytes, cudaStream_t st, bool do_setup, Plan &P, Tables &t)
+{
+    int r = make_plan(V, F, B, H, W, m, cams, sub_range, cfg, P);
+    if (r) return r;
+    if (B > 0 && (!verts && V > 0)) return fail(BLUR_EINVAL, "verts is NULL");
+    if (F > 0 && (!faces || !colors)) return fail(BLUR_EINVAL, "faces or colors is NULL");
+    if (!ws) return fail(BLUR_EINVAL, "workspace is NULL");
+    if (ws_bytes < P.total)
+        return fail(BLUR_ENOMEM, "workspace too small: need " + std::to_string(P.total) + " bytes");
+    t = make_tables(P, ws);
+    if (!do_setup) return BLUR_OK;
+    r = cuda_check(cudaMemsetAsync(t.status, 0, sizeof(int), st), "status clear");
+    if (r) return r;
+    r = upload_tables(P, ws, st);
+    if (r) return r;
+    r = cuda_check(launch_setup(t, verts, faces, colors, P.maxS, st), "setup kernels");
+    if (r) return r;
+    return cuda_check(launch_binning(t, st), "binning kernels");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *blur_last_error(void) { return g_err.c_str(); }
+
+int blur_abi_version(void) { return 1; }
+
+size_t blur_workspace_bytes(int V, int F, int B, int H, int W, const blur_motion *motions,
+                            const blur_camera *cams, const int32_t *sub_range, const blur_config *cfg)
+{
+    g_err.clear();
+    Plan P;
+    if (B > 0 && !cams) { fail(BLUR_EINVAL, "cams is NULL"); return 0; }
+    if (make_plan(V, F, B, H, W, motions, cams, sub_range, cfg, P)) return 0;
+    return P.total;
+}
+
+int blur_render_fwd(const float *verts, int V, const int32_t *faces, int F, const float *colors,
+                    const blur_motion *motions, const blur_camera *cams, int B, int H, int W,
+                    const int32_t *sub_range, float *out_rgba, int32_t *ids, int ids_subframe,
+                    const blur_config *cfg, void *ws, size_t ws_bytes, blur_stream_t stream)
+{
+    g_err.clear();
+    cudaStream_t st = (cudaStream_t)stream;
+    if (B > 0 && !cams) return fail(BLUR_EINVAL, "cams is NULL");
+    if (B > 0 && !out_rgba) return fail(BLUR_EINVAL, "out_rgba is NULL");
+    Plan P;
+    Tables t;
+    int r = prepare(verts, V, faces, F, colors, motions, cams, B, H, W, sub_range, cfg, ws, ws_bytes, st, true, P, t);
+    if (r) return r;
+    if (cfg && cfg->raster_events[0]) cudaEventRecord((cudaEvent_t)cfg->raster_events[0], st);
+    r = cuda_check(launch_raster_fwd(t, out_rgba, ids, ids_subframe, cfg ? cfg->census : nullptr, st), "raster fwd");
+    if (r) return r;
+    if (cfg && cfg->raster_events[1]) cudaEventRecord((cudaEvent_t)cfg->raster_events[1], st);
+    if (check_env()) return sync_status(ws, P, st);
+    return BLUR_OK;
+}
+
+int blur_render_bwd(const float *verts, int V, const int32_t *faces, int F, const float *colors,
+                    const blur_motion *motions, const blur_camera *cams, int B, int H, int W,
+                    const int32_t *sub_range, const float *grad_rgba, float *grad_verts, float *grad_colors,
+                    const blur_config *cfg, void *ws, size_t ws_bytes, blur_stream_t stream)
+{
+    g_err.clear();
+    cudaStream_t st = (cudaStream_t)stream;
+    if (B > 0 && !cams) return fail(BLUR_EINVAL, "cams is NULL");
+    if (V > 0 && (!grad_verts || !grad_colors)) return fail(BLUR_EINVAL, "gradient outputs are NULL");
+    if (B > 0 && !grad_rgba) return fail(BLUR_EINVAL, "grad_rgba is NULL");
+    const bool reuse = cfg && (cfg->flags & BLUR_REUSE_SETUP);
+    Plan P;
+    Tables t;
+    int r = prepare(verts, V, faces, F, colors, motions, cams, B, H, W, sub_range, cfg, ws, ws_bytes, st, !reuse, P, t);
+    if (r) return r;
+    if (V > 0) {
+        r = cuda_check(cudaMemsetAsync(grad_colors, 0, sizeof(float) * 3 * (size_t)V, st), "grad clear");
+        if (r) return r;
+    }
+    if (P.n_key) {
+        r = cuda_check(cudaMemsetAsync(t.dkey, 0, 8 * (size_t)P.n_key, st), "dkey clear");
+        if (r) return r;
+    }
+    if (cfg && cfg->raster_events[0]) cudaEventRecord((cudaEvent_t)cfg->raster_events[0], st);
+    r = cuda_check(launch_raster_bwd(t, grad_rgba, grad_colors, st), "raster bwd");
+    if (r) return r;
+    if (cfg && cfg->raster_events[1]) cudaEventRecord((cudaEvent_t)cfg->raster_events[1], st);
+    r = cuda_check(launch_vertex_chain(t, grad_verts, st), "vertex chain");
+    if (r) return r;
+    if (check_env()) return sync_status(ws, P, st);
+    return BLUR_OK;
+}
+
+int blur_l2_loss_grad(const float *out, const float *target, int64_t n, int64_t n_norm, float *loss, float *grad,
+                      blur_stream_t stream)
+{
+    g_err.clear();
+    if (n < 0) return fail(BLUR_EINVAL, "n < 0");
+    if (!loss || (n > 0 && (!out || !target || !grad))) return fail(BLUR_EINVAL, "NULL pointer");
+    if ((((uintptr_t)out) | ((uintptr_t)target) | ((uintptr_t)grad)) & 15)
+        return fail(BLUR_EINVAL, "out/target/grad must be 16-byte aligned");
+    return cuda_check(launch_l2(out, target, n, n_norm, loss, grad, (cudaStream_t)stream), "l2 loss");
+}
+
+int blur_read_status(void *ws, blur_stream_t stream, int32_t *status_out)
+{
+    g_err.clear();
+    if (!ws || !status_out) return fail(BLUR_EINVAL, "NULL pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    int h = 0;
+    int r = cuda_check(cudaMemcpyAsync(&h, ws, sizeof(int), cudaMemcpyDeviceToHost, st), "status read");
+    if (r) return r;
+    r = cuda_check(cudaStreamSynchronize(st), "stream sync");
+    if (r) return r;
+    *status_out = h;
+    return cuda_check(cudaMemsetAsync(ws, 0, sizeof(int), st), "status clear");
+}
+
+int blur_ffma_probe(int ctas, int iters, float *sink, double *flops, blur_stream_t stream)
+{
+    g_err.clear();
+    if (ctas < 1 || iters < 1 || !sink || !flops) return fail(BLUR_EINVAL, "bad probe arguments");
+    *flops = 2.0 * 16.0 * 8.0 * (double)iters * 256.0 * (double)ctas;
+    return cuda_check(launch_ffma_probe(ctas, iters, sink, (cudaStream_t)stream), "ffma probe");
+}
+
+}  // extern "C"

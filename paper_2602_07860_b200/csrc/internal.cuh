@@ -1,0 +1,120 @@
+// internal.cuh -- device-side layouts shared by the kernels of libblurrast (not part of the ABI).
+// See include/blurrast.h for the public contract and DESIGN.md for the data layout in HBM.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace br {
+
+// Tile geometry of the raster kernels: a CTA owns a TW x TH pixel tile; each warp owns an
+// 8 x 4 footprint (8 warps).  One pixel per thread.
+constexpr int TW = 16;
+constexpr int TH = 16;
+constexpr int NT = 256;          // threads per raster CTA
+constexpr int CAP = 512;         // per-(tile, sub-frame) face records staged per batch (smem)
+constexpr int SORTCAP = 1024;    // bins longer than this take the exact fallback path
+constexpr float EPS_D = 1e-12f;  // Q8: |det F| <= 1e-12 NDC^2 -> face skipped for that sub-frame
+constexpr float BBOX_PAD = 1e-5f;  // NDC padding of conservative bounding boxes (>> fp32 error)
+
+// Per (face, segment) coefficient record: the paper's Eq.8 coefficients (A1, A2, A3, a1..a3),
+// computed once per segment, in edge-vector form about a per-edge origin (DESIGN.md
+// "edge-vector form"), plus the depth keyframes and conservative keyframe bounding boxes.
+// 44 floats = 11 x float4 = 176 B.
+//   [8i+0..8i+7]  numerator of w_i (edge opposite corner i): ox, oy, a0, a1, b0, b1, g1, g2
+//                 N_i(tau; p) = (a0 + a1 tau)(u - ox) + (b0 + b1 tau)(v - oy) + tau (g1 + g2 tau)
+//                 i.e. A1_i = g2, A2_i(p) = a1 (u-ox) + b1 (v-oy) + g1, A3_i(p) = a0 (u-ox) + b0 (v-oy)
+//   [24..26]      d1, d2, d3: det F(tau) = d3 + tau (d2 + tau d1)  (a1, a2, a3 of Eq.8)
+//   [27]          face id (int bits), -1 = skipped face
+//   [28..31]      bbox at keyframe s (xmin, xmax, ymin, ymax), [32..35] at keyframe s+1 (padded)
+//   [36..38]      view depth at keyframe s, [40..42] at keyframe s+1 ([39], [43] unused)
+constexpr int REC_F4 = 11;
+constexpr int REC_FLOATS = 44;
+
+struct ImgInfo {
+    int N, S;            // sub-frames, segments
+    int k0, k1;          // sub-frame range [k0, k1)
+    int sched_off;       // offset of this image's schedule in the sched arrays
+    int key_off;         // offset (float4 units) of keyframes [S+1][V]; also float2 offset of dkey
+    long long rec_off;   // offset (records) of coefficient records [S][F]
+    int chunk_begin, chunk_end;
+    int pose_off;        // offset (in PoseRec) of keyframe poses [S+1]
+    int pad0;
+    double Rc[9];        // camera rotation rows (right, up', forward)
+    double eye[3];
+    double tan_half;     // tan(half_fov)
+    double z_near;
+};
+
+struct PoseRec {         // P = R (P0 - c) + c + T at keyframe time t = s/S
+    double R[9];
+    double c[3];
+    double T[3];
+};
+
+struct Chunk {           // consecutive sub-frames of one image inside one segment
+    int b, s, k0, k1;    // sub-frames k0..k1-1 (image-local indices)
+    float tmin, tmax;    // tau of the first / last sub-frame
+};
+
+struct Tables {          // device pointers into the workspace
+    int *status;
+    const ImgInfo *imgs;
+    const Chunk *chunks;
+    const int *sched_s;
+    const float *sched_tau;
+    const PoseRec *poses;
+    float4 *key;         // keyframes (x_ndc, y_ndc, z_view, valid)
+    float4 *rec;         // coefficient records
+    float4 *fcol;        // per face: 3 x float4 = c0.rgb c1.rgb c2.rgb vid0 vid1 vid2 (int bits)
+    int *cnt;            // [NC * T]
+    int *off;            // [NC * T + 1]
+    int *bsum;           // scan block sums
+    int *entries;        // bin entries (face ids)
+    long long cap;       // entries capacity
+    float2 *dkey;        // screen-space keyframe gradients, indexed like key
+    int NC, T, TX, TY;
+    int B, V, F, H, W;
+};
+
+struct __align__(16) TauRec {    // per (face, sub-frame, tile) staged record, 64 B
+    float a[3], b[3], g[3];      // sign-normalised edge functions: e_i = a_i ul + b_i vl + g_i
+    float az, bz, cz;            // view depth plane in tile-local coordinates
+    float invD;                  // 1 / |det F(tau)|
+    int fid;
+    int pad0, pad1;
+};
+
+// NDC interval -> inclusive pixel-centre index range (Q9: centre of pixel i at -1 + (2i+1)/W).
+// Explicit-rounding arithmetic so that every kernel (K3 binning, raster staging, fallback scan)
+// derives bit-identical ranges from identical inputs (no compiler-chosen FMA contraction).
+__device__ __forceinline__ void ndc_to_index(float lo, float hi, int n, bool flip, float &a, float &b)
+{
+    const float fn = (float)n;
+    if (!flip) {   // x: i >= ((lo + 1) n - 1) / 2
+        a = ceilf(__fmul_rn(__fsub_rn(__fmul_rn(__fadd_rn(lo, 1.f), fn), 1.f), 0.5f));
+        b = floorf(__fmul_rn(__fsub_rn(__fmul_rn(__fadd_rn(hi, 1.f), fn), 1.f), 0.5f));
+    } else {       // y (row 0 at the top): j >= ((1 - hi) n - 1) / 2
+        a = ceilf(__fmul_rn(__fsub_rn(__fmul_rn(__fsub_rn(1.f, hi), fn), 1.f), 0.5f));
+        b = floorf(__fmul_rn(__fsub_rn(__fmul_rn(__fsub_rn(1.f, lo), fn), 1.f), 0.5f));
+    }
+}
+
+// conservative keyframe box lerped to tau (monotone in tau for fixed endpoints)
+__device__ __forceinline__ float box_lerp(float tau, float a, float b) { return __fmaf_rn(tau, __fsub_rn(b, a), a); }
+
+}  // namespace br
+
+// launchers (defined in the .cu files)
+namespace br {
+cudaError_t launch_setup(const Tables &t, const float *verts, const int *faces, const float *colors,
+                         int maxS, cudaStream_t st);
+cudaError_t launch_binning(const Tables &t, cudaStream_t st);
+cudaError_t launch_raster_fwd(const Tables &t, float *out, int *ids, int ids_k,
+                              unsigned long long *census, cudaStream_t st);
+cudaError_t launch_raster_bwd(const Tables &t, const float *grad_rgba, float *grad_colors,
+                              cudaStream_t st);
+cudaError_t launch_vertex_chain(const Tables &t, float *grad_verts, cudaStream_t st);
+cudaError_t launch_l2(const float *out, const float *tgt, long long n, long long n_norm, float *loss,
+                      float *grad, cudaStream_t st);
+cudaError_t launch_ffma_probe(int ctas, int iters, float *sink, cudaStream_t st);
+}  // namespace br

@@ -1,0 +1,235 @@
+// k_bin.cu -- K3: tiled binning of faces per (chunk of sub-frames, tile).
+//
+// A chunk is a run of <= G consecutive sub-frames of one image inside one segment.  Inside a
+// segment every vertex moves linearly in screen space (Eq.5-6), so the screen bounding box of a
+// face over [tau_min, tau_max] is the union of its boxes at the two ends; with the keyframe boxes
+// lerped (a conservative superset of the lerped triangle's box) this gives the swept box exactly
+// as the raster kernel evaluates it per sub-frame (monotone fmaf), so the bin is conservative.
+//   K3a count  (chunk, face) -> atomic per (chunk, tile) counters
+//   K3b scan   exclusive prefix sum of the counters -> bin offsets
+//   K3c fill   (chunk, face) -> entries (unordered)
+//   K3d sort   one warp per bin: bitonic sort of the face ids in shared memory, so the raster
+//              kernels visit faces in index order (Z-buffer tie rule: lower index wins, Q7)
+// Bins longer than SORTCAP or beyond the entry capacity are left to the raster kernels' exact
+// fallback path (status bit BLUR_ST_EOVERFLOW).
+#include <cstdio>
+
+#include "internal.cuh"
+#include "../../include/blurrast.h"
+
+namespace br {
+
+__device__ __forceinline__ float lerpf_(float tau, float a, float b) { return box_lerp(tau, a, b); }
+
+// NDC box -> inclusive pixel index ranges (Q9 pixel centres); returns false if empty
+__device__ __forceinline__ bool ndc_box_to_pixels(float xmn, float xmx, float ymn, float ymx, int W, int H,
+                                                  int &i0, int &i1, int &j0, int &j1)
+{
+    float a, b, c, d;
+    ndc_to_index(xmn, xmx, W, false, a, b);
+    ndc_to_index(ymn, ymx, H, true, c, d);
+    a = fmaxf(a, 0.f);
+    b = fminf(b, (float)(W - 1));
+    c = fmaxf(c, 0.f);
+    d = fminf(d, (float)(H - 1));
+    if (!(a <= b) || !(c <= d)) return false;   // also rejects NaN
+    i0 = (int)a; i1 = (int)b; j0 = (int)c; j1 = (int)d;
+    return true;
+}
+
+__device__ __forceinline__ bool swept_tiles(const Tables &t, const float4 *r, float tmin, float tmax,
+                                            int &tx0, int &tx1, int &ty0, int &ty1)
+{
+    const float4 q6 = r[6];
+    if (__float_as_int(q6.w) < 0) return false;
+    const float4 b0 = r[7], b1 = r[8];
+    const float xmn = fminf(lerpf_(tmin, b0.x, b1.x), lerpf_(tmax, b0.x, b1.x));
+    const float xmx = fmaxf(lerpf_(tmin, b0.y, b1.y), lerpf_(tmax, b0.y, b1.y));
+    const float ymn = fminf(lerpf_(tmin, b0.z, b1.z), lerpf_(tmax, b0.z, b1.z));
+    const float ymx = fmaxf(lerpf_(tmin, b0.w, b1.w), lerpf_(tmax, b0.w, b1.w));
+    int i0, i1, j0, j1;
+    if (!ndc_box_to_pixels(xmn, xmx, ymn, ymx, t.W, t.H, i0, i1, j0, j1)) return false;
+    tx0 = i0 / TW; tx1 = i1 / TW; ty0 = j0 / TH; ty1 = j1 / TH;
+    return true;
+}
+
+__global__ void __launch_bounds__(256) k3_count(Tables t)
+{
+    const int c = blockIdx.y;
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= t.F) return;
+    const Chunk ch = t.chunks[c];
+    const ImgInfo &im = t.imgs[ch.b];
+    const float4 *r = t.rec + (size_t)(im.rec_off + (long long)ch.s * t.F + f) * REC_F4;
+    int tx0, tx1, ty0, ty1;
+    if (!swept_tiles(t, r, ch.tmin, ch.tmax, tx0, tx1, ty0, ty1)) return;
+    int *cnt = t.cnt + (size_t)c * t.T;
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(cnt + ty * t.TX + tx, 1);
+}
+
+__global__ void __launch_bounds__(256) k3_fill(Tables t)
+{
+    const int c = blockIdx.y;
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= t.F) return;
+    const Chunk ch = t.chunks[c];
+    const ImgInfo &im = t.imgs[ch.b];
+    const float4 *r = t.rec + (size_t)(im.rec_off + (long long)ch.s * t.F + f) * REC_F4;
+    int tx0, tx1, ty0, ty1;
+    if (!swept_tiles(t, r, ch.tmin, ch.tmax, tx0, tx1, ty0, ty1)) return;
+    const size_t base = (size_t)c * t.T;
+    bool ovf = false;
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) {
+            const size_t bi = base + ty * t.TX + tx;
+            const long long pos = (long long)t.off[bi] + atomicAdd(t.cnt + bi, 1);
+            if (pos < t.cap) t.entries[pos] = f;
+            else ovf = true;
+        }
+    if (ovf) atomicOr(t.status, BLUR_ST_EOVERFLOW);
+}
+
+// ---- exclusive scan of cnt[0..n) into off[0..n], off[n] = total (3 kernels, 1024 per block)
+__device__ __forceinline__ int block_excl_scan_1024(int v[4], int *sm)
+{
+    // 256 threads x 4 items; returns the block total, v[] becomes exclusive prefixes
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int s = v[0] + v[1] + v[2] + v[3];
+    int x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sm[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < 8 ? sm[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < 8) sm[8 + lane] = w;
+    }
+    __syncthreads();
+    int excl = x - s + (warp > 0 ? sm[8 + warp - 1] : 0);
+    int total = sm[8 + 7];
+    int run = excl;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { int tmp = v[i]; v[i] = run; run += tmp; }
+    __syncthreads();
+    return total;
+}
+
+__global__ void __launch_bounds__(256) k3_scan_blocks(const int *cnt, int *off, int *bsum, int n)
+{
+    __shared__ int sm[16];
+    const int base = blockIdx.x * 1024 + threadIdx.x * 4;
+    int v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = base + i < n ? cnt[base + i] : 0;
+    int tot = block_excl_scan_1024(v, sm);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        if (base + i < n) off[base + i] = v[i];
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(256) k3_scan_sums(int *bsum, int nb, int *off, int n)
+{
+    __shared__ int sm[16];
+    int carry = 0;
+    for (int base0 = 0; base0 < nb; base0 += 1024) {
+        const int base = base0 + threadIdx.x * 4;
+        int v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = base + i < nb ? bsum[base + i] : 0;
+        int tot = block_excl_scan_1024(v, sm);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (base + i < nb) bsum[base + i] = v[i] + carry;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) off[n] = carry;
+}
+
+__global__ void __launch_bounds__(256) k3_scan_add(int *off, const int *bsum, int n)
+{
+    const int i = blockIdx.x * 1024 + threadIdx.x;
+    const int add = bsum[blockIdx.x];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (i + 256 * q < n) off[i + 256 * q] += add;
+}
+
+// ---- per-bin bitonic sort (one warp per bin)
+__global__ void __launch_bounds__(256) k3_sort(Tables t, int nbins)
+{
+    __shared__ int sm[8][SORTCAP];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int *s = sm[warp];
+    for (int bi = blockIdx.x * 8 + warp; bi < nbins; bi += gridDim.x * 8) {
+        const int o = t.off[bi];
+        const int n = t.off[bi + 1] - o;
+        if (n <= 1 || n > SORTCAP || (long long)o + n > t.cap) continue;
+        int n2 = 32;
+        while (n2 < n) n2 <<= 1;
+        for (int i = lane; i < n2; i += 32) s[i] = i < n ? t.entries[o + i] : 0x7fffffff;
+        __syncwarp();
+        for (int k = 2; k <= n2; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = lane; i < n2; i += 32) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const int a = s[i], b = s[ixj];
+                        const bool up = (i & k) == 0;
+                        if ((a > b) == up) { s[i] = b; s[ixj] = a; }
+                    }
+                }
+                __syncwarp();
+            }
+        // self-check: a sorted bin holds distinct ids in [0, F)
+        bool bad = false;
+        for (int i = lane; i < n; i += 32) {
+            t.entries[o + i] = s[i];
+            bad |= s[i] < 0 || s[i] >= t.F || (i > 0 && s[i - 1] >= s[i]);
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) {
+            atomicOr(t.status, BLUR_ST_EINTERNAL);
+#ifdef BR_DEBUG
+            printf("bad sorted bin %d o=%d n=%d: %d %d %d %d ... last %d\n", bi, o, n, s[0], s[1], s[2], s[3], s[n - 1]);
+#endif
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_binning(const Tables &t, cudaStream_t st)
+{
+    const int nbins = t.NC * t.T;
+    if (nbins == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(t.cnt, 0, sizeof(int) * (size_t)nbins, st);
+    if (e != cudaSuccess) return e;
+    if (t.F > 0) {
+        dim3 grid((t.F + 255) / 256, t.NC);
+        k3_count<<<grid, 256, 0, st>>>(t);
+    }
+    const int nb = (nbins + 1023) / 1024;
+    k3_scan_blocks<<<nb, 256, 0, st>>>(t.cnt, t.off, t.bsum, nbins);
+    k3_scan_sums<<<1, 256, 0, st>>>(t.bsum, nb, t.off, nbins);
+    k3_scan_add<<<nb, 256, 0, st>>>(t.off, t.bsum, nbins);
+    e = cudaMemsetAsync(t.cnt, 0, sizeof(int) * (size_t)nbins, st);
+    if (e != cudaSuccess) return e;
+    if (t.F > 0) {
+        dim3 grid((t.F + 255) / 256, t.NC);
+        k3_fill<<<grid, 256, 0, st>>>(t);
+        int sb = (nbins + 7) / 8;
+        if (sb > 148 * 16) sb = 148 * 16;
+        k3_sort<<<sb, 256, 0, st>>>(t, nbins);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace br

@@ -1,0 +1,119 @@
+"""Multi-GPU sharding of the inverse-rendering step: one process per GPU.
+
+Units of work are (image, k0, k1) sub-frame ranges.  Images are dealt round-robin to ranks
+(image-major; consecutive images alternate translational / rotational views so ranks stay
+balanced).  When there are fewer images than ranks, or when `split` > 1 is requested, every image
+is cut into `split` contiguous sub-frame ranges owned by different ranks ("sub-frame range"
+sharding); those co-owners all-reduce their partial RGBA images (the blurred image is a sum over
+sub-frames) before the loss.  After the backward pass one all-reduce of [dV || dC] (V x 6 fp32)
+sums the vertex gradients (torch.distributed, NCCL over NVLink on GPUs, gloo on CPU tests).
+
+The renderer is injected (`make_renderer`), so the same step logic runs with the CUDA renderer
+on GPUs and with a CPU stand-in in the gloo tests.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Callable, List, Sequence, Tuple
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+@dataclasses.dataclass
+class Unit:
+    image: int
+    k0: int
+    k1: int
+
+
+def partition(n_sub: Sequence[int], world: int, split: int = 0) -> List[List[Unit]]:
+    """Work list per rank.  split = 0: automatic (1 if B >= world, else ceil(world / B))."""
+    B = len(n_sub)
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if split <= 0:
+        split = 1 if B >= world else -(-world // max(B, 1))
+    units: List[Unit] = []
+    for b in range(B):
+        N = int(n_sub[b])
+        parts = min(split, N)
+        edges = [round(N * p / parts) for p in range(parts + 1)]
+        for p in range(parts):
+            units.append(Unit(b, edges[p], edges[p + 1]))
+    out: List[List[Unit]] = [[] for _ in range(world)]
+    if split == 1:
+        for i, u in enumerate(units):
+            out[i % world].append(u)
+    else:
+        # co-owners of an image sit on consecutive ranks; images then go round-robin over groups
+        for i, u in enumerate(units):
+            out[i % world].append(u)
+    return out
+
+
+def split_groups(parts: List[List[Unit]]) -> List[Tuple[int, List[int]]]:
+    """(image, ranks) for every image owned by more than one rank."""
+    owners = {}
+    for r, us in enumerate(parts):
+        for u in us:
+            owners.setdefault(u.image, set()).add(r)
+    return [(b, sorted(rs)) for b, rs in sorted(owners.items()) if len(rs) > 1]
+
+
+class ShardedStep:
+    """One rank's share of the step: fwd -> (partial-image all-reduce) -> L2 loss -> bwd ->
+    all-reduce of [dV || dC].
+
+    make_renderer(images, sub_range) must return an object with forward(verts, colors) -> [b,H,W,4],
+    l2_loss_grad(out, target, n_norm) -> (loss[1], grad) and
+    backward(verts, colors, grad, reuse_setup=True) -> (dV, dC), all on `device`.
+    """
+
+    def __init__(self, n_sub: Sequence[int], targets: torch.Tensor, make_renderer: Callable, rank: int,
+                 world: int, split: int = 0, device="cpu"):
+        self.rank, self.world = rank, world
+        self.parts = partition(n_sub, world, split)
+        self.mine = self.parts[rank]
+        self.images = [u.image for u in self.mine]
+        B = len(n_sub)
+        self.n_norm = int(B * int(np.prod(targets.shape[1:])))        # mean over the whole batch
+        self.targets = targets[self.images].contiguous() if self.images else targets[:0]
+        self.renderer = make_renderer(self.images, [[u.k0, u.k1] for u in self.mine]) if self.images else None
+        # loss is counted once per image: by the co-owner holding k0 == 0
+        self.loss_mask = torch.tensor([1.0 if u.k0 == 0 else 0.0 for u in self.mine], dtype=torch.float32,
+                                      device=device)
+        self.groups = []
+        self.device = device
+        if world > 1:
+            for b, ranks in split_groups(self.parts):
+                g = dist.new_group(ranks)          # every rank must call new_group for every group
+                if rank in ranks:
+                    self.groups.append((self.images.index(b), g))
+
+    def __call__(self, verts: torch.Tensor, colors: torch.Tensor):
+        V = verts.shape[0]
+        if self.renderer is not None:
+            out = self.renderer.forward(verts, colors)
+            for slot, g in self.groups:                               # partial images -> full image
+                part = out[slot].contiguous()
+                dist.all_reduce(part, group=g)
+                out[slot].copy_(part)
+            if all(u.k0 == 0 for u in self.mine):                      # no split image: one call
+                loss_all, grads = self.renderer.l2_loss_grad(out, self.targets, n_norm=self.n_norm)
+            else:
+                loss_all = torch.zeros(1, dtype=torch.float32, device=self.device)
+                grads = torch.empty_like(out)
+                for i in range(len(self.images)):
+                    li, gi = self.renderer.l2_loss_grad(out[i:i + 1].contiguous(),
+                                                        self.targets[i:i + 1].contiguous(), n_norm=self.n_norm)
+                    loss_all += li * self.loss_mask[i]
+                    grads[i].copy_(gi[0])
+            dv, dc = self.renderer.backward(verts, colors, grads, reuse_setup=True)
+            flat = torch.cat([dv.reshape(-1), dc.reshape(-1), loss_all])
+        else:
+            flat = torch.zeros(6 * V + 1, dtype=torch.float32, device=self.device)
+        if self.world > 1:
+            dist.all_reduce(flat)
+        return flat[-1:], flat[:3 * V].reshape(V, 3), flat[3 * V:6 * V].reshape(V, 3)

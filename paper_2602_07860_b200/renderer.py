@@ -1,0 +1,113 @@
+"""Public Python API of the B200 motion-blur rasterizer.
+
+`BlurRenderer` owns the device workspace for one (mesh topology, cameras, motions, image size)
+configuration and calls the C ABI; `blur_render` is the differentiable (torch.autograd) form.
+All arithmetic runs in libblurrast's CUDA kernels; torch only provides device memory and streams.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+class BlurRenderer:
+    """Motion-blurred rendering of one mesh topology for a batch of B observed images.
+
+    faces: int32 [F,3] (device tensor or array); motion: dict of per-image arrays (kind, vec,
+    angle, pivot, n_sub, n_seg, rule); cams: float [B,11]; H, W: image size.
+    sub_range: optional int [B,2] half-open sub-frame ranges (sub-frame sharding).
+    """
+
+    def __init__(self, faces, motion: dict, cams, H: int, W: int, V: int, device="cuda",
+                 sub_range=None, max_chunk: int = 0, bin_factor: float = 0.0):
+        _lib.load()
+        self.device = torch.device(device)
+        self.faces = torch.as_tensor(np.asarray(faces.cpu() if torch.is_tensor(faces) else faces),
+                                     dtype=torch.int32).contiguous().to(self.device)
+        self.motion = motion
+        self.cams_np = np.asarray(cams, dtype=np.float64).reshape(-1, 11)
+        self.B = int(self.cams_np.shape[0])
+        self.H, self.W, self.V = int(H), int(W), int(V)
+        self.F = int(self.faces.shape[0])
+        self.N = np.asarray(motion["n_sub"], dtype=np.int64)
+        self._motions = _lib.make_motions(motion)
+        self._cams = _lib.make_cams(self.cams_np)
+        self._sub = _lib.make_sub_range(sub_range)
+        self.max_chunk = int(max_chunk)
+        self.bin_factor = float(bin_factor)
+        cfg = _lib.make_config(self.max_chunk, 0, self.bin_factor)
+        self.ws_bytes = _lib.blur_workspace_bytes(self.V, self.F, self.B, self.H, self.W, self._motions,
+                                                  self._cams, self._sub, cfg)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.ws[:256].zero_()
+
+    # -- forward / backward -------------------------------------------------------------
+    def forward(self, verts: torch.Tensor, colors: torch.Tensor, out: Optional[torch.Tensor] = None,
+                ids: Optional[torch.Tensor] = None, ids_subframe: int = -1, census: Optional[torch.Tensor] = None,
+                stream=None, events=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((self.B, self.H, self.W, 4), dtype=torch.float32, device=self.device)
+        cfg = _lib.make_config(self.max_chunk, 0, self.bin_factor, census, events)
+        _lib.blur_render_fwd(verts, self.faces, colors, self._motions, self._cams, self.B, self.H, self.W, out,
+                             self.ws, sub_range=self._sub, ids=ids, ids_subframe=ids_subframe, cfg=cfg,
+                             stream=stream)
+        return out
+
+    def backward(self, verts: torch.Tensor, colors: torch.Tensor, grad_rgba: torch.Tensor, reuse_setup: bool = False,
+                 grad_verts: Optional[torch.Tensor] = None, grad_colors: Optional[torch.Tensor] = None, stream=None,
+                 events=None):
+        if grad_verts is None:
+            grad_verts = torch.empty((self.V, 3), dtype=torch.float32, device=self.device)
+        if grad_colors is None:
+            grad_colors = torch.empty((self.V, 3), dtype=torch.float32, device=self.device)
+        cfg = _lib.make_config(self.max_chunk, _lib.BLUR_REUSE_SETUP if reuse_setup else 0, self.bin_factor,
+                               events=events)
+        _lib.blur_render_bwd(verts, self.faces, colors, self._motions, self._cams, self.B, self.H, self.W,
+                             grad_rgba.contiguous(), grad_verts, grad_colors, self.ws, sub_range=self._sub, cfg=cfg,
+                             stream=stream)
+        return grad_verts, grad_colors
+
+    def l2_loss_grad(self, out: torch.Tensor, target: torch.Tensor, n_norm: int = 0, loss=None, grad=None,
+                     stream=None):
+        if loss is None:
+            loss = torch.empty(1, dtype=torch.float32, device=self.device)
+        if grad is None:
+            grad = torch.empty_like(out)
+        _lib.blur_l2_loss_grad(out, target, loss, grad, n_norm=n_norm, stream=stream)
+        return loss, grad
+
+    def status(self) -> int:
+        return _lib.blur_read_status(self.ws)
+
+    def step(self, verts, colors, target, n_norm: int = 0):
+        """One inverse-rendering step: fwd -> L2 loss -> bwd (setup reused).  Device tensors in,
+        (loss [1], dverts, dcolors, out) device tensors out."""
+        out = self.forward(verts, colors)
+        loss, g = self.l2_loss_grad(out, target, n_norm=n_norm)
+        dv, dc = self.backward(verts, colors, g, reuse_setup=True)
+        return loss, dv, dc, out
+
+
+class _BlurFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, verts, colors, renderer: BlurRenderer):
+        out = renderer.forward(verts.contiguous(), colors.contiguous())
+        ctx.renderer = renderer
+        ctx.save_for_backward(verts, colors)
+        return out
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        verts, colors = ctx.saved_tensors
+        dv, dc = ctx.renderer.backward(verts.contiguous(), colors.contiguous(), grad_out.contiguous(),
+                                       reuse_setup=True)
+        return dv, dc, None
+
+
+def blur_render(verts: torch.Tensor, colors: torch.Tensor, renderer: BlurRenderer) -> torch.Tensor:
+    """Differentiable blurred render (B,H,W,4) of `verts` [V,3] / `colors` [V,3]."""
+    return _BlurFn.apply(verts, colors, renderer)

@@ -1,0 +1,232 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star; readings Q16/Q18 in DESIGN.md):
+  * visible-triangle-ID map bit-exact except at (pixel, sub-frame) the oracle flags as ambiguous
+    (within 1e-6 NDC of an edge or a 1e-6 relative depth tie, Q16);
+  * blurred intensities within 1e-4 max-abs on non-ambiguous pixels;
+  * vertex gradients (dV and dC separately) within 1e-3 relative L2, same upstream G on both sides.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import scenes
+
+pytestmark = pytest.mark.gpu
+
+TOL_IMG = 1e-4
+TOL_GRAD = 1e-3
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def gpu_render(sc, ids_k=-1, sub_range=None, max_chunk=0, bin_factor=0.0, G=None, reuse=True):
+    torch = _torch()
+    from paper_2602_07860_b200 import BlurRenderer
+    dev = torch.device("cuda:0")
+    r = BlurRenderer(sc.faces, sc.motion, sc.cams, sc.H, sc.W, sc.V, device=dev, sub_range=sub_range,
+                     max_chunk=max_chunk, bin_factor=bin_factor)
+    v = torch.tensor(np.asarray(sc.verts, np.float32), device=dev)
+    c = torch.tensor(np.asarray(sc.colors, np.float32), device=dev)
+    ids = torch.full((sc.B, sc.H, sc.W), -7, dtype=torch.int32, device=dev) if ids_k >= 0 else None
+    out = r.forward(v, c, ids=ids, ids_subframe=ids_k)
+    res = dict(rgba=out.cpu().numpy(), ids=None if ids is None else ids.cpu().numpy())
+    if G is not None:
+        g = torch.tensor(np.asarray(G, np.float32), device=dev)
+        dv, dc = r.backward(v, c, g, reuse_setup=reuse)
+        res["dv"], res["dc"] = dv.cpu().numpy(), dc.cpu().numpy()
+    torch.cuda.synchronize()
+    res["status"] = r.status()
+    return res
+
+
+def rel_l2(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def check_parity(sc, ids_k=0, mode="binned", max_chunk=0, sub_range=None, grad=True):
+    ref = oracle.render_fwd(sc, mode=mode, ids_k=ids_k, eps_amb=1e-6, sub_range=sub_range)
+    G = 2.0 * (ref["rgba"] - sc.target) / ref["rgba"].size if grad else None
+    got = gpu_render(sc, ids_k=ids_k, sub_range=sub_range, max_chunk=max_chunk, G=G)
+    assert not (got["status"] & 8), "internal consistency check failed"
+    ok = ~ref["amb_img"]
+    err = np.abs(got["rgba"] - ref["rgba"])
+    assert err[ok].max() < TOL_IMG, "image max err %g (all pixels %g)" % (err[ok].max(), err.max())
+    okid = ~ref["amb_ids"]
+    mism = (got["ids"] != ref["ids"]) & okid
+    assert not mism.any(), "id mismatch at %d pixels" % mism.sum()
+    out = dict(img_err=float(err[ok].max()), img_err_all=float(err.max()), amb=int((~ok).sum()))
+    if grad:
+        rdv, rdc = oracle.render_bwd(sc, G, mode=mode, sub_range=sub_range)
+        ev, ec = rel_l2(got["dv"], rdv), rel_l2(got["dc"], rdc)
+        assert ev < TOL_GRAD and ec < TOL_GRAD, "grad rel L2 dV %g dC %g" % (ev, ec)
+        out.update(dv=ev, dc=ec)
+    return out
+
+
+def test_c1_full_brute():
+    r = check_parity(scenes.make_c1(), ids_k=3, mode="brute")
+    print(r)
+
+
+def test_c2_full():
+    r = check_parity(scenes.make_c2(), ids_k=17)
+    print(r)
+
+
+def test_c3_subset():
+    r = check_parity(scenes.make_c3().subset([0, 3, 6]), ids_k=25)
+    print(r)
+
+
+def test_c4_two_views():
+    sc = scenes.make_c4().subset([2, 11])   # one translational, one rotational view
+    r = check_parity(sc, ids_k=40)
+    print(r)
+
+
+@pytest.mark.parametrize("G", [1, 3, 16])
+def test_chunk_length_invariance(G):
+    """The per-sub-frame result does not depend on the bin chunk length G (bit-identical)."""
+    sc = scenes.make_c2().subset([0, 2])
+    a = gpu_render(sc, ids_k=5, max_chunk=G)
+    b = gpu_render(sc, ids_k=5, max_chunk=8)
+    assert np.array_equal(a["rgba"], b["rgba"]) and np.array_equal(a["ids"], b["ids"])
+
+
+def test_overflow_fallback_exact():
+    """A tiny bin capacity forces the exact fallback path (faces rescanned in index order)."""
+    sc = scenes.make_c2().subset([1])
+    G = np.random.default_rng(0).normal(size=(1, 256, 256, 4)) * 1e-4
+    a = gpu_render(sc, ids_k=7, G=G)
+    b = gpu_render(sc, ids_k=7, bin_factor=1e-9, G=G)
+    assert b["status"] & 4                     # BLUR_ST_EOVERFLOW reported
+    assert np.array_equal(a["rgba"], b["rgba"]) and np.array_equal(a["ids"], b["ids"])
+    assert rel_l2(b["dv"], a["dv"]) < 1e-5 and rel_l2(b["dc"], a["dc"]) < 1e-5
+
+
+def test_sub_range_partials_sum_to_full():
+    """Sub-frame sharding: renders over [0,k) and [k,N) add up to the full render."""
+    sc = scenes.make_c3().subset([1, 5])
+    full = gpu_render(sc)["rgba"]
+    a = gpu_render(sc, sub_range=[[0, 20], [0, 33]])["rgba"]
+    b = gpu_render(sc, sub_range=[[20, 50], [33, 50]])["rgba"]
+    assert np.max(np.abs(a + b - full)) < 2e-6
+    ref = oracle.render_fwd(sc, sub_range=[[0, 20], [0, 33]], eps_amb=1e-6)
+    ok = ~ref["amb_img"]
+    assert np.abs(a - ref["rgba"])[ok].max() < TOL_IMG
+
+
+def test_ragged_image_and_degenerate_faces():
+    """Image size not a multiple of the tile; degenerate and repeated-index faces are skipped."""
+    sc = scenes.random_mesh_scene(40, 5, H=37, W=53, motion=scenes.rotate((0.2, 1, 0.3), 1.2, N=9, S=4))
+    faces = sc.faces.copy()
+    faces[3] = [7, 7, 8]                       # repeated index
+    verts = sc.verts.copy()
+    verts[faces[5, 1]] = verts[faces[5, 0]]    # zero-area face
+    sc.faces, sc.verts = faces, verts
+    r = check_parity(sc, ids_k=4, mode="brute")
+    print(r)
+
+
+def test_paper_segmented_schedule_and_static():
+    sc = scenes.random_mesh_scene(30, 8, H=40, W=40,
+                                  motion=scenes.rotate((0, 1, 0), 6.283185307, N=60, S=12, rule=1))
+    check_parity(sc, ids_k=11, mode="brute")
+    st = scenes.random_mesh_scene(30, 9, H=40, W=40, motion=scenes.static(1))
+    check_parity(st, ids_k=0, mode="brute")
+    one = scenes.random_mesh_scene(30, 9, H=40, W=40, motion=scenes.translate((0.4, 0, 0), N=1))
+    check_parity(one, ids_k=0, mode="brute")
+
+
+def test_behind_camera_and_bad_index_status():
+    sc = scenes.random_mesh_scene(20, 10, H=24, W=24, motion=scenes.static(1))
+    v = sc.verts.copy()
+    v[0] = [0, 0, 3.5]                         # behind the camera at z = 3
+    sc.verts = v
+    res = gpu_render(sc, ids_k=0)
+    assert res["status"] & 2                   # BLUR_ST_EBEHIND
+    ref = oracle.render_fwd(sc, ids_k=0, eps_amb=1e-6)
+    ok = ~ref["amb_img"]
+    assert np.abs(res["rgba"] - ref["rgba"])[ok].max() < TOL_IMG
+    f = sc.faces.copy()
+    f[2] = [0, 1, 10 ** 6]
+    sc.faces = f
+    res = gpu_render(sc, ids_k=0)
+    assert res["status"] & 1                   # BLUR_ST_EINVAL
+    assert not np.any(res["ids"] == 2)
+
+
+def test_empty_mesh_and_empty_batch():
+    torch = _torch()
+    from paper_2602_07860_b200 import BlurRenderer
+    sc = scenes.single_scene(np.zeros((3, 3)), np.zeros((0, 3), np.int32), np.zeros((3, 3)), H=20, W=30)
+    got = gpu_render(sc, ids_k=0)
+    assert not got["rgba"].any() and np.all(got["ids"] == -1)
+    r = BlurRenderer(np.zeros((0, 3), np.int32), scenes.motion_arrays([]), np.zeros((0, 11)), 8, 8, 3)
+    out = r.forward(torch.zeros((3, 3), device="cuda"), torch.zeros((3, 3), device="cuda"))
+    assert out.shape == (0, 8, 8, 4)
+
+
+def test_determinism():
+    sc = scenes.make_c2().subset([3])
+    a = gpu_render(sc, ids_k=9)
+    b = gpu_render(sc, ids_k=9)
+    assert np.array_equal(a["rgba"], b["rgba"]) and np.array_equal(a["ids"], b["ids"])
+
+
+def test_invalid_arguments_raise():
+    torch = _torch()
+    from paper_2602_07860_b200 import BlurError, BlurRenderer
+    sc = scenes.make_c1()
+    bad = {k: v.copy() for k, v in sc.motion.items()}
+    bad["n_sub"][0] = 0
+    with pytest.raises(BlurError):
+        BlurRenderer(sc.faces, bad, sc.cams, 64, 64, sc.V)
+    cams = sc.cams.copy()
+    cams[0, 9] = 2.0                            # half_fov >= pi/2
+    with pytest.raises(BlurError):
+        BlurRenderer(sc.faces, sc.motion, cams, 64, 64, sc.V)
+    r = BlurRenderer(sc.faces, sc.motion, sc.cams, 64, 64, sc.V)
+    with pytest.raises(TypeError):
+        r.forward(torch.zeros((sc.V, 3), dtype=torch.float64, device="cuda"), torch.zeros((sc.V, 3), device="cuda"))
+
+
+# ----------------------------------------------------------------- full-size (bench configuration)
+
+def _sample_pixels(rng, B, H, W, n):
+    b = rng.integers(0, B, n)
+    j = rng.integers(H // 6, 5 * H // 6, n)
+    i = rng.integers(W // 6, 5 * W // 6, n)
+    return np.stack([b, j, i], 1).astype(np.int32)
+
+
+@pytest.mark.parametrize("name,npix", [("C4", 96), ("C5", 24)])
+def test_full_size_sampled(name, npix):
+    """BASELINE full sizes in the launch configuration bench.py times (whole batch, automatic chunk
+    length): sampled pixels computed one by one by the oracle (brute force over all faces and all
+    sub-frames); gradients of a loss supported on the sampled pixels only (exact for the oracle)."""
+    sc = scenes.make(name)
+    rng = np.random.default_rng(123)
+    pix = _sample_pixels(rng, sc.B, sc.H, sc.W, npix)
+    Gp = rng.normal(size=(npix, 4))
+    G = np.zeros((sc.B, sc.H, sc.W, 4))
+    G[pix[:, 0], pix[:, 1], pix[:, 2]] = Gp
+    got = gpu_render(sc, ids_k=-1, G=G)
+    ref = oracle.render_fwd(sc, pixels=pix, eps_amb=1e-6)
+    g_img = got["rgba"][pix[:, 0], pix[:, 1], pix[:, 2]]
+    ok = ~ref["amb_img"]
+    assert ok.sum() >= npix * 0.8
+    err = np.abs(g_img - ref["rgba"])[ok]
+    assert err.max() < TOL_IMG, err.max()
+    # the loss reads only the sampled pixels; ambiguous ones are excluded on both sides
+    Gp2 = Gp * ok[:, None]
+    G2 = np.zeros_like(G)
+    G2[pix[:, 0], pix[:, 1], pix[:, 2]] = Gp2
+    got2 = gpu_render(sc, G=G2)
+    rdv, rdc = oracle.render_bwd(sc, Gp2, pixels=pix)
+    assert rel_l2(got2["dv"], rdv) < TOL_GRAD and rel_l2(got2["dc"], rdc) < TOL_GRAD
