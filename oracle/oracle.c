@@ -367,14 +367,16 @@ typedef struct {
     double z[3];      /* 0 nominal, 1 loose (-eps), 2 strict (+eps) */
     int id[3];
     double w[3];      /* nominal winner weights */
-    int amb_val, amb_id;
+    double delta;     /* max |value change| of this sub-frame under the Q16 perturbations */
+    int amb_id;       /* the winner (id) can change under the Q16 perturbations */
 } pixstate;
 
 static void ps_reset(pixstate *p)
 {
     for (int i = 0; i < 3; ++i) { p->z[i] = INFINITY; p->id[i] = -1; }
     p->w[0] = p->w[1] = p->w[2] = 0;
-    p->amb_val = p->amb_id = 0;
+    p->delta = 0;
+    p->amb_id = 0;
 }
 
 typedef struct {
@@ -434,9 +436,78 @@ typedef struct {
     double covered;     /* covered (pixel, sub-frame) */
 } om_stats_t;
 
+/* per-sub-frame context for the ambiguity analysis */
+typedef struct {
+    const double *X, *Y, *Z;
+    const unsigned char *okv;
+    const int *nbr;    /* 3F: neighbour across the edge opposite corner i, as 3*g + i_g, or -1 */
+} sub_ctx;
+
+static int cmp_edge(const void *pa, const void *pb)
+{
+    const int *a = (const int *)pa, *b = (const int *)pb;
+    if (a[0] != b[0]) return a[0] < b[0] ? -1 : 1;
+    if (a[1] != b[1]) return a[1] < b[1] ? -1 : 1;
+    return a[2] < b[2] ? -1 : (a[2] > b[2]);
+}
+
+/* Edge adjacency by vertex indices: two faces share an edge iff they share its two vertex
+ * indices (edges with more than two faces are treated as boundaries). */
+static int *build_nbr(const om_scene *sc)
+{
+    int F = sc->F;
+    int *e = (int *)malloc(sizeof(int) * 3 * 3 * (size_t)(F > 0 ? F : 1));
+    int *nbr = (int *)malloc(sizeof(int) * 3 * (size_t)(F > 0 ? F : 1));
+    for (int f = 0; f < F; ++f)
+        for (int i = 0; i < 3; ++i) {
+            int a = sc->faces[3 * f + (i + 1) % 3], b = sc->faces[3 * f + (i + 2) % 3];
+            int *r = e + 3 * (3 * f + i);
+            r[0] = a < b ? a : b;
+            r[1] = a < b ? b : a;
+            r[2] = 3 * f + i;
+            nbr[3 * f + i] = -1;
+        }
+    qsort(e, 3 * (size_t)F, 3 * sizeof(int), cmp_edge);
+    for (int q = 0; q < 3 * F;) {
+        int r = q + 1;
+        while (r < 3 * F && e[3 * r] == e[3 * q] && e[3 * r + 1] == e[3 * q + 1]) ++r;
+        if (r - q == 2) {
+            nbr[e[3 * q + 2]] = e[3 * (q + 1) + 2];
+            nbr[e[3 * (q + 1) + 2]] = e[3 * q + 2];
+        }
+        q = r;
+    }
+    free(e);
+    return nbr;
+}
+
+/* Q16 strict scenario (inside test at +eps), watertight reading: a nominally covering face whose
+ * pixel lies within eps of one of its edges is dropped, unless across every such edge the
+ * neighbouring face (same two vertex indices) lies on the other side of the edge at this pixel --
+ * then the pixel belongs to one of the two faces under any consistent rounding (no crack can open
+ * inside a mesh), which the loose scenario and the depth ties already cover. */
+static int strict_member(const om_scene *sc, const sub_ctx *cx, int f, const double w[3], double ad,
+                         const double len[3], double u, double v, double eps)
+{
+    for (int i = 0; i < 3; ++i) {
+        double sd = w[i] * ad / len[i];
+        if (sd >= eps) continue;
+        int nb = cx->nbr[3 * f + i];
+        if (nb < 0) return 0;
+        int g = nb / 3, ig = nb % 3;
+        face_geo gg;
+        if (!face_setup(sc, g, cx->X, cx->Y, cx->Z, cx->okv, eps, &gg)) return 0;
+        double wg[3], detg;
+        if (!om_bary_textbook(gg.x, gg.y, u, v, wg, &detg)) return 0;
+        double sdg = wg[ig] * fabs(detg) / gg.len[ig];
+        if (!(sdg <= 0.0)) return 0;      /* same side (a fold) or no neighbour coverage */
+    }
+    return 1;
+}
+
 /* pass 1 per pair: nominal / loose / strict z-buffers */
-static void pair_pass1(const om_scene *sc, const face_geo *g, int f, double u, double v, double eps,
-                       pixstate *ps, const img_state *st, int k, om_stats_t *stt, int check_fast)
+static void pair_pass1(const om_scene *sc, const sub_ctx *cx, const face_geo *g, int f, double u, double v,
+                       double eps, pixstate *ps, const img_state *st, int k, om_stats_t *stt, int check_fast)
 {
     double w[3], det;
     if (!om_bary_textbook(g->x, g->y, u, v, w, &det)) return;
@@ -474,7 +545,10 @@ static void pair_pass1(const om_scene *sc, const face_geo *g, int f, double u, d
             if (sd < sdmin) sdmin = sd;
         }
         if (sdmin >= -eps && z < ps->z[1]) { ps->z[1] = z; ps->id[1] = f; }
-        if (sdmin >= eps && z < ps->z[2]) { ps->z[2] = z; ps->id[2] = f; }
+        if (cov && z < ps->z[2] && (sdmin >= eps || strict_member(sc, cx, f, w, ad, g->len, u, v, eps))) {
+            ps->z[2] = z;
+            ps->id[2] = f;
+        }
     }
 }
 
@@ -486,9 +560,10 @@ static void shade_w(const om_scene *sc, int f, const double w[3], double rgb[3])
 }
 
 /* pass 2 per pair (ambiguity): any face within the depth tolerance of a set's minimum is a
- * possible outcome (Q16); flag if its shaded value or id differs from the nominal one. */
-static void pair_pass2(const om_scene *sc, const face_geo *g, int f, double u, double v, double eps,
-                       const om_opts *op, pixstate *ps, const double nom_rgb[3])
+ * possible outcome (Q16); record how far its shaded value is from the nominal one and whether its
+ * id differs. */
+static void pair_pass2(const om_scene *sc, const sub_ctx *cx, const face_geo *g, int f, double u, double v,
+                       double eps, const om_opts *op, pixstate *ps, const double nom_rgb[3])
 {
     double w[3], det;
     if (!om_bary_textbook(g->x, g->y, u, v, w, &det)) return;
@@ -498,26 +573,30 @@ static void pair_pass2(const om_scene *sc, const face_geo *g, int f, double u, d
         double sd = w[i] * ad / g->len[i];
         if (sd < sdmin) sdmin = sd;
     }
-    int in[3] = {w[0] >= 0 && w[1] >= 0 && w[2] >= 0, sdmin >= -eps, sdmin >= eps};
+    const int cov = w[0] >= 0 && w[1] >= 0 && w[2] >= 0;
+    int in[3] = {cov, sdmin >= -eps,
+                 cov && (sdmin >= eps || strict_member(sc, cx, f, w, ad, g->len, u, v, eps))};
     for (int sidx = 0; sidx < 3; ++sidx) {
         if (!in[sidx] || !(ps->z[sidx] < INFINITY)) continue;
         if (z <= ps->z[sidx] + op->amb_z_rel * fabs(ps->z[sidx])) {
             if (f != ps->id[0]) ps->amb_id = 1;
             double rgb[3];
             shade_w(sc, f, w, rgb);
-            if (ps->id[0] < 0) ps->amb_val = 1;
-            else
-                for (int c = 0; c < 3; ++c)
-                    if (fabs(rgb[c] - nom_rgb[c]) > op->amb_val_tol) ps->amb_val = 1;
+            if (ps->id[0] < 0) {
+                ps->delta = fmax(ps->delta, 1.0);
+            } else {
+                for (int c = 0; c < 3; ++c) ps->delta = fmax(ps->delta, fabs(rgb[c] - nom_rgb[c]));
+            }
         }
     }
 }
 
 static void pix_finalize_amb(pixstate *ps)
 {
-    /* a perturbed set that is empty while the nominal pixel is covered (or vice versa) */
+    /* a perturbed set that is empty while the nominal pixel is covered (or vice versa):
+     * the alpha channel changes by 1 */
     for (int sidx = 1; sidx < 3; ++sidx) {
-        if ((ps->id[sidx] < 0) != (ps->id[0] < 0)) { ps->amb_val = 1; ps->amb_id = 1; }
+        if ((ps->id[sidx] < 0) != (ps->id[0] < 0)) { ps->delta = fmax(ps->delta, 1.0); ps->amb_id = 1; }
     }
 }
 
@@ -525,11 +604,13 @@ static void pix_finalize_amb(pixstate *ps)
  * binned); otherwise only the listed pixel indices (brute over faces). */
 static void render_subframe(const om_scene *sc, const om_opts *op, const img_state *st, int k,
                             pixstate *ps, const int *pix_idx, int npix, om_stats_t *stt,
-                            double *X, double *Y, double *Z, unsigned char *okv)
+                            double *X, double *Y, double *Z, unsigned char *okv, const int *nbr)
 {
     int H = sc->H, W = sc->W, P = H * W;
     double eps = op->eps_amb;
     lerp_subframe(sc, st, k, X, Y, Z, okv);
+    sub_ctx cxv = {X, Y, Z, okv, nbr};
+    const sub_ctx *cx = &cxv;
     int nloop = pix_idx ? npix : P;
     for (int q = 0; q < nloop; ++q) ps_reset(&ps[q]);
     face_geo g;
@@ -539,14 +620,14 @@ static void render_subframe(const om_scene *sc, const om_opts *op, const img_sta
             double u = pix_u(i, W), v = pix_v(j, H);
             for (int f = 0; f < sc->F; ++f) {
                 if (!face_setup(sc, f, X, Y, Z, okv, eps, &g)) continue;
-                pair_pass1(sc, &g, f, u, v, eps, &ps[q], st, k, stt, op->check_fast);
+                pair_pass1(sc, cx, &g, f, u, v, eps, &ps[q], st, k, stt, op->check_fast);
             }
             if (eps > 0) {
                 double nom[3] = {0, 0, 0};
                 if (ps[q].id[0] >= 0) shade_w(sc, ps[q].id[0], ps[q].w, nom);
                 for (int f = 0; f < sc->F; ++f) {
                     if (!face_setup(sc, f, X, Y, Z, okv, eps, &g)) continue;
-                    pair_pass2(sc, &g, f, u, v, eps, op, &ps[q], nom);
+                    pair_pass2(sc, cx, &g, f, u, v, eps, op, &ps[q], nom);
                 }
                 pix_finalize_amb(&ps[q]);
             }
@@ -559,7 +640,7 @@ static void render_subframe(const om_scene *sc, const om_opts *op, const img_sta
         if (op->mode == 1) face_bbox(&g, H, W, &i0, &i1, &j0, &j1);
         for (int j = j0; j <= j1; ++j)
             for (int i = i0; i <= i1; ++i)
-                pair_pass1(sc, &g, f, pix_u(i, W), pix_v(j, H), eps, &ps[j * W + i], st, k, stt, op->check_fast);
+                pair_pass1(sc, cx, &g, f, pix_u(i, W), pix_v(j, H), eps, &ps[j * W + i], st, k, stt, op->check_fast);
     }
     if (eps > 0) {
         double *nom = (double *)malloc(sizeof(double) * 3 * (size_t)P);
@@ -573,7 +654,7 @@ static void render_subframe(const om_scene *sc, const om_opts *op, const img_sta
             if (op->mode == 1) face_bbox(&g, H, W, &i0, &i1, &j0, &j1);
             for (int j = j0; j <= j1; ++j)
                 for (int i = i0; i <= i1; ++i)
-                    pair_pass2(sc, &g, f, pix_u(i, W), pix_v(j, H), eps, op, &ps[j * W + i], nom + 3 * (j * W + i));
+                    pair_pass2(sc, cx, &g, f, pix_u(i, W), pix_v(j, H), eps, op, &ps[j * W + i], nom + 3 * (j * W + i));
         }
         for (int p = 0; p < P; ++p) pix_finalize_amb(&ps[p]);
         free(nom);
@@ -602,14 +683,19 @@ static int pixlist_for(const om_opts *op, int b, int W, int *idx, int *slot)
 /* Forward render.
  *   out_rgba: B*H*W*4 (full mode) or npix*4 (pixel-list mode): (1/N) * sum over k in [k0,k1)
  *   ids: B*H*W (or npix) winner id at sub-frame ids_k (-1 none), may be NULL
- *   amb_img / amb_ids: Q16 ambiguity flags (need eps_amb > 0), may be NULL
+ *   amb_img / amb_ids / amb_win: Q16 ambiguity flags (need eps_amb > 0), may be NULL:
+ *     amb_img: the Q16 perturbations can move the BLURRED value by more than amb_val_tol
+ *              (sum over sub-frames of the per-sub-frame change / N);
+ *     amb_ids: the winner at sub-frame ids_k can change;
+ *     amb_win: the winner can change at some sub-frame (gradient exclusion, Q18)
  *   frozen: per (b, k, pixel) face ids [sum_b N_b * H * W]; when non-NULL the value of each
  *           (pixel, k) is evaluated for the given face without a coverage test (frozen-visibility
  *           forward used by the finite-difference pin; full mode only)
  *   stats: om_stats_t (4 doubles) or NULL
  * Returns 0 ok, 1 a vertex was behind the near plane (its faces skipped), -1 invalid input. */
 int om_render_fwd(const om_scene *sc, const om_opts *op, double *out_rgba, int *ids, int ids_k,
-                  unsigned char *amb_img, unsigned char *amb_ids, const int *frozen, double *stats)
+                  unsigned char *amb_img, unsigned char *amb_ids, unsigned char *amb_win, const int *frozen,
+                  double *stats)
 {
     int H = sc->H, W = sc->W, P = H * W, ret = 0;
     int list = op->npix > 0;
@@ -618,8 +704,10 @@ int om_render_fwd(const om_scene *sc, const om_opts *op, double *out_rgba, int *
     if (ids) for (int q = 0; q < nout; ++q) ids[q] = -1;
     if (amb_img) memset(amb_img, 0, (size_t)nout);
     if (amb_ids) memset(amb_ids, 0, (size_t)nout);
+    if (amb_win) memset(amb_win, 0, (size_t)nout);
     om_stats_t tot = {0, 0, 0, 0};
     size_t frozen_off = 0;
+    int *nbr = op->eps_amb > 0 ? build_nbr(sc) : NULL;
     int *lidx = (int *)malloc(sizeof(int) * (size_t)(op->npix + 1));
     int *lslot = (int *)malloc(sizeof(int) * (size_t)(op->npix + 1));
     for (int b = 0; b < sc->B; ++b) {
@@ -630,7 +718,7 @@ int om_render_fwd(const om_scene *sc, const om_opts *op, double *out_rgba, int *
         int nth = nthreads_of(op);
         if (nth > st.N) nth = st.N;
         if (nth < 1) nth = 1;
-        double *acc = (double *)calloc((size_t)nth * 4 * np, sizeof(double));
+        double *acc = (double *)calloc((size_t)nth * 5 * np, sizeof(double));   /* rgba + sum delta/N */
         om_stats_t *tst = (om_stats_t *)calloc((size_t)nth, sizeof(om_stats_t));
         int N = st.N;
 #pragma omp parallel num_threads(nth)
@@ -644,7 +732,7 @@ int om_render_fwd(const om_scene *sc, const om_opts *op, double *out_rgba, int *
             double *Y = (double *)malloc(sizeof(double) * (size_t)(sc->V + 1));
             double *Z = (double *)malloc(sizeof(double) * (size_t)(sc->V + 1));
             unsigned char *okv = (unsigned char *)malloc((size_t)(sc->V + 1));
-            double *a = acc + (size_t)tid * 4 * np;
+            double *a = acc + (size_t)tid * 5 * np;
 #pragma omp for schedule(static)
             for (int k = st.k0; k < st.k1; ++k) {
                 if (frozen) {
@@ -659,21 +747,22 @@ int om_render_fwd(const om_scene *sc, const om_opts *op, double *out_rgba, int *
                         double w[3], det, rgb[3];
                         if (!om_bary_textbook(g.x, g.y, pix_u(p % W, W), pix_v(p / W, H), w, &det)) continue;
                         shade_w(sc, f, w, rgb);
-                        a[4 * p] += rgb[0]; a[4 * p + 1] += rgb[1]; a[4 * p + 2] += rgb[2]; a[4 * p + 3] += 1.0;
+                        a[5 * p] += rgb[0]; a[5 * p + 1] += rgb[1]; a[5 * p + 2] += rgb[2]; a[5 * p + 3] += 1.0;
                     }
                     continue;
                 }
-                render_subframe(sc, op, &st, k, ps, list ? lidx : NULL, np, &tst[tid], X, Y, Z, okv);
+                render_subframe(sc, op, &st, k, ps, list ? lidx : NULL, np, &tst[tid], X, Y, Z, okv, nbr);
                 for (int q = 0; q < np; ++q) {
                     int oq = list ? lslot[q] : b * P + q;
                     if (ps[q].id[0] >= 0) {
                         double rgb[3];
                         shade_w(sc, ps[q].id[0], ps[q].w, rgb);      /* Eq.9 */
-                        a[4 * q] += rgb[0]; a[4 * q + 1] += rgb[1]; a[4 * q + 2] += rgb[2]; a[4 * q + 3] += 1.0;
+                        a[5 * q] += rgb[0]; a[5 * q + 1] += rgb[1]; a[5 * q + 2] += rgb[2]; a[5 * q + 3] += 1.0;
                         tst[tid].covered += 1;
                     }
+                    a[5 * q + 4] += ps[q].delta;
                     if (ids && k == ids_k) ids[oq] = ps[q].id[0];
-                    if (amb_img && ps[q].amb_val) amb_img[oq] = 1;   /* distinct k write the same 1 */
+                    if (amb_win && ps[q].amb_id) amb_win[oq] = 1;    /* distinct k write the same 1 */
                     if (amb_ids && k == ids_k && ps[q].amb_id) amb_ids[oq] = 1;
                 }
             }
@@ -683,8 +772,13 @@ int om_render_fwd(const om_scene *sc, const om_opts *op, double *out_rgba, int *
             int oq = list ? lslot[q] : b * P + q;
             for (int c = 0; c < 4; ++c) {
                 double s = 0;
-                for (int t = 0; t < nth; ++t) s += acc[(size_t)t * 4 * np + 4 * q + c];
+                for (int t = 0; t < nth; ++t) s += acc[(size_t)t * 5 * np + 5 * q + c];
                 out_rgba[4 * (size_t)oq + c] = s / (double)N;   /* uniform mean */
+            }
+            if (amb_img) {
+                double d = 0;
+                for (int t = 0; t < nth; ++t) d += acc[(size_t)t * 5 * np + 5 * q + 4];
+                if (d / (double)N > op->amb_val_tol) amb_img[oq] = 1;
             }
         }
         for (int t = 0; t < nth; ++t) {
@@ -697,7 +791,7 @@ int om_render_fwd(const om_scene *sc, const om_opts *op, double *out_rgba, int *
         frozen_off += (size_t)N * P;
         img_free(&st);
     }
-    free(lidx); free(lslot);
+    free(lidx); free(lslot); free(nbr);
     if (stats) { stats[0] = tot.maxdev; stats[1] = tot.nchecked; stats[2] = tot.necessary; stats[3] = tot.covered; }
     return ret;
 }
@@ -747,7 +841,7 @@ int om_render_bwd(const om_scene *sc, const om_opts *op, const double *grad_rgba
             double *mk = gk + (size_t)tid * nkv, *mc = gc + (size_t)tid * 3 * V;
 #pragma omp for schedule(static)
             for (int k = st.k0; k < st.k1; ++k) {
-                render_subframe(sc, &op1, &st, k, ps, list ? lidx : NULL, np, NULL, X, Y, Z, okv);
+                render_subframe(sc, &op1, &st, k, ps, list ? lidx : NULL, np, NULL, X, Y, Z, okv, NULL);
                 int s = st.sk[k];
                 double tau = st.tk[k];
                 for (int q = 0; q < np; ++q) {

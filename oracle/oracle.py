@@ -54,7 +54,7 @@ def lib():
             _lib.om_fast_coeffs.argtypes = [P, P, P, P, C.c_double, C.c_double, P, P, P, P]
             _lib.om_fast_coeffs.restype = None
             _lib.om_fast_eval.argtypes = [P, P, P, P, C.c_double, C.c_double, C.c_double, P, P]
-            _lib.om_render_fwd.argtypes = [P, P, P, P, C.c_int, P, P, P, P]
+            _lib.om_render_fwd.argtypes = [P, P, P, P, C.c_int, P, P, P, P, P]
             _lib.om_render_bwd.argtypes = [P, P, P, P, P, P]
             _lib.om_num_threads.argtypes = [C.c_int]
         return _lib
@@ -147,7 +147,9 @@ def fast_eval(X0, Y0, X1, Y1, u, v, t):
 def render_fwd(sc, mode="binned", threads=0, ids_k=-1, eps_amb=0.0, check_fast=False, sub_range=None,
                frozen=None, pixels=None, colors=None, verts=None):
     """Blurred RGBA (B,H,W,4) fp64 (or (npix,4) in pixel-list mode).
-    Returns dict(rgba, ids, amb_img, amb_ids, stats, behind)."""
+    Returns dict(rgba, ids, amb_img, amb_ids, amb_win, stats, behind); the amb_* maps are the Q16
+    exclusion masks: blurred value movable by > 1e-5, winner at ids_k ambiguous,
+    winner ambiguous at some sub-frame."""
     import dataclasses
     if colors is not None or verts is not None:
         sc = dataclasses.replace(sc, colors=sc.colors if colors is None else colors,
@@ -159,14 +161,17 @@ def render_fwd(sc, mode="binned", threads=0, ids_k=-1, eps_amb=0.0, check_fast=F
     ids = np.full(shape, -1, np.int32)
     amb_i = np.zeros(shape, np.uint8)
     amb_d = np.zeros(shape, np.uint8)
+    amb_w = np.zeros(shape, np.uint8)
     stats = np.zeros(4)
     fz = None if frozen is None else _i(frozen)
+    on = eps_amb > 0
     r = lib().om_render_fwd(C.byref(pk.s), C.byref(o), _p(rgba), _p(ids), int(ids_k),
-                            _p(amb_i) if eps_amb > 0 else None, _p(amb_d) if eps_amb > 0 else None,
+                            _p(amb_i) if on else None, _p(amb_d) if on else None, _p(amb_w) if on else None,
                             _p(fz), _p(stats))
     if r < 0:
         raise ValueError("oracle: invalid input")
     return dict(rgba=rgba, ids=ids, amb_img=amb_i.astype(bool), amb_ids=amb_d.astype(bool),
+                amb_win=amb_w.astype(bool),
                 stats=dict(max_fast_dev=stats[0], n_checked=stats[1], necessary_pairs=stats[2],
                            covered=stats[3]), behind=bool(r == 1))
 

@@ -82,7 +82,7 @@ class ShardedStep:
         self.targets = targets[self.images].contiguous() if self.images else targets[:0]
         self.renderer = make_renderer(self.images, [[u.k0, u.k1] for u in self.mine]) if self.images else None
         # loss is counted once per image: by the co-owner holding k0 == 0
-        self.loss_mask = torch.tensor([1.0 if u.k0 == 0 else 0.0 for u in self.mine], dtype=torch.float32,
+        self.loss_mask = torch.tensor([1.0 if u.k0 == 0 else 0.0 for u in self.mine], dtype=targets.dtype,
                                       device=device)
         self.groups = []
         self.device = device
@@ -103,7 +103,7 @@ class ShardedStep:
             if all(u.k0 == 0 for u in self.mine):                      # no split image: one call
                 loss_all, grads = self.renderer.l2_loss_grad(out, self.targets, n_norm=self.n_norm)
             else:
-                loss_all = torch.zeros(1, dtype=torch.float32, device=self.device)
+                loss_all = torch.zeros(1, dtype=out.dtype, device=self.device)
                 grads = torch.empty_like(out)
                 for i in range(len(self.images)):
                     li, gi = self.renderer.l2_loss_grad(out[i:i + 1].contiguous(),
@@ -113,7 +113,7 @@ class ShardedStep:
             dv, dc = self.renderer.backward(verts, colors, grads, reuse_setup=True)
             flat = torch.cat([dv.reshape(-1), dc.reshape(-1), loss_all])
         else:
-            flat = torch.zeros(6 * V + 1, dtype=torch.float32, device=self.device)
+            flat = torch.zeros(6 * V + 1, dtype=verts.dtype, device=self.device)
         if self.world > 1:
             dist.all_reduce(flat)
         return flat[-1:], flat[:3 * V].reshape(V, 3), flat[3 * V:6 * V].reshape(V, 3)

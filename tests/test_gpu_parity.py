@@ -50,7 +50,11 @@ def rel_l2(a, b):
 
 def check_parity(sc, ids_k=0, mode="binned", max_chunk=0, sub_range=None, grad=True):
     ref = oracle.render_fwd(sc, mode=mode, ids_k=ids_k, eps_amb=1e-6, sub_range=sub_range)
+    # the same upstream G on both sides (the oracle's image), zero where the winner of some
+    # sub-frame is ambiguous: the frozen-winner derivative is discontinuous there (Q18)
     G = 2.0 * (ref["rgba"] - sc.target) / ref["rgba"].size if grad else None
+    if grad:
+        G = G * (~ref["amb_win"])[..., None]
     got = gpu_render(sc, ids_k=ids_k, sub_range=sub_range, max_chunk=max_chunk, G=G)
     assert not (got["status"] & 8), "internal consistency check failed"
     ok = ~ref["amb_img"]
@@ -59,7 +63,8 @@ def check_parity(sc, ids_k=0, mode="binned", max_chunk=0, sub_range=None, grad=T
     okid = ~ref["amb_ids"]
     mism = (got["ids"] != ref["ids"]) & okid
     assert not mism.any(), "id mismatch at %d pixels" % mism.sum()
-    out = dict(img_err=float(err[ok].max()), img_err_all=float(err.max()), amb=int((~ok).sum()))
+    out = dict(img_err=float(err[ok].max()), img_err_all=float(err.max()), amb=int((~ok).sum()),
+               amb_win=int(ref["amb_win"].sum()), pixels=int(ok.size))
     if grad:
         rdv, rdc = oracle.render_bwd(sc, G, mode=mode, sub_range=sub_range)
         ev, ec = rel_l2(got["dv"], rdv), rel_l2(got["dc"], rdc)
@@ -223,8 +228,8 @@ def test_full_size_sampled(name, npix):
     assert ok.sum() >= npix * 0.8
     err = np.abs(g_img - ref["rgba"])[ok]
     assert err.max() < TOL_IMG, err.max()
-    # the loss reads only the sampled pixels; ambiguous ones are excluded on both sides
-    Gp2 = Gp * ok[:, None]
+    # the loss reads only the sampled pixels; winner-ambiguous ones are excluded on both sides (Q18)
+    Gp2 = Gp * (~ref["amb_win"])[:, None]
     G2 = np.zeros_like(G)
     G2[pix[:, 0], pix[:, 1], pix[:, 2]] = Gp2
     got2 = gpu_render(sc, G=G2)
