@@ -350,45 +350,61 @@ __device__ __forceinline__ void acc_zero(FaceAcc &a)
 }
 
 // Gather the pixels this staged face won at tau: dv (6) = dL/dv_i(tau), dc (9).  Returns true if any.
+// The face's gradient is linear in dL/dI and w_i(p) = (A_i u + B_i v + G_i)/|D| is affine in the
+// tile-local pixel position, so only nine moments of g = dL/dI_k over the won pixels are needed:
+// m0 = sum g, mu = sum u g, mv = sum v g.  Then (Eq.9; dw/dv_i = -w_i dw/dp)
+//   dL/dc_i = sum_p w_i g = (A_i mu + B_i mv + G_i m0) / |D|
+//   dL/dv_i = -sum_p w_i sigma(p),  sigma = sum_j (g.c_j) grad_p w_j = (g.PA, g.PB) / |D|,
+//   PA = sum_j A_j c_j, PB = sum_j B_j c_j   ->  -(A_i (PA.mu) + B_i (PA.mv) + G_i (PA.m0)) / D^2, ...
 __device__ __forceinline__ bool gather(const TauRec &r, uint32_t bx, int myid, const int *swin, const float4 *sg,
                                        const float4 *__restrict__ fcol, const TileCtx &tc, float dv[6], float dc[9])
 {
     if (bx == EMPTY_BOX) return false;
     const int x0 = bx & 0xff, x1 = (bx >> 8) & 0xff, y0 = (bx >> 16) & 0xff, y1 = bx >> 24;
+    float m0x = 0.f, m0y = 0.f, m0z = 0.f, mux = 0.f, muy = 0.f, muz = 0.f, mvx = 0.f, mvy = 0.f, mvz = 0.f;
     bool any = false;
-    float4 c0, c1, c2;
-    for (int y = y0; y <= y1; ++y)
+    for (int y = y0; y <= y1; ++y) {
+        const float vl = (float)(TH / 2 - y) * tc.sy;
         for (int x = x0; x <= x1; ++x) {
             const int p = y * TW + x;
             if (swin[p] != myid) continue;
-            if (!any) {
-                const float4 *fc = fcol + 3 * (size_t)r.fid;
-                c0 = __ldg(fc); c1 = __ldg(fc + 1); c2 = __ldg(fc + 2);
-#pragma unroll
-                for (int i = 0; i < 6; ++i) dv[i] = 0.f;
-#pragma unroll
-                for (int i = 0; i < 9; ++i) dc[i] = 0.f;
-                any = true;
-            }
-            const float ul = (float)(x - TW / 2) * tc.sx, vl = (float)(TH / 2 - y) * tc.sy;
-            float w[3];
-            weights(r, ul, vl, w);
             const float4 g = sg[p];            // dL/dI / N
-            // dI/dc_i = w_i (Eq.9)
-            dc[0] += w[0] * g.x; dc[1] += w[0] * g.y; dc[2] += w[0] * g.z;
-            dc[3] += w[1] * g.x; dc[4] += w[1] * g.y; dc[5] += w[1] * g.z;
-            dc[6] += w[2] * g.x; dc[7] += w[2] * g.y; dc[8] += w[2] * g.z;
-            // s_j = g . c_j ; sigma = sum_j s_j dw_j/dp ; dL/dv_i = -w_i sigma
-            const float s0 = g.x * c0.x + g.y * c0.y + g.z * c0.z;
-            const float s1 = g.x * c0.w + g.y * c1.x + g.z * c1.y;
-            const float s2 = g.x * c1.z + g.y * c1.w + g.z * c2.x;
-            const float su = (s0 * r.a[0] + s1 * r.a[1] + s2 * r.a[2]) * r.invD;
-            const float sv = (s0 * r.b[0] + s1 * r.b[1] + s2 * r.b[2]) * r.invD;
-            dv[0] -= w[0] * su; dv[1] -= w[0] * sv;
-            dv[2] -= w[1] * su; dv[3] -= w[1] * sv;
-            dv[4] -= w[2] * su; dv[5] -= w[2] * sv;
+            const float ul = (float)(x - TW / 2) * tc.sx;
+            m0x += g.x; m0y += g.y; m0z += g.z;
+            mux = __fmaf_rn(ul, g.x, mux); muy = __fmaf_rn(ul, g.y, muy); muz = __fmaf_rn(ul, g.z, muz);
+            mvx = __fmaf_rn(vl, g.x, mvx); mvy = __fmaf_rn(vl, g.y, mvy); mvz = __fmaf_rn(vl, g.z, mvz);
+            any = true;
         }
-    return any;
+    }
+    if (!any) return false;
+    const float4 *fc = fcol + 3 * (size_t)r.fid;
+    const float4 c0 = __ldg(fc), c1 = __ldg(fc + 1), c2 = __ldg(fc + 2);
+    const float iD = r.invD;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float A = r.a[i], B = r.b[i], G = r.g[i];
+        dc[3 * i + 0] = (A * mux + B * mvx + G * m0x) * iD;
+        dc[3 * i + 1] = (A * muy + B * mvy + G * m0y) * iD;
+        dc[3 * i + 2] = (A * muz + B * mvz + G * m0z) * iD;
+    }
+    // colour-weighted edge normals: PA = sum_j A_j c_j, PB = sum_j B_j c_j
+    const float pax = r.a[0] * c0.x + r.a[1] * c0.w + r.a[2] * c1.z;
+    const float pay = r.a[0] * c0.y + r.a[1] * c1.x + r.a[2] * c1.w;
+    const float paz = r.a[0] * c0.z + r.a[1] * c1.y + r.a[2] * c2.x;
+    const float pbx = r.b[0] * c0.x + r.b[1] * c0.w + r.b[2] * c1.z;
+    const float pby = r.b[0] * c0.y + r.b[1] * c1.x + r.b[2] * c1.w;
+    const float pbz = r.b[0] * c0.z + r.b[1] * c1.y + r.b[2] * c2.x;
+    const float qa0 = pax * m0x + pay * m0y + paz * m0z, qau = pax * mux + pay * muy + paz * muz;
+    const float qav = pax * mvx + pay * mvy + paz * mvz;
+    const float qb0 = pbx * m0x + pby * m0y + pbz * m0z, qbu = pbx * mux + pby * muy + pbz * muz;
+    const float qbv = pbx * mvx + pby * mvy + pbz * mvz;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float A = r.a[i], B = r.b[i], G = r.g[i];
+        dv[2 * i + 0] = -((A * qau + B * qav + G * qa0) * iD) * iD;
+        dv[2 * i + 1] = -((A * qbu + B * qbv + G * qb0) * iD) * iD;
+    }
+    return true;
 }
 
 __device__ __forceinline__ void flush(const Tables &t, const ImgInfo &im, int s, int fid, const float k0[6],
