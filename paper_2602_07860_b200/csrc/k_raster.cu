@@ -247,7 +247,7 @@ __device__ __forceinline__ void tile_ctx(const Tables &t, int tile, TileCtx &tc,
 }
 
 template <bool CENSUS>
-__global__ void __launch_bounds__(NT) k4_raster_fwd(Tables t, float *__restrict__ out, int *__restrict__ ids,
+__global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restrict__ out, int *__restrict__ ids,
                                                     int ids_k, unsigned long long *census)
 {
     __shared__ TauRec srec[CAP];
@@ -334,6 +334,58 @@ __global__ void __launch_bounds__(NT) k4_raster_fwd(Tables t, float *__restrict_
 }
 
 // ------------------------------------------------------------------ backward
+//
+// Per (tile, sub-frame): the face's gradient is linear in g = dL/dI_k and w_i(p) is affine in the
+// tile-local pixel position, so each face only needs nine moments of g over the pixels it won:
+// m0 = sum g, mu = sum u g, mv = sum v g (u, v tile-local).  Then (Eq.9, dw/dv_i = -w_i dw/dp)
+//   dL/dc_i = (A_i mu + B_i mv + G_i m0) / |D|
+//   dL/dv_i = -( A_i (PA.mu) + B_i (PA.mv) + G_i (PA.m0),  same with PB ) / D^2,
+//   PA = sum_j A_j c_j, PB = sum_j B_j c_j  (A, B, G the sign-normalised numerator coefficients).
+// The moments are reduced pixel-parallel: the won pixels are counting-sorted by winning slot
+// (integer shared-memory atomics), every thread forms the 9 moment terms of one won pixel, a warp
+// segmented scan sums runs of equal slots, and each face thread combines its (<= 1 + crossings)
+// partial sums and evaluates the closed form.  Every phase is balanced over the CTA.
+
+struct BwdSmem {
+    TauRec rec[CAP];
+    uint32_t box[CAP];
+    int sid[CAP];
+    int cnt[CAP];          // won-pixel count per staged slot
+    int off[CAP];          // exclusive prefix of cnt
+    int key[TW * TH];      // sorted won pixels: slot
+    int pix[TW * TH];      //                    pixel
+    float mom[9][TW * TH]; // segment partial moments at the run's last position (per warp)
+    float4 g[TW * TH];     // dL/dI / N of the tile
+    int wsum[NT / 32];
+    int total;
+};
+
+// block-wide exclusive scan of cnt[0..nb) (nb <= CAP = 2 NT) into off[]; returns the total
+__device__ __forceinline__ int scan_counts(BwdSmem &S, int nb)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int j0 = 2 * tid;
+    const int c0 = j0 < nb ? S.cnt[j0] : 0, c1 = j0 + 1 < nb ? S.cnt[j0 + 1] : 0;
+    int x = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) S.wsum[warp] = x;
+    __syncthreads();
+    int pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+        const int v = S.wsum[w];
+        pre += w < warp ? v : 0;
+        tot += v;
+    }
+    const int ex = pre + x - (c0 + c1);
+    if (j0 < nb) S.off[j0] = ex;
+    if (j0 + 1 < nb) S.off[j0 + 1] = ex + c0;
+    return tot;
+}
 
 struct FaceAcc {
     float k0[6];   // d/d keyframe s position of corners 0..2 (x, y)
@@ -349,34 +401,12 @@ __device__ __forceinline__ void acc_zero(FaceAcc &a)
     for (int i = 0; i < 9; ++i) a.c[i] = 0.f;
 }
 
-// Gather the pixels this staged face won at tau: dv (6) = dL/dv_i(tau), dc (9).  Returns true if any.
-// The face's gradient is linear in dL/dI and w_i(p) = (A_i u + B_i v + G_i)/|D| is affine in the
-// tile-local pixel position, so only nine moments of g = dL/dI_k over the won pixels are needed:
-// m0 = sum g, mu = sum u g, mv = sum v g.  Then (Eq.9; dw/dv_i = -w_i dw/dp)
-//   dL/dc_i = sum_p w_i g = (A_i mu + B_i mv + G_i m0) / |D|
-//   dL/dv_i = -sum_p w_i sigma(p),  sigma = sum_j (g.c_j) grad_p w_j = (g.PA, g.PB) / |D|,
-//   PA = sum_j A_j c_j, PB = sum_j B_j c_j   ->  -(A_i (PA.mu) + B_i (PA.mv) + G_i (PA.m0)) / D^2, ...
-__device__ __forceinline__ bool gather(const TauRec &r, uint32_t bx, int myid, const int *swin, const float4 *sg,
-                                       const float4 *__restrict__ fcol, const TileCtx &tc, float dv[6], float dc[9])
+// closed-form face gradient at tau from its moments (see the comment above)
+__device__ __forceinline__ void face_grad(const TauRec &r, const float m[9], const float4 *__restrict__ fcol,
+                                          float dv[6], float dc[9])
 {
-    if (bx == EMPTY_BOX) return false;
-    const int x0 = bx & 0xff, x1 = (bx >> 8) & 0xff, y0 = (bx >> 16) & 0xff, y1 = bx >> 24;
-    float m0x = 0.f, m0y = 0.f, m0z = 0.f, mux = 0.f, muy = 0.f, muz = 0.f, mvx = 0.f, mvy = 0.f, mvz = 0.f;
-    bool any = false;
-    for (int y = y0; y <= y1; ++y) {
-        const float vl = (float)(TH / 2 - y) * tc.sy;
-        for (int x = x0; x <= x1; ++x) {
-            const int p = y * TW + x;
-            if (swin[p] != myid) continue;
-            const float4 g = sg[p];            // dL/dI / N
-            const float ul = (float)(x - TW / 2) * tc.sx;
-            m0x += g.x; m0y += g.y; m0z += g.z;
-            mux = __fmaf_rn(ul, g.x, mux); muy = __fmaf_rn(ul, g.y, muy); muz = __fmaf_rn(ul, g.z, muz);
-            mvx = __fmaf_rn(vl, g.x, mvx); mvy = __fmaf_rn(vl, g.y, mvy); mvz = __fmaf_rn(vl, g.z, mvz);
-            any = true;
-        }
-    }
-    if (!any) return false;
+    const float m0x = m[0], m0y = m[1], m0z = m[2], mux = m[3], muy = m[4], muz = m[5], mvx = m[6], mvy = m[7],
+                mvz = m[8];
     const float4 *fc = fcol + 3 * (size_t)r.fid;
     const float4 c0 = __ldg(fc), c1 = __ldg(fc + 1), c2 = __ldg(fc + 2);
     const float iD = r.invD;
@@ -387,7 +417,6 @@ __device__ __forceinline__ bool gather(const TauRec &r, uint32_t bx, int myid, c
         dc[3 * i + 1] = (A * muy + B * mvy + G * m0y) * iD;
         dc[3 * i + 2] = (A * muz + B * mvz + G * m0z) * iD;
     }
-    // colour-weighted edge normals: PA = sum_j A_j c_j, PB = sum_j B_j c_j
     const float pax = r.a[0] * c0.x + r.a[1] * c0.w + r.a[2] * c1.z;
     const float pay = r.a[0] * c0.y + r.a[1] * c1.x + r.a[2] * c1.w;
     const float paz = r.a[0] * c0.z + r.a[1] * c1.y + r.a[2] * c2.x;
@@ -404,7 +433,6 @@ __device__ __forceinline__ bool gather(const TauRec &r, uint32_t bx, int myid, c
         dv[2 * i + 0] = -((A * qau + B * qav + G * qa0) * iD) * iD;
         dv[2 * i + 1] = -((A * qbu + B * qbv + G * qb0) * iD) * iD;
     }
-    return true;
 }
 
 __device__ __forceinline__ void flush(const Tables &t, const ImgInfo &im, int s, int fid, const float k0[6],
@@ -424,14 +452,95 @@ __device__ __forceinline__ void flush(const Tables &t, const ImgInfo &im, int s,
     }
 }
 
-__global__ void __launch_bounds__(NT) k6_raster_bwd(Tables t, const float *__restrict__ grad, float *__restrict__ dC)
+// Reduce the moments of the won pixels whose winner lies in the staged batch [base, base+nb) and
+// hand each face with winners its closed-form gradient: persistent slots (single batch, slot ==
+// thread) accumulate in registers across the chunk, the others flush immediately.
+__device__ __forceinline__ void bwd_batch(BwdSmem &S, const Tables &t, const ImgInfo &im, int s, float tau, int base,
+                                          int nb, bool persist_ok, int ebest, int myp, const TileCtx &tc,
+                                          FaceAcc &acc, float *dC)
 {
-    __shared__ TauRec srec[CAP];
-    __shared__ uint32_t sbox[CAP];
-    __shared__ int sid[CAP];
-    __shared__ int swsum[NT / 32];
-    __shared__ int swin[TW * TH];
-    __shared__ float4 sg[TW * TH];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int j = tid; j < nb; j += NT) S.cnt[j] = 0;
+    __syncthreads();
+    const int e = ebest - base;
+    const bool mine = ebest >= 0 && e >= 0 && e < nb;
+    int rank = 0;
+    if (mine) rank = atomicAdd(&S.cnt[e], 1);
+    __syncthreads();
+    const int total = scan_counts(S, nb);
+    __syncthreads();
+    if (mine) {
+        const int pos = S.off[e] + rank;
+        S.key[pos] = e;
+        S.pix[pos] = myp;
+    }
+    __syncthreads();
+    // moment terms of one won pixel per thread, warp segmented inclusive scan over equal slots
+    {
+        int key = -1 - tid;   // unique keys for idle threads (never merged)
+        float m[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) m[q] = 0.f;
+        if (tid < total) {
+            key = S.key[tid];
+            const int p = S.pix[tid];
+            const float4 g = S.g[p];
+            const float ul = (float)((p & (TW - 1)) - TW / 2) * tc.sx;
+            const float vl = (float)(TH / 2 - (p / TW)) * tc.sy;
+            m[0] = g.x; m[1] = g.y; m[2] = g.z;
+            m[3] = ul * g.x; m[4] = ul * g.y; m[5] = ul * g.z;
+            m[6] = vl * g.x; m[7] = vl * g.y; m[8] = vl * g.z;
+        }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int ku = __shfl_up_sync(0xffffffffu, key, d);
+            const bool take = lane >= d && ku == key;
+#pragma unroll
+            for (int q = 0; q < 9; ++q) {
+                const float v = __shfl_up_sync(0xffffffffu, m[q], d);
+                if (take) m[q] += v;
+            }
+        }
+        const int knext = __shfl_down_sync(0xffffffffu, key, 1);
+        if (tid < total && (lane == 31 || tid == total - 1 || knext != key)) {
+#pragma unroll
+            for (int q = 0; q < 9; ++q) S.mom[q][tid] = m[q];
+        }
+    }
+    __syncthreads();
+    for (int j = tid; j < nb; j += NT) {
+        const int c = S.cnt[j];
+        if (c == 0) continue;
+        const int st = S.off[j], en = st + c - 1;
+        float m[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) m[q] = S.mom[q][en];
+        for (int i = st | 31; i < en; i += 32)        // partial sums ending at warp boundaries
+#pragma unroll
+            for (int q = 0; q < 9; ++q) m[q] += S.mom[q][i];
+        float dv[6], dc[9];
+        face_grad(S.rec[j], m, t.fcol, dv, dc);
+        if (persist_ok && j == tid) {
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                acc.k0[i] = __fmaf_rn(1.f - tau, dv[i], acc.k0[i]);
+                acc.k1[i] = __fmaf_rn(tau, dv[i], acc.k1[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < 9; ++i) acc.c[i] += dc[i];
+        } else {
+            float a0[6], a1[6];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) { a0[i] = (1.f - tau) * dv[i]; a1[i] = tau * dv[i]; }
+            flush(t, im, s, S.rec[j].fid, a0, a1, dc, dC);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__restrict__ grad, float *__restrict__ dC)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BwdSmem &S = *reinterpret_cast<BwdSmem *>(smem_raw);
     const int b = blockIdx.y, tile = blockIdx.x;
     const ImgInfo &im = t.imgs[b];
     const int N = im.N, c_begin = im.chunk_begin, c_end = im.chunk_end, sched_off = im.sched_off;
@@ -454,7 +563,7 @@ __global__ void __launch_bounds__(NT) k6_raster_bwd(Tables t, const float *__res
             const float inv = 1.0f / (float)N;   // dI/dI_k = 1/N (uniform mean)
             g.x *= inv; g.y *= inv; g.z *= inv; g.w = 0.f;
         }
-        sg[myp] = g;
+        S.g[myp] = g;
     }
     __syncthreads();
     unsigned long long dummy0 = 0, dummy1 = 0;
@@ -482,52 +591,27 @@ __global__ void __launch_bounds__(NT) k6_raster_bwd(Tables t, const float *__res
             int base = 0, fpos = 0;
             // visibility (identical to the forward pass)
             while (true) {
-                const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, base, fpos, sid, swsum);
+                const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, base, fpos, S.sid, S.wsum);
                 if (nb == 0) break;
-                stage_batch(bc, nb, base, tau, tc, t.W, t.H, t.F, sid, srec, sbox);
+                stage_batch(bc, nb, base, tau, tc, t.W, t.H, t.F, S.sid, S.rec, S.box);
                 __syncthreads();
-                vis_batch<false>(srec, sbox, nb, base, wx0, wy0, ul, vl, zbest, ebest, dummy0, dummy1, false);
+                vis_batch<false>(S.rec, S.box, nb, base, wx0, wy0, ul, vl, zbest, ebest, dummy0, dummy1, false);
                 base += nb;
-                if (!single) __syncthreads();
+                __syncthreads();
             }
-            swin[myp] = inimg ? ebest : -1;
-            __syncthreads();
+            if (!inimg) ebest = -1;
             if (single) {
-                for (int j = threadIdx.x; j < n; j += NT) {
-                    float dv[6], dc[9];
-                    if (!gather(srec[j], sbox[j], j, swin, sg, t.fcol, tc, dv, dc)) continue;
-                    if (j == (int)threadIdx.x) {
-#pragma unroll
-                        for (int i = 0; i < 6; ++i) {
-                            acc.k0[i] = __fmaf_rn(1.f - tau, dv[i], acc.k0[i]);
-                            acc.k1[i] = __fmaf_rn(tau, dv[i], acc.k1[i]);
-                        }
-#pragma unroll
-                        for (int i = 0; i < 9; ++i) acc.c[i] += dc[i];
-                    } else {
-                        float a0[6], a1[6];
-#pragma unroll
-                        for (int i = 0; i < 6; ++i) { a0[i] = (1.f - tau) * dv[i]; a1[i] = tau * dv[i]; }
-                        flush(t, im, ch.s, srec[j].fid, a0, a1, dc, dC);
-                    }
-                }
+                bwd_batch(S, t, im, ch.s, tau, 0, n, true, ebest, myp, tc, acc, dC);
             } else {
                 // several batches: re-stage each batch and flush per sub-frame
                 base = 0;
                 fpos = 0;
                 while (true) {
-                    const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, base, fpos, sid, swsum);
+                    const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, base, fpos, S.sid, S.wsum);
                     if (nb == 0) break;
-                    stage_batch(bc, nb, base, tau, tc, t.W, t.H, t.F, sid, srec, sbox);
+                    stage_batch(bc, nb, base, tau, tc, t.W, t.H, t.F, S.sid, S.rec, S.box);
                     __syncthreads();
-                    for (int j = threadIdx.x; j < nb; j += NT) {
-                        float dv[6], dc[9];
-                        if (!gather(srec[j], sbox[j], base + j, swin, sg, t.fcol, tc, dv, dc)) continue;
-                        float a0[6], a1[6];
-#pragma unroll
-                        for (int i = 0; i < 6; ++i) { a0[i] = (1.f - tau) * dv[i]; a1[i] = tau * dv[i]; }
-                        flush(t, im, ch.s, srec[j].fid, a0, a1, dc, dC);
-                    }
+                    bwd_batch(S, t, im, ch.s, tau, base, nb, false, ebest, myp, tc, acc, dC);
                     base += nb;
                     __syncthreads();
                 }
@@ -559,7 +643,10 @@ cudaError_t launch_raster_bwd(const Tables &t, const float *grad, float *dC, cud
 {
     if (t.B == 0 || t.T == 0 || t.F == 0) return cudaSuccess;
     dim3 grid(t.T, t.B);
-    k6_raster_bwd<<<grid, NT, 0, st>>>(t, grad, dC);
+    const int smem = (int)sizeof(BwdSmem);
+    cudaError_t e = cudaFuncSetAttribute(k6_raster_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k6_raster_bwd<<<grid, NT, smem, st>>>(t, grad, dC);
     return cudaGetLastError();
 }
 
