@@ -1,24 +1,23 @@
 // k_raster.cu -- K4 fused raster-forward and K6 fused raster-backward.
 //
-// One CTA = one 16x16 pixel tile of one image; 8 warps, each owning an 8x4 footprint, one pixel
-// per thread.  For every chunk of sub-frames the CTA reads the tile's bin (faces sorted by index).
-// For every sub-frame tau of the chunk:
-//   stage   each face of the bin evaluates its segment coefficients at tau (Eq.8 numerators and
-//           denominator, Horner in tau -- "compute once, evaluate per sample") about the tile
-//           centre, normalises the sign by det F(tau) and writes a 64 B record to shared memory,
-//           with its per-tau pixel box (tile-level cull) -> sbox
-//   vis     each warp culls the staged faces against its 8x4 footprint (lanes test 32 boxes at a
-//           time, ballot) and every lane evaluates the three numerators at its pixel centre
-//           (2 FMA each), tests coverage by sign (all w_i >= 0), and keeps the nearest face
-//           (z-buffer in registers, strict <, faces in index order -> lower index wins ties, Q7)
+// One CTA = one 16x16 pixel tile of one image; 8 warps, each owning an 8x4 footprint, one pixel per
+// thread.  For every chunk of sub-frames the CTA reads the tile's bin (faces sorted by index).
+//   stage   every bin face loads its (face, segment) coefficient record ONCE and evaluates it at
+//           each sub-frame tau of the chunk (Eq.8 numerators and denominator, Horner in tau: the
+//           paper's "compute once, evaluate per sample"), re-centred at the tile centre and
+//           sign-normalised by det F(tau), into a 64 B shared-memory record per (tau, face); it
+//           also marks, in a per-(tau, warp) bitmask over the bin slots, the warp footprints its
+//           per-tau box and edge functions can reach (integer atomicOr).
+//   vis     each warp walks the set bits of its mask (faces in index order) and every lane
+//           evaluates the three numerators at its pixel centre (2 FMA each), tests coverage by sign
+//           (all w_i >= 0), and keeps the nearest face (z-buffer in registers, strict <, lower
+//           index wins exact ties, Q7).  No barrier between the sub-frames of a group.
 //   shade   fwd: w_i = N_i / |D|, I = sum w_i c_i (Eq.9), accumulated in registers over all
 //           sub-frames; the sub-frames never reach HBM.  Output (1/N) sum, written once.
-//           bwd: the winner map goes to shared memory; each face thread walks its pixel box,
-//           gathers dL/dI at the pixels it won and accumulates colour and screen-position
-//           gradients in registers (aggregated over pixels and over the chunk's sub-frames), then
-//           flushes them with one vector atomic per (vertex, keyframe).
+//           bwd: see the comment above k6_raster_bwd.
 // Bins that overflowed (or exceed SORTCAP) are regenerated exactly by scanning all faces in index
-// order (slow path).  Faces of a bin above CAP are processed in several batches.
+// order (slow path); bins longer than the shared-memory record capacity are processed per
+// sub-frame in several batches.
 #include <cstdio>
 
 #include "internal.cuh"
@@ -26,7 +25,11 @@
 
 namespace br {
 
-constexpr uint32_t EMPTY_BOX = 0x001F001Fu;   // x0 = 31 > x1 = 0 -> never overlaps
+constexpr int NWARP = NT / 32;
+constexpr int SREC_F = 768;    // fwd: staged (tau, face) records per CTA (48 KB)
+constexpr int SREC_B = 512;    // bwd: staged records per CTA (32 KB); also the gather's slot limit
+constexpr int GMAX_F = 16;     // max sub-frames staged together
+constexpr int GMAX_B = 8;
 
 struct TileCtx {
     float uc, vc;     // NDC of the tile's reference pixel centre (TW/2, TH/2)
@@ -55,29 +58,49 @@ __device__ __forceinline__ bool tile_pixels(float xmn, float xmx, float ymn, flo
     return true;
 }
 
-// Evaluate the (face, segment) record at tau for this tile -> TauRec + packed pixel box.
-__device__ __forceinline__ void stage_one(const float4 *__restrict__ r, float tau, const TileCtx &tc,
-                                          int W, int H, TauRec &out, uint32_t &box)
+struct FaceRec {            // a (face, segment) coefficient record held in registers
+    float4 q[REC_F4];
+};
+
+__device__ __forceinline__ void load_rec(const float4 *__restrict__ r, FaceRec &fr)
 {
-    box = EMPTY_BOX;
-    const float4 q6 = __ldg(r + 6);
-    const int fid = __float_as_int(q6.w);
-    out.fid = fid;
-    if (fid < 0) return;
+#pragma unroll
+    for (int i = 0; i < REC_F4; ++i) fr.q[i] = __ldg(r + i);
+}
+
+// max over the pixel centres of a local rect [x0..x1] x [y0..y1] of the edge function, >= -tol ?
+__device__ __forceinline__ bool rect_reaches(const float A[3], const float B[3], const float G[3], int x0, int x1,
+                                             int y0, int y1, const TileCtx &tc)
+{
+    const float ulmin = (float)(x0 - TW / 2) * tc.sx, ulmax = (float)(x1 - TW / 2) * tc.sx;
+    const float vlmin = (float)(TH / 2 - y1) * tc.sy, vlmax = (float)(TH / 2 - y0) * tc.sy;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float m = G[i] + (A[i] > 0.f ? A[i] * ulmax : A[i] * ulmin) + (B[i] > 0.f ? B[i] * vlmax : B[i] * vlmin);
+        const float tol = 1e-6f * (fabsf(A[i]) * fmaxf(-ulmin, ulmax) + fabsf(B[i]) * fmaxf(-vlmin, vlmax) +
+                                   fabsf(G[i])) + 1e-30f;
+        if (m < -tol) return false;
+    }
+    return true;
+}
+
+// Evaluate a record at tau for this tile -> TauRec + the mask of warp footprints it can reach
+// (bit w = warp w's 8x4 footprint; 0 = the face cannot cover any pixel of the tile at tau).
+__device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, const TileCtx &tc, int W, int H,
+                                              TauRec &out)
+{
+    const float4 q6 = fr.q[6];
     const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);   // a1 t^2 + a2 t + a3
-    if (!(fabsf(D) > EPS_D)) return;                                    // Q8
-    const float4 b0 = __ldg(r + 7), b1 = __ldg(r + 8);
+    if (!(fabsf(D) > EPS_D)) return 0u;                                 // Q8
+    const float4 b0 = fr.q[7], b1 = fr.q[8];
     int x0, x1, y0, y1;
     if (!tile_pixels(box_lerp(tau, b0.x, b1.x), box_lerp(tau, b0.y, b1.y), box_lerp(tau, b0.z, b1.z),
                      box_lerp(tau, b0.w, b1.w), W, H, tc, x0, x1, y0, y1))
-        return;
+        return 0u;
     const float sg = D < 0.f ? -1.f : 1.f;
     const float invD = 1.0f / fabsf(D);
     float A[3], B[3], G[3];
-    float4 e[6];
-#pragma unroll
-    for (int q = 0; q < 6; ++q) e[q] = __ldg(r + q);
-    const float *ef = reinterpret_cast<const float *>(e);
+    const float *ef = reinterpret_cast<const float *>(fr.q);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         const float ox = ef[8 * i], oy = ef[8 * i + 1];
@@ -90,16 +113,16 @@ __device__ __forceinline__ void stage_one(const float4 *__restrict__ r, float ta
         B[i] = be * sg;
         G[i] = gp * sg;
     }
-    // tile-level reject: the edge function's maximum over the tile's pixel centres
-    const float ulmin = -(TW / 2) * tc.sx, ulmax = (TW / 2 - 1) * tc.sx;
-    const float vlmin = -(TH / 2 - 1) * tc.sy, vlmax = (TH / 2) * tc.sy;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        const float m = G[i] + (A[i] > 0.f ? A[i] * ulmax : A[i] * ulmin) + (B[i] > 0.f ? B[i] * vlmax : B[i] * vlmin);
-        const float tol = 1e-6f * (fabsf(A[i]) * ulmax + fabsf(B[i]) * vlmax + fabsf(G[i])) + 1e-30f;
-        if (m < -tol) return;
-    }
-    const float4 z0 = __ldg(r + 9), z1 = __ldg(r + 10);
+    // warp footprints (8x4, arranged 2 x 4) reached by the box and the three edge half-planes
+    uint32_t fm = 0u;
+    for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
+        for (int wx = x0 >> 3; wx <= (x1 >> 3); ++wx) {
+            const int rx0 = max(x0, wx * 8), rx1 = min(x1, wx * 8 + 7);
+            const int ry0 = max(y0, wy * 4), ry1 = min(y1, wy * 4 + 3);
+            if (rect_reaches(A, B, G, rx0, rx1, ry0, ry1, tc)) fm |= 1u << (wy * 2 + wx);
+        }
+    if (!fm) return 0u;
+    const float4 z0 = fr.q[9], z1 = fr.q[10];
     const float za = __fmaf_rn(tau, z1.x - z0.x, z0.x);
     const float zb = __fmaf_rn(tau, z1.y - z0.y, z0.y);
     const float zc = __fmaf_rn(tau, z1.z - z0.z, z0.z);
@@ -114,13 +137,14 @@ __device__ __forceinline__ void stage_one(const float4 *__restrict__ r, float ta
     out.bz = __fmaf_rn(B[1], dzb, B[2] * dzc) * invD;
     out.cz = __fmaf_rn(__fmaf_rn(G[1], dzb, G[2] * dzc), invD, za);
     out.invD = invD;
-    box = (uint32_t)x0 | ((uint32_t)x1 << 8) | ((uint32_t)y0 << 16) | ((uint32_t)y1 << 24);
+    out.fid = __float_as_int(q6.w);
+    return fm;
 }
 
 // Fallback batch builder: faces whose per-tau box overlaps the tile, in index order, from fpos on.
 // Block-uniform.  Returns the batch size (0 when all faces are consumed).
-__device__ int fallback_fill(const float4 *__restrict__ rseg, int F, float tau, const TileCtx &tc, int W,
-                             int H, int &fpos, int *sid, int *swsum)
+__device__ int fallback_fill(const float4 *__restrict__ rseg, int F, float tau, const TileCtx &tc, int W, int H,
+                             int cap, int &fpos, int *sid, int *swsum)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int nb = 0;
@@ -142,13 +166,13 @@ __device__ int fallback_fill(const float4 *__restrict__ rseg, int F, float tau, 
         __syncthreads();
         int pre = 0, tot = 0;
 #pragma unroll
-        for (int w = 0; w < NT / 32; ++w) {
+        for (int w = 0; w < NWARP; ++w) {
             const int c = swsum[w];
             pre += w < warp ? c : 0;
             tot += c;
         }
         __syncthreads();
-        if (nb + tot > CAP) break;                       // uniform: batch full
+        if (nb + tot > cap) break;                       // uniform: batch full
         if (hit) sid[nb + pre + __popc(m & ((1u << lane) - 1u))] = f;
         nb += tot;
         fpos += NT;
@@ -165,53 +189,59 @@ struct BinCtx {
     bool fb;              // fallback path
 };
 
-// Batch iteration shared by the passes: returns nb (0 = done).  Normal path: contiguous slices of
-// the sorted bin.  Fallback: regenerated by scanning faces.
+// Per-sub-frame batch iteration (bins longer than the record capacity, fallback): returns nb
+// (0 = done).  Normal path: contiguous slices of the sorted bin.  Fallback: faces rescanned.
 __device__ __forceinline__ int next_batch(const BinCtx &bc, int F, float tau, const TileCtx &tc, int W, int H,
-                                          int base, int &fpos, int *sid, int *swsum)
+                                          int cap, int base, int &fpos, int *sid, int *swsum)
 {
-    if (!bc.fb) return base < bc.n ? min(CAP, bc.n - base) : 0;
-    return fallback_fill(bc.rseg, F, tau, tc, W, H, fpos, sid, swsum);
+    if (!bc.fb) return base < bc.n ? min(cap, bc.n - base) : 0;
+    return fallback_fill(bc.rseg, F, tau, tc, W, H, cap, fpos, sid, swsum);
 }
 
-__device__ __forceinline__ void stage_batch(const BinCtx &bc, int nb, int base, float tau, const TileCtx &tc,
-                                            int W, int H, int F, const int *sid, TauRec *srec, uint32_t *sbox)
+// Stage faces [base, base+nb) of the bin (or sid[] in fallback mode) at the ng sub-frames
+// taus[0..ng): records rec[l*nb + j], masks wm[(l*NWARP + w)*nw + j/32].  Masks must be clear.
+// Work is spread over (face, sub-frame) pairs, face-major, so the lanes that share a face load its
+// record with broadcast loads.
+template <bool CENSUS>
+__device__ __forceinline__ void stage_group(const BinCtx &bc, int nb, int base, const float *taus, int ng,
+                                            const TileCtx &tc, int W, int H, int F, const int *sid, TauRec *rec,
+                                            uint32_t *wm, unsigned long long &nstage)
 {
-    for (int j = threadIdx.x; j < nb; j += NT) {
+    const int nw = (nb + 31) >> 5;
+    const int npair = nb * ng;
+    for (int p = threadIdx.x; p < npair; p += NT) {
+        const int j = p / ng, l = p - j * ng;
         const int f = bc.fb ? sid[j] : __ldg(bc.ent + base + j);
         if ((unsigned)f >= (unsigned)F) {     // never expected: bins hold valid face ids
 #ifdef BR_DEBUG
             printf("bad face id %d (F=%d) fb=%d n=%d base=%d j=%d nb=%d tile=%d img=%d\n", f, F, (int)bc.fb, bc.n,
                    base, j, nb, blockIdx.x, blockIdx.y);
 #endif
-            srec[j].fid = -1;
-            sbox[j] = EMPTY_BOX;
             atomicOr(bc.status, BLUR_ST_EINTERNAL);
             continue;
         }
-        stage_one(bc.rseg + (size_t)f * REC_F4, tau, tc, W, H, srec[j], sbox[j]);
+        const float4 *r = bc.rseg + (size_t)f * REC_F4;
+        if (__float_as_int(__ldg(r + 6).w) < 0) continue;     // skipped face (Q8, behind, bad index)
+        FaceRec fr;
+        load_rec(r, fr);
+        const uint32_t fm = stage_tau(fr, taus[l], tc, W, H, rec[l * nb + j]);
+        if (CENSUS) nstage += fm != 0u;
+        const uint32_t bit = 1u << (j & 31);
+        for (uint32_t m = fm; m; m &= m - 1) atomicOr(wm + (l * NWARP + (__ffs(m) - 1)) * nw + (j >> 5), bit);
     }
 }
 
 template <bool CENSUS>
-__device__ __forceinline__ void vis_batch(const TauRec *srec, const uint32_t *sbox, int nb, int base, int wx0,
-                                          int wy0, float ul, float vl, float &zbest, int &ebest,
-                                          unsigned long long &ncov, unsigned long long &ntest, bool count)
+__device__ __forceinline__ void vis_mask(const TauRec *rec, const uint32_t *wm, int nw, int ebase, float ul,
+                                         float vl, float &zbest, int &ebest, unsigned long long &ncov,
+                                         unsigned long long &ntest, bool count)
 {
-    const int lane = threadIdx.x & 31;
-    for (int j0 = 0; j0 < nb; j0 += 32) {
-        const int j = j0 + lane;
-        bool hit = false;
-        if (j < nb) {
-            const uint32_t bx = sbox[j];
-            const int x0 = bx & 0xff, x1 = (bx >> 8) & 0xff, y0 = (bx >> 16) & 0xff, y1 = bx >> 24;
-            hit = x0 <= wx0 + 7 && x1 >= wx0 && y0 <= wy0 + 3 && y1 >= wy0;
-        }
-        unsigned m = __ballot_sync(0xffffffffu, hit);
+    for (int wd = 0; wd < nw; ++wd) {
+        uint32_t m = wm[wd];
         while (m) {
-            const int k = __ffs(m) - 1;
+            const int j = (wd << 5) + __ffs(m) - 1;
             m &= m - 1;
-            const float4 *rp = reinterpret_cast<const float4 *>(srec + j0 + k);
+            const float4 *rp = reinterpret_cast<const float4 *>(rec + j);
             const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
             const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
             const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
@@ -219,7 +249,7 @@ __device__ __forceinline__ void vis_batch(const TauRec *srec, const uint32_t *sb
             const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
             const bool cov = fminf(fminf(e0, e1), e2) >= 0.f;
             if (CENSUS && count) { ncov += cov; ntest += 1; }
-            if (cov && z < zbest) { zbest = z; ebest = base + j0 + k; }
+            if (cov && z < zbest) { zbest = z; ebest = ebase + j; }
         }
     }
 }
@@ -231,10 +261,21 @@ __device__ __forceinline__ void weights(const TauRec &r, float ul, float vl, flo
     w[2] = edge_eval(r.a[2], r.b[2], r.g[2], ul, vl) * r.invD;
 }
 
-__device__ __forceinline__ void tile_ctx(const Tables &t, int tile, TileCtx &tc, int &tx, int &ty)
+__device__ __forceinline__ void shade(const TauRec &r, const float4 *__restrict__ fcol, float ul, float vl,
+                                      float &pr, float &pg, float &pb)
 {
-    tx = tile % t.TX;
-    ty = tile / t.TX;
+    float w[3];
+    weights(r, ul, vl, w);
+    const float4 *fc = fcol + 3 * (size_t)r.fid;
+    const float4 c0 = __ldg(fc), c1 = __ldg(fc + 1), c2 = __ldg(fc + 2);
+    pr = __fmaf_rn(w[0], c0.x, __fmaf_rn(w[1], c0.w, w[2] * c1.z));
+    pg = __fmaf_rn(w[0], c0.y, __fmaf_rn(w[1], c1.x, w[2] * c1.w));
+    pb = __fmaf_rn(w[0], c0.z, __fmaf_rn(w[1], c1.y, w[2] * c2.x));
+}
+
+__device__ __forceinline__ void tile_ctx(const Tables &t, int tile, TileCtx &tc)
+{
+    const int tx = tile % t.TX, ty = tile / t.TX;
     tc.px0 = tx * TW;
     tc.py0 = ty * TH;
     tc.lxmax = min(TW - 1, t.W - 1 - tc.px0);
@@ -246,24 +287,33 @@ __device__ __forceinline__ void tile_ctx(const Tables &t, int tile, TileCtx &tc,
     tc.sy = (float)(2.0 / t.H);
 }
 
+__device__ __forceinline__ void clear_words(uint32_t *w, int n)
+{
+    for (int i = threadIdx.x; i < n; i += NT) w[i] = 0u;
+}
+
+struct FwdSmem {
+    TauRec rec[SREC_F];
+    uint32_t wm[NWARP * (SREC_F / 32 + GMAX_F)];
+    int sid[SREC_F];
+    float taus[GMAX_F];
+    int wsum[NWARP];
+};
+
 template <bool CENSUS>
 __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restrict__ out, int *__restrict__ ids,
-                                                    int ids_k, unsigned long long *census)
+                                                       int ids_k, unsigned long long *census)
 {
-    __shared__ TauRec srec[CAP];
-    __shared__ uint32_t sbox[CAP];
-    __shared__ int sid[CAP];
-    __shared__ int swsum[NT / 32];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    FwdSmem &S = *reinterpret_cast<FwdSmem *>(smem_raw);
     const int b = blockIdx.y, tile = blockIdx.x;
     const ImgInfo &im = t.imgs[b];
     const int N = im.N, c_begin = im.chunk_begin, c_end = im.chunk_end, sched_off = im.sched_off;
     const long long rec_off = im.rec_off;
     TileCtx tc;
-    int tx, ty;
-    tile_ctx(t, tile, tc, tx, ty);
+    tile_ctx(t, tile, tc);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 4;
-    const int lx = wx0 + (lane & 7), ly = wy0 + (lane >> 3);
+    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
     const int px = tc.px0 + lx, py = tc.py0 + ly;
     const bool inimg = px < t.W && py < t.H;
     const float ul = (float)(lx - TW / 2) * tc.sx;
@@ -287,38 +337,64 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
         bc.ent = t.entries + o;
         bc.n = n;
         bc.fb = n > SORTCAP || (long long)o + n > t.cap;
-        for (int k = ch.k0; k < ch.k1; ++k) {
-            const float tau = t.sched_tau[sched_off + k];
-            float zbest = __int_as_float(0x7f800000);
-            int ebest = -1;
-            bool has = false;
-            int bfid = -1;
-            float pr = 0.f, pg = 0.f, pb = 0.f;
-            int base = 0, fpos = 0;
-            while (true) {
-                const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, base, fpos, sid, swsum);
-                if (nb == 0) break;
-                stage_batch(bc, nb, base, tau, tc, t.W, t.H, t.F, sid, srec, sbox);
-                if (CENSUS) nstage += (threadIdx.x < nb) ? (nb - threadIdx.x + NT - 1) / NT : 0;
+        if (!bc.fb && n <= SREC_F) {
+            // grouped path: the whole bin staged for up to Gs sub-frames at once
+            const int Gs = min(GMAX_F, SREC_F / n), nw = (n + 31) >> 5;
+            for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
+                const int ng = min(Gs, ch.k1 - kg);
+                clear_words(S.wm, ng * NWARP * nw);
+                if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();
-                vis_batch<CENSUS>(srec, sbox, nb, base, wx0, wy0, ul, vl, zbest, ebest, ncov, ntest, inimg);
-                if (ebest >= base) {   // winner changed in this batch: shade now (Eq.9)
-                    const TauRec &r = srec[ebest - base];
-                    float w[3];
-                    weights(r, ul, vl, w);
-                    const float4 *fc = t.fcol + 3 * (size_t)r.fid;
-                    const float4 c0 = __ldg(fc), c1 = __ldg(fc + 1), c2 = __ldg(fc + 2);
-                    pr = __fmaf_rn(w[0], c0.x, __fmaf_rn(w[1], c0.w, w[2] * c1.z));
-                    pg = __fmaf_rn(w[0], c0.y, __fmaf_rn(w[1], c1.x, w[2] * c1.w));
-                    pb = __fmaf_rn(w[0], c0.z, __fmaf_rn(w[1], c1.y, w[2] * c2.x));
-                    has = true;
-                    bfid = r.fid;
+                stage_group<CENSUS>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.wm, nstage);
+                __syncthreads();
+                for (int l = 0; l < ng; ++l) {
+                    float zbest = __int_as_float(0x7f800000);
+                    int ebest = -1;
+                    const TauRec *rl = S.rec + l * n;
+                    vis_mask<CENSUS>(rl, S.wm + (l * NWARP + warp) * nw, nw, 0, ul, vl, zbest, ebest, ncov, ntest,
+                                     inimg);
+                    int fid = -1;
+                    if (ebest >= 0) {
+                        float pr, pg, pb;
+                        shade(rl[ebest], t.fcol, ul, vl, pr, pg, pb);      // Eq.9
+                        ar += pr; ag += pg; ab += pb; aa += 1.f;
+                        fid = rl[ebest].fid;
+                        if (CENSUS) nshade++;
+                    }
+                    if (ids && inimg && kg + l == ids_k) ids[pix] = fid;
                 }
-                base += nb;
                 __syncthreads();
             }
-            if (has) { ar += pr; ag += pg; ab += pb; aa += 1.f; if (CENSUS) nshade++; }
-            if (ids && inimg && k == ids_k) ids[pix] = has ? bfid : -1;
+        } else {
+            // per sub-frame, several batches (long bins) or the exact fallback scan (overflow)
+            for (int k = ch.k0; k < ch.k1; ++k) {
+                const float tau = t.sched_tau[sched_off + k];
+                float zbest = __int_as_float(0x7f800000);
+                int ebest = -1, bfid = -1;
+                bool has = false;
+                float pr = 0.f, pg = 0.f, pb = 0.f;
+                int base = 0, fpos = 0;
+                if (threadIdx.x == 0) S.taus[0] = tau;
+                while (true) {
+                    const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SREC_F, base, fpos, S.sid, S.wsum);
+                    if (nb == 0) break;
+                    const int nw = (nb + 31) >> 5;
+                    clear_words(S.wm, NWARP * nw);
+                    __syncthreads();
+                    stage_group<CENSUS>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.wm, nstage);
+                    __syncthreads();
+                    vis_mask<CENSUS>(S.rec, S.wm + warp * nw, nw, base, ul, vl, zbest, ebest, ncov, ntest, inimg);
+                    if (ebest >= base) {   // winner changed in this batch: shade now (Eq.9)
+                        shade(S.rec[ebest - base], t.fcol, ul, vl, pr, pg, pb);
+                        has = true;
+                        bfid = S.rec[ebest - base].fid;
+                    }
+                    base += nb;
+                    __syncthreads();
+                }
+                if (has) { ar += pr; ag += pg; ab += pb; aa += 1.f; if (CENSUS) nshade++; }
+                if (ids && inimg && k == ids_k) ids[pix] = has ? bfid : -1;
+            }
         }
     }
     if (inimg) {
@@ -335,32 +411,35 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
 
 // ------------------------------------------------------------------ backward
 //
-// Per (tile, sub-frame): the face's gradient is linear in g = dL/dI_k and w_i(p) is affine in the
-// tile-local pixel position, so each face only needs nine moments of g over the pixels it won:
-// m0 = sum g, mu = sum u g, mv = sum v g (u, v tile-local).  Then (Eq.9, dw/dv_i = -w_i dw/dp)
+// Visibility as in the forward pass.  Then, per (tile, sub-frame): the face's gradient is linear in
+// g = dL/dI_k and w_i(p) is affine in the tile-local pixel position, so each face only needs nine
+// moments of g over the pixels it won: m0 = sum g, mu = sum u g, mv = sum v g.  Then (Eq.9 and
+// dw/dv_i = -w_i dw/dp)
 //   dL/dc_i = (A_i mu + B_i mv + G_i m0) / |D|
 //   dL/dv_i = -( A_i (PA.mu) + B_i (PA.mv) + G_i (PA.m0),  same with PB ) / D^2,
 //   PA = sum_j A_j c_j, PB = sum_j B_j c_j  (A, B, G the sign-normalised numerator coefficients).
 // The moments are reduced pixel-parallel: the won pixels are counting-sorted by winning slot
 // (integer shared-memory atomics), every thread forms the 9 moment terms of one won pixel, a warp
-// segmented scan sums runs of equal slots, and each face thread combines its (<= 1 + crossings)
-// partial sums and evaluates the closed form.  Every phase is balanced over the CTA.
+// segmented scan sums runs of equal slots, and each face thread combines its partial sums and
+// evaluates the closed form.  Face gradients accumulate in registers over the chunk's sub-frames
+// (slot == thread) and are flushed with one vector RED per (vertex, keyframe) at the chunk's end.
 
 struct BwdSmem {
-    TauRec rec[CAP];
-    uint32_t box[CAP];
-    int sid[CAP];
-    int cnt[CAP];          // won-pixel count per staged slot
-    int off[CAP];          // exclusive prefix of cnt
-    int key[TW * TH];      // sorted won pixels: slot
-    int pix[TW * TH];      //                    pixel
-    float mom[9][TW * TH]; // segment partial moments at the run's last position (per warp)
-    float4 g[TW * TH];     // dL/dI / N of the tile
-    int wsum[NT / 32];
-    int total;
+    TauRec rec[SREC_B];
+    uint32_t wm[NWARP * (SREC_B / 32 + GMAX_B)];
+    int sid[SREC_B];
+    int win[GMAX_B][TW * TH]; // winning slot per (sub-frame of the group, pixel)
+    int cnt[SREC_B];          // won-pixel count per staged slot
+    int off[SREC_B];          // exclusive prefix of cnt
+    int key[TW * TH];         // sorted won pixels: slot
+    int pix[TW * TH];         //                    pixel
+    float mom[9][TW * TH];    // segment partial moments at the run's last position (per warp)
+    float4 g[TW * TH];        // dL/dI / N of the tile
+    float taus[GMAX_B];
+    int wsum[NWARP];
 };
 
-// block-wide exclusive scan of cnt[0..nb) (nb <= CAP = 2 NT) into off[]; returns the total
+// block-wide exclusive scan of cnt[0..nb) (nb <= 2 NT) into off[]; returns the total
 __device__ __forceinline__ int scan_counts(BwdSmem &S, int nb)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -376,7 +455,7 @@ __device__ __forceinline__ int scan_counts(BwdSmem &S, int nb)
     __syncthreads();
     int pre = 0, tot = 0;
 #pragma unroll
-    for (int w = 0; w < NT / 32; ++w) {
+    for (int w = 0; w < NWARP; ++w) {
         const int v = S.wsum[w];
         pre += w < warp ? v : 0;
         tot += v;
@@ -452,12 +531,12 @@ __device__ __forceinline__ void flush(const Tables &t, const ImgInfo &im, int s,
     }
 }
 
-// Reduce the moments of the won pixels whose winner lies in the staged batch [base, base+nb) and
-// hand each face with winners its closed-form gradient: persistent slots (single batch, slot ==
-// thread) accumulate in registers across the chunk, the others flush immediately.
-__device__ __forceinline__ void bwd_batch(BwdSmem &S, const Tables &t, const ImgInfo &im, int s, float tau, int base,
-                                          int nb, bool persist_ok, int ebest, int myp, const TileCtx &tc,
-                                          FaceAcc &acc, float *dC)
+// Reduce the moments of the won pixels whose winner lies in the staged batch [base, base+nb)
+// (records rec[0..nb)) and give each face with winners its closed-form gradient: persistent slots
+// (slot == thread) accumulate in registers across the chunk, the others flush immediately.
+__device__ __forceinline__ void bwd_gather(BwdSmem &S, const TauRec *rec, const Tables &t, const ImgInfo &im, int s,
+                                           float tau, int base, int nb, bool persist_ok, int ebest, int myp,
+                                           const TileCtx &tc, FaceAcc &acc, float *dC)
 {
     const int tid = threadIdx.x, lane = tid & 31;
     for (int j = tid; j < nb; j += NT) S.cnt[j] = 0;
@@ -519,7 +598,7 @@ __device__ __forceinline__ void bwd_batch(BwdSmem &S, const Tables &t, const Img
 #pragma unroll
             for (int q = 0; q < 9; ++q) m[q] += S.mom[q][i];
         float dv[6], dc[9];
-        face_grad(S.rec[j], m, t.fcol, dv, dc);
+        face_grad(rec[j], m, t.fcol, dv, dc);
         if (persist_ok && j == tid) {
 #pragma unroll
             for (int i = 0; i < 6; ++i) {
@@ -532,9 +611,10 @@ __device__ __forceinline__ void bwd_batch(BwdSmem &S, const Tables &t, const Img
             float a0[6], a1[6];
 #pragma unroll
             for (int i = 0; i < 6; ++i) { a0[i] = (1.f - tau) * dv[i]; a1[i] = tau * dv[i]; }
-            flush(t, im, s, S.rec[j].fid, a0, a1, dc, dC);
+            flush(t, im, s, rec[j].fid, a0, a1, dc, dC);
         }
     }
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__restrict__ grad, float *__restrict__ dC)
@@ -546,11 +626,9 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
     const int N = im.N, c_begin = im.chunk_begin, c_end = im.chunk_end, sched_off = im.sched_off;
     const long long rec_off = im.rec_off;
     TileCtx tc;
-    int tx, ty;
-    tile_ctx(t, tile, tc, tx, ty);
+    tile_ctx(t, tile, tc);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 4;
-    const int lx = wx0 + (lane & 7), ly = wy0 + (lane >> 3);
+    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
     const int px = tc.px0 + lx, py = tc.py0 + ly;
     const bool inimg = px < t.W && py < t.H;
     const float ul = (float)(lx - TW / 2) * tc.sx;
@@ -566,7 +644,7 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
         S.g[myp] = g;
     }
     __syncthreads();
-    unsigned long long dummy0 = 0, dummy1 = 0;
+    unsigned long long d0 = 0, d1 = 0, d2 = 0;
 
     for (int c = c_begin; c < c_end; ++c) {
         const Chunk ch = t.chunks[c];
@@ -580,45 +658,64 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
         bc.ent = t.entries + o;
         bc.n = n;
         bc.fb = n > SORTCAP || (long long)o + n > t.cap;
-        const bool single = !bc.fb && n <= CAP;
-        const bool persist = single && (int)threadIdx.x < n;
         FaceAcc acc;
         acc_zero(acc);
-        for (int k = ch.k0; k < ch.k1; ++k) {
-            const float tau = t.sched_tau[sched_off + k];
-            float zbest = __int_as_float(0x7f800000);
-            int ebest = -1;
-            int base = 0, fpos = 0;
-            // visibility (identical to the forward pass)
-            while (true) {
-                const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, base, fpos, S.sid, S.wsum);
-                if (nb == 0) break;
-                stage_batch(bc, nb, base, tau, tc, t.W, t.H, t.F, S.sid, S.rec, S.box);
+        if (!bc.fb && n <= SREC_B) {
+            const int Gs = min(GMAX_B, SREC_B / n), nw = (n + 31) >> 5;
+            for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
+                const int ng = min(Gs, ch.k1 - kg);
+                clear_words(S.wm, ng * NWARP * nw);
+                if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();
-                vis_batch<false>(S.rec, S.box, nb, base, wx0, wy0, ul, vl, zbest, ebest, dummy0, dummy1, false);
-                base += nb;
+                stage_group<false>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.wm, d2);
                 __syncthreads();
+                for (int l = 0; l < ng; ++l) {       // visibility for the group (no barriers)
+                    float zbest = __int_as_float(0x7f800000);
+                    int ebest = -1;
+                    vis_mask<false>(S.rec + l * n, S.wm + (l * NWARP + warp) * nw, nw, 0, ul, vl, zbest, ebest, d0,
+                                    d1, false);
+                    S.win[l][myp] = inimg ? ebest : -1;
+                }
+                __syncthreads();
+                for (int l = 0; l < ng; ++l)
+                    bwd_gather(S, S.rec + l * n, t, im, ch.s, S.taus[l], 0, n, true, S.win[l][myp], myp, tc, acc, dC);
             }
-            if (!inimg) ebest = -1;
-            if (single) {
-                bwd_batch(S, t, im, ch.s, tau, 0, n, true, ebest, myp, tc, acc, dC);
-            } else {
-                // several batches: re-stage each batch and flush per sub-frame
-                base = 0;
-                fpos = 0;
-                while (true) {
-                    const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, base, fpos, S.sid, S.wsum);
+        } else {
+            for (int k = ch.k0; k < ch.k1; ++k) {
+                const float tau = t.sched_tau[sched_off + k];
+                float zbest = __int_as_float(0x7f800000);
+                int ebest = -1;
+                int base = 0, fpos = 0;
+                if (threadIdx.x == 0) S.taus[0] = tau;
+                while (true) {                         // visibility over all batches
+                    const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SREC_B, base, fpos, S.sid, S.wsum);
                     if (nb == 0) break;
-                    stage_batch(bc, nb, base, tau, tc, t.W, t.H, t.F, S.sid, S.rec, S.box);
+                    const int nw = (nb + 31) >> 5;
+                    clear_words(S.wm, NWARP * nw);
                     __syncthreads();
-                    bwd_batch(S, t, im, ch.s, tau, base, nb, false, ebest, myp, tc, acc, dC);
+                    stage_group<false>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.wm, d2);
+                    __syncthreads();
+                    vis_mask<false>(S.rec, S.wm + warp * nw, nw, base, ul, vl, zbest, ebest, d0, d1, false);
                     base += nb;
                     __syncthreads();
                 }
+                if (!inimg) ebest = -1;
+                base = 0;
+                fpos = 0;
+                while (true) {                         // re-stage each batch and gather
+                    const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SREC_B, base, fpos, S.sid, S.wsum);
+                    if (nb == 0) break;
+                    const int nw = (nb + 31) >> 5;
+                    clear_words(S.wm, NWARP * nw);
+                    __syncthreads();
+                    stage_group<false>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.wm, d2);
+                    __syncthreads();
+                    bwd_gather(S, S.rec, t, im, ch.s, tau, base, nb, false, ebest, myp, tc, acc, dC);
+                    base += nb;
+                }
             }
-            __syncthreads();
         }
-        if (persist) {
+        if (!bc.fb && n <= SREC_B && (int)threadIdx.x < n) {
             bool nz = false;
 #pragma unroll
             for (int i = 0; i < 9; ++i) nz |= acc.c[i] != 0.f;
@@ -634,8 +731,17 @@ cudaError_t launch_raster_fwd(const Tables &t, float *out, int *ids, int ids_k, 
 {
     if (t.B == 0 || t.T == 0) return cudaSuccess;
     dim3 grid(t.T, t.B);
-    if (census) k4_raster_fwd<true><<<grid, NT, 0, st>>>(t, out, ids, ids_k, census);
-    else k4_raster_fwd<false><<<grid, NT, 0, st>>>(t, out, ids, ids_k, nullptr);
+    const int smem = (int)sizeof(FwdSmem);
+    cudaError_t e;
+    if (census) {
+        e = cudaFuncSetAttribute(k4_raster_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        k4_raster_fwd<true><<<grid, NT, smem, st>>>(t, out, ids, ids_k, census);
+    } else {
+        e = cudaFuncSetAttribute(k4_raster_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        k4_raster_fwd<false><<<grid, NT, smem, st>>>(t, out, ids, ids_k, nullptr);
+    }
     return cudaGetLastError();
 }
 
