@@ -221,12 +221,23 @@ __device__ __forceinline__ void stage_group(const BinCtx &bc, int nb, int base, 
             continue;
         }
         const float4 *r = bc.rseg + (size_t)f * REC_F4;
-        if (__float_as_int(__ldg(r + 6).w) < 0) continue;     // skipped face (Q8, behind, bad index)
+        const float4 q6 = __ldg(r + 6);
+        if (__float_as_int(q6.w) < 0) continue;               // skipped face (Q8, behind, bad index)
+        const float tau = taus[l];
+        {   // cheap rejects before the full record is loaded: degenerate at tau, box off the tile
+            const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);
+            if (!(fabsf(D) > EPS_D)) continue;
+            const float4 b0 = __ldg(r + 7), b1 = __ldg(r + 8);
+            int x0, x1, y0, y1;
+            if (!tile_pixels(box_lerp(tau, b0.x, b1.x), box_lerp(tau, b0.y, b1.y), box_lerp(tau, b0.z, b1.z),
+                             box_lerp(tau, b0.w, b1.w), W, H, tc, x0, x1, y0, y1))
+                continue;
+        }
         FaceRec fr;
         load_rec(r, fr);
-        const uint32_t fm = stage_tau(fr, taus[l], tc, W, H, rec[l * nb + j]);
+        const uint32_t fm = stage_tau(fr, tau, tc, W, H, rec[l * nb + j]);
         if (CENSUS) nstage += fm != 0u;
-        const uint32_t bit = 1u << (j & 31);
+        const uint32_t bit = 0x80000000u >> (j & 31);          // bit-reversed: clz gives ascending slots
         for (uint32_t m = fm; m; m &= m - 1) atomicOr(wm + (l * NWARP + (__ffs(m) - 1)) * nw + (j >> 5), bit);
     }
 }
@@ -238,10 +249,12 @@ __device__ __forceinline__ void vis_mask(const TauRec *rec, const uint32_t *wm, 
 {
     for (int wd = 0; wd < nw; ++wd) {
         uint32_t m = wm[wd];
+        const TauRec *rw = rec + (wd << 5);
         while (m) {
-            const int j = (wd << 5) + __ffs(m) - 1;
-            m &= m - 1;
-            const float4 *rp = reinterpret_cast<const float4 *>(rec + j);
+            const int k = __clz(m);
+            m ^= 0x80000000u >> k;
+            const int j = (wd << 5) + k;
+            const float4 *rp = reinterpret_cast<const float4 *>(rw + k);
             const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
             const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
             const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
