@@ -123,31 +123,45 @@ def make_target(sc, dev):
 
 
 def cpu_baseline(sc, target_seconds: float):
-    """Time the fp64 oracle (as it stands) fwd + bwd on a bounded sample of the same workload:
-    image 0 (and image B-1, the other motion kind) over a leading sub-frame range sized for about
-    `target_seconds` of CPU time, all host cores.  Returns images/s and the sample description."""
+    """Time the fp64 oracle (as it stands) fwd + bwd on a bounded sample of the same workload, all
+    host cores: whole images (translational and rotational views alternately) until about
+    `target_seconds` of CPU time, or a leading sub-frame range of one image if a single image
+    already takes longer.  Returns images/s and the sample description."""
     import oracle
     cores = oracle.num_threads(0)
-    imgs = sorted({0, sc.B - 1})
-    sub = sc.subset(imgs)
-    N = int(sub.motion["n_sub"][0])
-    G = np.zeros((sub.B, sub.H, sub.W, 4))
+    N = int(sc.motion["n_sub"][0])
+    order = []
+    lo, hi = 0, sc.B - 1
+    while lo <= hi:                       # 0, B-1, 1, B-2, ... (both motion kinds)
+        order.append(lo)
+        if hi != lo:
+            order.append(hi)
+        lo, hi = lo + 1, hi - 1
 
-    def run(ks):
+    def run(imgs, ks):
+        sub = sc.subset(imgs)
         rng = [[0, ks]] * sub.B
         t0 = time.perf_counter()
         fw = oracle.render_fwd(sub, sub_range=rng)
-        G[:] = 2.0 * (fw["rgba"] - (sub.target if sub.target is not None else 0.0)) / fw["rgba"].size
+        G = 2.0 * (fw["rgba"] - (sub.target if sub.target is not None else 0.0)) / fw["rgba"].size
         oracle.render_bwd(sub, G, sub_range=rng)
         return time.perf_counter() - t0
 
-    t_probe = run(min(2, N))
-    ks = max(1, min(N, int(min(2, N) * target_seconds / max(t_probe, 1e-3))))
-    t = run(ks) if ks != min(2, N) else t_probe
-    images = sub.B * ks / N
+    t1 = run(order[:1], N)                 # one whole image
+    ks, reps = N, 1
+    if t1 >= target_seconds:
+        imgs, t = order[:1], t1
+    else:
+        imgs = sorted(order[:max(1, min(sc.B, int(target_seconds / t1)))])
+        if len(imgs) == 1:                   # tiny workloads: repeat the sample
+            reps = max(1, min(1000, int(target_seconds / max(t1, 1e-6))))
+            t = sum(run(imgs, N) for _ in range(reps))
+        else:
+            t = run(imgs, ks)
+    images = len(imgs) * reps
     return {"value": images / t, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": "fp64 oracle (binned) fwd+bwd of images %s of %s, sub-frames [0,%d) of %d, %.1f s on %d "
-                      "threads = %.4f images" % (imgs, sc.name, ks, N, t, cores, images),
+            "sample": "fp64 oracle (binned) fwd+bwd of %d of %d images of %s (%s) x %d repetitions, all %d "
+                      "sub-frames: %.1f s on %d threads" % (len(imgs), sc.B, sc.name, imgs, reps, N, t, cores),
             "seconds": t}
 
 
