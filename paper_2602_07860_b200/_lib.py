@@ -13,7 +13,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libblurrast.so")
+LIB_PATH = os.environ.get("BLURRAST_LIB") or os.path.join(_HERE, "libblurrast.so")   # override: A/B builds
 _lock = threading.Lock()
 _lib = None
 
