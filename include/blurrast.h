@@ -63,13 +63,16 @@ typedef enum {
 #define BLUR_ST_EOVERFLOW 4
 #define BLUR_ST_EINTERNAL 8   /* internal consistency check failed (a bug: please report) */
 
-typedef enum { BLUR_STATIC = 0, BLUR_TRANSLATE = 1, BLUR_ROTATE = 2 } blur_motion_kind;
+typedef enum { BLUR_STATIC = 0, BLUR_TRANSLATE = 1, BLUR_ROTATE = 2, BLUR_PARABOLIC = 3 } blur_motion_kind;
 typedef enum { BLUR_SCHED_GLOBAL_INCLUSIVE = 0, BLUR_SCHED_PAPER_SEGMENTED = 1 } blur_sched_rule;
 
 /* Motion over the exposure t in [0,1] (host struct, one per image).
  *  BLUR_TRANSLATE: P(t) = P0 + (t - 0.5) vec          (A30, generalised; Q2)
  *  BLUR_ROTATE:    P(t) = c + R(vec, angle t)(P0 - c)  (A31, generalised; Q3, Q4:
  *                  right-handed Rodrigues rotation about the unit axis vec through c = pivot)
+ *  BLUR_PARABOLIC: P(t) = c + R(vec, angle t)(P0 - c) + (s, -4 s^2 + 0.5, s), s = 0.5 - t
+ *                  (composite rotation + parabolic translation, A35-A37; the paper's
+ *                  case is vec = +y, angle = pi, c = 0).  Not linear in t: use several segments.
  *  n_subframes N >= 1; n_segments S >= 1 (linear segments); sched_rule as Q1:
  *   GLOBAL_INCLUSIVE: t_k = k/(N-1) (N=1: 0.5), s_k = min(floor(t_k S), S-1), tau_k = t_k S - s_k;
  *   PAPER_SEGMENTED:  S | N, K = N/S, s_k = k div K, tau_k = (k mod K)/(K-1) (K=1: 0.5). */

@@ -48,6 +48,7 @@
 #define OM_STATIC 0
 #define OM_TRANSLATE 1
 #define OM_ROTATE 2
+#define OM_PARABOLIC 3
 #define OM_GLOBAL_INCLUSIVE 0
 #define OM_PAPER_SEGMENTED 1
 
@@ -149,23 +150,38 @@ static void rodrigues(const double ax[3], double th, double R[9])
     for (int i = 0; i < 9; ++i) R[i] = ((i % 4) == 0 ? 1.0 : 0.0) + sn * K[i] + cs * K2[i];
 }
 
-/* Rigid pose at exposure time t (A30 P:L1417-1424 generalised to P0 + (t-0.5)T, Q2;
- * A31 P:L1430-1432 generalised to c + R(a, Theta t)(P0 - c), Q3/Q4).
- * Returns R (3x3) and the pose applied as P = R (P0 - c) + c + T_t. */
-static void pose_rt(const om_scene *sc, int b, double t, double R[9], double tr[3])
+/* Rigid pose at exposure time t, written P(t) = R (P0 - c) + c + T for every kind:
+ *  translate (A30 P:L1417-1424 generalised, Q2): R = I, T = (t - 0.5) vec
+ *  rotate    (A31 P:L1430-1432 generalised, Q3/Q4): R = R(a, Theta t), c = pivot
+ *  parabolic (A35-A37 P:L1613-1629 generalised): R = R(a, Theta t), c = pivot,
+ *            T = (s, -4 s^2 + 0.5, s) with s = 0.5 - t (the paper's case: a = y, Theta = pi, c = 0) */
+static void pose_rct(const om_scene *sc, int b, double t, double R[9], double c[3], double T[3])
 {
     int kind = sc->kind[b];
     const double *vec = sc->vec + 3 * b, *piv = sc->pivot + 3 * b;
     for (int i = 0; i < 9; ++i) R[i] = (i % 4) == 0 ? 1.0 : 0.0;
-    tr[0] = tr[1] = tr[2] = 0.0;
+    c[0] = c[1] = c[2] = 0.0;
+    T[0] = T[1] = T[2] = 0.0;
     if (kind == OM_TRANSLATE) {
-        for (int i = 0; i < 3; ++i) tr[i] = (t - 0.5) * vec[i];
-    } else if (kind == OM_ROTATE) {
+        for (int i = 0; i < 3; ++i) T[i] = (t - 0.5) * vec[i];
+    } else if (kind == OM_ROTATE || kind == OM_PARABOLIC) {
         rodrigues(vec, sc->angle[b] * t, R);
-        double Rc[3];
-        for (int i = 0; i < 3; ++i) Rc[i] = R[i * 3] * piv[0] + R[i * 3 + 1] * piv[1] + R[i * 3 + 2] * piv[2];
-        for (int i = 0; i < 3; ++i) tr[i] = piv[i] - Rc[i];
+        for (int i = 0; i < 3; ++i) c[i] = piv[i];
+        if (kind == OM_PARABOLIC) {
+            double s = 0.5 - t;
+            T[0] = s;
+            T[1] = -4.0 * s * s + 0.5;
+            T[2] = s;
+        }
     }
+}
+
+/* the rotation part only (for the backward chain) */
+static void pose_rt(const om_scene *sc, int b, double t, double R[9], double tr[3])
+{
+    double c[3], T[3];
+    pose_rct(sc, b, t, R, c, T);
+    (void)tr;
 }
 
 /* Camera frame: forward f = normalize(target - eye), right r = normalize(f x up), up' = r x f.
@@ -193,19 +209,14 @@ int om_keyframes(const om_scene *sc, int b, double *key, unsigned char *valid, d
     double ta = tan(cam[9]);
     int bad = 0;
     for (int s = 0; s <= S; ++s) {
-        double R[9], tr[3];
-        pose_rt(sc, b, (double)s / (double)S, R, tr);
-        const double *piv = sc->pivot + 3 * b;
+        double R[9], c[3], T[3];
+        pose_rct(sc, b, (double)s / (double)S, R, c, T);
         for (int v = 0; v < V; ++v) {
             const double *P0 = sc->verts + 3 * v;
             double P[3], d[3], Q[3];
-            if (sc->kind[b] == OM_ROTATE) {
-                double q[3] = {P0[0] - piv[0], P0[1] - piv[1], P0[2] - piv[2]};
-                for (int i = 0; i < 3; ++i)
-                    P[i] = R[i * 3] * q[0] + R[i * 3 + 1] * q[1] + R[i * 3 + 2] * q[2] + piv[i];
-            } else {
-                for (int i = 0; i < 3; ++i) P[i] = P0[i] + tr[i];
-            }
+            double q[3] = {P0[0] - c[0], P0[1] - c[1], P0[2] - c[2]};
+            for (int i = 0; i < 3; ++i)
+                P[i] = R[i * 3] * q[0] + R[i * 3 + 1] * q[1] + R[i * 3 + 2] * q[2] + c[i] + T[i];
             for (int i = 0; i < 3; ++i) d[i] = P[i] - cam[i];
             for (int i = 0; i < 3; ++i) Q[i] = Rc[i * 3] * d[0] + Rc[i * 3 + 1] * d[1] + Rc[i * 3 + 2] * d[2];
             size_t o = ((size_t)s * V + v);

@@ -96,6 +96,8 @@ int auto_chunk(const blur_motion &m, const blur_camera &c, int H, int W)
         world = std::sqrt((double)m.vec[0] * m.vec[0] + (double)m.vec[1] * m.vec[1] + (double)m.vec[2] * m.vec[2]);
     else if (m.kind == BLUR_ROTATE)
         world = std::fabs((double)m.angle);   // unit-size object
+    else if (m.kind == BLUR_PARABOLIC)
+        world = std::fabs((double)m.angle) + 2.0;
     const double disp = world * ndc_per_world * px_per_ndc / (N - 1);
     if (disp <= 1e-6) return 16;
     int g = (int)std::floor(TW / disp);
@@ -121,13 +123,13 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
     for (int b = 0; b < B; ++b) {
         const blur_motion &mo = m[b];
         const int N = mo.n_subframes, S = mo.n_segments;
-        if (mo.kind < 0 || mo.kind > 2) return fail(BLUR_EINVAL, "motion kind must be 0, 1 or 2");
+        if (mo.kind < 0 || mo.kind > 3) return fail(BLUR_EINVAL, "motion kind must be 0, 1, 2 or 3");
         if (N < 1) return fail(BLUR_EINVAL, "n_subframes must be >= 1");
         if (S < 1) return fail(BLUR_EINVAL, "n_segments must be >= 1");
         if (mo.sched_rule == BLUR_SCHED_PAPER_SEGMENTED && N % S)
             return fail(BLUR_EINVAL, "PAPER_SEGMENTED needs n_segments | n_subframes");
         if (mo.sched_rule != 0 && mo.sched_rule != 1) return fail(BLUR_EINVAL, "bad sched_rule");
-        if (mo.kind == BLUR_ROTATE) {
+        if (mo.kind == BLUR_ROTATE || mo.kind == BLUR_PARABOLIC) {
             const double n = std::sqrt((double)mo.vec[0] * mo.vec[0] + (double)mo.vec[1] * mo.vec[1] +
                                        (double)mo.vec[2] * mo.vec[2]);
             if (!(n > 0)) return fail(BLUR_EINVAL, "rotation axis is zero");
@@ -179,10 +181,16 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
             for (int i = 0; i < 3; ++i) pr.R[4 * i] = 1.0;
             if (mo.kind == BLUR_TRANSLATE) {
                 for (int i = 0; i < 3; ++i) pr.T[i] = (t - 0.5) * (double)mo.vec[i];
-            } else if (mo.kind == BLUR_ROTATE) {
+            } else if (mo.kind == BLUR_ROTATE || mo.kind == BLUR_PARABOLIC) {
                 const double ax[3] = {mo.vec[0], mo.vec[1], mo.vec[2]};
                 rodrigues(ax, (double)mo.angle * t, pr.R);
                 for (int i = 0; i < 3; ++i) pr.c[i] = mo.pivot[i];
+                if (mo.kind == BLUR_PARABOLIC) {    // A36: T(t) = (s, -4 s^2 + 0.5, s), s = 0.5 - t
+                    const double sp = 0.5 - t;
+                    pr.T[0] = sp;
+                    pr.T[1] = -4.0 * sp * sp + 0.5;
+                    pr.T[2] = sp;
+                }
             }
             P.poses.push_back(pr);
         }

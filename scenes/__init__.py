@@ -29,7 +29,7 @@ from typing import Optional
 
 import numpy as np
 
-STATIC, TRANSLATE, ROTATE = 0, 1, 2
+STATIC, TRANSLATE, ROTATE, PARABOLIC = 0, 1, 2, 3
 GLOBAL_INCLUSIVE, PAPER_SEGMENTED = 0, 1
 
 HALF_FOV = math.radians(30.0)      # A34, P:L1455 ("fixed half-angular field of view alpha = 30 deg")
@@ -222,6 +222,22 @@ def rotate(axis, angle, N, S, pivot=(0, 0, 0), rule=GLOBAL_INCLUSIVE):
     """P(t) = c + R(axis, angle * t)(P0 - c)  (A31 generalised)."""
     a = np.asarray(axis, float)
     return dict(kind=ROTATE, vec=a / np.linalg.norm(a), angle=angle, pivot=pivot, N=N, S=S, rule=rule)
+
+
+def parabolic(N, S, axis=(0, 1, 0), angle=math.pi, pivot=(0, 0, 0), rule=GLOBAL_INCLUSIVE):
+    """A35-A37: rotation R(axis, angle t) then translation (s, -4s^2 + 0.5, s),
+    s = 0.5 - t; the paper's case is axis y, angle pi."""
+    a = np.asarray(axis, float)
+    return dict(kind=PARABOLIC, vec=a / np.linalg.norm(a), angle=angle, pivot=pivot, N=N, S=S, rule=rule)
+
+
+def exact_pose(motion: dict) -> dict:
+    """The same motion sampled at its exact poses: N sub-frames on N-1 segments (GLOBAL_INCLUSIVE
+    puts sub-frame k on the keyframe t = k/(N-1)), the segmentation-error reference of NEXT-3."""
+    m = dict(motion)
+    m["S"] = max(1, int(m["N"]) - 1)
+    m["rule"] = GLOBAL_INCLUSIVE
+    return m
 
 
 def static(N=1, S=1, rule=GLOBAL_INCLUSIVE):

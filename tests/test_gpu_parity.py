@@ -235,3 +235,19 @@ def test_full_size_sampled(name, npix):
     got2 = gpu_render(sc, G=G2)
     rdv, rdc = oracle.render_bwd(sc, Gp2, pixels=pix)
     assert rel_l2(got2["dv"], rdv) < TOL_GRAD and rel_l2(got2["dc"], rdc) < TOL_GRAD
+
+
+# ----------------------------------------------------------------- NEXT-3: parabolic motion, exact-pose reference
+
+def test_parabolic_motion_parity():
+    sc = scenes.make_c2().subset([0, 1])
+    sc.motion = scenes.motion_arrays([scenes.parabolic(N=40, S=8)] * 2)
+    r = check_parity(sc, ids_k=13)
+    print(r)
+
+
+def test_exact_pose_reference_parity():
+    sc = scenes.make_c3().subset([2])
+    sc.motion = scenes.motion_arrays([scenes.exact_pose(scenes.rotate((0, 1, 0), 6.283185307, N=30, S=1))])
+    r = check_parity(sc, ids_k=7)
+    print(r)

@@ -188,11 +188,14 @@ def _np_keyframes(sc, b):
         t = s / S
         if m["kind"][b] == 1:
             P = P0 + (t - 0.5) * m["vec"][b].astype(np.float64)
-        elif m["kind"][b] == 2:
+        elif m["kind"][b] in (2, 3):
             ax = m["vec"][b].astype(np.float64)
             rot = Rotation.from_rotvec(ax / np.linalg.norm(ax) * float(m["angle"][b]) * t)
             c = m["pivot"][b].astype(np.float64)
             P = rot.apply(P0 - c) + c
+            if m["kind"][b] == 3:                       # A36: T(t) = (s, -4 s^2 + 0.5, s), s = 0.5 - t
+                sp = 0.5 - t
+                P = P + np.array([sp, -4 * sp * sp + 0.5, sp])
         else:
             P = P0.copy()
         Q = (P - cam[0:3]) @ R.T
@@ -513,3 +516,57 @@ def test_pixel_list_mode_matches_full():
     a = oracle.render_bwd(sc, G)
     b = oracle.render_bwd(sc, Gp, pixels=pix)
     assert np.allclose(a[0], b[0], atol=1e-13) and np.allclose(a[1], b[1], atol=1e-13)
+
+
+# ----------------------------------------------------------------------------- NEXT-3 motions
+
+def test_parabolic_pose_midpoint():
+    """S:L82 / A35-A37: at t = 0.5 the parabolic composite is a rotation by pi/2 about y plus the
+    translation (0, 0.5, 0); keyframes match the independent scipy construction at every t = s/S."""
+    sc = scenes.random_mesh_scene(6, 81, motion=scenes.parabolic(N=5, S=4))
+    sc.cams[0, 0:3] = [0.3, 0.2, 4.0]
+    key, valid, Q = oracle.keyframes(sc, 0)
+    assert np.allclose(key, _np_keyframes(sc, 0), atol=1e-12)
+    P0 = sc.verts.astype(np.float64)
+    mid = np.stack([P0[:, 2], P0[:, 1] + 0.5, -P0[:, 0]], 1)     # R_y(pi/2) (x, y, z) = (z, y, -x)
+    R = _look_at(sc.cams[0, 0:3].astype(np.float64), [0, 0, 0], [0, 1, 0])
+    Qm = (mid - sc.cams[0, 0:3].astype(np.float64)) @ R.T
+    assert np.allclose(Q[2], Qm, atol=1e-6)       # float32 angle pi
+
+
+def test_exact_pose_reference_is_mean_of_static_renders():
+    """NEXT-3 reference: N sub-frames on N-1 segments sample the exact rigid poses, so the blurred
+    image equals the mean of N static renders of the mesh posed (by scipy) at t_k = k/(N-1)."""
+    from scipy.spatial.transform import Rotation
+    N = 5
+    sc = scenes.random_mesh_scene(10, 91, H=14, W=14,
+                                  motion=scenes.exact_pose(scenes.rotate((0.1, 1.0, 0.2), 2.5, N=N, S=1)))
+    blur = oracle.render_fwd(sc)["rgba"]
+    acc = np.zeros_like(blur)
+    ax = sc.motion["vec"][0].astype(np.float64)
+    for k in range(N):
+        rot = Rotation.from_rotvec(ax / np.linalg.norm(ax) * float(sc.motion["angle"][0]) * k / (N - 1))
+        st = scenes.random_mesh_scene(10, 91, H=14, W=14, motion=scenes.static(1))
+        st.verts = rot.apply(st.verts.astype(np.float64))
+        acc += oracle.render_fwd(st)["rgba"]
+    assert np.max(np.abs(blur - acc / N)) < 1e-9
+
+
+def test_segmentation_converges_to_exact_pose():
+    """Appendix 'Segmentation Analysis': more linear segments approach the
+    exact-pose render (monotone PSNR on a spinning mesh)."""
+    base = scenes.random_mesh_scene(30, 93, H=24, W=24, motion=scenes.rotate((0, 1, 0), 2 * math.pi, N=48, S=1))
+    ref = oracle.render_fwd(dataclasses_replace_motion(base, scenes.exact_pose(scenes.rotate((0, 1, 0), 2 * math.pi,
+                                                                                             N=48, S=1))))["rgba"]
+    psnr = []
+    for S in (3, 6, 12, 24):
+        img = oracle.render_fwd(dataclasses_replace_motion(base, scenes.rotate((0, 1, 0), 2 * math.pi, N=48,
+                                                                               S=S)))["rgba"]
+        mse = np.mean((img[..., :3] - ref[..., :3]) ** 2)
+        psnr.append(10 * np.log10(1.0 / max(mse, 1e-30)))
+    assert all(b > a for a, b in zip(psnr, psnr[1:])), psnr
+
+
+def dataclasses_replace_motion(sc, motion):
+    import dataclasses
+    return dataclasses.replace(sc, motion=scenes.motion_arrays([motion] * sc.B))
