@@ -110,6 +110,12 @@ typedef struct {
     void *raster_events[2];        /* host cudaEvent_t pair or NULLs: recorded on `stream` right
                                       before / after the raster kernel (K4 in fwd, K6 in bwd), for
                                       timing the dominant kernel inside a step */
+    int32_t solver;                /* barycentric solver (NEXT-2 ablation of P:L447-479):
+                                      0 = fast (default): Eq.8 with the per-segment coefficients,
+                                      1 = naive per-frame: lerp the keyframe vertices and set the
+                                          triangle up again at every sub-frame (same per-pixel work),
+                                      2 = naive per-pixel: re-solve w = F(tau)^-1 p (Eq.3) for every
+                                          (pixel, face, sub-frame) test (the SoftRas-style baseline) */
 } blur_config;
 
 /* Bytes of device workspace the render calls need for these arguments (0 + blur_last_error() on

@@ -45,7 +45,7 @@ class blur_camera(C.Structure):
 
 class blur_config(C.Structure):
     _fields_ = [("max_chunk", C.c_int32), ("flags", C.c_int32), ("bin_factor", C.c_float),
-                ("census", C.c_void_p), ("raster_events", C.c_void_p * 2)]
+                ("census", C.c_void_p), ("raster_events", C.c_void_p * 2), ("solver", C.c_int32)]
 
 
 def load():
@@ -137,10 +137,11 @@ def make_sub_range(sub_range):
     return a
 
 
-def make_config(max_chunk=0, flags=0, bin_factor=0.0, census=None, events=None):
+def make_config(max_chunk=0, flags=0, bin_factor=0.0, census=None, events=None, solver=0):
     """events: optional (torch.cuda.Event, torch.cuda.Event) recorded around the raster kernel."""
     cfg = blur_config(int(max_chunk), int(flags), float(bin_factor),
                       None if census is None else C.c_void_p(census.data_ptr()))
+    cfg.solver = int(solver)
     if events is not None:
         cfg.raster_events[0] = events[0].cuda_event
         cfg.raster_events[1] = events[1].cuda_event

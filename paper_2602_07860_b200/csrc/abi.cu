@@ -325,6 +325,8 @@ int prepare(const float *verts, int V, const int32_t *faces, int F, const float 
     if (ws_bytes < P.total)
         return fail(BLUR_ENOMEM, "workspace too small: need " + std::to_string(P.total) + " bytes");
     t = make_tables(P, ws);
+    t.solver = cfg ? cfg->solver : 0;
+    if (t.solver < 0 || t.solver > 2) return fail(BLUR_EINVAL, "solver must be 0, 1 or 2");
     if (!do_setup) return BLUR_OK;
     r = cuda_check(cudaMemsetAsync(t.status, 0, sizeof(int), st), "status clear");
     if (r) return r;

@@ -74,6 +74,7 @@ struct Tables {          // device pointers into the workspace
     float2 *dkey;        // screen-space keyframe gradients, indexed like key
     int NC, T, TX, TY;
     int B, V, F, H, W;
+    int solver;          // 0 fast (Eq.8 coefficients), 1 naive per-frame setup, 2 naive per-pixel solve
 };
 
 struct __align__(16) TauRec {    // per (face, sub-frame, tile) staged record, 64 B

@@ -184,6 +184,9 @@ __device__ int fallback_fill(const float4 *__restrict__ rseg, int F, float tau, 
 struct BinCtx {
     int *status;
     const float4 *rseg;   // records of (image, segment)
+    const float4 *key0;   // keyframes s and s+1 of the image (naive solvers, NEXT-2)
+    const float4 *key1;
+    const float4 *fcol;
     const int *ent;       // sorted bin entries (normal path)
     int n;                // bin length
     bool fb;              // fallback path
@@ -198,14 +201,81 @@ __device__ __forceinline__ int next_batch(const BinCtx &bc, int F, float tau, co
     return fallback_fill(bc.rseg, F, tau, tc, W, H, cap, fpos, sid, swsum);
 }
 
+// NEXT-2 ablation (the paper's per-frame baseline): instead of evaluating
+// the per-segment coefficients, lerp the three keyframe vertices to tau (Eq.5-6) and set the
+// triangle up from scratch for this sub-frame (edge functions = rows of adj F(tau), det F(tau)).
+// solver 1 ("naive per-frame") keeps the same per-pixel work as the fast path; solver 2 ("naive
+// per-pixel") additionally stores the lerped vertices so that every (pixel, face, sub-frame) test
+// re-solves w = F(tau)^-1 p (Eq.3) -- the SoftRas-style cost the paper accelerates.
+template <int MODE>
+__device__ __forceinline__ uint32_t stage_tau_naive(const BinCtx &bc, int f, float tau, const TileCtx &tc, int W,
+                                                    int H, TauRec &out, float4 *vout)
+{
+    const float4 q = __ldg(bc.fcol + 3 * (size_t)f + 2);
+    const int vid[3] = {__float_as_int(q.y), __float_as_int(q.z), __float_as_int(q.w)};
+    float X[3], Y[3], Z[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float4 a = __ldg(bc.key0 + vid[i]), b = __ldg(bc.key1 + vid[i]);
+        X[i] = __fsub_rn(__fmaf_rn(tau, __fsub_rn(b.x, a.x), a.x), tc.uc);     // tile-centred
+        Y[i] = __fsub_rn(__fmaf_rn(tau, __fsub_rn(b.y, a.y), a.y), tc.vc);
+        Z[i] = __fmaf_rn(tau, b.z - a.z, a.z);
+    }
+    const float D = __fsub_rn(__fmul_rn(__fsub_rn(X[1], X[0]), __fsub_rn(Y[2], Y[0])),
+                              __fmul_rn(__fsub_rn(Y[1], Y[0]), __fsub_rn(X[2], X[0])));
+    if (!(fabsf(D) > EPS_D)) return 0u;
+    const float xmn = fminf(fminf(X[0], X[1]), X[2]) + tc.uc - BBOX_PAD, xmx = fmaxf(fmaxf(X[0], X[1]), X[2]) + tc.uc + BBOX_PAD;
+    const float ymn = fminf(fminf(Y[0], Y[1]), Y[2]) + tc.vc - BBOX_PAD, ymx = fmaxf(fmaxf(Y[0], Y[1]), Y[2]) + tc.vc + BBOX_PAD;
+    int x0, x1, y0, y1;
+    if (!tile_pixels(xmn, xmx, ymn, ymx, W, H, tc, x0, x1, y0, y1)) return 0u;
+    const float sg = D < 0.f ? -1.f : 1.f;
+    const float invD = 1.0f / fabsf(D);
+    float A[3], B[3], G[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {   // edge opposite corner i, canonical direction (lower vertex id first)
+        const int j = (i + 1) % 3, l = (i + 2) % 3;
+        const bool fwd = vid[j] < vid[l];
+        const int a = fwd ? j : l, c = fwd ? l : j;
+        const float ex = __fsub_rn(X[c], X[a]), ey = __fsub_rn(Y[c], Y[a]);
+        const float g = __fsub_rn(__fmul_rn(X[a], ey), __fmul_rn(Y[a], ex));   // N at the tile centre
+        const float cs = (fwd ? 1.f : -1.f) * sg;
+        A[i] = -ey * cs;
+        B[i] = ex * cs;
+        G[i] = g * cs;
+    }
+    uint32_t fm = 0u;
+    for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
+        for (int wx = x0 >> 3; wx <= (x1 >> 3); ++wx) {
+            const int rx0 = max(x0, wx * 8), rx1 = min(x1, wx * 8 + 7);
+            const int ry0 = max(y0, wy * 4), ry1 = min(y1, wy * 4 + 3);
+            if (rect_reaches(A, B, G, rx0, rx1, ry0, ry1, tc)) fm |= 1u << (wy * 2 + wx);
+        }
+    if (!fm) return 0u;
+    out.a[0] = A[0]; out.a[1] = A[1]; out.a[2] = A[2];
+    out.b[0] = B[0]; out.b[1] = B[1]; out.b[2] = B[2];
+    out.g[0] = G[0]; out.g[1] = G[1]; out.g[2] = G[2];
+    const float dzb = Z[1] - Z[0], dzc = Z[2] - Z[0];
+    out.az = __fmaf_rn(A[1], dzb, A[2] * dzc) * invD;
+    out.bz = __fmaf_rn(B[1], dzb, B[2] * dzc) * invD;
+    out.cz = __fmaf_rn(__fmaf_rn(G[1], dzb, G[2] * dzc), invD, Z[0]);
+    out.invD = invD;
+    out.fid = f;
+    if (MODE == 2) {
+        vout[0] = make_float4(X[0], Y[0], Z[0], X[1]);
+        vout[1] = make_float4(Y[1], Z[1], X[2], Y[2]);
+        vout[2] = make_float4(Z[2], 0.f, 0.f, 0.f);
+    }
+    return fm;
+}
+
 // Stage faces [base, base+nb) of the bin (or sid[] in fallback mode) at the ng sub-frames
 // taus[0..ng): records rec[l*nb + j], masks wm[(l*NWARP + w)*nw + j/32].  Masks must be clear.
 // Work is spread over (face, sub-frame) pairs, face-major, so the lanes that share a face load its
 // record with broadcast loads.
-template <bool CENSUS>
+template <bool CENSUS, int MODE>
 __device__ __forceinline__ void stage_group(const BinCtx &bc, int nb, int base, const float *taus, int ng,
                                             const TileCtx &tc, int W, int H, int F, const int *sid, TauRec *rec,
-                                            uint32_t *wm, unsigned long long &nstage)
+                                            float4 *vtx, uint32_t *wm, unsigned long long &nstage)
 {
     const int nw = (nb + 31) >> 5;
     const int npair = nb * ng;
@@ -233,19 +303,24 @@ __device__ __forceinline__ void stage_group(const BinCtx &bc, int nb, int base, 
                              box_lerp(tau, b0.w, b1.w), W, H, tc, x0, x1, y0, y1))
                 continue;
         }
-        FaceRec fr;
-        load_rec(r, fr);
-        const uint32_t fm = stage_tau(fr, tau, tc, W, H, rec[l * nb + j]);
+        uint32_t fm;
+        if (MODE == 0) {
+            FaceRec fr;
+            load_rec(r, fr);
+            fm = stage_tau(fr, tau, tc, W, H, rec[l * nb + j]);
+        } else {
+            fm = stage_tau_naive<MODE>(bc, f, tau, tc, W, H, rec[l * nb + j], vtx + 3 * (l * nb + j));
+        }
         if (CENSUS) nstage += fm != 0u;
         const uint32_t bit = 0x80000000u >> (j & 31);          // bit-reversed: clz gives ascending slots
         for (uint32_t m = fm; m; m &= m - 1) atomicOr(wm + (l * NWARP + (__ffs(m) - 1)) * nw + (j >> 5), bit);
     }
 }
 
-template <bool CENSUS>
-__device__ __forceinline__ void vis_mask(const TauRec *rec, const uint32_t *wm, int nw, int ebase, float ul,
-                                         float vl, float &zbest, int &ebest, unsigned long long &ncov,
-                                         unsigned long long &ntest, bool count)
+template <bool CENSUS, int MODE>
+__device__ __forceinline__ void vis_mask(const TauRec *rec, const float4 *vtx, const uint32_t *wm, int nw,
+                                         int ebase, float ul, float vl, float &zbest, int &ebest,
+                                         unsigned long long &ncov, unsigned long long &ntest, bool count)
 {
     for (int wd = 0; wd < nw; ++wd) {
         uint32_t m = wm[wd];
@@ -254,13 +329,30 @@ __device__ __forceinline__ void vis_mask(const TauRec *rec, const uint32_t *wm, 
             const int k = __clz(m);
             m ^= 0x80000000u >> k;
             const int j = (wd << 5) + k;
-            const float4 *rp = reinterpret_cast<const float4 *>(rw + k);
-            const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
-            const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
-            const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
-            const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
-            const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
-            const bool cov = fminf(fminf(e0, e1), e2) >= 0.f;
+            bool cov;
+            float z;
+            if (MODE != 2) {
+                const float4 *rp = reinterpret_cast<const float4 *>(rw + k);
+                const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
+                const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
+                const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
+                const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
+                z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
+                cov = fminf(fminf(e0, e1), e2) >= 0.f;
+            } else {
+                // per-pixel textbook solve w = F(tau)^-1 p (Eq.3): sub-triangle areas over det F
+                const float4 a = vtx[3 * j], b = vtx[3 * j + 1], c = vtx[3 * j + 2];
+                const float dx0 = a.x - ul, dy0 = a.y - vl, dx1 = a.w - ul, dy1 = b.x - vl, dx2 = b.z - ul,
+                            dy2 = b.w - vl;
+                const float n0 = __fsub_rn(__fmul_rn(dx1, dy2), __fmul_rn(dx2, dy1));
+                const float n1 = __fsub_rn(__fmul_rn(dx2, dy0), __fmul_rn(dx0, dy2));
+                const float n2 = __fsub_rn(__fmul_rn(dx0, dy1), __fmul_rn(dx1, dy0));
+                const float det = n0 + n1 + n2;
+                const float id = 1.0f / det;
+                const float w0 = n0 * id, w1 = n1 * id, w2 = n2 * id;
+                z = w0 * a.z + w1 * b.y + w2 * c.x;
+                cov = fminf(fminf(w0, w1), w2) >= 0.f && det != 0.f;
+            }
             if (CENSUS && count) { ncov += cov; ntest += 1; }
             if (cov && z < zbest) { zbest = z; ebest = ebase + j; }
         }
@@ -305,20 +397,22 @@ __device__ __forceinline__ void clear_words(uint32_t *w, int n)
     for (int i = threadIdx.x; i < n; i += NT) w[i] = 0u;
 }
 
+template <int MODE>
 struct FwdSmem {
     TauRec rec[SREC_F];
+    float4 vtx[MODE == 2 ? 3 * SREC_F : 1];   // solver 2: lerped vertices per staged record
     uint32_t wm[NWARP * (SREC_F / 32 + GMAX_F)];
     int sid[SREC_F];
     float taus[GMAX_F];
     int wsum[NWARP];
 };
 
-template <bool CENSUS>
+template <bool CENSUS, int MODE>
 __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restrict__ out, int *__restrict__ ids,
                                                        int ids_k, unsigned long long *census)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    FwdSmem &S = *reinterpret_cast<FwdSmem *>(smem_raw);
+    FwdSmem<MODE> &S = *reinterpret_cast<FwdSmem<MODE> *>(smem_raw);
     const int b = blockIdx.y, tile = blockIdx.x;
     const ImgInfo &im = t.imgs[b];
     const int N = im.N, c_begin = im.chunk_begin, c_end = im.chunk_end, sched_off = im.sched_off;
@@ -347,6 +441,9 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
         BinCtx bc;
         bc.status = t.status;
         bc.rseg = t.rec + (size_t)(rec_off + (long long)ch.s * t.F) * REC_F4;
+        bc.key0 = t.key + im.key_off + (size_t)ch.s * t.V;
+        bc.key1 = bc.key0 + t.V;
+        bc.fcol = t.fcol;
         bc.ent = t.entries + o;
         bc.n = n;
         bc.fb = n > SORTCAP || (long long)o + n > t.cap;
@@ -358,14 +455,14 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
                 clear_words(S.wm, ng * NWARP * nw);
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();
-                stage_group<CENSUS>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.wm, nstage);
+                stage_group<CENSUS, MODE>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, nstage);
                 __syncthreads();
                 for (int l = 0; l < ng; ++l) {
                     float zbest = __int_as_float(0x7f800000);
                     int ebest = -1;
                     const TauRec *rl = S.rec + l * n;
-                    vis_mask<CENSUS>(rl, S.wm + (l * NWARP + warp) * nw, nw, 0, ul, vl, zbest, ebest, ncov, ntest,
-                                     inimg);
+                    vis_mask<CENSUS, MODE>(rl, S.vtx + 3 * l * n, S.wm + (l * NWARP + warp) * nw, nw, 0, ul, vl,
+                                           zbest, ebest, ncov, ntest, inimg);
                     int fid = -1;
                     if (ebest >= 0) {
                         float pr, pg, pb;
@@ -394,9 +491,9 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
                     const int nw = (nb + 31) >> 5;
                     clear_words(S.wm, NWARP * nw);
                     __syncthreads();
-                    stage_group<CENSUS>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.wm, nstage);
+                    stage_group<CENSUS, MODE>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, nstage);
                     __syncthreads();
-                    vis_mask<CENSUS>(S.rec, S.wm + warp * nw, nw, base, ul, vl, zbest, ebest, ncov, ntest, inimg);
+                    vis_mask<CENSUS, MODE>(S.rec, S.vtx, S.wm + warp * nw, nw, base, ul, vl, zbest, ebest, ncov, ntest, inimg);
                     if (ebest >= base) {   // winner changed in this batch: shade now (Eq.9)
                         shade(S.rec[ebest - base], t.fcol, ul, vl, pr, pg, pb);
                         has = true;
@@ -437,8 +534,10 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
 // evaluates the closed form.  Face gradients accumulate in registers over the chunk's sub-frames
 // (slot == thread) and are flushed with one vector RED per (vertex, keyframe) at the chunk's end.
 
+template <int MODE>
 struct BwdSmem {
     TauRec rec[SREC_B];
+    float4 vtx[MODE == 2 ? 3 * SREC_B : 1];
     uint32_t wm[NWARP * (SREC_B / 32 + GMAX_B)];
     int sid[SREC_B];
     int win[GMAX_B][TW * TH]; // winning slot per (sub-frame of the group, pixel)
@@ -453,7 +552,8 @@ struct BwdSmem {
 };
 
 // block-wide exclusive scan of cnt[0..nb) (nb <= 2 NT) into off[]; returns the total
-__device__ __forceinline__ int scan_counts(BwdSmem &S, int nb)
+template <class Sm>
+__device__ __forceinline__ int scan_counts(Sm &S, int nb)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int j0 = 2 * tid;
@@ -547,7 +647,8 @@ __device__ __forceinline__ void flush(const Tables &t, const ImgInfo &im, int s,
 // Reduce the moments of the won pixels whose winner lies in the staged batch [base, base+nb)
 // (records rec[0..nb)) and give each face with winners its closed-form gradient: persistent slots
 // (slot == thread) accumulate in registers across the chunk, the others flush immediately.
-__device__ __forceinline__ void bwd_gather(BwdSmem &S, const TauRec *rec, const Tables &t, const ImgInfo &im, int s,
+template <class Sm>
+__device__ __forceinline__ void bwd_gather(Sm &S, const TauRec *rec, const Tables &t, const ImgInfo &im, int s,
                                            float tau, int base, int nb, bool persist_ok, int ebest, int myp,
                                            const TileCtx &tc, FaceAcc &acc, float *dC)
 {
@@ -630,10 +731,11 @@ __device__ __forceinline__ void bwd_gather(BwdSmem &S, const TauRec *rec, const 
     __syncthreads();
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__restrict__ grad, float *__restrict__ dC)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    BwdSmem &S = *reinterpret_cast<BwdSmem *>(smem_raw);
+    BwdSmem<MODE> &S = *reinterpret_cast<BwdSmem<MODE> *>(smem_raw);
     const int b = blockIdx.y, tile = blockIdx.x;
     const ImgInfo &im = t.imgs[b];
     const int N = im.N, c_begin = im.chunk_begin, c_end = im.chunk_end, sched_off = im.sched_off;
@@ -668,6 +770,9 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
         BinCtx bc;
         bc.status = t.status;
         bc.rseg = t.rec + (size_t)(rec_off + (long long)ch.s * t.F) * REC_F4;
+        bc.key0 = t.key + im.key_off + (size_t)ch.s * t.V;
+        bc.key1 = bc.key0 + t.V;
+        bc.fcol = t.fcol;
         bc.ent = t.entries + o;
         bc.n = n;
         bc.fb = n > SORTCAP || (long long)o + n > t.cap;
@@ -680,13 +785,13 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
                 clear_words(S.wm, ng * NWARP * nw);
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();
-                stage_group<false>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.wm, d2);
+                stage_group<false, MODE>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, d2);
                 __syncthreads();
                 for (int l = 0; l < ng; ++l) {       // visibility for the group (no barriers)
                     float zbest = __int_as_float(0x7f800000);
                     int ebest = -1;
-                    vis_mask<false>(S.rec + l * n, S.wm + (l * NWARP + warp) * nw, nw, 0, ul, vl, zbest, ebest, d0,
-                                    d1, false);
+                    vis_mask<false, MODE>(S.rec + l * n, S.vtx + 3 * l * n, S.wm + (l * NWARP + warp) * nw, nw, 0, ul,
+                                          vl, zbest, ebest, d0, d1, false);
                     S.win[l][myp] = inimg ? ebest : -1;
                 }
                 __syncthreads();
@@ -706,9 +811,9 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
                     const int nw = (nb + 31) >> 5;
                     clear_words(S.wm, NWARP * nw);
                     __syncthreads();
-                    stage_group<false>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.wm, d2);
+                    stage_group<false, MODE>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, d2);
                     __syncthreads();
-                    vis_mask<false>(S.rec, S.wm + warp * nw, nw, base, ul, vl, zbest, ebest, d0, d1, false);
+                    vis_mask<false, MODE>(S.rec, S.vtx, S.wm + warp * nw, nw, base, ul, vl, zbest, ebest, d0, d1, false);
                     base += nb;
                     __syncthreads();
                 }
@@ -721,7 +826,7 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
                     const int nw = (nb + 31) >> 5;
                     clear_words(S.wm, NWARP * nw);
                     __syncthreads();
-                    stage_group<false>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.wm, d2);
+                    stage_group<false, MODE>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, d2);
                     __syncthreads();
                     bwd_gather(S, S.rec, t, im, ch.s, tau, base, nb, false, ebest, myp, tc, acc, dC);
                     base += nb;
@@ -739,34 +844,51 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
     }
 }
 
+template <bool CENSUS, int MODE>
+static cudaError_t launch_fwd_t(const Tables &t, float *out, int *ids, int ids_k, unsigned long long *census,
+                                cudaStream_t st)
+{
+    dim3 grid(t.T, t.B);
+    const int smem = (int)sizeof(FwdSmem<MODE>);
+    cudaError_t e = cudaFuncSetAttribute(k4_raster_fwd<CENSUS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k4_raster_fwd<CENSUS, MODE><<<grid, NT, smem, st>>>(t, out, ids, ids_k, census);
+    return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t launch_bwd_t(const Tables &t, const float *grad, float *dC, cudaStream_t st)
+{
+    dim3 grid(t.T, t.B);
+    const int smem = (int)sizeof(BwdSmem<MODE>);
+    cudaError_t e = cudaFuncSetAttribute(k6_raster_bwd<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k6_raster_bwd<MODE><<<grid, NT, smem, st>>>(t, grad, dC);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_raster_fwd(const Tables &t, float *out, int *ids, int ids_k, unsigned long long *census,
                               cudaStream_t st)
 {
     if (t.B == 0 || t.T == 0) return cudaSuccess;
-    dim3 grid(t.T, t.B);
-    const int smem = (int)sizeof(FwdSmem);
-    cudaError_t e;
-    if (census) {
-        e = cudaFuncSetAttribute(k4_raster_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        k4_raster_fwd<true><<<grid, NT, smem, st>>>(t, out, ids, ids_k, census);
-    } else {
-        e = cudaFuncSetAttribute(k4_raster_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        k4_raster_fwd<false><<<grid, NT, smem, st>>>(t, out, ids, ids_k, nullptr);
+    switch (t.solver * 2 + (census ? 1 : 0)) {
+    case 0: return launch_fwd_t<false, 0>(t, out, ids, ids_k, nullptr, st);
+    case 1: return launch_fwd_t<true, 0>(t, out, ids, ids_k, census, st);
+    case 2: return launch_fwd_t<false, 1>(t, out, ids, ids_k, nullptr, st);
+    case 3: return launch_fwd_t<true, 1>(t, out, ids, ids_k, census, st);
+    case 4: return launch_fwd_t<false, 2>(t, out, ids, ids_k, nullptr, st);
+    default: return launch_fwd_t<true, 2>(t, out, ids, ids_k, census, st);
     }
-    return cudaGetLastError();
 }
 
 cudaError_t launch_raster_bwd(const Tables &t, const float *grad, float *dC, cudaStream_t st)
 {
     if (t.B == 0 || t.T == 0 || t.F == 0) return cudaSuccess;
-    dim3 grid(t.T, t.B);
-    const int smem = (int)sizeof(BwdSmem);
-    cudaError_t e = cudaFuncSetAttribute(k6_raster_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    k6_raster_bwd<<<grid, NT, smem, st>>>(t, grad, dC);
-    return cudaGetLastError();
+    switch (t.solver) {
+    case 0: return launch_bwd_t<0>(t, grad, dC, st);
+    case 1: return launch_bwd_t<1>(t, grad, dC, st);
+    default: return launch_bwd_t<2>(t, grad, dC, st);
+    }
 }
 
 }  // namespace br

@@ -23,7 +23,7 @@ class BlurRenderer:
     """
 
     def __init__(self, faces, motion: dict, cams, H: int, W: int, V: int, device="cuda",
-                 sub_range=None, max_chunk: int = 0, bin_factor: float = 0.0):
+                 sub_range=None, max_chunk: int = 0, bin_factor: float = 0.0, solver: int = 0):
         _lib.load()
         self.device = torch.device(device)
         self.faces = torch.as_tensor(np.asarray(faces.cpu() if torch.is_tensor(faces) else faces),
@@ -39,6 +39,7 @@ class BlurRenderer:
         self._sub = _lib.make_sub_range(sub_range)
         self.max_chunk = int(max_chunk)
         self.bin_factor = float(bin_factor)
+        self.solver = int(solver)
         cfg = _lib.make_config(self.max_chunk, 0, self.bin_factor)
         self.ws_bytes = _lib.blur_workspace_bytes(self.V, self.F, self.B, self.H, self.W, self._motions,
                                                   self._cams, self._sub, cfg)
@@ -51,7 +52,7 @@ class BlurRenderer:
                 stream=None, events=None) -> torch.Tensor:
         if out is None:
             out = torch.empty((self.B, self.H, self.W, 4), dtype=torch.float32, device=self.device)
-        cfg = _lib.make_config(self.max_chunk, 0, self.bin_factor, census, events)
+        cfg = _lib.make_config(self.max_chunk, 0, self.bin_factor, census, events, self.solver)
         _lib.blur_render_fwd(verts, self.faces, colors, self._motions, self._cams, self.B, self.H, self.W, out,
                              self.ws, sub_range=self._sub, ids=ids, ids_subframe=ids_subframe, cfg=cfg,
                              stream=stream)
@@ -65,7 +66,7 @@ class BlurRenderer:
         if grad_colors is None:
             grad_colors = torch.empty((self.V, 3), dtype=torch.float32, device=self.device)
         cfg = _lib.make_config(self.max_chunk, _lib.BLUR_REUSE_SETUP if reuse_setup else 0, self.bin_factor,
-                               events=events)
+                               events=events, solver=self.solver)
         _lib.blur_render_bwd(verts, self.faces, colors, self._motions, self._cams, self.B, self.H, self.W,
                              grad_rgba.contiguous(), grad_verts, grad_colors, self.ws, sub_range=self._sub, cfg=cfg,
                              stream=stream)

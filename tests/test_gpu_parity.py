@@ -251,3 +251,23 @@ def test_exact_pose_reference_parity():
     sc.motion = scenes.motion_arrays([scenes.exact_pose(scenes.rotate((0, 1, 0), 6.283185307, N=30, S=1))])
     r = check_parity(sc, ids_k=7)
     print(r)
+
+
+# ----------------------------------------------------------------- NEXT-2: naive solvers (ablation baselines)
+
+@pytest.mark.parametrize("solver", [1, 2])
+def test_naive_solvers_match_oracle(solver):
+    """The ablation baselines compute the same images/gradients (per-frame set-up, per-pixel solve)."""
+    torch = _torch()
+    from paper_2602_07860_b200 import BlurRenderer
+    sc = scenes.make_c2().subset([0])
+    ref = oracle.render_fwd(sc, eps_amb=1e-6)
+    r = BlurRenderer(sc.faces, sc.motion, sc.cams, sc.H, sc.W, sc.V, solver=solver)
+    out = r.forward(torch.tensor(sc.verts, device="cuda"), torch.tensor(sc.colors, device="cuda")).cpu().numpy()
+    ok = ~ref["amb_img"]
+    assert np.abs(out - ref["rgba"])[ok].max() < TOL_IMG
+    G = 2.0 * (ref["rgba"] - sc.target) / ref["rgba"].size * (~ref["amb_win"])[..., None]
+    dv, dc = r.backward(torch.tensor(sc.verts, device="cuda"), torch.tensor(sc.colors, device="cuda"),
+                        torch.tensor(G, dtype=torch.float32, device="cuda"), reuse_setup=True)
+    rdv, rdc = oracle.render_bwd(sc, G)
+    assert rel_l2(dv.cpu().numpy(), rdv) < TOL_GRAD and rel_l2(dc.cpu().numpy(), rdc) < TOL_GRAD
