@@ -1,5 +1,6 @@
 // abi.cu -- the C ABI of libblurrast (include/blurrast.h): argument validation, the host-side
 // schedule/pose/chunk plan (L0), workspace carving and the launch sequence K1..K7.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -71,7 +72,7 @@ void rodrigues(const double ax_in[3], double th, double R[9])
 }
 
 struct Plan {
-    int B = 0, V = 0, F = 0, H = 0, W = 0, TX = 0, TY = 0, T = 0, NC = 0, maxS = 1;
+    int B = 0, V = 0, F = 0, H = 0, W = 0, TX = 0, TY = 0, T = 0, NC = 0, maxS = 1, splits = 1;
     std::vector<ImgInfo> imgs;
     std::vector<Chunk> chunks;
     std::vector<int> sched_s;
@@ -80,7 +81,8 @@ struct Plan {
     long long n_key = 0, n_rec = 0, cap = 0;
     size_t nbins = 0;
     size_t o_status = 0, o_imgs = 0, o_chunks = 0, o_ss = 0, o_st = 0, o_poses = 0, o_tables_end = 0;
-    size_t o_key = 0, o_rec = 0, o_fcol = 0, o_cnt = 0, o_off = 0, o_bsum = 0, o_ent = 0, o_dkey = 0, total = 0;
+    size_t o_key = 0, o_rec = 0, o_fcol = 0, o_cnt = 0, o_off = 0, o_bsum = 0, o_ent = 0, o_dkey = 0, o_part = 0;
+    size_t total = 0;
 };
 
 int auto_chunk(const blur_motion &m, const blur_camera &c, int H, int W)
@@ -212,6 +214,20 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
         im.chunk_end = (int)P.chunks.size();
     }
     P.NC = (int)P.chunks.size();
+    // small launches (few tiles x images) split each tile's sub-frame chunks over several CTAs so
+    // that the grid fills the 148 SMs; partial images are reduced in a fixed order (deterministic)
+    {
+        int maxc = 1;
+        for (const ImgInfo &im : P.imgs) maxc = std::max(maxc, im.chunk_end - im.chunk_begin);
+        const long long ctas = (long long)P.T * B, target = 148LL * 8;
+        P.splits = 1;
+        if (ctas > 0 && ctas < target) {
+            long long sp = (target + ctas - 1) / ctas;
+            if (sp > maxc) sp = maxc;
+            if (sp > 32) sp = 32;
+            P.splits = (int)std::max(1LL, sp);
+        }
+    }
     P.n_key = key_off;
     P.n_rec = rec_off;
     P.nbins = (size_t)P.NC * P.T;
@@ -237,6 +253,7 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
     P.o_bsum = o; o = align256(o + 4 * ((P.nbins + 1023) / 1024 + 1));
     P.o_ent = o; o = align256(o + 4 * (size_t)P.cap);
     P.o_dkey = o; o = align256(o + 8 * (size_t)P.n_key);
+    P.o_part = o; o = align256(o + (P.splits > 1 ? 16 * (size_t)P.splits * B * H * W : 0));
     P.total = o;
     return BLUR_OK;
 }
@@ -262,6 +279,8 @@ Tables make_tables(const Plan &P, void *ws)
     t.cap = P.cap;
     t.dkey = (float2 *)(w + P.o_dkey);
     t.NC = P.NC; t.T = P.T; t.TX = P.TX; t.TY = P.TY;
+    t.splits = P.splits;
+    t.part = (float4 *)(w + P.o_part);
     t.B = P.B; t.V = P.V; t.F = P.F; t.H = P.H; t.W = P.W;
     return t;
 }
@@ -371,6 +390,10 @@ int blur_render_fwd(const float *verts, int V, const int32_t *faces, int F, cons
     if (cfg && cfg->raster_events[0]) cudaEventRecord((cudaEvent_t)cfg->raster_events[0], st);
     r = cuda_check(launch_raster_fwd(t, out_rgba, ids, ids_subframe, cfg ? cfg->census : nullptr, st), "raster fwd");
     if (r) return r;
+    if (P.splits > 1) {
+        r = cuda_check(launch_split_reduce(t, out_rgba, st), "split reduce");
+        if (r) return r;
+    }
     if (cfg && cfg->raster_events[1]) cudaEventRecord((cudaEvent_t)cfg->raster_events[1], st);
     if (check_env()) return sync_status(ws, P, st);
     return BLUR_OK;

@@ -75,6 +75,8 @@ struct Tables {          // device pointers into the workspace
     int NC, T, TX, TY;
     int B, V, F, H, W;
     int solver;          // 0 fast (Eq.8 coefficients), 1 naive per-frame setup, 2 naive per-pixel solve
+    int splits;          // CTAs sharing one (image, tile) by sub-frame chunks (small launches)
+    float4 *part;        // splits > 1: per-split partial images [splits][B*H*W]
 };
 
 struct __align__(16) TauRec {    // per (face, sub-frame, tile) staged record, 64 B
@@ -115,6 +117,7 @@ cudaError_t launch_raster_fwd(const Tables &t, float *out, int *ids, int ids_k,
 cudaError_t launch_raster_bwd(const Tables &t, const float *grad_rgba, float *grad_colors,
                               cudaStream_t st);
 cudaError_t launch_vertex_chain(const Tables &t, float *grad_verts, cudaStream_t st);
+cudaError_t launch_split_reduce(const Tables &t, float *out, cudaStream_t st);
 cudaError_t launch_l2(const float *out, const float *tgt, long long n, long long n_norm, float *loss,
                       float *grad, cudaStream_t st);
 cudaError_t launch_ffma_probe(int ctas, int iters, float *sink, cudaStream_t st);

@@ -18,6 +18,7 @@
 // Bins that overflowed (or exceed SORTCAP) are regenerated exactly by scanning all faces in index
 // order (slow path); bins longer than the shared-memory record capacity are processed per
 // sub-frame in several batches.
+#include <algorithm>
 #include <cstdio>
 
 #include "internal.cuh"
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
     float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
     unsigned long long ncov = 0, ntest = 0, nshade = 0, nstage = 0;
 
-    for (int c = c_begin; c < c_end; ++c) {
+    for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
         const Chunk ch = t.chunks[c];
         const size_t bi = (size_t)c * t.T + tile;
         const int o = t.off[bi];
@@ -509,7 +510,9 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
     }
     if (inimg) {
         const float inv = 1.0f / (float)N;
-        reinterpret_cast<float4 *>(out)[pix] = make_float4(ar * inv, ag * inv, ab * inv, aa * inv);
+        const float4 v = make_float4(ar * inv, ag * inv, ab * inv, aa * inv);
+        if (t.splits == 1) reinterpret_cast<float4 *>(out)[pix] = v;
+        else t.part[(size_t)blockIdx.z * ((size_t)t.B * t.H * t.W) + pix] = v;
     }
     if (CENSUS) {
         atomicAdd(census + 0, ncov);
@@ -761,7 +764,7 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
     __syncthreads();
     unsigned long long d0 = 0, d1 = 0, d2 = 0;
 
-    for (int c = c_begin; c < c_end; ++c) {
+    for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
         const Chunk ch = t.chunks[c];
         const size_t bi = (size_t)c * t.T + tile;
         const int o = t.off[bi];
@@ -848,7 +851,7 @@ template <bool CENSUS, int MODE>
 static cudaError_t launch_fwd_t(const Tables &t, float *out, int *ids, int ids_k, unsigned long long *census,
                                 cudaStream_t st)
 {
-    dim3 grid(t.T, t.B);
+    dim3 grid(t.T, t.B, t.splits);
     const int smem = (int)sizeof(FwdSmem<MODE>);
     cudaError_t e = cudaFuncSetAttribute(k4_raster_fwd<CENSUS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
@@ -859,11 +862,34 @@ static cudaError_t launch_fwd_t(const Tables &t, float *out, int *ids, int ids_k
 template <int MODE>
 static cudaError_t launch_bwd_t(const Tables &t, const float *grad, float *dC, cudaStream_t st)
 {
-    dim3 grid(t.T, t.B);
+    dim3 grid(t.T, t.B, t.splits);
     const int smem = (int)sizeof(BwdSmem<MODE>);
     cudaError_t e = cudaFuncSetAttribute(k6_raster_bwd<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     k6_raster_bwd<MODE><<<grid, NT, smem, st>>>(t, grad, dC);
+    return cudaGetLastError();
+}
+
+// out = sum over splits of the partial images, in split order (deterministic)
+__global__ void __launch_bounds__(256) k_split_reduce(const float4 *__restrict__ part, float4 *__restrict__ out,
+                                                      size_t n, int splits)
+{
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        float4 a = part[i];
+        for (int z = 1; z < splits; ++z) {
+            const float4 b = part[(size_t)z * n + i];
+            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+        }
+        out[i] = a;
+    }
+}
+
+cudaError_t launch_split_reduce(const Tables &t, float *out, cudaStream_t st)
+{
+    const size_t n = (size_t)t.B * t.H * t.W;
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 16);
+    k_split_reduce<<<blocks, 256, 0, st>>>(t.part, reinterpret_cast<float4 *>(out), n, t.splits);
     return cudaGetLastError();
 }
 

@@ -96,11 +96,14 @@ def test_c4_two_views():
 
 @pytest.mark.parametrize("G", [1, 3, 16])
 def test_chunk_length_invariance(G):
-    """The per-sub-frame result does not depend on the bin chunk length G (bit-identical)."""
+    """The per-sub-frame result does not depend on the bin chunk length G: ID maps bit-identical;
+    images equal up to the order of the fp32 sub-frame sum (small launches split the sub-frames
+    over several CTAs, see K4)."""
     sc = scenes.make_c2().subset([0, 2])
     a = gpu_render(sc, ids_k=5, max_chunk=G)
     b = gpu_render(sc, ids_k=5, max_chunk=8)
-    assert np.array_equal(a["rgba"], b["rgba"]) and np.array_equal(a["ids"], b["ids"])
+    assert np.array_equal(a["ids"], b["ids"])
+    assert np.abs(a["rgba"] - b["rgba"]).max() < 1e-6
 
 
 def test_overflow_fallback_exact():
@@ -110,7 +113,7 @@ def test_overflow_fallback_exact():
     a = gpu_render(sc, ids_k=7, G=G)
     b = gpu_render(sc, ids_k=7, bin_factor=1e-9, G=G)
     assert b["status"] & 4                     # BLUR_ST_EOVERFLOW reported
-    assert np.array_equal(a["rgba"], b["rgba"]) and np.array_equal(a["ids"], b["ids"])
+    assert np.array_equal(a["ids"], b["ids"]) and np.abs(a["rgba"] - b["rgba"]).max() < 1e-6
     assert rel_l2(b["dv"], a["dv"]) < 1e-5 and rel_l2(b["dc"], a["dc"]) < 1e-5
 
 
