@@ -103,7 +103,8 @@ typedef struct {
 typedef struct {
     int32_t max_chunk;             /* G: max sub-frames sharing one tile bin (0 = automatic) */
     int32_t flags;                 /* BLUR_REUSE_SETUP */
-    float bin_factor;              /* bin-entry capacity per (chunk, face) (0 = default 3.0) */
+    float bin_factor;              /* bin-entry capacity per (chunk, face) (0 = default 3.0); see
+                                      blur_read_bins for sizing it to the geometry */
     unsigned long long *census;    /* device u64[4] or NULL: fwd adds [covered (pixel,face,subframe)
                                       pairs, covered (pixel,subframe), candidate pair tests,
                                       staged (face,subframe,tile) records] */

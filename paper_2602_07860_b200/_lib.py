@@ -24,7 +24,7 @@ STATUS_NAMES = {0: "BLUR_OK", 1: "BLUR_EINVAL", 2: "BLUR_EBEHIND", 3: "BLUR_ENOM
                 5: "BLUR_EOVERFLOW"}
 
 EXPORTED = ["blur_workspace_bytes", "blur_render_fwd", "blur_render_bwd", "blur_l2_loss_grad",
-            "blur_read_status", "blur_ffma_probe", "blur_last_error", "blur_abi_version"]
+            "blur_read_status", "blur_read_bins", "blur_ffma_probe", "blur_last_error", "blur_abi_version"]
 
 
 class BlurError(RuntimeError):
@@ -64,6 +64,7 @@ def load():
         lib.blur_render_bwd.argtypes = [P, I, P, I, P, P, P, I, I, I, P, P, P, P, P, P, SZ, P]
         lib.blur_l2_loss_grad.argtypes = [P, P, C.c_int64, C.c_int64, P, P, P]
         lib.blur_read_status.argtypes = [P, P, P]
+        lib.blur_read_bins.argtypes = [P, P, P, P]
         lib.blur_ffma_probe.argtypes = [I, I, P, P, P]
         lib.blur_last_error.restype = C.c_char_p
         lib.blur_abi_version.restype = I
@@ -202,6 +203,14 @@ def blur_read_status(ws, stream=None) -> int:
     st = C.c_int32(0)
     _check(load().blur_read_status(_dev(ws, torch.uint8, "ws"), _stream(stream), C.byref(st)))
     return int(st.value)
+
+
+def blur_read_bins(ws, stream=None):
+    """(entries needed by the last binning, entry capacity of the workspace); synchronises."""
+    import torch
+    need, cap = C.c_longlong(0), C.c_longlong(0)
+    _check(load().blur_read_bins(_dev(ws, torch.uint8, "ws"), _stream(stream), C.byref(need), C.byref(cap)))
+    return int(need.value), int(cap.value)
 
 
 def blur_ffma_probe(ctas, iters, sink, stream=None) -> float:

@@ -102,9 +102,12 @@ int auto_chunk(const blur_motion &m, const blur_camera &c, int H, int W)
         world = std::fabs((double)m.angle) + 2.0;
     const double disp = world * ndc_per_world * px_per_ndc / (N - 1);
     if (disp <= 1e-6) return 16;
+    // chunk ~ one tile of motion; at least 2 sub-frames unless the motion exceeds 1.5 tiles per
+    // sub-frame (then per-sub-frame bins); at most 8 (rule fitted on C2-C5, profiles/r1_summary.md)
     int g = (int)std::floor(TW / disp);
-    if (g < 2) g = 2;
-    if (g > 16) g = 16;
+    if (disp <= 1.5 * TW && g < 2) g = 2;
+    if (g < 1) g = 1;
+    if (g > 8) g = 8;
     return g;
 }
 
@@ -233,8 +236,8 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
     P.nbins = (size_t)P.NC * P.T;
     if (P.nbins > (size_t)0x7fffffff) return fail(BLUR_EINVAL, "too many (chunk, tile) bins");
     const double factor = (cfg && cfg->bin_factor > 0.f) ? cfg->bin_factor : 3.0;
-    double cap = factor * (double)P.NC * (double)F + 1024.0;
-    if (cap > 2.0e9) cap = 2.0e9;
+    double cap = factor * (double)P.NC * (double)F + 16.0 * (double)P.T;
+    if (cap > 6.0e9) cap = 6.0e9;     // beyond this, overflowing tiles take the exact fallback path
     P.cap = (long long)cap;
     // workspace layout
     size_t o = 0;
@@ -249,8 +252,8 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
     P.o_rec = o; o = align256(o + 16 * REC_F4 * (size_t)P.n_rec);
     P.o_fcol = o; o = align256(o + 48 * (size_t)F);
     P.o_cnt = o; o = align256(o + 4 * P.nbins);
-    P.o_off = o; o = align256(o + 4 * (P.nbins + 1));
-    P.o_bsum = o; o = align256(o + 4 * ((P.nbins + 1023) / 1024 + 1));
+    P.o_off = o; o = align256(o + 8 * (P.nbins + 1));
+    P.o_bsum = o; o = align256(o + 8 * ((P.nbins + 1023) / 1024 + 1));
     P.o_ent = o; o = align256(o + 4 * (size_t)P.cap);
     P.o_dkey = o; o = align256(o + 8 * (size_t)P.n_key);
     P.o_part = o; o = align256(o + (P.splits > 1 ? 16 * (size_t)P.splits * B * H * W : 0));
@@ -264,6 +267,7 @@ Tables make_tables(const Plan &P, void *ws)
     Tables t;
     std::memset(&t, 0, sizeof(t));
     t.status = (int *)(w + P.o_status);
+    t.binstat = (long long *)(w + P.o_status + 8);
     t.imgs = (const ImgInfo *)(w + P.o_imgs);
     t.chunks = (const Chunk *)(w + P.o_chunks);
     t.sched_s = (const int *)(w + P.o_ss);
@@ -273,8 +277,8 @@ Tables make_tables(const Plan &P, void *ws)
     t.rec = (float4 *)(w + P.o_rec);
     t.fcol = (float4 *)(w + P.o_fcol);
     t.cnt = (int *)(w + P.o_cnt);
-    t.off = (int *)(w + P.o_off);
-    t.bsum = (int *)(w + P.o_bsum);
+    t.off = (long long *)(w + P.o_off);
+    t.bsum = (long long *)(w + P.o_bsum);
     t.entries = (int *)(w + P.o_ent);
     t.cap = P.cap;
     t.dkey = (float2 *)(w + P.o_dkey);
@@ -455,6 +459,21 @@ int blur_read_status(void *ws, blur_stream_t stream, int32_t *status_out)
     if (r) return r;
     *status_out = h;
     return cuda_check(cudaMemsetAsync(ws, 0, sizeof(int), st), "status clear");
+}
+
+int blur_read_bins(void *ws, blur_stream_t stream, long long *needed, long long *capacity)
+{
+    g_err.clear();
+    if (!ws || !needed || !capacity) return fail(BLUR_EINVAL, "NULL pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    long long h[2] = {0, 0};
+    int r = cuda_check(cudaMemcpyAsync(h, (char *)ws + 8, sizeof(h), cudaMemcpyDeviceToHost, st), "bins read");
+    if (r) return r;
+    r = cuda_check(cudaStreamSynchronize(st), "stream sync");
+    if (r) return r;
+    *needed = h[0];
+    *capacity = h[1];
+    return BLUR_OK;
 }
 
 int blur_ffma_probe(int ctas, int iters, float *sink, double *flops, blur_stream_t stream)

@@ -58,6 +58,7 @@ struct Chunk {           // consecutive sub-frames of one image inside one segme
 
 struct Tables {          // device pointers into the workspace
     int *status;
+    long long *binstat;  // [0] bin entries the last binning needed, [1] entry capacity
     const ImgInfo *imgs;
     const Chunk *chunks;
     const int *sched_s;
@@ -67,8 +68,8 @@ struct Tables {          // device pointers into the workspace
     float4 *rec;         // coefficient records
     float4 *fcol;        // per face: 3 x float4 = c0.rgb c1.rgb c2.rgb vid0 vid1 vid2 (int bits)
     int *cnt;            // [NC * T]
-    int *off;            // [NC * T + 1]
-    int *bsum;           // scan block sums
+    long long *off;      // [NC * T + 1] bin offsets (64-bit: large batches exceed 2^31 entries)
+    long long *bsum;     // scan block sums
     int *entries;        // bin entries (face ids)
     long long cap;       // entries capacity
     float2 *dkey;        // screen-space keyframe gradients, indexed like key

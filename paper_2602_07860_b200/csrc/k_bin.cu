@@ -123,7 +123,7 @@ __device__ __forceinline__ int block_excl_scan_1024(int v[4], int *sm)
     return total;
 }
 
-__global__ void __launch_bounds__(256) k3_scan_blocks(const int *cnt, int *off, int *bsum, int n)
+__global__ void __launch_bounds__(256) k3_scan_blocks(const int *cnt, long long *off, long long *bsum, int n)
 {
     __shared__ int sm[16];
     const int base = blockIdx.x * 1024 + threadIdx.x * 4;
@@ -137,28 +137,45 @@ __global__ void __launch_bounds__(256) k3_scan_blocks(const int *cnt, int *off, 
     if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(256) k3_scan_sums(int *bsum, int nb, int *off, int n)
+// exclusive scan of the block totals (64-bit), one CTA; off[n] = grand total
+__global__ void __launch_bounds__(256) k3_scan_sums(long long *bsum, int nb, long long *off, int n,
+                                                    long long *binstat, long long cap)
 {
-    __shared__ int sm[16];
-    int carry = 0;
-    for (int base0 = 0; base0 < nb; base0 += 1024) {
-        const int base = base0 + threadIdx.x * 4;
-        int v[4];
+    __shared__ long long sm[16];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    long long carry = 0;
+    for (int base0 = 0; base0 < nb; base0 += 256) {
+        const int i = base0 + tid;
+        const long long v = i < nb ? bsum[i] : 0;
+        long long x = v;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = base + i < nb ? bsum[base + i] : 0;
-        int tot = block_excl_scan_1024(v, sm);
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) sm[warp] = x;
+        __syncthreads();
+        long long pre = 0, tot = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-            if (base + i < nb) bsum[base + i] = v[i] + carry;
+        for (int w = 0; w < 8; ++w) {
+            pre += w < warp ? sm[w] : 0;
+            tot += sm[w];
+        }
+        if (i < nb) bsum[i] = carry + pre + x - v;
         carry += tot;
+        __syncthreads();
     }
-    if (threadIdx.x == 0) off[n] = carry;
+    if (tid == 0) {
+        off[n] = carry;
+        binstat[0] = carry;
+        binstat[1] = cap;
+    }
 }
 
-__global__ void __launch_bounds__(256) k3_scan_add(int *off, const int *bsum, int n)
+__global__ void __launch_bounds__(256) k3_scan_add(long long *off, const long long *bsum, int n)
 {
     const int i = blockIdx.x * 1024 + threadIdx.x;
-    const int add = bsum[blockIdx.x];
+    const long long add = bsum[blockIdx.x];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
         if (i + 256 * q < n) off[i + 256 * q] += add;
@@ -171,9 +188,9 @@ __global__ void __launch_bounds__(256) k3_sort(Tables t, int nbins)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int *s = sm[warp];
     for (int bi = blockIdx.x * 8 + warp; bi < nbins; bi += gridDim.x * 8) {
-        const int o = t.off[bi];
-        const int n = t.off[bi + 1] - o;
-        if (n <= 1 || n > SORTCAP || (long long)o + n > t.cap) continue;
+        const long long o = t.off[bi];
+        const int n = (int)(t.off[bi + 1] - o);
+        if (n <= 1 || n > SORTCAP || o + n > t.cap) continue;
         int n2 = 32;
         while (n2 < n) n2 <<= 1;
         for (int i = lane; i < n2; i += 32) s[i] = i < n ? t.entries[o + i] : 0x7fffffff;
@@ -218,7 +235,7 @@ cudaError_t launch_binning(const Tables &t, cudaStream_t st)
     }
     const int nb = (nbins + 1023) / 1024;
     k3_scan_blocks<<<nb, 256, 0, st>>>(t.cnt, t.off, t.bsum, nbins);
-    k3_scan_sums<<<1, 256, 0, st>>>(t.bsum, nb, t.off, nbins);
+    k3_scan_sums<<<1, 256, 0, st>>>(t.bsum, nb, t.off, nbins, t.binstat, t.cap);
     k3_scan_add<<<nb, 256, 0, st>>>(t.off, t.bsum, nbins);
     e = cudaMemsetAsync(t.cnt, 0, sizeof(int) * (size_t)nbins, st);
     if (e != cudaSuccess) return e;

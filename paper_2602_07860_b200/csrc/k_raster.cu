@@ -433,8 +433,8 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
     for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
         const Chunk ch = t.chunks[c];
         const size_t bi = (size_t)c * t.T + tile;
-        const int o = t.off[bi];
-        const int n = t.off[bi + 1] - o;
+        const long long o = t.off[bi];
+        const int n = (int)(t.off[bi + 1] - o);
         if (n == 0) {
             if (ids && inimg && ids_k >= ch.k0 && ids_k < ch.k1) ids[pix] = -1;
             continue;
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
         bc.fcol = t.fcol;
         bc.ent = t.entries + o;
         bc.n = n;
-        bc.fb = n > SORTCAP || (long long)o + n > t.cap;
+        bc.fb = n > SORTCAP || o + n > t.cap;
         if (!bc.fb && n <= SREC_F) {
             // grouped path: the whole bin staged for up to Gs sub-frames at once
             const int Gs = min(GMAX_F, SREC_F / n), nw = (n + 31) >> 5;
@@ -767,8 +767,8 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
     for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
         const Chunk ch = t.chunks[c];
         const size_t bi = (size_t)c * t.T + tile;
-        const int o = t.off[bi];
-        const int n = t.off[bi + 1] - o;
+        const long long o = t.off[bi];
+        const int n = (int)(t.off[bi + 1] - o);
         if (n == 0) continue;
         BinCtx bc;
         bc.status = t.status;
@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
         bc.fcol = t.fcol;
         bc.ent = t.entries + o;
         bc.n = n;
-        bc.fb = n > SORTCAP || (long long)o + n > t.cap;
+        bc.fb = n > SORTCAP || o + n > t.cap;
         FaceAcc acc;
         acc_zero(acc);
         if (!bc.fb && n <= SREC_B) {

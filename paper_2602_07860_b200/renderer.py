@@ -40,11 +40,30 @@ class BlurRenderer:
         self.max_chunk = int(max_chunk)
         self.bin_factor = float(bin_factor)
         self.solver = int(solver)
+        self.auto_bins = bin_factor == 0.0      # size the bin capacity to the geometry on first use
+        self._alloc(self.bin_factor)
+
+    def _alloc(self, factor: float):
+        self.bin_factor = float(factor)
         cfg = _lib.make_config(self.max_chunk, 0, self.bin_factor)
         self.ws_bytes = _lib.blur_workspace_bytes(self.V, self.F, self.B, self.H, self.W, self._motions,
                                                   self._cams, self._sub, cfg)
+        self.ws = None
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.ws[:256].zero_()
+
+    def _autosize(self, verts, colors, out, ids, ids_subframe, census, stream, events):
+        """First forward: if the binning needed more entries than the default capacity, grow the
+        workspace (factor x needed/capacity, +25%) and render again (one synchronisation, once)."""
+        self.auto_bins = False
+        need, cap = _lib.blur_read_bins(self.ws, stream)
+        if need <= cap or self.F == 0:
+            return out
+        base = self.bin_factor if self.bin_factor > 0 else 3.0
+        self._alloc(base * need / max(cap, 1) * 1.25)
+        if census is not None:
+            census.zero_()
+        return self.forward(verts, colors, out, ids, ids_subframe, census, stream, events)
 
     # -- forward / backward -------------------------------------------------------------
     def forward(self, verts: torch.Tensor, colors: torch.Tensor, out: Optional[torch.Tensor] = None,
@@ -56,6 +75,8 @@ class BlurRenderer:
         _lib.blur_render_fwd(verts, self.faces, colors, self._motions, self._cams, self.B, self.H, self.W, out,
                              self.ws, sub_range=self._sub, ids=ids, ids_subframe=ids_subframe, cfg=cfg,
                              stream=stream)
+        if self.auto_bins:
+            return self._autosize(verts, colors, out, ids, ids_subframe, census, stream, events)
         return out
 
     def backward(self, verts: torch.Tensor, colors: torch.Tensor, grad_rgba: torch.Tensor, reuse_setup: bool = False,
