@@ -32,6 +32,11 @@
  *   fast-solver cross-check: Eq.8 with the coefficients A11-A16 transcribed
  *     literally evaluated for every covered pair.
  *
+ *   soft background coverage (NEXT-1; opts.delta > 0): a pixel with no covering face at a
+ *     sub-frame gets RGB 0 and alpha A_i(t) = 1 - prod_j (1 - A_i^j(t)) over all faces valid at
+ *     tau (Eq.15), A = exp(-d/delta) (Eq.10, A20), d from the closest point on the keyframe
+ *     triangle F(X) (Eq.13, A17-A18) mapped to F(tau) (Eq.14); backward with w^* frozen.
+ *
  * Modes: brute (all pixels x all faces) and binned (per face, pixels inside
  * the face's bounding box -- an exact cull for this coverage rule; the per
  * pixel arithmetic and the face order are unchanged, so the two modes are
@@ -79,6 +84,8 @@ typedef struct {
     double amb_z_rel;      /* Q16 relative depth-tie tolerance (1e-6) */
     int npix;              /* >0: evaluate only the listed pixels (pixel-list mode) */
     const int *pix;        /* npix*3: (b, row, col) */
+    double delta;          /* soft background bandwidth (NDC^2, Eq.10); 0 = hard coverage only */
+    int soft_exact;        /* 1: Eq.12 (closest point on F(tau) itself) instead of Eq.13's F(X) */
 } om_opts;
 
 /* --------------------------------------------------------------- schedule */
@@ -319,6 +326,108 @@ int om_fast_eval(const double X0[3], const double Y0[3], const double X1[3], con
     return 1;
 }
 
+/* --------------------------------------------------------------- soft background coverage (NEXT-1) */
+
+/* Closest point of the triangle (x, y) to the point (pu, pv), as weights (appendix "Euclidean
+ * Distance Approximation", A17-A18):
+ *   if the point is inside (all barycentric weights w >= 0) the weights are w itself;
+ *   otherwise, for the edges v0v1, v1v2, v2v0 in this order, the projection parameter
+ *     t = ((u - x_i)(x_j - x_i) + (v - y_i)(y_j - y_i)) / ((x_j - x_i)^2 + (y_j - y_i)^2)   (A17)
+ *   gives w'_i = 1 - t, w'_j = t for 0 <= t <= 1, vertex i for t < 0, vertex j for t > 1 (A18
+ *   text), and the edge candidate with the smallest squared distance is taken (first
+ *   in edge order on exact ties; a zero-length edge is its vertex i -- reading Q19).
+ * w_in: barycentric weights of the point w.r.t. this triangle (used for the inside test); may be
+ * NULL (then the inside test is skipped).  Outputs: what (the chosen weights), dist2 (its squared
+ * distance in this triangle's plane); cand[9]/cd[3] (optional) the three edge candidates and their
+ * squared distances (for the ambiguity analysis).  Returns the chosen edge (0..2) or -1 (inside). */
+int om_closest_w(const double x[3], const double y[3], double pu, double pv, const double *w_in,
+                 double what[3], double *dist2, double *cand, double *cd)
+{
+    if (w_in && w_in[0] >= 0.0 && w_in[1] >= 0.0 && w_in[2] >= 0.0) {
+        for (int i = 0; i < 3; ++i) what[i] = w_in[i];
+        *dist2 = 0.0;
+        if (cand) for (int e = 0; e < 3; ++e) { cd[e] = 0.0; for (int i = 0; i < 3; ++i) cand[3 * e + i] = w_in[i]; }
+        return -1;
+    }
+    int best = -1;
+    double bestd = INFINITY;
+    for (int e = 0; e < 3; ++e) {
+        int i = e, j = (e + 1) % 3;
+        double ex = x[j] - x[i], ey = y[j] - y[i];
+        double l2 = ex * ex + ey * ey;
+        double t = l2 > 0.0 ? ((pu - x[i]) * ex + (pv - y[i]) * ey) / l2 : 0.0;
+        double wc[3] = {0.0, 0.0, 0.0};
+        if (t < 0.0) {
+            wc[i] = 1.0;
+        } else if (t > 1.0) {
+            wc[j] = 1.0;
+        } else {
+            wc[i] = 1.0 - t;
+            wc[j] = t;
+        }
+        double qx = wc[0] * x[0] + wc[1] * x[1] + wc[2] * x[2];
+        double qy = wc[0] * y[0] + wc[1] * y[1] + wc[2] * y[2];
+        double d = (pu - qx) * (pu - qx) + (pv - qy) * (pv - qy);
+        if (cand) { cd[e] = d; for (int q = 0; q < 3; ++q) cand[3 * e + q] = wc[q]; }
+        if (d < bestd) {
+            bestd = d;
+            best = e;
+            for (int q = 0; q < 3; ++q) what[q] = wc[q];
+        }
+    }
+    *dist2 = bestd;
+    return best;
+}
+
+/* One (pixel, face, sub-frame) background term (Eq.10-14).
+ * Keyframe triangles F(0) = (X0, Y0), F(1) = (X1, Y1) of the segment, segment time tau, pixel
+ * (u, v), bandwidth delta (NDC^2; Q9).  Steps, in the paper's order:
+ *   F(tau) = (1 - tau) F(0) + tau F(1) (Eq.5-6); w(tau) = F(tau)^-1 p (Eq.3, textbook solve);
+ *   X = 0 if tau <= 0.5 else 1 (Eq.13), or F(X) = F(tau) itself when exact != 0 (Eq.12);
+ *   p' = F(X) w(tau); w^* = closest-point weights of p' on F(X) (A17-A18, om_closest_w);
+ *   d = || F(tau) w(tau) - F(tau) w^* ||^2 = || p - F(tau) w^* ||^2 (Eq.14);
+ *   A = exp(-d / delta) (Eq.10 with the exponential kernel, A20).
+ * Outputs A, d, what (w^*), pstar = F(tau) w^* (2), and, when amb != NULL, amb[0] = the largest
+ * |A' - A| over the edge candidates whose F(X) distance is within eps of the chosen one (their
+ * sqrt distances differ by <= eps NDC: a rounding-level tie, Q16/Q20).  Returns 0 if F(tau) is
+ * degenerate (Q8: the face is skipped for this sub-frame), else 1. */
+int om_soft_pair(const double X0[3], const double Y0[3], const double X1[3], const double Y1[3], double tau,
+                 double u, double v, double delta, int exact, double eps, double *A, double *d, double what[3],
+                 double pstar[2], double *amb)
+{
+    double xt[3], yt[3], w[3], det;
+    for (int i = 0; i < 3; ++i) {
+        xt[i] = (1.0 - tau) * X0[i] + tau * X1[i];
+        yt[i] = (1.0 - tau) * Y0[i] + tau * Y1[i];
+    }
+    if (!om_bary_textbook(xt, yt, u, v, w, &det)) return 0;
+    const double *xk = exact ? xt : (tau <= 0.5 ? X0 : X1);
+    const double *yk = exact ? yt : (tau <= 0.5 ? Y0 : Y1);
+    double pu = w[0] * xk[0] + w[1] * xk[1] + w[2] * xk[2];
+    double pv = w[0] * yk[0] + w[1] * yk[1] + w[2] * yk[2];
+    double cand[9], cd[3], dX;
+    int e = om_closest_w(xk, yk, pu, pv, w, what, &dX, cand, cd);
+    pstar[0] = what[0] * xt[0] + what[1] * xt[1] + what[2] * xt[2];
+    pstar[1] = what[0] * yt[0] + what[1] * yt[1] + what[2] * yt[2];
+    *d = (u - pstar[0]) * (u - pstar[0]) + (v - pstar[1]) * (v - pstar[1]);
+    *A = exp(-*d / delta);
+    if (amb) {
+        amb[0] = 0.0;
+        if (e >= 0 && eps > 0) {
+            for (int c = 0; c < 3; ++c) {
+                if (c == e || !(fabs(sqrt(cd[c]) - sqrt(dX)) <= eps)) continue;
+                const double *wc = cand + 3 * c;
+                double qx = wc[0] * xt[0] + wc[1] * xt[1] + wc[2] * xt[2];
+                double qy = wc[0] * yt[0] + wc[1] * yt[1] + wc[2] * yt[2];
+                double d2 = (u - qx) * (u - qx) + (v - qy) * (v - qy);
+                double dA = fabs(exp(-d2 / delta) - *A);
+                if (dA > amb[0]) amb[0] = dA;
+            }
+        }
+    }
+    return 1;
+}
+
 /* --------------------------------------------------------------- per-image state */
 
 typedef struct {
@@ -380,6 +489,10 @@ typedef struct {
     double w[3];      /* nominal winner weights */
     double delta;     /* max |value change| of this sub-frame under the Q16 perturbations */
     int amb_id;       /* the winner (id) can change under the Q16 perturbations */
+    double P;         /* soft background: prod_j (1 - A_j) (Eq.15) over all faces, uncovered pixels */
+    double Pnz;       /*   the same product over the factors that are not exactly 0 */
+    int nz;           /*   number of factors exactly 0 */
+    int amb_soft;     /*   a closest-edge choice was a rounding-level tie (Q20) */
 } pixstate;
 
 static void ps_reset(pixstate *p)
@@ -388,6 +501,10 @@ static void ps_reset(pixstate *p)
     p->w[0] = p->w[1] = p->w[2] = 0;
     p->delta = 0;
     p->amb_id = 0;
+    p->P = 1.0;
+    p->Pnz = 1.0;
+    p->nz = 0;
+    p->amb_soft = 0;
 }
 
 typedef struct {
@@ -611,6 +728,84 @@ static void pix_finalize_amb(pixstate *ps)
     }
 }
 
+/* Keyframe triangles of face f in segment s (NDC x, y of keyframes s and s+1). */
+static void face_keys(const om_scene *sc, const img_state *st, int s, int f, double X0[3], double Y0[3],
+                      double X1[3], double Y1[3])
+{
+    const int *fv = sc->faces + 3 * f;
+    for (int i = 0; i < 3; ++i) {
+        const double *a = st->key + 3 * ((size_t)s * sc->V + fv[i]);
+        const double *b = st->key + 3 * ((size_t)(s + 1) * sc->V + fv[i]);
+        X0[i] = a[0]; Y0[i] = a[1];
+        X1[i] = b[0]; Y1[i] = b[1];
+    }
+}
+
+/* Fold one face's background term into an uncovered pixel's product (Eq.15). */
+static void soft_accum(pixstate *ps, double A, double ambA)
+{
+    double fac = 1.0 - A;
+    ps->P *= fac;
+    if (fac == 0.0) ps->nz += 1;
+    else ps->Pnz *= fac;
+    if (ambA > 0.0) { ps->amb_soft = 1; ps->delta += ambA; }   /* d alpha / d A_j <= 1 */
+}
+
+/* Pixel range whose soft term can be non-zero: the box of F(tau) grown by sqrt(760 delta) (beyond
+ * it d / delta > 760 and exp(-d / delta) is exactly 0 in fp64, so skipping those factors of exactly
+ * 1 leaves the product bit-identical to the brute loop).  Returns 0 if empty. */
+static int soft_range(const face_geo *g, double delta, int H, int W, int *i0, int *i1, int *j0, int *j1)
+{
+    face_geo gg = *g;
+    gg.pad = sqrt(760.0 * delta) + 1e-9;
+    face_bbox(&gg, H, W, i0, i1, j0, j1);
+    return *i0 <= *i1 && *j0 <= *j1;
+}
+
+/* Soft background pass of one sub-frame: for every nominally uncovered pixel, the product over all
+ * faces valid at tau, in face-index order. */
+static void soft_subframe(const om_scene *sc, const om_opts *op, const img_state *st, int k, pixstate *ps,
+                          const int *pix_idx, int npix, const double *X, const double *Y, const double *Z,
+                          const unsigned char *okv)
+{
+    int H = sc->H, W = sc->W;
+    int s = st->sk[k];
+    double tau = st->tk[k];
+    face_geo g;
+    double X0[3], Y0[3], X1[3], Y1[3], A, d, wh[3], ps2[2], amb;
+    if (pix_idx) {
+        for (int q = 0; q < npix; ++q) {
+            if (ps[q].id[0] >= 0) continue;
+            int p = pix_idx[q];
+            double u = pix_u(p % W, W), v = pix_v(p / W, H);
+            for (int f = 0; f < sc->F; ++f) {
+                if (!face_setup(sc, f, X, Y, Z, okv, 0.0, &g)) continue;
+                face_keys(sc, st, s, f, X0, Y0, X1, Y1);
+                if (!om_soft_pair(X0, Y0, X1, Y1, tau, u, v, op->delta, op->soft_exact, op->eps_amb, &A, &d, wh, ps2,
+                                  &amb))
+                    continue;
+                soft_accum(&ps[q], A, amb);
+            }
+        }
+        return;
+    }
+    for (int f = 0; f < sc->F; ++f) {
+        if (!face_setup(sc, f, X, Y, Z, okv, 0.0, &g)) continue;
+        int i0 = 0, i1 = W - 1, j0 = 0, j1 = H - 1;
+        if (op->mode == 1 && !soft_range(&g, op->delta, H, W, &i0, &i1, &j0, &j1)) continue;
+        face_keys(sc, st, s, f, X0, Y0, X1, Y1);
+        for (int j = j0; j <= j1; ++j)
+            for (int i = i0; i <= i1; ++i) {
+                pixstate *pp = &ps[j * W + i];
+                if (pp->id[0] >= 0) continue;
+                if (!om_soft_pair(X0, Y0, X1, Y1, tau, pix_u(i, W), pix_v(j, H), op->delta, op->soft_exact, op->eps_amb,
+                                  &A, &d, wh, ps2, &amb))
+                    continue;
+                soft_accum(pp, A, amb);
+            }
+    }
+}
+
 /* Render one sub-frame (b, k) into per-pixel states.  pix_idx == NULL: all pixels (brute or
  * binned); otherwise only the listed pixel indices (brute over faces). */
 static void render_subframe(const om_scene *sc, const om_opts *op, const img_state *st, int k,
@@ -643,6 +838,7 @@ static void render_subframe(const om_scene *sc, const om_opts *op, const img_sta
                 pix_finalize_amb(&ps[q]);
             }
         }
+        if (op->delta > 0) soft_subframe(sc, op, st, k, ps, pix_idx, npix, X, Y, Z, okv);
         return;
     }
     for (int f = 0; f < sc->F; ++f) {
@@ -670,6 +866,7 @@ static void render_subframe(const om_scene *sc, const om_opts *op, const img_sta
         for (int p = 0; p < P; ++p) pix_finalize_amb(&ps[p]);
         free(nom);
     }
+    if (op->delta > 0) soft_subframe(sc, op, st, k, ps, NULL, P, X, Y, Z, okv);
 }
 
 static int nthreads_of(const om_opts *op)
@@ -750,6 +947,12 @@ int om_render_fwd(const om_scene *sc, const om_opts *op, double *out_rgba, int *
                     /* frozen-visibility evaluation (FD pin only) */
                     lerp_subframe(sc, &st, k, X, Y, Z, okv);
                     const int *fz = frozen + frozen_off + (size_t)k * P;
+                    if (op->delta > 0) {   /* frozen coverage: soft alpha of the frozen-uncovered pixels */
+                        for (int p = 0; p < P; ++p) { ps_reset(&ps[p]); ps[p].id[0] = fz[p]; }
+                        soft_subframe(sc, op, &st, k, ps, NULL, P, X, Y, Z, okv);
+                        for (int p = 0; p < P; ++p)
+                            if (fz[p] < 0) a[5 * p + 3] += 1.0 - ps[p].P;
+                    }
                     for (int p = 0; p < P; ++p) {
                         int f = fz[p];
                         if (f < 0) continue;
@@ -770,10 +973,12 @@ int om_render_fwd(const om_scene *sc, const om_opts *op, double *out_rgba, int *
                         shade_w(sc, ps[q].id[0], ps[q].w, rgb);      /* Eq.9 */
                         a[5 * q] += rgb[0]; a[5 * q + 1] += rgb[1]; a[5 * q + 2] += rgb[2]; a[5 * q + 3] += 1.0;
                         tst[tid].covered += 1;
+                    } else if (op->delta > 0) {
+                        a[5 * q + 3] += 1.0 - ps[q].P;                 /* A_i(t), Eq.15 (background RGB 0) */
                     }
                     a[5 * q + 4] += ps[q].delta;
                     if (ids && k == ids_k) ids[oq] = ps[q].id[0];
-                    if (amb_win && ps[q].amb_id) amb_win[oq] = 1;    /* distinct k write the same 1 */
+                    if (amb_win && (ps[q].amb_id || ps[q].amb_soft)) amb_win[oq] = 1;    /* distinct k write the same 1 */
                     if (amb_ids && k == ids_k && ps[q].amb_id) amb_ids[oq] = 1;
                 }
             }
@@ -807,12 +1012,61 @@ int om_render_fwd(const om_scene *sc, const om_opts *op, double *out_rgba, int *
     return ret;
 }
 
+/* Soft background gradient of one sub-frame (P:L341-342 through Eq.10-15; w^* frozen; Q11):
+ * for an uncovered pixel with alpha = 1 - prod_j (1 - A_j) and G_a = dL/dalpha_k,
+ *   dalpha/dA_j = prod_{l != j} (1 - A_l)  (Pnz / (1 - A_j) when no factor is 0; Pnz for the single
+ *                 zero factor; 0 otherwise),  dA_j/dd = -A_j / delta,
+ *   dd/dv_i(tau) = -2 w^*_i (p - F(tau) w^*)  (Eq.14 with w^* constant),
+ * then split (1 - tau), tau onto the keyframes like the foreground term. */
+static void soft_grad_subframe(const om_scene *sc, const om_opts *op, const img_state *st, int k,
+                               const pixstate *ps, const int *pix_idx, int npix, const double *gal,
+                               const double *X, const double *Y, const double *Z, const unsigned char *okv,
+                               double *mk)
+{
+    int H = sc->H, W = sc->W, V = sc->V;
+    int s = st->sk[k];
+    double tau = st->tk[k];
+    face_geo g;
+    double X0[3], Y0[3], X1[3], Y1[3], A, d, wh[3], pst[2];
+    for (int f = 0; f < sc->F; ++f) {
+        if (!face_setup(sc, f, X, Y, Z, okv, 0.0, &g)) continue;
+        int i0 = 0, i1 = W - 1, j0 = 0, j1 = H - 1;
+        if (!pix_idx && op->mode == 1 && !soft_range(&g, op->delta, H, W, &i0, &i1, &j0, &j1)) continue;
+        face_keys(sc, st, s, f, X0, Y0, X1, Y1);
+        const int *fv = sc->faces + 3 * f;
+        int bw = i1 - i0 + 1, nloop = pix_idx ? npix : bw * (j1 - j0 + 1);
+        for (int r = 0; r < nloop; ++r) {
+            int q = pix_idx ? r : (j0 + r / bw) * W + i0 + r % bw;
+            int p = pix_idx ? pix_idx[r] : q;
+            int i = p % W, j = p / W;
+            const pixstate *pp = &ps[q];
+            if (pp->id[0] >= 0 || gal[q] == 0.0) continue;
+            double u = pix_u(i, W), v = pix_v(j, H);
+            if (!om_soft_pair(X0, Y0, X1, Y1, tau, u, v, op->delta, op->soft_exact, 0.0, &A, &d, wh, pst, NULL)) continue;
+            if (A == 0.0) continue;
+            double fac = 1.0 - A, dadA;
+            if (pp->nz == 0) dadA = pp->Pnz / fac;
+            else if (pp->nz == 1 && fac == 0.0) dadA = pp->Pnz;
+            else dadA = 0.0;
+            double c = gal[q] * dadA * A / op->delta * 2.0;
+            for (int a = 0; a < 3; ++a) {
+                if (wh[a] == 0.0) continue;
+                double gx = c * wh[a] * (u - pst[0]), gy = c * wh[a] * (v - pst[1]);
+                size_t o0 = ((size_t)s * V + fv[a]) * 2, o1 = ((size_t)(s + 1) * V + fv[a]) * 2;
+                mk[o0] += (1.0 - tau) * gx; mk[o0 + 1] += (1.0 - tau) * gy;
+                mk[o1] += tau * gx;         mk[o1 + 1] += tau * gy;
+            }
+        }
+    }
+}
+
 /* Backward (frozen winners Q11).
  *   grad_rgba: dL/dI, B*H*W*4 (or npix*4 in pixel-list mode; the gradient is then the one of a
  *              loss that only reads the listed pixels)
  *   dverts, dcolors: V*3 outputs (overwritten)
  *   dkey: optional sum_b (S_b+1)*V*2 screen-space keyframe gradients (overwritten)
- * Alpha carries no position gradient in the hard-coverage path. */
+ * Alpha carries no position gradient in the hard-coverage path; with op->delta > 0 the
+ * background alpha of Eq.10-15 does (soft_grad_subframe). */
 int om_render_bwd(const om_scene *sc, const om_opts *op, const double *grad_rgba, double *dverts,
                   double *dcolors, double *dkey)
 {
@@ -850,11 +1104,16 @@ int om_render_bwd(const om_scene *sc, const om_opts *op, const double *grad_rgba
             double *Z = (double *)malloc(sizeof(double) * (size_t)(V + 1));
             unsigned char *okv = (unsigned char *)malloc((size_t)(V + 1));
             double *mk = gk + (size_t)tid * nkv, *mc = gc + (size_t)tid * 3 * V;
+            double *gal = op->delta > 0 ? (double *)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1)) : NULL;
 #pragma omp for schedule(static)
             for (int k = st.k0; k < st.k1; ++k) {
                 render_subframe(sc, &op1, &st, k, ps, list ? lidx : NULL, np, NULL, X, Y, Z, okv, NULL);
                 int s = st.sk[k];
                 double tau = st.tk[k];
+                if (gal) {   /* soft background: dL/dalpha_k = G_alpha / N */
+                    for (int q = 0; q < np; ++q) gal[q] = grad_rgba[4 * (size_t)(list ? lslot[q] : b * P + q) + 3] / N;
+                    soft_grad_subframe(sc, &op1, &st, k, ps, list ? lidx : NULL, np, gal, X, Y, Z, okv, mk);
+                }
                 for (int q = 0; q < np; ++q) {
                     int f = ps[q].id[0];
                     if (f < 0) continue;
@@ -887,7 +1146,7 @@ int om_render_bwd(const om_scene *sc, const om_opts *op, const double *grad_rgba
                     }
                 }
             }
-            free(ps); free(X); free(Y); free(Z); free(okv);
+            free(ps); free(X); free(Y); free(Z); free(okv); free(gal);
         }
         /* reduce thread partials (static order) */
         double *K = (double *)calloc(nkv, sizeof(double));

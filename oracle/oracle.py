@@ -15,7 +15,7 @@ _lock = threading.Lock()
 _lib = None
 
 __all__ = ["build", "lib", "schedule", "keyframes", "bary_textbook", "fast_coeffs", "fast_eval",
-           "render_fwd", "render_bwd", "num_threads"]
+           "render_fwd", "render_bwd", "num_threads", "closest_w", "soft_pair"]
 
 
 def build(force: bool = False) -> str:
@@ -39,7 +39,7 @@ class _Scene(C.Structure):
 class _Opts(C.Structure):
     _fields_ = [("mode", C.c_int), ("threads", C.c_int), ("check_fast", C.c_int),
                 ("eps_amb", C.c_double), ("amb_val_tol", C.c_double), ("amb_z_rel", C.c_double),
-                ("npix", C.c_int), ("pix", C.c_void_p)]
+                ("npix", C.c_int), ("pix", C.c_void_p), ("delta", C.c_double), ("soft_exact", C.c_int)]
 
 
 def lib():
@@ -57,6 +57,9 @@ def lib():
             _lib.om_render_fwd.argtypes = [P, P, P, P, C.c_int, P, P, P, P, P]
             _lib.om_render_bwd.argtypes = [P, P, P, P, P, P]
             _lib.om_num_threads.argtypes = [C.c_int]
+            _lib.om_closest_w.argtypes = [P, P, C.c_double, C.c_double, P, P, P, P, P]
+            _lib.om_soft_pair.argtypes = [P, P, P, P, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int,
+                                          C.c_double, P, P, P, P, P]
         return _lib
 
 
@@ -92,10 +95,10 @@ class _Pack:
 
 
 def _opts(mode="binned", threads=0, check_fast=False, eps_amb=0.0, amb_val_tol=1e-5, amb_z_rel=1e-6,
-          pixels=None):
+          pixels=None, delta=0.0, soft_exact=False):
     pix = None if pixels is None else _i(pixels).reshape(-1, 3)
     o = _Opts(1 if mode == "binned" else 0, threads, int(check_fast), eps_amb, amb_val_tol, amb_z_rel,
-              0 if pix is None else pix.shape[0], _p(pix))
+              0 if pix is None else pix.shape[0], _p(pix), float(delta), int(soft_exact))
     return o, pix
 
 
@@ -145,8 +148,9 @@ def fast_eval(X0, Y0, X1, Y1, u, v, t):
 
 
 def render_fwd(sc, mode="binned", threads=0, ids_k=-1, eps_amb=0.0, check_fast=False, sub_range=None,
-               frozen=None, pixels=None, colors=None, verts=None):
+               frozen=None, pixels=None, colors=None, verts=None, delta=0.0, soft_exact=False):
     """Blurred RGBA (B,H,W,4) fp64 (or (npix,4) in pixel-list mode).
+    delta > 0 adds the soft background alpha of Eq.10-15 (NEXT-1; soft_exact: Eq.12 instead of Eq.13).
     Returns dict(rgba, ids, amb_img, amb_ids, amb_win, stats, behind); the amb_* maps are the Q16
     exclusion masks: blurred value movable by > 1e-5, winner at ids_k ambiguous,
     winner ambiguous at some sub-frame."""
@@ -155,7 +159,7 @@ def render_fwd(sc, mode="binned", threads=0, ids_k=-1, eps_amb=0.0, check_fast=F
         sc = dataclasses.replace(sc, colors=sc.colors if colors is None else colors,
                                  verts=sc.verts if verts is None else verts)
     pk = _Pack(sc, sub_range)
-    o, pix = _opts(mode, threads, check_fast, eps_amb, pixels=pixels)
+    o, pix = _opts(mode, threads, check_fast, eps_amb, pixels=pixels, delta=delta, soft_exact=soft_exact)
     shape = (pix.shape[0],) if pix is not None else (sc.B, sc.H, sc.W)
     rgba = np.zeros(shape + (4,))
     ids = np.full(shape, -1, np.int32)
@@ -177,14 +181,15 @@ def render_fwd(sc, mode="binned", threads=0, ids_k=-1, eps_amb=0.0, check_fast=F
 
 
 def render_bwd(sc, grad_rgba, mode="binned", threads=0, sub_range=None, pixels=None, want_dkey=False,
-               colors=None, verts=None):
-    """(dverts (V,3), dcolors (V,3)[, dkey list per image (S+1,V,2)]) in fp64."""
+               colors=None, verts=None, delta=0.0, soft_exact=False):
+    """(dverts (V,3), dcolors (V,3)[, dkey list per image (S+1,V,2)]) in fp64.
+    delta > 0: the alpha channel of grad_rgba also flows through the soft background (Eq.10-15)."""
     import dataclasses
     if colors is not None or verts is not None:
         sc = dataclasses.replace(sc, colors=sc.colors if colors is None else colors,
                                  verts=sc.verts if verts is None else verts)
     pk = _Pack(sc, sub_range)
-    o, pix = _opts(mode, threads, pixels=pixels)
+    o, pix = _opts(mode, threads, pixels=pixels, delta=delta, soft_exact=soft_exact)
     g = _d(grad_rgba)
     dv = np.zeros((sc.V, 3))
     dc = np.zeros((sc.V, 3))
@@ -201,3 +206,22 @@ def render_bwd(sc, grad_rgba, mode="binned", threads=0, sub_range=None, pixels=N
         out.append(dk[off:off + n].reshape(int(S) + 1, sc.V, 2))
         off += n
     return dv, dc, out
+
+
+def closest_w(x, y, pu, pv, w_in=None):
+    """Appendix A17-A18 closest-point weights of (pu, pv) on triangle (x, y): (what, dist2, edge,
+    candidates (3,3), candidate dist2 (3,)).  edge = -1 when w_in says the point is inside."""
+    what, d2, cand, cd = np.zeros(3), np.zeros(1), np.zeros(9), np.zeros(3)
+    e = lib().om_closest_w(_p(_d(x)), _p(_d(y)), float(pu), float(pv), _p(None if w_in is None else _d(w_in)),
+                           _p(what), _p(d2), _p(cand), _p(cd))
+    return what, float(d2[0]), int(e), cand.reshape(3, 3), cd
+
+
+def soft_pair(X0, Y0, X1, Y1, tau, u, v, delta, exact=False, eps=0.0):
+    """One background term (Eq.10-14): dict(A, d, what, pstar, amb) or None if F(tau) is degenerate."""
+    A, d, wh, pst, amb = np.zeros(1), np.zeros(1), np.zeros(3), np.zeros(2), np.zeros(1)
+    ok = lib().om_soft_pair(_p(_d(X0)), _p(_d(Y0)), _p(_d(X1)), _p(_d(Y1)), float(tau), float(u), float(v),
+                            float(delta), int(exact), float(eps), _p(A), _p(d), _p(wh), _p(pst), _p(amb))
+    if not ok:
+        return None
+    return dict(A=float(A[0]), d=float(d[0]), what=wh, pstar=pst, amb=float(amb[0]))
