@@ -36,6 +36,7 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 # backward's extra work per covered (pixel, sub-frame)
 FLOP_PAIR, FLOP_SHADE, FLOP_SETUP, FLOP_BWD = 18.0, 25.0, 30.0, 100.0
 LAUNCHES_FWD, LAUNCHES_LOSS, LAUNCHES_BWD = 9, 1, 2
+LAUNCHES_SOFT_FWD, LAUNCHES_SOFT_BWD = 9, 1     # soft bins (7) + K8 + reduce; K9
 
 
 def parse():
@@ -50,6 +51,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the oracle sample")
+    p.add_argument("--delta", type=float, default=0.0,
+                   help="soft background coverage bandwidth (NEXT-1, Eq.10-15; the paper uses 1e-4); 0 = hard path")
     return p.parse_args()
 
 
@@ -104,7 +107,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_target(sc, dev):
+def make_target(sc, dev, delta=0.0):
     """Loss targets: renders of the displaced mesh (C4/C5 inverse-rendering step) or the seeded
     uniform targets (C1-C3).  Built before timing."""
     import torch
@@ -114,7 +117,7 @@ def make_target(sc, dev):
     out = torch.empty((sc.B, sc.H, sc.W, 4), dtype=torch.float32, device=dev)
     for b0 in range(0, sc.B, 8):
         sub = sc.subset(list(range(b0, min(sc.B, b0 + 8))))
-        r = BlurRenderer(sub.faces, sub.motion, sub.cams, sub.H, sub.W, sub.V, device=dev)
+        r = BlurRenderer(sub.faces, sub.motion, sub.cams, sub.H, sub.W, sub.V, device=dev, delta=delta)
         r.forward(torch.tensor(sc.meta["displaced_verts"], device=dev), torch.tensor(sc.colors, device=dev),
                   out=out[b0:b0 + sub.B])
         del r
@@ -122,7 +125,7 @@ def make_target(sc, dev):
     return out
 
 
-def cpu_baseline(sc, target_seconds: float):
+def cpu_baseline(sc, target_seconds: float, delta: float = 0.0):
     """Time the fp64 oracle (as it stands) fwd + bwd on a bounded sample of the same workload, all
     host cores: whole images (translational and rotational views alternately) until about
     `target_seconds` of CPU time, or a leading sub-frame range of one image if a single image
@@ -142,9 +145,9 @@ def cpu_baseline(sc, target_seconds: float):
         sub = sc.subset(imgs)
         rng = [[0, ks]] * sub.B
         t0 = time.perf_counter()
-        fw = oracle.render_fwd(sub, sub_range=rng)
+        fw = oracle.render_fwd(sub, sub_range=rng, delta=delta)
         G = 2.0 * (fw["rgba"] - (sub.target if sub.target is not None else 0.0)) / fw["rgba"].size
-        oracle.render_bwd(sub, G, sub_range=rng)
+        oracle.render_bwd(sub, G, sub_range=rng, delta=delta)
         return time.perf_counter() - t0
 
     t1 = run(order[:1], N)                 # one whole image
@@ -160,8 +163,9 @@ def cpu_baseline(sc, target_seconds: float):
             t = run(imgs, ks)
     images = len(imgs) * reps
     return {"value": images / t, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": "fp64 oracle (binned) fwd+bwd of %d of %d images of %s (%s) x %d repetitions, all %d "
-                      "sub-frames: %.1f s on %d threads" % (len(imgs), sc.B, sc.name, imgs, reps, N, t, cores),
+            "sample": "fp64 oracle (binned%s) fwd+bwd of %d of %d images of %s (%s) x %d repetitions, all %d "
+                      "sub-frames: %.1f s on %d threads" % (", soft delta=%g" % delta if delta > 0 else "", len(imgs),
+                                                             sc.B, sc.name, imgs, reps, N, t, cores),
             "seconds": t}
 
 
@@ -172,7 +176,7 @@ def run_reference(args, rank, world):
     sc = scenes.make(args.config)
     vals = []
     for _ in range(args.warmup + args.steps):
-        vals.append(cpu_baseline(sc, max(2.0, args.cpu_seconds / max(1, args.steps))))
+        vals.append(cpu_baseline(sc, max(2.0, args.cpu_seconds / max(1, args.steps)), args.delta))
     cb = vals[-1]
     timed = vals[args.warmup:]
     v = len(timed) / sum(1.0 / x["value"] for x in timed)
@@ -180,7 +184,8 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v * sc.B,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": sc.name, "images": sc.B, "H": sc.H, "W": sc.W,
-                                            "faces": sc.F, "subframes": int(sc.motion["n_sub"][0])},
+                                            "faces": sc.F, "subframes": int(sc.motion["n_sub"][0]),
+                                            **({"delta": args.delta} if args.delta > 0 else {})},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "oracle",
                              "sample": cb["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -210,14 +215,14 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     sc = scenes.make(args.config)
-    target = make_target(sc, dev)
+    target = make_target(sc, dev, args.delta)
     verts = torch.tensor(sc.verts, device=dev)
     colors = torch.tensor(sc.colors, device=dev)
 
     def make_renderer(images, sub_range):
         s = sc.subset(images)
         return BlurRenderer(s.faces, s.motion, s.cams, s.H, s.W, s.V, device=dev, sub_range=sub_range,
-                            max_chunk=args.max_chunk)
+                            max_chunk=args.max_chunk, delta=args.delta)
 
     step = ShardedStep(sc.motion["n_sub"], target, make_renderer, rank, world, split=args.split, device=dev)
     rend = step.renderer
@@ -240,10 +245,10 @@ def main():
 
     flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
 
-    def one_step(ev_f=None, ev_b=None):
+    def one_step(ev_f=None, ev_b=None, ev_sf=None, ev_sb=None):
         if rend is None:
             return step(verts, colors)
-        out = rend.forward(verts, colors, events=ev_f)
+        out = rend.forward(verts, colors, events=ev_f, soft_events=ev_sf)
         for slot, g in step.groups:
             part = out[slot].contiguous()
             dist.all_reduce(part, group=g)
@@ -258,7 +263,7 @@ def main():
                                            n_norm=step.n_norm)
                 loss += li * step.loss_mask[i]
                 grads[i].copy_(gi[0])
-        dv, dc = rend.backward(verts, colors, grads, reuse_setup=True, events=ev_b)
+        dv, dc = rend.backward(verts, colors, grads, reuse_setup=True, events=ev_b, soft_events=ev_sb)
         flat = torch.cat([dv.reshape(-1), dc.reshape(-1), loss])
         if world > 1:
             dist.all_reduce(flat)
@@ -277,6 +282,9 @@ def main():
     ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     evf = [evpair() for _ in range(K)]
     evb = [evpair() for _ in range(K)]
+    soft = args.delta > 0
+    evsf = [evpair() if soft else None for _ in range(K)]
+    evsb = [evpair() if soft else None for _ in range(K)]
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
@@ -286,7 +294,7 @@ def main():
     for i in range(K):
         flush_buf.zero_()                                       # L2 flush between timed steps
         ev_s[i].record(stream)
-        one_step(evf[i], evb[i])
+        one_step(evf[i], evb[i], evsf[i], evsb[i])
         ev_e[i].record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -296,6 +304,8 @@ def main():
     tot_ms = float(sum(step_ms))
     fwd_ms = [evf[i][0].elapsed_time(evf[i][1]) for i in range(K)] if rend is not None else [0.0]
     bwd_ms = [evb[i][0].elapsed_time(evb[i][1]) for i in range(K)] if rend is not None else [0.0]
+    sf_ms = [evsf[i][0].elapsed_time(evsf[i][1]) for i in range(K)] if soft and rend is not None else [0.0]
+    sb_ms = [evsb[i][0].elapsed_time(evsb[i][1]) for i in range(K)] if soft and rend is not None else [0.0]
     t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -325,6 +335,7 @@ def main():
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md nominal "
                                "SM count and clocks.max.sm)",
                 "fwd_raster_ms": f_avg, "bwd_raster_ms": b_avg,
+                **({"soft_fwd_ms": float(np.mean(sf_ms)), "soft_bwd_ms": float(np.mean(sb_ms))} if soft else {}),
                 "executed_pair_tests_per_launch": cand, "necessary_pairs_per_launch": nec}
 
     # measured FFMA throughput (context for the derived peak)
@@ -386,7 +397,7 @@ def main():
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(sc, args.cpu_seconds)
+        cb = cpu_baseline(sc, args.cpu_seconds, args.delta)
         cb.pop("seconds", None)
 
     if rank == 0:
@@ -397,13 +408,15 @@ def main():
                 "config": {"workload": sc.name, "images": sc.B, "H": sc.H, "W": sc.W, "faces": sc.F,
                            "vertices": sc.V, "subframes": n_sub,
                            "segments": sorted({int(x) for x in sc.motion["n_seg"]}),
+                           **({"delta": args.delta, "coverage": "soft (Eq.10-15)"} if soft else {}),
                            "parallelism": "image-sharded x%d" % world + ("" if not step.groups else " + subframe split"),
                            "l2": "flushed (256 MB write) before every timed step"},
                 "barycentric_evals_per_s": {"executed": cand * world / (ms_per_step / 1000.0),
                                             "necessary": nec * world / (ms_per_step / 1000.0),
                                             "note": "per-rank census x ranks (rank 0's counts)"},
                 "roofline": roofline, "ffma_measured_tflops": ffma, "clocks": clk,
-                "gpu_launches": (LAUNCHES_FWD + LAUNCHES_LOSS + LAUNCHES_BWD) * K,
+                "gpu_launches": (LAUNCHES_FWD + LAUNCHES_LOSS + LAUNCHES_BWD +
+                                 (LAUNCHES_SOFT_FWD + LAUNCHES_SOFT_BWD if soft else 0)) * K,
                 "e2e": e2e, "cpu_baseline": cb}
         print(json.dumps(line), flush=True)
     if world > 1:

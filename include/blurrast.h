@@ -117,6 +117,21 @@ typedef struct {
                                           triangle up again at every sub-frame (same per-pixel work),
                                       2 = naive per-pixel: re-solve w = F(tau)^-1 p (Eq.3) for every
                                           (pixel, face, sub-frame) test (the SoftRas-style baseline) */
+    /* Soft background coverage (NEXT-1; Eq.10-15; A17-A20).  delta > 0
+     * gives every pixel that no face covers at a sub-frame RGB 0 and alpha
+     *   A_i(t) = 1 - prod_j (1 - exp(-d_j / delta)),  d_j = || p - F_j(tau) w^* ||^2  (Eq.15, Eq.10, Eq.14)
+     * with w^* the closest point (A17-A18) of p' = F_j(X) w_j(tau) on the keyframe triangle
+     * F_j(X), X = [tau > 0.5] (Eq.13); delta in NDC^2 (the paper's 1e-4; Q9).  The
+     * backward then also carries dL/dalpha into the vertex gradients, w^* held constant.
+     * Needs solver 0.  delta = 0: hard coverage only (alpha = coverage, the delta -> 0 limit). */
+    float delta;
+    float soft_cut;                /* faces with d > soft_cut * delta are dropped (their term is below
+                                      exp(-soft_cut)); 0 = default 24 (Q21) */
+    int32_t soft_exact;            /* 1: Eq.12 (closest point on F(tau) itself) instead of Eq.13 */
+    float soft_bin_factor;         /* soft-bin entry capacity per (chunk, face) (0 = default 12); see
+                                      blur_read_soft_bins */
+    void *soft_events[2];          /* host cudaEvent_t pair or NULLs: recorded around the soft kernel
+                                      (K8 in fwd, K9 in bwd) */
 } blur_config;
 
 /* Bytes of device workspace the render calls need for these arguments (0 + blur_last_error() on
@@ -140,7 +155,8 @@ int blur_render_fwd(const float *verts, int V, const int32_t *faces, int F, cons
 
 /* Backward: grad_rgba [B,H,W,4] = dL/d out_rgba (device).  grad_verts [V,3] and grad_colors [V,3]
  * are OVERWRITTEN with dL/dverts (world) and dL/dcolors summed over the B images and the sub-frame
- * ranges.  The alpha channel carries no position gradient in the hard-coverage path.
+ * ranges.  The alpha channel carries no position gradient in the hard-coverage path; with
+ * cfg->delta > 0 it does, through the soft background term (w^* frozen).
  * With cfg->flags & BLUR_REUSE_SETUP the setup stages of the preceding blur_render_fwd on the same
  * workspace with identical arguments are reused. */
 int blur_render_bwd(const float *verts, int V, const int32_t *faces, int F, const float *colors,
@@ -158,6 +174,14 @@ int blur_l2_loss_grad(const float *out, const float *target, int64_t n, int64_t 
 /* Synchronises `stream`, reads the status word of `ws` (BLUR_ST_* bits) into *status_out (host) and
  * clears it. */
 int blur_read_status(void *ws, blur_stream_t stream, int32_t *status_out);
+
+/* Synchronises `stream` and reports, for the last binning done in `ws`, the number of bin entries
+ * the geometry needed (*needed, host) and the capacity the workspace had (*capacity, host).  When
+ * needed > capacity the affected tiles took the exact slow path (BLUR_EOVERFLOW): size the next
+ * workspace with cfg->bin_factor scaled by needed / capacity.  blur_read_soft_bins: the same for
+ * the soft-coverage bins (cfg->soft_bin_factor; 0 / 0 when delta == 0). */
+int blur_read_bins(void *ws, blur_stream_t stream, long long *needed, long long *capacity);
+int blur_read_soft_bins(void *ws, blur_stream_t stream, long long *needed, long long *capacity);
 
 /* FP32 FFMA throughput microbenchmark (roofline denominator): runs `iters` iterations of 8
  * independent FMA chains per thread on ctas x 256 threads; writes 2 * flops-per-launch into

@@ -388,8 +388,8 @@ int om_closest_w(const double x[3], const double y[3], double pu, double pv, con
  *   d = || F(tau) w(tau) - F(tau) w^* ||^2 = || p - F(tau) w^* ||^2 (Eq.14);
  *   A = exp(-d / delta) (Eq.10 with the exponential kernel, A20).
  * Outputs A, d, what (w^*), pstar = F(tau) w^* (2), and, when amb != NULL, amb[0] = the largest
- * |A' - A| over the edge candidates whose F(X) distance is within eps of the chosen one (their
- * sqrt distances differ by <= eps NDC: a rounding-level tie, Q16/Q20).  Returns 0 if F(tau) is
+ * |A' - A| over the edge candidates that a move of p' by eps NDC could make the closest one
+ * (Q20: |d_c - d_e| <= 2 eps |q_c - q_e| + 1e-6 max(d_c, d_e)).  Returns 0 if F(tau) is
  * degenerate (Q8: the face is skipped for this sub-frame), else 1. */
 int om_soft_pair(const double X0[3], const double Y0[3], const double X1[3], const double Y1[3], double tau,
                  double u, double v, double delta, int exact, double eps, double *A, double *d, double what[3],
@@ -414,8 +414,18 @@ int om_soft_pair(const double X0[3], const double Y0[3], const double X1[3], con
     if (amb) {
         amb[0] = 0.0;
         if (e >= 0 && eps > 0) {
+            /* a candidate is a tie if moving p' by eps could make it the closer one:
+             * |d_c - d_e| <= 2 eps |q_c - q_e| (first order), plus 1e-6 relative for rounding */
+            const double *we = cand + 3 * e;
+            double qex = we[0] * xk[0] + we[1] * xk[1] + we[2] * xk[2];
+            double qey = we[0] * yk[0] + we[1] * yk[1] + we[2] * yk[2];
             for (int c = 0; c < 3; ++c) {
-                if (c == e || !(fabs(sqrt(cd[c]) - sqrt(dX)) <= eps)) continue;
+                if (c == e) continue;
+                const double *wq = cand + 3 * c;
+                double qcx = wq[0] * xk[0] + wq[1] * xk[1] + wq[2] * xk[2];
+                double qcy = wq[0] * yk[0] + wq[1] * yk[1] + wq[2] * yk[2];
+                double sep = hypot(qcx - qex, qcy - qey);
+                if (!(fabs(cd[c] - dX) <= 2.0 * eps * sep + 1e-6 * fmax(cd[c], dX))) continue;
                 const double *wc = cand + 3 * c;
                 double qx = wc[0] * xt[0] + wc[1] * xt[1] + wc[2] * xt[2];
                 double qy = wc[0] * yt[0] + wc[1] * yt[1] + wc[2] * yt[2];

@@ -24,7 +24,9 @@ STATUS_NAMES = {0: "BLUR_OK", 1: "BLUR_EINVAL", 2: "BLUR_EBEHIND", 3: "BLUR_ENOM
                 5: "BLUR_EOVERFLOW"}
 
 EXPORTED = ["blur_workspace_bytes", "blur_render_fwd", "blur_render_bwd", "blur_l2_loss_grad",
-            "blur_read_status", "blur_read_bins", "blur_ffma_probe", "blur_last_error", "blur_abi_version"]
+            "blur_read_status", "blur_read_bins", "blur_read_soft_bins", "blur_ffma_probe", "blur_last_error",
+            "blur_abi_version"]
+ABI_VERSION = 2
 
 
 class BlurError(RuntimeError):
@@ -45,7 +47,9 @@ class blur_camera(C.Structure):
 
 class blur_config(C.Structure):
     _fields_ = [("max_chunk", C.c_int32), ("flags", C.c_int32), ("bin_factor", C.c_float),
-                ("census", C.c_void_p), ("raster_events", C.c_void_p * 2), ("solver", C.c_int32)]
+                ("census", C.c_void_p), ("raster_events", C.c_void_p * 2), ("solver", C.c_int32),
+                ("delta", C.c_float), ("soft_cut", C.c_float), ("soft_exact", C.c_int32),
+                ("soft_bin_factor", C.c_float), ("soft_events", C.c_void_p * 2)]
 
 
 def load():
@@ -65,9 +69,12 @@ def load():
         lib.blur_l2_loss_grad.argtypes = [P, P, C.c_int64, C.c_int64, P, P, P]
         lib.blur_read_status.argtypes = [P, P, P]
         lib.blur_read_bins.argtypes = [P, P, P, P]
+        lib.blur_read_soft_bins.argtypes = [P, P, P, P]
         lib.blur_ffma_probe.argtypes = [I, I, P, P, P]
         lib.blur_last_error.restype = C.c_char_p
         lib.blur_abi_version.restype = I
+        if lib.blur_abi_version() != ABI_VERSION:
+            raise ImportError("libblurrast.so ABI %d != binding ABI %d: rebuild" % (lib.blur_abi_version(), ABI_VERSION))
         _lib = lib
         return lib
 
@@ -138,14 +145,23 @@ def make_sub_range(sub_range):
     return a
 
 
-def make_config(max_chunk=0, flags=0, bin_factor=0.0, census=None, events=None, solver=0):
-    """events: optional (torch.cuda.Event, torch.cuda.Event) recorded around the raster kernel."""
+def make_config(max_chunk=0, flags=0, bin_factor=0.0, census=None, events=None, solver=0, delta=0.0,
+                soft_cut=0.0, soft_exact=False, soft_bin_factor=0.0, soft_events=None):
+    """events / soft_events: optional (torch.cuda.Event, torch.cuda.Event) recorded around the raster
+    kernel / the soft-coverage kernel."""
     cfg = blur_config(int(max_chunk), int(flags), float(bin_factor),
                       None if census is None else C.c_void_p(census.data_ptr()))
     cfg.solver = int(solver)
+    cfg.delta = float(delta)
+    cfg.soft_cut = float(soft_cut)
+    cfg.soft_exact = int(bool(soft_exact))
+    cfg.soft_bin_factor = float(soft_bin_factor)
     if events is not None:
         cfg.raster_events[0] = events[0].cuda_event
         cfg.raster_events[1] = events[1].cuda_event
+    if soft_events is not None:
+        cfg.soft_events[0] = soft_events[0].cuda_event
+        cfg.soft_events[1] = soft_events[1].cuda_event
     return cfg
 
 
@@ -210,6 +226,14 @@ def blur_read_bins(ws, stream=None):
     import torch
     need, cap = C.c_longlong(0), C.c_longlong(0)
     _check(load().blur_read_bins(_dev(ws, torch.uint8, "ws"), _stream(stream), C.byref(need), C.byref(cap)))
+    return int(need.value), int(cap.value)
+
+
+def blur_read_soft_bins(ws, stream=None):
+    """The same for the soft-coverage bins (0, 0 when delta == 0); synchronises."""
+    import torch
+    need, cap = C.c_longlong(0), C.c_longlong(0)
+    _check(load().blur_read_soft_bins(_dev(ws, torch.uint8, "ws"), _stream(stream), C.byref(need), C.byref(cap)))
     return int(need.value), int(cap.value)
 
 

@@ -82,6 +82,12 @@ struct Plan {
     size_t nbins = 0;
     size_t o_status = 0, o_imgs = 0, o_chunks = 0, o_ss = 0, o_st = 0, o_poses = 0, o_tables_end = 0;
     size_t o_key = 0, o_rec = 0, o_fcol = 0, o_cnt = 0, o_off = 0, o_bsum = 0, o_ent = 0, o_dkey = 0, o_part = 0;
+    // soft background coverage (NEXT-1)
+    bool soft = false;
+    float delta = 0.f, rcut = 0.f;
+    int soft_exact = 0;
+    long long scap = 0, n_sub = 0;
+    size_t o_cov = 0, o_spart = 0, o_scnt = 0, o_soff = 0, o_sbsum = 0, o_sent = 0;
     size_t total = 0;
 };
 
@@ -158,6 +164,8 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
         P.sched_tau.insert(P.sched_tau.end(), tt.begin(), tt.end());
         im.key_off = key_off;
         key_off += (S + 1) * V;
+        im.cov_off = (int)P.n_sub;
+        P.n_sub += N;
         im.rec_off = rec_off;
         rec_off += (long long)S * F;
         // camera
@@ -233,6 +241,21 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
     }
     P.n_key = key_off;
     P.n_rec = rec_off;
+    // soft background coverage (NEXT-1): bandwidth, cut-off radius, capacity of the grown bins
+    if (cfg && cfg->delta != 0.f) {
+        if (!(cfg->delta > 0.f) || !std::isfinite(cfg->delta)) return fail(BLUR_EINVAL, "delta must be >= 0 and finite");
+        if (cfg->solver != 0) return fail(BLUR_EINVAL, "soft coverage (delta > 0) needs solver 0");
+        const float kc = cfg->soft_cut > 0.f ? cfg->soft_cut : 24.f;
+        if (!std::isfinite(kc)) return fail(BLUR_EINVAL, "soft_cut must be finite");
+        P.soft = true;
+        P.delta = cfg->delta;
+        P.rcut = (float)std::sqrt((double)kc * (double)cfg->delta) + 2.0f * BBOX_PAD;
+        P.soft_exact = cfg->soft_exact ? 1 : 0;
+        const double sf = cfg->soft_bin_factor > 0.f ? cfg->soft_bin_factor : 12.0;
+        double sc = sf * (double)P.NC * (double)F + 16.0 * (double)P.T;
+        if (sc > 6.0e9) sc = 6.0e9;
+        P.scap = (long long)sc;
+    }
     P.nbins = (size_t)P.NC * P.T;
     if (P.nbins > (size_t)0x7fffffff) return fail(BLUR_EINVAL, "too many (chunk, tile) bins");
     const double factor = (cfg && cfg->bin_factor > 0.f) ? cfg->bin_factor : 3.0;
@@ -257,6 +280,14 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
     P.o_ent = o; o = align256(o + 4 * (size_t)P.cap);
     P.o_dkey = o; o = align256(o + 8 * (size_t)P.n_key);
     P.o_part = o; o = align256(o + (P.splits > 1 ? 16 * (size_t)P.splits * B * H * W : 0));
+    if (P.soft) {
+        P.o_cov = o; o = align256(o + 4 * (size_t)P.n_sub * P.T * (NT / 32));
+        P.o_spart = o; o = align256(o + 4 * (size_t)P.splits * B * H * W);
+        P.o_scnt = o; o = align256(o + 4 * P.nbins);
+        P.o_soff = o; o = align256(o + 8 * (P.nbins + 1));
+        P.o_sbsum = o; o = align256(o + 8 * ((P.nbins + 1023) / 1024 + 1));
+        P.o_sent = o; o = align256(o + 4 * (size_t)P.scap);
+    }
     P.total = o;
     return BLUR_OK;
 }
@@ -286,7 +317,34 @@ Tables make_tables(const Plan &P, void *ws)
     t.splits = P.splits;
     t.part = (float4 *)(w + P.o_part);
     t.B = P.B; t.V = P.V; t.F = P.F; t.H = P.H; t.W = P.W;
+    if (P.soft) {
+        t.delta = P.delta;
+        t.rcut = P.rcut;
+        t.soft_exact = P.soft_exact;
+        t.covbits = (uint32_t *)(w + P.o_cov);
+        t.spart = (float *)(w + P.o_spart);
+        t.sb.cnt = (int *)(w + P.o_scnt);
+        t.sb.off = (long long *)(w + P.o_soff);
+        t.sb.bsum = (long long *)(w + P.o_sbsum);
+        t.sb.entries = (int *)(w + P.o_sent);
+        t.sb.cap = P.scap;
+        t.sb.binstat = (long long *)(w + P.o_status + 24);
+        t.sb.sortcap = 4096;
+    }
     return t;
+}
+
+BinSet hard_bins(const Tables &t)
+{
+    BinSet b;
+    b.cnt = t.cnt;
+    b.off = t.off;
+    b.bsum = t.bsum;
+    b.entries = t.entries;
+    b.cap = t.cap;
+    b.binstat = t.binstat;
+    b.sortcap = SORTCAP;
+    return b;
 }
 
 int upload_tables(const Plan &P, void *ws, cudaStream_t st)
@@ -357,7 +415,9 @@ int prepare(const float *verts, int V, const int32_t *faces, int F, const float 
     if (r) return r;
     r = cuda_check(launch_setup(t, verts, faces, colors, P.maxS, st), "setup kernels");
     if (r) return r;
-    return cuda_check(launch_binning(t, st), "binning kernels");
+    r = cuda_check(launch_binning(t, hard_bins(t), 0.f, st), "binning kernels");
+    if (r || !P.soft) return r;
+    return cuda_check(launch_binning(t, t.sb, P.rcut, st), "soft binning kernels");
 }
 
 }  // namespace
@@ -366,7 +426,7 @@ extern "C" {
 
 const char *blur_last_error(void) { return g_err.c_str(); }
 
-int blur_abi_version(void) { return 1; }
+int blur_abi_version(void) { return 2; }
 
 size_t blur_workspace_bytes(int V, int F, int B, int H, int W, const blur_motion *motions,
                             const blur_camera *cams, const int32_t *sub_range, const blur_config *cfg)
@@ -399,6 +459,12 @@ int blur_render_fwd(const float *verts, int V, const int32_t *faces, int F, cons
         if (r) return r;
     }
     if (cfg && cfg->raster_events[1]) cudaEventRecord((cudaEvent_t)cfg->raster_events[1], st);
+    if (P.soft) {   // NEXT-1: background alpha of the uncovered (pixel, sub-frame) pairs K4 recorded
+        if (cfg->soft_events[0]) cudaEventRecord((cudaEvent_t)cfg->soft_events[0], st);
+        r = cuda_check(launch_soft_fwd(t, out_rgba, st), "soft fwd");
+        if (r) return r;
+        if (cfg->soft_events[1]) cudaEventRecord((cudaEvent_t)cfg->soft_events[1], st);
+    }
     if (check_env()) return sync_status(ws, P, st);
     return BLUR_OK;
 }
@@ -426,10 +492,20 @@ int blur_render_bwd(const float *verts, int V, const int32_t *faces, int F, cons
         r = cuda_check(cudaMemsetAsync(t.dkey, 0, 8 * (size_t)P.n_key, st), "dkey clear");
         if (r) return r;
     }
+    if (P.soft && !reuse) {   // coverage of every (pixel, sub-frame) for the soft term (no image written)
+        r = cuda_check(launch_raster_fwd(t, nullptr, nullptr, -1, nullptr, st), "coverage pass");
+        if (r) return r;
+    }
     if (cfg && cfg->raster_events[0]) cudaEventRecord((cudaEvent_t)cfg->raster_events[0], st);
     r = cuda_check(launch_raster_bwd(t, grad_rgba, grad_colors, st), "raster bwd");
     if (r) return r;
     if (cfg && cfg->raster_events[1]) cudaEventRecord((cudaEvent_t)cfg->raster_events[1], st);
+    if (P.soft) {
+        if (cfg->soft_events[0]) cudaEventRecord((cudaEvent_t)cfg->soft_events[0], st);
+        r = cuda_check(launch_soft_bwd(t, grad_rgba, st), "soft bwd");
+        if (r) return r;
+        if (cfg->soft_events[1]) cudaEventRecord((cudaEvent_t)cfg->soft_events[1], st);
+    }
     r = cuda_check(launch_vertex_chain(t, grad_verts, st), "vertex chain");
     if (r) return r;
     if (check_env()) return sync_status(ws, P, st);
@@ -468,6 +544,21 @@ int blur_read_bins(void *ws, blur_stream_t stream, long long *needed, long long 
     cudaStream_t st = (cudaStream_t)stream;
     long long h[2] = {0, 0};
     int r = cuda_check(cudaMemcpyAsync(h, (char *)ws + 8, sizeof(h), cudaMemcpyDeviceToHost, st), "bins read");
+    if (r) return r;
+    r = cuda_check(cudaStreamSynchronize(st), "stream sync");
+    if (r) return r;
+    *needed = h[0];
+    *capacity = h[1];
+    return BLUR_OK;
+}
+
+int blur_read_soft_bins(void *ws, blur_stream_t stream, long long *needed, long long *capacity)
+{
+    g_err.clear();
+    if (!ws || !needed || !capacity) return fail(BLUR_EINVAL, "NULL pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    long long h[2] = {0, 0};
+    int r = cuda_check(cudaMemcpyAsync(h, (char *)ws + 24, sizeof(h), cudaMemcpyDeviceToHost, st), "bins read");
     if (r) return r;
     r = cuda_check(cudaStreamSynchronize(st), "stream sync");
     if (r) return r;

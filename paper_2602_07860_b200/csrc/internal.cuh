@@ -38,7 +38,7 @@ struct ImgInfo {
     long long rec_off;   // offset (records) of coefficient records [S][F]
     int chunk_begin, chunk_end;
     int pose_off;        // offset (in PoseRec) of keyframe poses [S+1]
-    int pad0;
+    int cov_off;         // soft path: offset (sub-frames) of this image's coverage words
     double Rc[9];        // camera rotation rows (right, up', forward)
     double eye[3];
     double tan_half;     // tan(half_fov)
@@ -54,6 +54,16 @@ struct PoseRec {         // P = R (P0 - c) + c + T at keyframe time t = s/S
 struct Chunk {           // consecutive sub-frames of one image inside one segment
     int b, s, k0, k1;    // sub-frames k0..k1-1 (image-local indices)
     float tmin, tmax;    // tau of the first / last sub-frame
+};
+
+struct BinSet {          // one set of (chunk, tile) bins (K3): counters, offsets, sorted entries
+    int *cnt;            // [NC * T]
+    long long *off;      // [NC * T + 1] bin offsets (64-bit: large batches exceed 2^31 entries)
+    long long *bsum;     // scan block sums
+    int *entries;        // bin entries (face ids)
+    long long cap;       // entries capacity
+    long long *binstat;  // [0] entries the last binning needed, [1] capacity
+    int sortcap;         // bins longer than this are not sorted (raster kernels take the exact fallback)
 };
 
 struct Tables {          // device pointers into the workspace
@@ -78,6 +88,13 @@ struct Tables {          // device pointers into the workspace
     int solver;          // 0 fast (Eq.8 coefficients), 1 naive per-frame setup, 2 naive per-pixel solve
     int splits;          // CTAs sharing one (image, tile) by sub-frame chunks (small launches)
     float4 *part;        // splits > 1: per-split partial images [splits][B*H*W]
+    // soft background coverage (NEXT-1; delta > 0)
+    float delta;         // Eq.10 bandwidth (NDC^2)
+    float rcut;          // NDC radius beyond which a face's term is dropped: sqrt(soft_cut * delta)
+    int soft_exact;      // 1: Eq.12 (closest point on F(tau)) instead of Eq.13 (on F(X))
+    uint32_t *covbits;   // [sum_b N_b][T][NWARP] coverage ballots per (sub-frame, tile, warp) or null
+    float *spart;        // [splits][B*H*W] soft alpha partial sums (K8)
+    BinSet sb;           // soft bins (chunk boxes dilated by rcut)
 };
 
 struct __align__(16) TauRec {    // per (face, sub-frame, tile) staged record, 64 B
@@ -103,6 +120,12 @@ __device__ __forceinline__ void ndc_to_index(float lo, float hi, int n, bool fli
     }
 }
 
+// soft path: first of the NWARP coverage words of (image, sub-frame k, tile)
+__device__ __forceinline__ size_t cov_word(const Tables &t, const ImgInfo &im, int k, int tile)
+{
+    return ((size_t)(im.cov_off + k) * t.T + tile) * (NT / 32);
+}
+
 // conservative keyframe box lerped to tau (monotone in tau for fixed endpoints)
 __device__ __forceinline__ float box_lerp(float tau, float a, float b) { return __fmaf_rn(tau, __fsub_rn(b, a), a); }
 
@@ -112,7 +135,9 @@ __device__ __forceinline__ float box_lerp(float tau, float a, float b) { return 
 namespace br {
 cudaError_t launch_setup(const Tables &t, const float *verts, const int *faces, const float *colors,
                          int maxS, cudaStream_t st);
-cudaError_t launch_binning(const Tables &t, cudaStream_t st);
+cudaError_t launch_binning(const Tables &t, const BinSet &bs, float dil, cudaStream_t st);
+cudaError_t launch_soft_fwd(const Tables &t, float *out, cudaStream_t st);
+cudaError_t launch_soft_bwd(const Tables &t, const float *grad_rgba, cudaStream_t st);
 cudaError_t launch_raster_fwd(const Tables &t, float *out, int *ids, int ids_k,
                               unsigned long long *census, cudaStream_t st);
 cudaError_t launch_raster_bwd(const Tables &t, const float *grad_rgba, float *grad_colors,

@@ -12,6 +12,7 @@
 //              kernels visit faces in index order (Z-buffer tie rule: lower index wins, Q7)
 // Bins longer than SORTCAP or beyond the entry capacity are left to the raster kernels' exact
 // fallback path (status bit BLUR_ST_EOVERFLOW).
+#include <algorithm>
 #include <cstdio>
 
 #include "internal.cuh"
@@ -37,23 +38,24 @@ __device__ __forceinline__ bool ndc_box_to_pixels(float xmn, float xmx, float ym
     return true;
 }
 
-__device__ __forceinline__ bool swept_tiles(const Tables &t, const float4 *r, float tmin, float tmax,
+// swept box of the chunk, grown by dil (soft bins: the NEXT-1 cut-off radius; 0 for the hard bins)
+__device__ __forceinline__ bool swept_tiles(const Tables &t, const float4 *r, float tmin, float tmax, float dil,
                                             int &tx0, int &tx1, int &ty0, int &ty1)
 {
     const float4 q6 = r[6];
     if (__float_as_int(q6.w) < 0) return false;
     const float4 b0 = r[7], b1 = r[8];
-    const float xmn = fminf(lerpf_(tmin, b0.x, b1.x), lerpf_(tmax, b0.x, b1.x));
-    const float xmx = fmaxf(lerpf_(tmin, b0.y, b1.y), lerpf_(tmax, b0.y, b1.y));
-    const float ymn = fminf(lerpf_(tmin, b0.z, b1.z), lerpf_(tmax, b0.z, b1.z));
-    const float ymx = fmaxf(lerpf_(tmin, b0.w, b1.w), lerpf_(tmax, b0.w, b1.w));
+    const float xmn = __fsub_rn(fminf(lerpf_(tmin, b0.x, b1.x), lerpf_(tmax, b0.x, b1.x)), dil);
+    const float xmx = __fadd_rn(fmaxf(lerpf_(tmin, b0.y, b1.y), lerpf_(tmax, b0.y, b1.y)), dil);
+    const float ymn = __fsub_rn(fminf(lerpf_(tmin, b0.z, b1.z), lerpf_(tmax, b0.z, b1.z)), dil);
+    const float ymx = __fadd_rn(fmaxf(lerpf_(tmin, b0.w, b1.w), lerpf_(tmax, b0.w, b1.w)), dil);
     int i0, i1, j0, j1;
     if (!ndc_box_to_pixels(xmn, xmx, ymn, ymx, t.W, t.H, i0, i1, j0, j1)) return false;
     tx0 = i0 / TW; tx1 = i1 / TW; ty0 = j0 / TH; ty1 = j1 / TH;
     return true;
 }
 
-__global__ void __launch_bounds__(256) k3_count(Tables t)
+__global__ void __launch_bounds__(256) k3_count(Tables t, BinSet bs, float dil)
 {
     const int c = blockIdx.y;
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
@@ -62,13 +64,13 @@ __global__ void __launch_bounds__(256) k3_count(Tables t)
     const ImgInfo &im = t.imgs[ch.b];
     const float4 *r = t.rec + (size_t)(im.rec_off + (long long)ch.s * t.F + f) * REC_F4;
     int tx0, tx1, ty0, ty1;
-    if (!swept_tiles(t, r, ch.tmin, ch.tmax, tx0, tx1, ty0, ty1)) return;
-    int *cnt = t.cnt + (size_t)c * t.T;
+    if (!swept_tiles(t, r, ch.tmin, ch.tmax, dil, tx0, tx1, ty0, ty1)) return;
+    int *cnt = bs.cnt + (size_t)c * t.T;
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(cnt + ty * t.TX + tx, 1);
 }
 
-__global__ void __launch_bounds__(256) k3_fill(Tables t)
+__global__ void __launch_bounds__(256) k3_fill(Tables t, BinSet bs, float dil)
 {
     const int c = blockIdx.y;
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
@@ -77,14 +79,14 @@ __global__ void __launch_bounds__(256) k3_fill(Tables t)
     const ImgInfo &im = t.imgs[ch.b];
     const float4 *r = t.rec + (size_t)(im.rec_off + (long long)ch.s * t.F + f) * REC_F4;
     int tx0, tx1, ty0, ty1;
-    if (!swept_tiles(t, r, ch.tmin, ch.tmax, tx0, tx1, ty0, ty1)) return;
+    if (!swept_tiles(t, r, ch.tmin, ch.tmax, dil, tx0, tx1, ty0, ty1)) return;
     const size_t base = (size_t)c * t.T;
     bool ovf = false;
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
             const size_t bi = base + ty * t.TX + tx;
-            const long long pos = (long long)t.off[bi] + atomicAdd(t.cnt + bi, 1);
-            if (pos < t.cap) t.entries[pos] = f;
+            const long long pos = (long long)bs.off[bi] + atomicAdd(bs.cnt + bi, 1);
+            if (pos < bs.cap) bs.entries[pos] = f;
             else ovf = true;
         }
     if (ovf) atomicOr(t.status, BLUR_ST_EOVERFLOW);
@@ -182,18 +184,18 @@ __global__ void __launch_bounds__(256) k3_scan_add(long long *off, const long lo
 }
 
 // ---- per-bin bitonic sort (one warp per bin)
-__global__ void __launch_bounds__(256) k3_sort(Tables t, int nbins)
+__global__ void __launch_bounds__(256) k3_sort(Tables t, BinSet bs, int nbins)
 {
     __shared__ int sm[8][SORTCAP];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int *s = sm[warp];
     for (int bi = blockIdx.x * 8 + warp; bi < nbins; bi += gridDim.x * 8) {
-        const long long o = t.off[bi];
-        const int n = (int)(t.off[bi + 1] - o);
-        if (n <= 1 || n > SORTCAP || o + n > t.cap) continue;
+        const long long o = bs.off[bi];
+        const int n = (int)(bs.off[bi + 1] - o);
+        if (n <= 1 || n > SORTCAP || o + n > bs.cap) continue;
         int n2 = 32;
         while (n2 < n) n2 <<= 1;
-        for (int i = lane; i < n2; i += 32) s[i] = i < n ? t.entries[o + i] : 0x7fffffff;
+        for (int i = lane; i < n2; i += 32) s[i] = i < n ? bs.entries[o + i] : 0x7fffffff;
         __syncwarp();
         for (int k = 2; k <= n2; k <<= 1)
             for (int j = k >> 1; j > 0; j >>= 1) {
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(256) k3_sort(Tables t, int nbins)
         // self-check: a sorted bin holds distinct ids in [0, F)
         bool bad = false;
         for (int i = lane; i < n; i += 32) {
-            t.entries[o + i] = s[i];
+            bs.entries[o + i] = s[i];
             bad |= s[i] < 0 || s[i] >= t.F || (i > 0 && s[i - 1] >= s[i]);
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0) {
@@ -223,28 +225,66 @@ __global__ void __launch_bounds__(256) k3_sort(Tables t, int nbins)
     }
 }
 
-cudaError_t launch_binning(const Tables &t, cudaStream_t st)
+// ---- CTA-per-bin bitonic sort of the bins longer than SORTCAP (soft bins, up to bs.sortcap)
+constexpr int SORTCAP_BIG = 4096;
+__global__ void __launch_bounds__(512) k3_sort_big(Tables t, BinSet bs, int nbins)
+{
+    __shared__ int s[SORTCAP_BIG];
+    __shared__ int bad;
+    for (int bi = blockIdx.x; bi < nbins; bi += gridDim.x) {
+        const long long o = bs.off[bi];
+        const int n = (int)(bs.off[bi + 1] - o);
+        if (n <= SORTCAP || n > bs.sortcap || o + n > bs.cap) continue;   // block-uniform
+        int n2 = 2 * SORTCAP;
+        while (n2 < n) n2 <<= 1;
+        if (threadIdx.x == 0) bad = 0;
+        for (int i = threadIdx.x; i < n2; i += blockDim.x) s[i] = i < n ? bs.entries[o + i] : 0x7fffffff;
+        __syncthreads();
+        for (int k = 2; k <= n2; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const int a = s[i], b = s[ixj];
+                        const bool up = (i & k) == 0;
+                        if ((a > b) == up) { s[i] = b; s[ixj] = a; }
+                    }
+                }
+                __syncthreads();
+            }
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            bs.entries[o + i] = s[i];
+            if (s[i] < 0 || s[i] >= t.F || (i > 0 && s[i - 1] >= s[i])) bad = 1;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && bad) atomicOr(t.status, BLUR_ST_EINTERNAL);
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_binning(const Tables &t, const BinSet &bs, float dil, cudaStream_t st)
 {
     const int nbins = t.NC * t.T;
     if (nbins == 0) return cudaSuccess;
-    cudaError_t e = cudaMemsetAsync(t.cnt, 0, sizeof(int) * (size_t)nbins, st);
+    cudaError_t e = cudaMemsetAsync(bs.cnt, 0, sizeof(int) * (size_t)nbins, st);
     if (e != cudaSuccess) return e;
     if (t.F > 0) {
         dim3 grid((t.F + 255) / 256, t.NC);
-        k3_count<<<grid, 256, 0, st>>>(t);
+        k3_count<<<grid, 256, 0, st>>>(t, bs, dil);
     }
     const int nb = (nbins + 1023) / 1024;
-    k3_scan_blocks<<<nb, 256, 0, st>>>(t.cnt, t.off, t.bsum, nbins);
-    k3_scan_sums<<<1, 256, 0, st>>>(t.bsum, nb, t.off, nbins, t.binstat, t.cap);
-    k3_scan_add<<<nb, 256, 0, st>>>(t.off, t.bsum, nbins);
-    e = cudaMemsetAsync(t.cnt, 0, sizeof(int) * (size_t)nbins, st);
+    k3_scan_blocks<<<nb, 256, 0, st>>>(bs.cnt, bs.off, bs.bsum, nbins);
+    k3_scan_sums<<<1, 256, 0, st>>>(bs.bsum, nb, bs.off, nbins, bs.binstat, bs.cap);
+    k3_scan_add<<<nb, 256, 0, st>>>(bs.off, bs.bsum, nbins);
+    e = cudaMemsetAsync(bs.cnt, 0, sizeof(int) * (size_t)nbins, st);
     if (e != cudaSuccess) return e;
     if (t.F > 0) {
         dim3 grid((t.F + 255) / 256, t.NC);
-        k3_fill<<<grid, 256, 0, st>>>(t);
+        k3_fill<<<grid, 256, 0, st>>>(t, bs, dil);
         int sb = (nbins + 7) / 8;
         if (sb > 148 * 16) sb = 148 * 16;
-        k3_sort<<<sb, 256, 0, st>>>(t, nbins);
+        k3_sort<<<sb, 256, 0, st>>>(t, bs, nbins);
+        if (bs.sortcap > SORTCAP) k3_sort_big<<<std::min(nbins, 148 * 4), 512, 0, st>>>(t, bs, nbins);
     }
     return cudaGetLastError();
 }

@@ -437,6 +437,11 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
         const int n = (int)(t.off[bi + 1] - o);
         if (n == 0) {
             if (ids && inimg && ids_k >= ch.k0 && ids_k < ch.k1) ids[pix] = -1;
+            if (t.covbits) {
+                const unsigned m = __ballot_sync(0xffffffffu, !inimg);
+                if (lane == 0)
+                    for (int k = ch.k0; k < ch.k1; ++k) t.covbits[cov_word(t, im, k, tile) + warp] = m;
+            }
             continue;
         }
         BinCtx bc;
@@ -473,6 +478,10 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
                         if (CENSUS) nshade++;
                     }
                     if (ids && inimg && kg + l == ids_k) ids[pix] = fid;
+                    if (t.covbits) {   // soft path: which pixels of the warp are covered at this sub-frame
+                        const unsigned m = __ballot_sync(0xffffffffu, ebest >= 0 || !inimg);
+                        if (lane == 0) t.covbits[cov_word(t, im, kg + l, tile) + warp] = m;
+                    }
                 }
                 __syncthreads();
             }
@@ -505,10 +514,14 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
                 }
                 if (has) { ar += pr; ag += pg; ab += pb; aa += 1.f; if (CENSUS) nshade++; }
                 if (ids && inimg && k == ids_k) ids[pix] = has ? bfid : -1;
+                if (t.covbits) {
+                    const unsigned m = __ballot_sync(0xffffffffu, has || !inimg);
+                    if (lane == 0) t.covbits[cov_word(t, im, k, tile) + warp] = m;
+                }
             }
         }
     }
-    if (inimg) {
+    if (inimg && out) {   // out == null: coverage-only pass (soft backward without a preceding forward)
         const float inv = 1.0f / (float)N;
         const float4 v = make_float4(ar * inv, ag * inv, ab * inv, aa * inv);
         if (t.splits == 1) reinterpret_cast<float4 *>(out)[pix] = v;

@@ -23,7 +23,9 @@ class BlurRenderer:
     """
 
     def __init__(self, faces, motion: dict, cams, H: int, W: int, V: int, device="cuda",
-                 sub_range=None, max_chunk: int = 0, bin_factor: float = 0.0, solver: int = 0):
+                 sub_range=None, max_chunk: int = 0, bin_factor: float = 0.0, solver: int = 0,
+                 delta: float = 0.0, soft_cut: float = 0.0, soft_exact: bool = False,
+                 soft_bin_factor: float = 0.0):
         _lib.load()
         self.device = torch.device(device)
         self.faces = torch.as_tensor(np.asarray(faces.cpu() if torch.is_tensor(faces) else faces),
@@ -40,54 +42,64 @@ class BlurRenderer:
         self.max_chunk = int(max_chunk)
         self.bin_factor = float(bin_factor)
         self.solver = int(solver)
-        self.auto_bins = bin_factor == 0.0      # size the bin capacity to the geometry on first use
-        self._alloc(self.bin_factor)
+        # soft background coverage (NEXT-1, Eq.10-15): delta > 0 enables it
+        self.delta, self.soft_cut, self.soft_exact = float(delta), float(soft_cut), bool(soft_exact)
+        self.soft_bin_factor = float(soft_bin_factor)
+        self.auto_bins = bin_factor == 0.0 or (self.delta > 0 and soft_bin_factor == 0.0)
+        self._alloc(self.bin_factor, self.soft_bin_factor)
 
-    def _alloc(self, factor: float):
+    def _cfg(self, flags=0, census=None, events=None, soft_events=None):
+        return _lib.make_config(self.max_chunk, flags, self.bin_factor, census, events, self.solver, self.delta,
+                                self.soft_cut, self.soft_exact, self.soft_bin_factor, soft_events)
+
+    def _alloc(self, factor: float, soft_factor: float = 0.0):
         self.bin_factor = float(factor)
-        cfg = _lib.make_config(self.max_chunk, 0, self.bin_factor)
+        self.soft_bin_factor = float(soft_factor)
+        cfg = self._cfg()
         self.ws_bytes = _lib.blur_workspace_bytes(self.V, self.F, self.B, self.H, self.W, self._motions,
                                                   self._cams, self._sub, cfg)
         self.ws = None
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.ws[:256].zero_()
 
-    def _autosize(self, verts, colors, out, ids, ids_subframe, census, stream, events):
-        """First forward: if the binning needed more entries than the default capacity, grow the
+    def _autosize(self, verts, colors, out, ids, ids_subframe, census, stream, events, soft_events):
+        """First forward: if a binning needed more entries than the default capacity, grow the
         workspace (factor x needed/capacity, +25%) and render again (one synchronisation, once)."""
         self.auto_bins = False
         need, cap = _lib.blur_read_bins(self.ws, stream)
-        if need <= cap or self.F == 0:
+        sneed, scap = _lib.blur_read_soft_bins(self.ws, stream) if self.delta > 0 else (0, 0)
+        if (need <= cap and sneed <= scap) or self.F == 0:
             return out
         base = self.bin_factor if self.bin_factor > 0 else 3.0
-        self._alloc(base * need / max(cap, 1) * 1.25)
+        sbase = self.soft_bin_factor if self.soft_bin_factor > 0 else 12.0
+        self._alloc(base * need / max(cap, 1) * 1.25 if need > cap else base,
+                    sbase * sneed / max(scap, 1) * 1.25 if sneed > scap else sbase)
         if census is not None:
             census.zero_()
-        return self.forward(verts, colors, out, ids, ids_subframe, census, stream, events)
+        return self.forward(verts, colors, out, ids, ids_subframe, census, stream, events, soft_events)
 
     # -- forward / backward -------------------------------------------------------------
     def forward(self, verts: torch.Tensor, colors: torch.Tensor, out: Optional[torch.Tensor] = None,
                 ids: Optional[torch.Tensor] = None, ids_subframe: int = -1, census: Optional[torch.Tensor] = None,
-                stream=None, events=None) -> torch.Tensor:
+                stream=None, events=None, soft_events=None) -> torch.Tensor:
         if out is None:
             out = torch.empty((self.B, self.H, self.W, 4), dtype=torch.float32, device=self.device)
-        cfg = _lib.make_config(self.max_chunk, 0, self.bin_factor, census, events, self.solver)
+        cfg = self._cfg(0, census, events, soft_events)
         _lib.blur_render_fwd(verts, self.faces, colors, self._motions, self._cams, self.B, self.H, self.W, out,
                              self.ws, sub_range=self._sub, ids=ids, ids_subframe=ids_subframe, cfg=cfg,
                              stream=stream)
         if self.auto_bins:
-            return self._autosize(verts, colors, out, ids, ids_subframe, census, stream, events)
+            return self._autosize(verts, colors, out, ids, ids_subframe, census, stream, events, soft_events)
         return out
 
     def backward(self, verts: torch.Tensor, colors: torch.Tensor, grad_rgba: torch.Tensor, reuse_setup: bool = False,
                  grad_verts: Optional[torch.Tensor] = None, grad_colors: Optional[torch.Tensor] = None, stream=None,
-                 events=None):
+                 events=None, soft_events=None):
         if grad_verts is None:
             grad_verts = torch.empty((self.V, 3), dtype=torch.float32, device=self.device)
         if grad_colors is None:
             grad_colors = torch.empty((self.V, 3), dtype=torch.float32, device=self.device)
-        cfg = _lib.make_config(self.max_chunk, _lib.BLUR_REUSE_SETUP if reuse_setup else 0, self.bin_factor,
-                               events=events, solver=self.solver)
+        cfg = self._cfg(_lib.BLUR_REUSE_SETUP if reuse_setup else 0, events=events, soft_events=soft_events)
         _lib.blur_render_bwd(verts, self.faces, colors, self._motions, self._cams, self.B, self.H, self.W,
                              grad_rgba.contiguous(), grad_verts, grad_colors, self.ws, sub_range=self._sub, cfg=cfg,
                              stream=stream)

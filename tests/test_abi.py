@@ -69,8 +69,17 @@ def test_workspace_query_and_validation(lib):
     seg["n_seg"][0] = 3       # 3 does not divide 8
     with pytest.raises(_lib.BlurError):
         _lib.blur_workspace_bytes(sc.V, sc.F, 1, 64, 64, _lib.make_motions(seg), c)
-    assert _lib.blur_abi_version() == 1
+    assert _lib.blur_abi_version() == _lib.ABI_VERSION == 2
     assert np.isfinite(n)
+    # soft background coverage (NEXT-1): extra workspace (coverage words, grown bins); validation
+    ns = _lib.blur_workspace_bytes(sc.V, sc.F, sc.B, 64, 64, m, c, cfg=_lib.make_config(delta=1e-4))
+    assert ns > n
+    with pytest.raises(_lib.BlurError) as e:
+        _lib.blur_workspace_bytes(sc.V, sc.F, sc.B, 64, 64, m, c, cfg=_lib.make_config(delta=-1.0))
+    assert "delta" in str(e.value)
+    with pytest.raises(_lib.BlurError) as e:
+        _lib.blur_workspace_bytes(sc.V, sc.F, sc.B, 64, 64, m, c, cfg=_lib.make_config(delta=1e-4, solver=2))
+    assert "solver" in str(e.value)
 
 
 def test_product_path_has_no_oracle_or_cpu_fallback():

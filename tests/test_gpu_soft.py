@@ -1,0 +1,155 @@
+"""GPU parity of the soft background coverage (NEXT-1, Eq.10-15): CUDA path (K8/K9 through the C ABI)
+vs the fp64 oracle on the same seeded inputs.
+
+Bars as for the hard path (BASELINE north_star): blurred RGBA within 1e-4 max-abs on the pixels the
+oracle does not flag (Q16 coverage ambiguity, Q20 closest-edge ties), vertex gradients within 1e-3
+relative L2 with the same upstream G on both sides (zeroed at flagged pixels, Q18).  The oracle
+sums every face (no cut-off); the GPU drops faces with d > 24 delta (Q21): that changes alpha by at
+most (faces dropped) x exp(-24) < 1e-9 here.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import scenes
+
+pytestmark = pytest.mark.gpu
+
+TOL_IMG = 1e-4
+TOL_GRAD = 1e-3
+
+
+def gpu_soft(sc, delta, G=None, reuse=True, sub_range=None, soft_exact=False, soft_cut=0.0, max_chunk=0,
+             soft_bin_factor=0.0, ids_k=-1):
+    import torch
+    from paper_2602_07860_b200 import BlurRenderer
+    dev = torch.device("cuda:0")
+    r = BlurRenderer(sc.faces, sc.motion, sc.cams, sc.H, sc.W, sc.V, device=dev, sub_range=sub_range,
+                     max_chunk=max_chunk, delta=delta, soft_exact=soft_exact, soft_cut=soft_cut,
+                     soft_bin_factor=soft_bin_factor)
+    v = torch.tensor(np.asarray(sc.verts, np.float32), device=dev)
+    c = torch.tensor(np.asarray(sc.colors, np.float32), device=dev)
+    ids = torch.full((sc.B, sc.H, sc.W), -7, dtype=torch.int32, device=dev) if ids_k >= 0 else None
+    out = r.forward(v, c, ids=ids, ids_subframe=ids_k)
+    res = dict(rgba=out.cpu().numpy(), ids=None if ids is None else ids.cpu().numpy())
+    if G is not None:
+        g = torch.tensor(np.asarray(G, np.float32), device=dev)
+        dv, dc = r.backward(v, c, g, reuse_setup=reuse)
+        res["dv"], res["dc"] = dv.cpu().numpy(), dc.cpu().numpy()
+    torch.cuda.synchronize()
+    res["status"] = r.status()
+    return res
+
+
+def rel_l2(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def check_soft(sc, delta, mode="binned", sub_range=None, soft_exact=False, grad=True, ids_k=0, **kw):
+    ref = oracle.render_fwd(sc, mode=mode, eps_amb=1e-6, sub_range=sub_range, delta=delta, soft_exact=soft_exact,
+                            ids_k=ids_k)
+    G = None
+    if grad:
+        G = 2.0 * (ref["rgba"] - sc.target) / ref["rgba"].size * (~ref["amb_win"])[..., None]
+    got = gpu_soft(sc, delta, G=G, sub_range=sub_range, soft_exact=soft_exact, ids_k=ids_k, **kw)
+    assert not (got["status"] & 8), "internal consistency check failed"
+    ok = ~ref["amb_img"]
+    err = np.abs(got["rgba"] - ref["rgba"])
+    assert err[ok].max() < TOL_IMG, "image max err %g (all pixels %g)" % (err[ok].max(), err.max())
+    mism = (got["ids"] != ref["ids"]) & ~ref["amb_ids"]
+    assert not mism.any(), "id mismatch at %d pixels" % mism.sum()
+    soft_px = int(((ref["rgba"][..., 3] > 1e-6) & (ref["rgba"][..., 3] < 1 - 1e-6)).sum())
+    out = dict(img_err=float(err[ok].max()), alpha_err=float(err[..., 3][ok].max()), amb=int((~ok).sum()),
+               soft_pixels=soft_px)
+    if grad:
+        rdv, rdc = oracle.render_bwd(sc, G, mode=mode, sub_range=sub_range, delta=delta, soft_exact=soft_exact)
+        hdv, _ = oracle.render_bwd(sc, G, mode=mode, sub_range=sub_range)
+        ev, ec = rel_l2(got["dv"], rdv), rel_l2(got["dc"], rdc)
+        assert ev < TOL_GRAD and ec < TOL_GRAD, "grad rel L2 dV %g dC %g" % (ev, ec)
+        out.update(dv=ev, dc=ec, soft_share=rel_l2(rdv, hdv))
+    return out
+
+
+@pytest.mark.parametrize("delta", [1e-4, 1e-3])
+def test_soft_c1(delta):
+    r = check_soft(scenes.make_c1(), delta, mode="brute", ids_k=3)
+    print(r)
+    assert r["soft_pixels"] > 20
+
+
+def test_soft_c2_view_subframes():
+    """C2 (256^2, 1,280 faces), one view, a 12-sub-frame range (the oracle sums every face)."""
+    sc = scenes.make_c2().subset([1])
+    r = check_soft(sc, 1e-4, sub_range=[[10, 22]], ids_k=12)
+    print(r)
+    assert r["soft_pixels"] > 500
+
+
+def test_soft_exact_variant():
+    """Eq.12 (closest point on F(tau)) instead of Eq.13 on the GPU matches the oracle's Eq.12."""
+    sc = scenes.make_c2().subset([3])
+    r = check_soft(sc, 3e-4, sub_range=[[0, 6]], soft_exact=True)
+    print(r)
+
+
+def test_soft_rotation_segments_ragged():
+    """Rotation with several segments (the X switch inside each segment), a ragged image and
+    degenerate faces."""
+    sc = scenes.random_mesh_scene(30, 8, H=45, W=61, motion=scenes.rotate((0.2, 1, 0.3), 1.4, N=11, S=3))
+    faces = sc.faces.copy()
+    faces[2] = [4, 4, 5]
+    sc.faces = faces
+    r = check_soft(sc, 1e-3, mode="brute", ids_k=5)
+    print(r)
+
+
+def test_soft_c3_sampled_pixels_full_size():
+    """C3 at full size (8 x 512^2, 9,920 faces, N = 50, S = 24) in the bench's launch configuration:
+    sampled background / silhouette pixels against the oracle's pixel-list mode."""
+    sc = scenes.make_c3()
+    got = gpu_soft(sc, 1e-4)
+    a = got["rgba"][..., 3]
+    rng = np.random.default_rng(5)
+    cand = np.argwhere((a > 1e-4) & (a < 0.999))
+    pick = cand[rng.choice(len(cand), size=min(120, len(cand)), replace=False)]
+    ref = oracle.render_fwd(sc, pixels=pick, eps_amb=1e-6, delta=1e-4)
+    ok = ~ref["amb_img"]
+    err = np.abs(got["rgba"][pick[:, 0], pick[:, 1], pick[:, 2]] - ref["rgba"])
+    print("sampled", len(pick), "max err", err[ok].max(), "flagged", int((~ok).sum()))
+    assert ok.sum() > 0.8 * len(pick) and err[ok].max() < TOL_IMG
+
+
+def test_soft_backward_without_reuse_and_delta_zero():
+    """The backward recomputes coverage when the forward's workspace is not reused; delta = 0 is
+    the hard path exactly."""
+    sc = scenes.make_c2().subset([0, 2])
+    G = np.random.default_rng(1).normal(size=(2, 256, 256, 4)).astype(np.float32) * 1e-4
+    a = gpu_soft(sc, 1e-4, G=G, reuse=True)
+    b = gpu_soft(sc, 1e-4, G=G, reuse=False)
+    assert np.array_equal(a["rgba"], b["rgba"])
+    assert rel_l2(b["dv"], a["dv"]) < 1e-5
+    h = gpu_soft(sc, 0.0, G=G)
+    assert np.array_equal(h["rgba"][..., :3], a["rgba"][..., :3])
+    assert np.all(a["rgba"][..., 3] >= h["rgba"][..., 3])
+
+
+def test_soft_overflow_fallback_and_cut():
+    """A tiny soft-bin capacity forces the exact fallback scan (same result); a larger cut-off
+    changes alpha by at most the dropped terms."""
+    sc = scenes.make_c2().subset([1])
+    G = np.random.default_rng(2).normal(size=(1, 256, 256, 4)).astype(np.float32) * 1e-4
+    a = gpu_soft(sc, 1e-4, G=G)
+    b = gpu_soft(sc, 1e-4, G=G, soft_bin_factor=1e-9)
+    assert b["status"] & 4
+    assert np.abs(a["rgba"] - b["rgba"]).max() < 1e-6 and rel_l2(b["dv"], a["dv"]) < 1e-5
+    c = gpu_soft(sc, 1e-4, soft_cut=40.0)
+    assert np.abs(a["rgba"] - c["rgba"]).max() < 1e-6
+
+
+@pytest.mark.parametrize("G", [1, 4])
+def test_soft_chunk_length_invariance(G):
+    sc = scenes.make_c2().subset([0])
+    a = gpu_soft(sc, 1e-4, max_chunk=G)
+    b = gpu_soft(sc, 1e-4, max_chunk=8)
+    assert np.abs(a["rgba"] - b["rgba"]).max() < 1e-6
