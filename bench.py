@@ -35,6 +35,10 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 # per covered (pixel, sub-frame) shade, per (face, sub-frame) coefficient evaluation, and the
 # backward's extra work per covered (pixel, sub-frame)
 FLOP_PAIR, FLOP_SHADE, FLOP_SETUP, FLOP_BWD = 18.0, 25.0, 30.0, 100.0
+# soft background coverage (NEXT-1): flop per evaluated (pixel, face, sub-frame) term in the forward
+# (w1, w2: 8; three projections + quadratic forms: 3 x 12; Eq.14 form + exp + product: 10) and in
+# the backward (pass 1 the same, pass 2 the same + 16 for the gradient and its keyframe split)
+FLOP_SOFT_FWD, FLOP_SOFT_BWD = 54.0, 124.0
 LAUNCHES_FWD, LAUNCHES_LOSS, LAUNCHES_BWD = 9, 1, 2
 LAUNCHES_SOFT_FWD, LAUNCHES_SOFT_BWD = 9, 1     # soft bins (7) + K8 + reduce; K9
 
@@ -229,8 +233,8 @@ def main():
     stream = torch.cuda.current_stream()
 
     # census (outside timing): algorithmic unit counts of this rank's forward
-    census = torch.zeros(4, dtype=torch.int64, device=dev)
-    units = np.zeros(4)
+    census = torch.zeros(6, dtype=torch.int64, device=dev)
+    units = np.zeros(6)
     if rend is not None:
         rend.forward(verts, colors, census=census)
         units = census.cpu().numpy().astype(np.float64)
@@ -314,14 +318,15 @@ def main():
     value = sc.B / (ms_per_step / 1000.0)
 
     # roofline of the dominant kernel (raster fwd K4 or raster bwd K6), this rank's launches
-    nec, cov, cand, staged = units
+    nec, cov, cand, staged, soft_terms, soft_staged = units
     fw_flop = FLOP_PAIR * nec + FLOP_SHADE * cov + FLOP_SETUP * n_fsub
     bw_flop = fw_flop + FLOP_BWD * cov
     f_avg, b_avg = float(np.mean(fwd_ms)), float(np.mean(bwd_ms))
-    if b_avg >= f_avg:
-        kname, flop, dur = "k6_raster_bwd", bw_flop, b_avg
-    else:
-        kname, flop, dur = "k4_raster_fwd", fw_flop, f_avg
+    kernels = [("k4_raster_fwd", fw_flop, f_avg), ("k6_raster_bwd", bw_flop, b_avg)]
+    if soft:
+        kernels += [("k8_soft_fwd", FLOP_SOFT_FWD * soft_terms, float(np.mean(sf_ms))),
+                    ("k9_soft_bwd", FLOP_SOFT_BWD * soft_terms, float(np.mean(sb_ms)))]
+    kname, flop, dur = max(kernels, key=lambda k: k[2])
     achieved = flop / (dur / 1000.0) / 1e12 if dur > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -336,7 +341,9 @@ def main():
                                "SM count and clocks.max.sm)",
                 "fwd_raster_ms": f_avg, "bwd_raster_ms": b_avg,
                 **({"soft_fwd_ms": float(np.mean(sf_ms)), "soft_bwd_ms": float(np.mean(sb_ms))} if soft else {}),
-                "executed_pair_tests_per_launch": cand, "necessary_pairs_per_launch": nec}
+                "executed_pair_tests_per_launch": cand, "necessary_pairs_per_launch": nec,
+                **({"soft_terms_per_launch": soft_terms, "soft_staged_records_per_launch": soft_staged,
+                    "kernels_ms": {k[0]: k[2] for k in kernels}} if soft else {})}
 
     # measured FFMA throughput (context for the derived peak)
     ffma = None

@@ -461,7 +461,7 @@ int blur_render_fwd(const float *verts, int V, const int32_t *faces, int F, cons
     if (cfg && cfg->raster_events[1]) cudaEventRecord((cudaEvent_t)cfg->raster_events[1], st);
     if (P.soft) {   // NEXT-1: background alpha of the uncovered (pixel, sub-frame) pairs K4 recorded
         if (cfg->soft_events[0]) cudaEventRecord((cudaEvent_t)cfg->soft_events[0], st);
-        r = cuda_check(launch_soft_fwd(t, out_rgba, st), "soft fwd");
+        r = cuda_check(launch_soft_fwd(t, out_rgba, cfg->census, st), "soft fwd");
         if (r) return r;
         if (cfg->soft_events[1]) cudaEventRecord((cudaEvent_t)cfg->soft_events[1], st);
     }

@@ -136,7 +136,7 @@ namespace br {
 cudaError_t launch_setup(const Tables &t, const float *verts, const int *faces, const float *colors,
                          int maxS, cudaStream_t st);
 cudaError_t launch_binning(const Tables &t, const BinSet &bs, float dil, cudaStream_t st);
-cudaError_t launch_soft_fwd(const Tables &t, float *out, cudaStream_t st);
+cudaError_t launch_soft_fwd(const Tables &t, float *out, unsigned long long *census, cudaStream_t st);
 cudaError_t launch_soft_bwd(const Tables &t, const float *grad_rgba, cudaStream_t st);
 cudaError_t launch_raster_fwd(const Tables &t, float *out, int *ids, int ids_k,
                               unsigned long long *census, cudaStream_t st);

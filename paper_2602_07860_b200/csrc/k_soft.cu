@@ -8,22 +8,34 @@
 // d = || p - F(tau) w^* ||^2.  Faces farther than rcut = sqrt(soft_cut * delta) from the pixel at
 // tau are dropped (their term is < exp(-soft_cut); Q21).
 //
+// Barycentric (Gram) form of A17-A18 (exact restatement): with E1 = v1 - v0,
+// E2 = v2 - v0 of F(X) and sum w = 1, p' - v0 = w1 E1 + w2 E2, so every projection parameter is an
+// affine function of (w1, w2):
+//     t01 = w1 + w2 (E1.E2)/|E1|^2,   t12 = ((w1 - 1) E1.E12 + w2 E2.E12) / |E12|^2,
+//     t20 = (1 - w2) - w1 (E1.E2)/|E2|^2,
+// clamped to [0, 1], and the residual of candidate w^* is Delta = w - w^* (sum 0): p' - F(X) w^* =
+// Delta1 E1 + Delta2 E2, and Eq.14's F(tau) w - F(tau) w^* = Delta1 E1(tau) + Delta2 E2(tau).  Per
+// (pixel, face, tau) this is ~50 flops on (w1, w2) and four edge vectors.  (The residuals are
+// formed as vectors, not as Gram quadratic forms: for sliver faces |Delta| reaches 1e3 and the
+// quadratic form loses d to cancellation, found on C2.)
+//
 // Which (pixel, sub-frame) are background comes from the hard raster pass (K4), which leaves one
 // coverage ballot per (sub-frame, tile, warp) in the workspace (1 bit per pixel and sub-frame).
 // The soft kernels use their own bins (K3 on the chunk boxes grown by rcut, faces in index order).
-//   K8 (fwd)  CTA = 16x16 tile, 8 warps of 8x4 pixels.  Per group of sub-frames: every
-//             (face, tau) pair whose grown box reaches the tile is staged once into a 96 B
-//             shared-memory record (w(tau) coefficients, F(X) and F(tau) tile-local vertices,
-//             inverse squared F(X) edge lengths) with a per-(tau, warp) bit mask of the warp
-//             footprints that need it (uncovered pixels within rcut of the face at tau); every
-//             uncovered lane then folds its faces into prod (1 - A) in registers, in face order.
-//             The per-split partial alphas are reduced in a fixed order (deterministic).
+//   K8 (fwd)  CTA = 16x16 tile.  Per group of sub-frames: every (face, tau) pair whose grown box
+//             reaches the tile is staged once into an 80 B shared-memory record with a per-(tau,
+//             8x4-footprint) bit mask of the footprints that need it (uncovered pixels within rcut
+//             of the face at tau).  Work items (tau, footprint) with uncovered pixels are handed
+//             to warps through a shared-memory queue (balances the very uneven silhouette tiles);
+//             a warp's lanes are the footprint's pixels and fold their faces into prod (1 - A) in
+//             face order; each pixel's thread then sums 1 - P over the group's sub-frames in order
+//             (deterministic).
 //   K9 (bwd)  w^* frozen: dalpha/dA_j = prod_{l != j} (1 - A_l), dA/dd = -A/delta,
-//             dd/dv_i(tau) = -2 w^*_i (p - F(tau) w^*).  Pass 1 (pixel-parallel) recomputes the
-//             product per background pixel; pass 2 (face-parallel: one thread per staged face)
-//             walks the needing pixels of the face's warp footprints and accumulates the face's
-//             corner gradients in registers over the chunk, split (1 - tau, tau) onto keyframes and
-//             flushed with one vector RED per (corner, keyframe).
+//             dd/dv_i(tau) = -2 w^*_i (p - F(tau) w^*).  Pass 1 = K8's products (kept per pixel);
+//             pass 2 re-walks the same items, each lane forms its pixel's corner gradient for the
+//             face, a warp reduce-scatter (9 shuffles for 6 values) sums them over the footprint,
+//             and 12 lanes add the (1 - tau, tau) keyframe split into the face slot's shared
+//             accumulators, flushed with one vector RED per (corner, keyframe) per chunk.
 #include <algorithm>
 #include <cstdio>
 
@@ -35,14 +47,17 @@ namespace br {
 namespace {
 
 constexpr int SNW = NT / 32;     // warps per CTA
-constexpr int SREC_S = 512;      // staged soft records per CTA (96 B each)
+constexpr int SREC_F8 = 512;     // K8: staged soft records per CTA (80 B each)
+constexpr int SREC_B9 = 384;     // K9: staged soft records per CTA
 constexpr int GMAX_S = 8;        // sub-frames staged together
 constexpr int NPX = TW * TH;
 
 struct __align__(16) SoftRec {
-    // q0: wa0 wa1 wa2 wb0 | q1: wb1 wb2 wg0 wg1 | q2: wg2 xX0 yX0 xX1 | q3: yX1 xX2 yX2 il01
-    // q4: il12 il20 xT0 yT0 | q5: xT1 yT1 xT2 yT2       (w_i = wa_i ul + wb_i vl + wg_i)
-    float4 q[6];
+    // q0: a1 b1 g1 a2 | q1: b2 g2 k01 r01 | q2: c1 c2 k20 r20 | q3: E1x E1y E2x E2y of F(X)
+    // q4: E1x E1y E2x E2y of F(tau)
+    //   w_i = a_i ul + b_i vl + g_i (i = 1, 2; fast solver at tau, tile-local pixel coordinates)
+    //   t01 = sat(k01 w1 + r01 w2), t12 = sat(c1 (w1 - 1) + c2 w2), t20 = sat(k20 (1 - w2) - r20 w1)
+    float4 q[5];
 };
 
 struct STile {
@@ -108,122 +123,6 @@ __device__ __forceinline__ bool rect_near(const float A[3], const float B[3], co
     return true;
 }
 
-// Stage one (face, tau) soft record for this tile.  need[w] = uncovered-pixel bits of warp w at
-// tau.  Returns the mask of warp footprints the record must visit (0 = none).
-__device__ __forceinline__ uint32_t soft_stage(const Tables &t, const float4 *__restrict__ r,
-                                               const float4 *__restrict__ key0, const float4 *__restrict__ key1,
-                                               int f, float tau, const STile &tc, const uint32_t *need,
-                                               SoftRec &out)
-{
-    const float4 q6 = __ldg(r + 6);
-    if (__float_as_int(q6.w) < 0) return 0u;                             // skipped face
-    const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);   // det F(tau) (Eq.8 a-coefficients)
-    if (!(fabsf(D) > EPS_D)) return 0u;                                 // Q8
-    int x0, x1, y0, y1;
-    if (!grown_box(r, tau, t.rcut, t.W, t.H, tc, x0, x1, y0, y1)) return 0u;
-    const float sg = D < 0.f ? -1.f : 1.f;
-    const float invD = 1.0f / fabsf(D);
-    float A[3], B[3], G[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {   // Eq.8 numerators at tau, re-centred at the tile centre
-        const float4 e0 = __ldg(r + 2 * i), e1 = __ldg(r + 2 * i + 1);   // ox oy a0 a1 | b0 b1 g1 g2
-        const float al = __fmaf_rn(tau, e0.w, e0.z);
-        const float be = __fmaf_rn(tau, e1.y, e1.x);
-        const float ga = __fmul_rn(tau, __fmaf_rn(tau, e1.w, e1.z));
-        const float dx = __fsub_rn(tc.uc, e0.x), dy = __fsub_rn(tc.vc, e0.y);
-        const float gp = __fmaf_rn(al, dx, __fmaf_rn(be, dy, ga));
-        A[i] = al * sg;
-        B[i] = be * sg;
-        G[i] = gp * sg;
-    }
-    uint32_t fm = 0u;
-    for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
-        for (int wx = x0 >> 3; wx <= (x1 >> 3); ++wx) {
-            const int w = wy * 2 + wx;
-            if (!need[w]) continue;
-            const int rx0 = max(x0, wx * 8), rx1 = min(x1, wx * 8 + 7);
-            const int ry0 = max(y0, wy * 4), ry1 = min(y1, wy * 4 + 3);
-            if (rect_near(A, B, G, rx0, rx1, ry0, ry1, t.rcut, tc)) fm |= 1u << w;
-        }
-    if (!fm) return 0u;
-    const float4 vc = __ldg(t.fcol + 3 * (size_t)f + 2);
-    const int vid[3] = {__float_as_int(vc.y), __float_as_int(vc.z), __float_as_int(vc.w)};
-    float xT[3], yT[3], xX[3], yX[3];
-    const bool useX1 = tau > 0.5f;                                      // Eq.13: X = 1 iff tau > 0.5
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        const float4 a = __ldg(key0 + vid[i]), b = __ldg(key1 + vid[i]);
-        xT[i] = __fsub_rn(__fmaf_rn(tau, __fsub_rn(b.x, a.x), a.x), tc.uc);   // F(tau), Eq.5-6
-        yT[i] = __fsub_rn(__fmaf_rn(tau, __fsub_rn(b.y, a.y), a.y), tc.vc);
-        if (t.soft_exact) {                                                // Eq.12: F(X) = F(tau)
-            xX[i] = xT[i];
-            yX[i] = yT[i];
-        } else {
-            xX[i] = __fsub_rn(useX1 ? b.x : a.x, tc.uc);
-            yX[i] = __fsub_rn(useX1 ? b.y : a.y, tc.vc);
-        }
-    }
-    float il[3];
-#pragma unroll
-    for (int e = 0; e < 3; ++e) {   // edges v0v1, v1v2, v2v0 of F(X) (A17)
-        const int j = (e + 1) % 3;
-        const float ex = xX[j] - xX[e], ey = yX[j] - yX[e];
-        const float l2 = ex * ex + ey * ey;
-        il[e] = l2 > 0.f ? 1.0f / l2 : 0.f;   // zero-length edge: t = 0, its vertex (Q19)
-    }
-    out.q[0] = make_float4(A[0] * invD, A[1] * invD, A[2] * invD, B[0] * invD);
-    out.q[1] = make_float4(B[1] * invD, B[2] * invD, G[0] * invD, G[1] * invD);
-    out.q[2] = make_float4(G[2] * invD, xX[0], yX[0], xX[1]);
-    out.q[3] = make_float4(yX[1], xX[2], yX[2], il[0]);
-    out.q[4] = make_float4(il[1], il[2], xT[0], yT[0]);
-    out.q[5] = make_float4(xT[1], yT[1], xT[2], yT[2]);
-    return fm;
-}
-
-// One (pixel, face, tau) term: d (Eq.14) and the chosen edge (e: corners e, (e+1)%3) / parameter t.
-struct SoftHit {
-    float d, t, psx, psy;
-    int e;
-};
-
-__device__ __forceinline__ SoftHit soft_eval(const SoftRec &r, float ul, float vl)
-{
-    const float4 q0 = r.q[0], q1 = r.q[1], q2 = r.q[2], q3 = r.q[3], q4 = r.q[4], q5 = r.q[5];
-    // w(tau) (fast solver, Eq.8) and p' = F(X) w(tau) (Eq.13)
-    const float w0 = __fmaf_rn(q0.x, ul, __fmaf_rn(q0.w, vl, q1.z));
-    const float w1 = __fmaf_rn(q0.y, ul, __fmaf_rn(q1.x, vl, q1.w));
-    const float w2 = __fmaf_rn(q0.z, ul, __fmaf_rn(q1.y, vl, q2.x));
-    const float xX[3] = {q2.y, q2.w, q3.y}, yX[3] = {q2.z, q3.x, q3.z}, il[3] = {q3.w, q4.x, q4.y};
-    const float px = __fmaf_rn(w0, xX[0], __fmaf_rn(w1, xX[1], w2 * xX[2]));
-    const float py = __fmaf_rn(w0, yX[0], __fmaf_rn(w1, yX[1], w2 * yX[2]));
-    // closest point on F(X): three edge projections, clamped (A17-A18), smallest distance (first on ties)
-    float best = __int_as_float(0x7f800000), bt = 0.f;
-    int be = 0;
-#pragma unroll
-    for (int e = 0; e < 3; ++e) {
-        const int j = (e + 1) % 3;
-        const float ex = xX[j] - xX[e], ey = yX[j] - yX[e];
-        const float dx = px - xX[e], dy = py - yX[e];
-        const float tt = __saturatef(__fmaf_rn(dx, ex, dy * ey) * il[e]);
-        const float rx = __fmaf_rn(-tt, ex, dx), ry = __fmaf_rn(-tt, ey, dy);
-        const float dd = __fmaf_rn(rx, rx, ry * ry);
-        if (dd < best) { best = dd; bt = tt; be = e; }
-    }
-    // F(tau) w^* (Eq.14)
-    const float xT[3] = {q4.z, q5.x, q5.z}, yT[3] = {q4.w, q5.y, q5.w};
-    float xa = xT[0], ya = yT[0], xb = xT[1], yb = yT[1];
-    if (be == 1) { xa = xT[1]; ya = yT[1]; xb = xT[2]; yb = yT[2]; }
-    else if (be == 2) { xa = xT[2]; ya = yT[2]; xb = xT[0]; yb = yT[0]; }
-    SoftHit h;
-    h.psx = __fmaf_rn(bt, xb - xa, xa);
-    h.psy = __fmaf_rn(bt, yb - ya, ya);
-    const float ddx = ul - h.psx, ddy = vl - h.psy;
-    h.d = __fmaf_rn(ddx, ddx, ddy * ddy);
-    h.t = bt;
-    h.e = be;
-    return h;
-}
-
 // Fallback batch builder: faces whose grown per-tau box overlaps the tile, in index order.
 __device__ int soft_fallback_fill(const Tables &t, const float4 *__restrict__ rseg, float tau, const STile &tc,
                                   int cap, int &fpos, int *sid, int *swsum)
@@ -278,11 +177,121 @@ __device__ __forceinline__ void soft_bin(const Tables &t, const ImgInfo &im, con
     sb.key1 = sb.key0 + t.V;
 }
 
+// Stage one (face, tau) soft record for this tile.  need[w] = uncovered-pixel bits of footprint w
+// at tau.  Returns the mask of footprints the record must visit (0 = none).
+__device__ __forceinline__ uint32_t soft_stage(const Tables &t, const float4 *__restrict__ r,
+                                               const float4 *__restrict__ key0, const float4 *__restrict__ key1,
+                                               int f, float tau, const STile &tc, const uint32_t *need,
+                                               SoftRec &out)
+{
+    const float4 q6 = __ldg(r + 6);
+    if (__float_as_int(q6.w) < 0) return 0u;                             // skipped face
+    const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);   // det F(tau) (Eq.8 a-coefficients)
+    if (!(fabsf(D) > EPS_D)) return 0u;                                 // Q8
+    int x0, x1, y0, y1;
+    if (!grown_box(r, tau, t.rcut, t.W, t.H, tc, x0, x1, y0, y1)) return 0u;
+    const float sg = D < 0.f ? -1.f : 1.f;
+    float A[3], B[3], G[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {   // Eq.8 numerators at tau, re-centred at the tile centre
+        const float4 e0 = __ldg(r + 2 * i), e1 = __ldg(r + 2 * i + 1);   // ox oy a0 a1 | b0 b1 g1 g2
+        const float al = __fmaf_rn(tau, e0.w, e0.z);
+        const float be = __fmaf_rn(tau, e1.y, e1.x);
+        const float ga = __fmul_rn(tau, __fmaf_rn(tau, e1.w, e1.z));
+        const float dx = __fsub_rn(tc.uc, e0.x), dy = __fsub_rn(tc.vc, e0.y);
+        const float gp = __fmaf_rn(al, dx, __fmaf_rn(be, dy, ga));
+        A[i] = al * sg;
+        B[i] = be * sg;
+        G[i] = gp * sg;
+    }
+    uint32_t fm = 0u;
+    for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
+        for (int wx = x0 >> 3; wx <= (x1 >> 3); ++wx) {
+            const int w = wy * 2 + wx;
+            if (!need[w]) continue;
+            const int rx0 = max(x0, wx * 8), rx1 = min(x1, wx * 8 + 7);
+            const int ry0 = max(y0, wy * 4), ry1 = min(y1, wy * 4 + 3);
+            if (rect_near(A, B, G, rx0, rx1, ry0, ry1, t.rcut, tc)) fm |= 1u << w;
+        }
+    if (!fm) return 0u;
+    const float invD = 1.0f / fabsf(D);
+    const float4 vc = __ldg(t.fcol + 3 * (size_t)f + 2);
+    const int vid[3] = {__float_as_int(vc.y), __float_as_int(vc.z), __float_as_int(vc.w)};
+    float xT[3], yT[3], xX[3], yX[3];
+    const bool useX1 = tau > 0.5f;                                      // Eq.13: X = 1 iff tau > 0.5
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float4 a = __ldg(key0 + vid[i]), b = __ldg(key1 + vid[i]);
+        xT[i] = __fmaf_rn(tau, __fsub_rn(b.x, a.x), a.x);              // F(tau), Eq.5-6
+        yT[i] = __fmaf_rn(tau, __fsub_rn(b.y, a.y), a.y);
+        xX[i] = t.soft_exact ? xT[i] : (useX1 ? b.x : a.x);            // Eq.12 (exact) / Eq.13
+        yX[i] = t.soft_exact ? yT[i] : (useX1 ? b.y : a.y);
+    }
+    // F(X): edge vectors, Gram entries and the projection coefficients (zero-length edge: t = 0, Q19)
+    const float e1x = xX[1] - xX[0], e1y = yX[1] - yX[0], e2x = xX[2] - xX[0], e2y = yX[2] - yX[0];
+    const float e3x = xX[2] - xX[1], e3y = yX[2] - yX[1];
+    const float g11 = e1x * e1x + e1y * e1y, g22 = e2x * e2x + e2y * e2y, g12 = e1x * e2x + e1y * e2y;
+    const float l12 = e3x * e3x + e3y * e3y;
+    const float k01 = g11 > 0.f ? 1.f : 0.f, r01 = g11 > 0.f ? g12 / g11 : 0.f;
+    const float k20 = g22 > 0.f ? 1.f : 0.f, r20 = g22 > 0.f ? g12 / g22 : 0.f;
+    const float c1 = l12 > 0.f ? (e1x * e3x + e1y * e3y) / l12 : 0.f;
+    const float c2 = l12 > 0.f ? (e2x * e3x + e2y * e3y) / l12 : 0.f;
+    out.q[0] = make_float4(A[1] * invD, B[1] * invD, G[1] * invD, A[2] * invD);
+    out.q[1] = make_float4(B[2] * invD, G[2] * invD, k01, r01);
+    out.q[2] = make_float4(c1, c2, k20, r20);
+    out.q[3] = make_float4(e1x, e1y, e2x, e2y);
+    out.q[4] = make_float4(xT[1] - xT[0], yT[1] - yT[0], xT[2] - xT[0], yT[2] - yT[0]);   // F(tau)
+    return fm;
+}
+
+// One (pixel, face, tau) term: d (Eq.14), the chosen edge e (corners e, (e+1)%3) with parameter t,
+// and the residual Delta = w - w^* in the (E1, E2) basis.
+struct SoftHit {
+    float d, t, d1, d2;
+    int e;
+};
+
+// || d1 E1 + d2 E2 ||^2
+__device__ __forceinline__ float resid2(float d1, float d2, const float4 &E)
+{
+    const float rx = __fmaf_rn(d1, E.x, d2 * E.z), ry = __fmaf_rn(d1, E.y, d2 * E.w);
+    return __fmaf_rn(rx, rx, ry * ry);
+}
+
+__device__ __forceinline__ SoftHit soft_eval(const SoftRec &r, float ul, float vl)
+{
+    const float4 q0 = r.q[0], q1 = r.q[1], q2 = r.q[2], q3 = r.q[3];
+    const float w1 = __fmaf_rn(q0.x, ul, __fmaf_rn(q0.y, vl, q0.z));   // w(tau), Eq.8
+    const float w2 = __fmaf_rn(q0.w, ul, __fmaf_rn(q1.x, vl, q1.y));
+    SoftHit h;
+    // edge v0v1: w^* = (1 - t, t, 0)
+    float tt = __saturatef(__fmaf_rn(w1, q1.z, w2 * q1.w));
+    float d1 = w1 - tt, d2 = w2;
+    float best = resid2(d1, d2, q3);
+    h.t = tt; h.d1 = d1; h.d2 = d2; h.e = 0;
+    // edge v1v2: w^* = (0, 1 - t, t)
+    const float w1m = w1 - 1.f;
+    tt = __saturatef(__fmaf_rn(w1m, q2.x, w2 * q2.y));
+    d1 = w1m + tt; d2 = w2 - tt;
+    float qq = resid2(d1, d2, q3);
+    if (qq < best) { best = qq; h.t = tt; h.d1 = d1; h.d2 = d2; h.e = 1; }
+    // edge v2v0: w^* = (t, 0, 1 - t)
+    const float w2m = w2 - 1.f;
+    tt = __saturatef(__fmaf_rn(-w1, q2.w, -w2m * q2.z));
+    d1 = w1; d2 = w2m + tt;
+    qq = resid2(d1, d2, q3);
+    if (qq < best) { h.t = tt; h.d1 = d1; h.d2 = d2; h.e = 2; }
+    // Eq.14: || F(tau) Delta ||^2
+    h.d = resid2(h.d1, h.d2, r.q[4]);
+    return h;
+}
+
 // Stage faces [base, base + nb) of the bin (or sid[] in fallback mode) at the ng sub-frames taus:
 // records rec[l * nb + j], masks wm[(l * SNW + w) * nw + j / 32] (cleared by the caller).
+template <bool CENSUS>
 __device__ __forceinline__ void soft_stage_group(const Tables &t, const SoftBin &sb, int nb, int base, const float *taus,
                                                  int ng, const STile &tc, const uint32_t (*need)[SNW], const int *sid,
-                                                 SoftRec *rec, uint32_t *wm)
+                                                 SoftRec *rec, uint32_t *wm, unsigned long long &nstage)
 {
     const int nw = (nb + 31) >> 5;
     for (int p = threadIdx.x; p < nb * ng; p += NT) {
@@ -298,15 +307,17 @@ __device__ __forceinline__ void soft_stage_group(const Tables &t, const SoftBin 
         }
         const uint32_t fm = soft_stage(t, sb.rseg + (size_t)f * REC_F4, sb.key0, sb.key1, f, taus[l], tc, need[l],
                                        rec[l * nb + j]);
+        if (CENSUS) nstage += fm != 0u;
         const uint32_t bit = 0x80000000u >> (j & 31);
         for (uint32_t m = fm; m; m &= m - 1) atomicOr(wm + (l * SNW + (__ffs(m) - 1)) * nw + (j >> 5), bit);
     }
 }
 
-// prod over the masked faces of (1 - A) for this lane's pixel (face order), with the product of
-// the non-zero factors and the count of zero factors (for dalpha/dA in the backward)
+// prod over the masked faces of (1 - A) for one pixel (face order), with the product of the
+// non-zero factors and the count of zero factors (for dalpha/dA in the backward)
+template <bool CENSUS>
 __device__ __forceinline__ void soft_product(const SoftRec *rec, const uint32_t *wm, int nw, float ul, float vl,
-                                             float kexp, float &P, float &Pnz, int &nz)
+                                             float kexp, float &P, float &Pnz, int &nz, unsigned long long &npair)
 {
     for (int wd = 0; wd < nw; ++wd) {
         uint32_t m = wm[wd];
@@ -319,6 +330,7 @@ __device__ __forceinline__ void soft_product(const SoftRec *rec, const uint32_t 
             P *= fac;                                                // Eq.15
             if (fac == 0.f) nz++;
             else Pnz *= fac;
+            if (CENSUS) npair++;
         }
     }
 }
@@ -331,16 +343,36 @@ __device__ __forceinline__ void load_need(const Tables &t, const ImgInfo &im, in
     if (lane == 0) *dst = m;
 }
 
+// next work item (sub-frame l, footprint w) of the shared queue for this warp; -1 when drained
+__device__ __forceinline__ int next_item(int *head, int nitems, int lane)
+{
+    int it = 0;
+    if (lane == 0) it = atomicAdd(head, 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    return it < nitems ? it : -1;
+}
+
+__device__ __forceinline__ void footprint_pixel(int w, int lane, const STile &tc, int &p, float &ul, float &vl)
+{
+    const int lx = (w & 1) * 8 + (lane & 7), ly = (w >> 1) * 4 + (lane >> 3);
+    p = ly * TW + lx;
+    ul = (float)(lx - TW / 2) * tc.sx;
+    vl = (float)(TH / 2 - ly) * tc.sy;
+}
+
 struct SoftFwdSmem {
-    SoftRec rec[SREC_S];
-    uint32_t wm[GMAX_S * SNW * (SREC_S / 32 + 1)];
+    SoftRec rec[SREC_F8];
+    uint32_t wm[GMAX_S * SNW * (SREC_F8 / 32 + 1)];
     uint32_t need[GMAX_S][SNW];
-    int sid[SREC_S];
+    float om[GMAX_S][NPX];     // 1 - P per (sub-frame of the group, pixel); P across batches
+    int sid[SREC_F8];
     float taus[GMAX_S];
     int wsum[SNW];
+    int head;
 };
 
-__global__ void __launch_bounds__(NT, 2) k8_soft_fwd(Tables t)
+template <bool CENSUS>
+__global__ void __launch_bounds__(NT, 3) k8_soft_fwd(Tables t, unsigned long long *census)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SoftFwdSmem &S = *reinterpret_cast<SoftFwdSmem *>(smem_raw);
@@ -350,69 +382,89 @@ __global__ void __launch_bounds__(NT, 2) k8_soft_fwd(Tables t)
     stile(t, tile, tc);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
-    const int px = tc.px0 + lx, py = tc.py0 + ly;
+    const int px = tc.px0 + lx, py = tc.py0 + ly, myp = ly * TW + lx;
     const bool inimg = px < t.W && py < t.H;
-    const float ul = (float)(lx - TW / 2) * tc.sx;
-    const float vl = (float)(TH / 2 - ly) * tc.sy;
     const float kexp = 1.0f / t.delta;
     float alpha = 0.f;
+    unsigned long long npair = 0, nstage = 0;
 
     for (int c = im.chunk_begin + (int)blockIdx.z; c < im.chunk_end; c += t.splits) {
         const Chunk ch = t.chunks[c];
         SoftBin sb;
         soft_bin(t, im, ch, c, tile, sb);
         if (sb.n == 0) continue;   // no face within rcut of the tile during the chunk: every P = 1
-        if (!sb.fb && sb.n <= SREC_S) {
-            const int n = sb.n, Gs = min(GMAX_S, SREC_S / n), nw = (n + 31) >> 5;
+        if (!sb.fb && sb.n <= SREC_F8) {
+            const int n = sb.n, Gs = min(GMAX_S, SREC_F8 / n), nw = (n + 31) >> 5;
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
                 for (int l = 0; l < ng; ++l) load_need(t, im, kg + l, tile, warp, lane, inimg, &S.need[l][warp]);
                 for (int i = threadIdx.x; i < ng * SNW * nw; i += NT) S.wm[i] = 0u;
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[im.sched_off + kg + threadIdx.x];
+                if (threadIdx.x == 0) S.head = 0;
                 __syncthreads();
-                soft_stage_group(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm);
+                soft_stage_group<CENSUS>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, nstage);
                 __syncthreads();
-                for (int l = 0; l < ng; ++l) {
-                    if (!((S.need[l][warp] >> lane) & 1u)) continue;
-                    float P = 1.f, Pnz = 1.f;
-                    int nz = 0;
-                    soft_product(S.rec + l * n, S.wm + (l * SNW + warp) * nw, nw, ul, vl, kexp, P, Pnz, nz);
-                    alpha += 1.f - P;
+                for (int it; (it = next_item(&S.head, ng * SNW, lane)) >= 0;) {   // warp-uniform loop
+                    const int l = it / SNW, w = it - l * SNW;
+                    if ((S.need[l][w] >> lane) & 1u) {
+                        int p;
+                        float ul, vl, P = 1.f, Pnz = 1.f;
+                        int nz = 0;
+                        footprint_pixel(w, lane, tc, p, ul, vl);
+                        soft_product<CENSUS>(S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, ul, vl, kexp, P, Pnz, nz,
+                                             npair);
+                        S.om[l][p] = 1.f - P;
+                    }
                 }
+                __syncthreads();
+                for (int l = 0; l < ng; ++l)                     // this pixel's sub-frames, in order
+                    if ((S.need[l][warp] >> lane) & 1u) alpha += S.om[l][myp];
                 __syncthreads();
             }
         } else {
             for (int k = ch.k0; k < ch.k1; ++k) {
                 load_need(t, im, k, tile, warp, lane, inimg, &S.need[0][warp]);
                 if (threadIdx.x == 0) S.taus[0] = t.sched_tau[im.sched_off + k];
+                S.om[0][myp] = 1.f;
                 __syncthreads();
                 uint32_t anyn = 0u;
 #pragma unroll
                 for (int w = 0; w < SNW; ++w) anyn |= S.need[0][w];
-                const bool mine = (S.need[0][warp] >> lane) & 1u;
-                float P = 1.f, Pnz = 1.f;
-                int nz = 0;
                 int base = 0, fpos = 0;
                 while (anyn) {
-                    const int nb = sb.fb ? soft_fallback_fill(t, sb.rseg, S.taus[0], tc, SREC_S, fpos, S.sid, S.wsum)
-                                         : (base < sb.n ? min(SREC_S, sb.n - base) : 0);
+                    const int nb = sb.fb ? soft_fallback_fill(t, sb.rseg, S.taus[0], tc, SREC_F8, fpos, S.sid, S.wsum)
+                                         : (base < sb.n ? min(SREC_F8, sb.n - base) : 0);
                     if (nb == 0) break;
                     const int nw = (nb + 31) >> 5;
                     for (int i = threadIdx.x; i < SNW * nw; i += NT) S.wm[i] = 0u;
+                    if (threadIdx.x == 0) S.head = 0;
                     __syncthreads();
-                    soft_stage_group(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm);
+                    soft_stage_group<CENSUS>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, nstage);
                     __syncthreads();
-                    if (mine) soft_product(S.rec, S.wm + warp * nw, nw, ul, vl, kexp, P, Pnz, nz);
+                    for (int it; (it = next_item(&S.head, SNW, lane)) >= 0;) {
+                        if ((S.need[0][it] >> lane) & 1u) {
+                            int p;
+                            float ul, vl, P = 1.f, Pnz = 1.f;
+                            int nz = 0;
+                            footprint_pixel(it, lane, tc, p, ul, vl);
+                            soft_product<CENSUS>(S.rec, S.wm + it * nw, nw, ul, vl, kexp, P, Pnz, nz, npair);
+                            S.om[0][p] *= P;
+                        }
+                    }
                     base += nb;
                     __syncthreads();
                 }
-                if (mine) alpha += 1.f - P;
+                if ((S.need[0][warp] >> lane) & 1u) alpha += 1.f - S.om[0][myp];
                 __syncthreads();
             }
         }
     }
     if (inimg) t.spart[(size_t)blockIdx.z * ((size_t)t.B * t.H * t.W) + ((size_t)b * t.H + py) * t.W + px] =
         alpha / (float)im.N;
+    if (CENSUS) {
+        atomicAdd(census + 4, npair);
+        atomicAdd(census + 5, nstage);
+    }
 }
 
 // out alpha += sum over splits of the soft partials (fixed order: deterministic)
@@ -429,19 +481,20 @@ __global__ void __launch_bounds__(256) k8_soft_reduce(const float *__restrict__ 
 // ------------------------------------------------------------------ backward
 
 struct SoftBwdSmem {
-    SoftRec rec[SREC_S];
-    uint32_t wm[GMAX_S * SNW * (SREC_S / 32 + 1)];
+    SoftRec rec[SREC_B9];
+    uint32_t wm[GMAX_S * SNW * (SREC_B9 / 32 + 1)];
     uint32_t need[GMAX_S][SNW];
     float pnz[GMAX_S][NPX];
-    int nz[GMAX_S][NPX];
+    unsigned short nz[GMAX_S][NPX];
     float ga[NPX];
-    int sid[SREC_S];
+    float acc[SREC_B9][12];    // per bin slot: d/d keyframe s (corners x, y), then keyframe s+1
+    int sid[SREC_B9];
     float taus[GMAX_S];
     int wsum[SNW];
+    int head, head2;
 };
 
-__device__ __forceinline__ void soft_flush(const Tables &t, const ImgInfo &im, int s, int f, const float k0[6],
-                                           const float k1[6])
+__device__ __forceinline__ void soft_flush(const Tables &t, const ImgInfo &im, int s, int f, const float *a)
 {
     const float4 q = __ldg(t.fcol + 3 * (size_t)f + 2);
     const int vid[3] = {__float_as_int(q.y), __float_as_int(q.z), __float_as_int(q.w)};
@@ -449,81 +502,103 @@ __device__ __forceinline__ void soft_flush(const Tables &t, const ImgInfo &im, i
     float2 *d1 = d0 + t.V;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        if (k0[2 * i] != 0.f || k0[2 * i + 1] != 0.f) atomicAdd(d0 + vid[i], make_float2(k0[2 * i], k0[2 * i + 1]));
-        if (k1[2 * i] != 0.f || k1[2 * i + 1] != 0.f) atomicAdd(d1 + vid[i], make_float2(k1[2 * i], k1[2 * i + 1]));
+        if (a[2 * i] != 0.f || a[2 * i + 1] != 0.f) atomicAdd(d0 + vid[i], make_float2(a[2 * i], a[2 * i + 1]));
+        if (a[6 + 2 * i] != 0.f || a[7 + 2 * i] != 0.f) atomicAdd(d1 + vid[i], make_float2(a[6 + 2 * i], a[7 + 2 * i]));
     }
 }
 
-// Face-parallel gradient of the staged records rec[l * nb + j] (j from this thread) at the ng
-// sub-frames: corner gradients accumulated over the needing pixels of the masked footprints.
-// Slot j == thread persists in acc (acc0/acc1, keyframes s / s+1); others flush immediately.
-__device__ __forceinline__ void soft_grad_group(SoftBwdSmem &S, const Tables &t, const ImgInfo &im, int s, int nb,
-                                                int ng, const STile &tc, int slot_base, bool persist_ok,
-                                                float acc0[6], float acc1[6], const int *fid_of)
+// flush and clear the slot accumulators [0, nb)
+__device__ __forceinline__ void flush_slots(SoftBwdSmem &S, const Tables &t, const ImgInfo &im, int s, int nb,
+                                            const int *fid_of)
 {
-    const int nw = (nb + 31) >> 5;
-    const float kexp = 1.0f / t.delta, c2 = 2.0f / t.delta;
     for (int j = threadIdx.x; j < nb; j += NT) {
-        float a0[6], a1[6];
+        float a[12];
+        bool nzf = false;
 #pragma unroll
-        for (int i = 0; i < 6; ++i) { a0[i] = 0.f; a1[i] = 0.f; }
-        bool any = false;
-        for (int l = 0; l < ng; ++l) {
-            const SoftRec &r = S.rec[l * nb + j];
-            float dv[6];
+        for (int i = 0; i < 12; ++i) { a[i] = S.acc[j][i]; nzf |= a[i] != 0.f; S.acc[j][i] = 0.f; }
+        if (nzf) soft_flush(t, im, s, fid_of[j], a);
+    }
+}
+
+// Pass 2 of one work item (sub-frame l, footprint w): for each masked face, every needing lane
+// forms its pixel's corner gradient; the warp reduce-scatters the 6 values (8 with padding: 9
+// shuffles) and the lanes holding the sums add the keyframe split into the slot accumulators.
+__device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *rec, const uint32_t *wm, int nw,
+                                               int l, int w, int lane, const STile &tc, float kexp, float c2)
+{
+    const bool mine = (S.need[l][w] >> lane) & 1u;
+    int p;
+    float ul, vl;
+    footprint_pixel(w, lane, tc, p, ul, vl);
+    const float ga = mine ? S.ga[p] : 0.f, pz = mine ? S.pnz[l][p] : 0.f;
+    const int z = mine ? S.nz[l][p] : 2;
+    const float tau = S.taus[l];
+    // lane owning reduced value vi after the reduce-scatter: vi = 4 b4 + 2 b3 + b2 (lanes with b1 = b0 = 0)
+    const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    for (int wd = 0; wd < nw; ++wd) {
+        uint32_t m = wm[wd];
+        while (m) {
+            const int k = __clz(m);
+            m ^= 0x80000000u >> k;
+            const int j = (wd << 5) + k;
+            float v[8];
 #pragma unroll
-            for (int i = 0; i < 6; ++i) dv[i] = 0.f;
-            bool hit = false;
-            for (int w = 0; w < SNW; ++w) {
-                if (!((S.wm[(l * SNW + w) * nw + (j >> 5)] << (j & 31)) & 0x80000000u)) continue;
-                uint32_t m = S.need[l][w];
-                while (m) {
-                    const int ln = __ffs(m) - 1;
-                    m &= m - 1;
-                    const int lx = (w & 1) * 8 + (ln & 7), ly = (w >> 1) * 4 + (ln >> 3), p = ly * TW + lx;
-                    const float ul = (float)(lx - TW / 2) * tc.sx;
-                    const float vl = (float)(TH / 2 - ly) * tc.sy;
-                    const SoftHit h = soft_eval(r, ul, vl);
-                    const float A = __expf(-h.d * kexp);
-                    if (A == 0.f) continue;
-                    const float fac = 1.0f - A;
-                    const int z = S.nz[l][p];
-                    const float pz = S.pnz[l][p];
-                    const float dadA = z == 0 ? pz / fac : ((z == 1 && fac == 0.f) ? pz : 0.f);
-                    // dL/dv_i(tau) = G_a dalpha/dA (A/delta) 2 w^*_i (p - F(tau) w^*)
-                    const float cc = S.ga[p] * dadA * A * c2;
-                    const float gx = cc * (ul - h.psx), gy = cc * (vl - h.psy);
+            for (int i = 0; i < 8; ++i) v[i] = 0.f;
+            bool any = false;
+            if (mine && z < 2) {
+                const SoftRec &r = rec[j];
+                const SoftHit h = soft_eval(r, ul, vl);
+                const float A = __expf(-h.d * kexp);
+                const float fac = 1.0f - A;
+                const float dadA = z == 0 ? pz / fac : (fac == 0.f ? pz : 0.f);
+                // dL/dv_i(tau) = G_a dalpha/dA (A / delta) 2 w^*_i (p - F(tau) w^*), p - F(tau) w^* = F(tau) Delta
+                const float cc = ga * dadA * A * c2;
+                if (cc != 0.f) {
+                    const float4 q4 = r.q[4];
+                    const float gx = cc * __fmaf_rn(h.d1, q4.x, h.d2 * q4.z);
+                    const float gy = cc * __fmaf_rn(h.d1, q4.y, h.d2 * q4.w);
                     const int ia = h.e, ib = h.e == 2 ? 0 : h.e + 1;
                     const float wa = 1.f - h.t, wb = h.t;
 #pragma unroll
                     for (int q = 0; q < 3; ++q) {
                         const float wq = (q == ia ? wa : 0.f) + (q == ib ? wb : 0.f);
-                        dv[2 * q] = __fmaf_rn(wq, gx, dv[2 * q]);
-                        dv[2 * q + 1] = __fmaf_rn(wq, gy, dv[2 * q + 1]);
+                        v[2 * q] = wq * gx;
+                        v[2 * q + 1] = wq * gy;
                     }
-                    hit = true;
+                    any = true;
                 }
             }
-            if (!hit) continue;
-            any = true;
-            const float tau = S.taus[l];
+            if (!__any_sync(0xffffffffu, any)) continue;
+            // reduce-scatter 8 -> 4 -> 2 -> 1 values, then a 4-lane all-reduce
+            const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+            float k4[4];
 #pragma unroll
-            for (int i = 0; i < 6; ++i) {
-                a0[i] = __fmaf_rn(1.f - tau, dv[i], a0[i]);
-                a1[i] = __fmaf_rn(tau, dv[i], a1[i]);
+            for (int i = 0; i < 4; ++i) {
+                const float keep = u16 ? v[4 + i] : v[i], send = u16 ? v[i] : v[4 + i];
+                k4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
             }
-        }
-        if (!any) continue;
-        if (persist_ok && j == (int)threadIdx.x) {
+            float k2[2];
 #pragma unroll
-            for (int i = 0; i < 6; ++i) { acc0[i] += a0[i]; acc1[i] += a1[i]; }
-        } else {
-            soft_flush(t, im, s, fid_of[j + slot_base], a0, a1);
+            for (int i = 0; i < 2; ++i) {
+                const float keep = u8 ? k4[2 + i] : k4[i], send = u8 ? k4[i] : k4[2 + i];
+                k2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
+            float s1;
+            {
+                const float keep = u4 ? k2[1] : k2[0], send = u4 ? k2[0] : k2[1];
+                s1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+            }
+            s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+            if ((lane & 3) == 0 && vi < 6 && s1 != 0.f) {
+                atomicAdd(&S.acc[j][vi], (1.f - tau) * s1);   // keyframe s
+                atomicAdd(&S.acc[j][6 + vi], tau * s1);       // keyframe s + 1
+            }
         }
     }
 }
 
-__global__ void __launch_bounds__(NT, 2) k9_soft_bwd(Tables t, const float *__restrict__ grad)
+__global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__restrict__ grad)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SoftBwdSmem &S = *reinterpret_cast<SoftBwdSmem *>(smem_raw);
@@ -535,12 +610,12 @@ __global__ void __launch_bounds__(NT, 2) k9_soft_bwd(Tables t, const float *__re
     const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
     const int px = tc.px0 + lx, py = tc.py0 + ly, myp = ly * TW + lx;
     const bool inimg = px < t.W && py < t.H;
-    const float ul = (float)(lx - TW / 2) * tc.sx;
-    const float vl = (float)(TH / 2 - ly) * tc.sy;
-    const float kexp = 1.0f / t.delta;
+    const float kexp = 1.0f / t.delta, c2 = 2.0f / t.delta;
     const float ga = inimg ? __ldg(grad + 4 * (((size_t)b * t.H + py) * t.W + px) + 3) / (float)im.N : 0.f;
     S.ga[myp] = ga;
     const bool want = inimg && ga != 0.f;
+    for (int i = threadIdx.x; i < SREC_B9 * 12; i += NT) (&S.acc[0][0])[i] = 0.f;
+    unsigned long long dummy = 0;
     __syncthreads();
 
     for (int c = im.chunk_begin + (int)blockIdx.z; c < im.chunk_end; c += t.splits) {
@@ -548,89 +623,107 @@ __global__ void __launch_bounds__(NT, 2) k9_soft_bwd(Tables t, const float *__re
         SoftBin sb;
         soft_bin(t, im, ch, c, tile, sb);
         if (sb.n == 0) continue;
-        float acc0[6], acc1[6];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) { acc0[i] = 0.f; acc1[i] = 0.f; }
-        const bool grouped = !sb.fb && sb.n <= SREC_S;
-        if (grouped) {
-            const int n = sb.n, Gs = min(GMAX_S, SREC_S / n), nw = (n + 31) >> 5;
+        if (!sb.fb && sb.n <= SREC_B9) {
+            const int n = sb.n, Gs = min(GMAX_S, SREC_B9 / n), nw = (n + 31) >> 5;
+            bool touched = false;
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
                 for (int l = 0; l < ng; ++l) load_need(t, im, kg + l, tile, warp, lane, want, &S.need[l][warp]);
                 for (int i = threadIdx.x; i < ng * SNW * nw; i += NT) S.wm[i] = 0u;
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[im.sched_off + kg + threadIdx.x];
+                if (threadIdx.x == 0) { S.head = 0; S.head2 = 0; }
                 __syncthreads();
                 uint32_t anyn = 0u;
                 for (int l = 0; l < ng; ++l)
 #pragma unroll
                     for (int w = 0; w < SNW; ++w) anyn |= S.need[l][w];
                 if (anyn) {   // block-uniform
-                    soft_stage_group(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm);
+                    touched = true;
+                    soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
-                    for (int l = 0; l < ng; ++l) {          // pass 1: products per background pixel
-                        if (!((S.need[l][warp] >> lane) & 1u)) continue;
-                        float P = 1.f, Pnz = 1.f;
-                        int nz = 0;
-                        soft_product(S.rec + l * n, S.wm + (l * SNW + warp) * nw, nw, ul, vl, kexp, P, Pnz, nz);
-                        S.pnz[l][myp] = Pnz;
-                        S.nz[l][myp] = nz;
+                    for (int it; (it = next_item(&S.head, ng * SNW, lane)) >= 0;) {   // pass 1: products
+                        const int l = it / SNW, w = it - l * SNW;
+                        if ((S.need[l][w] >> lane) & 1u) {
+                            int p;
+                            float ul, vl, P = 1.f, Pnz = 1.f;
+                            int nz = 0;
+                            footprint_pixel(w, lane, tc, p, ul, vl);
+                            soft_product<false>(S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, ul, vl, kexp, P, Pnz, nz,
+                                                dummy);
+                            S.pnz[l][p] = Pnz;
+                            S.nz[l][p] = (unsigned short)min(nz, 2);
+                        }
                     }
                     __syncthreads();
-                    soft_grad_group(S, t, im, ch.s, n, ng, tc, 0, true, acc0, acc1, sb.ent);   // pass 2
+                    for (int it; (it = next_item(&S.head2, ng * SNW, lane)) >= 0;) {  // pass 2: gradients
+                        const int l = it / SNW, w = it - l * SNW;
+                        if (!S.need[l][w]) continue;
+                        soft_grad_item(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc, kexp, c2);
+                    }
                 }
                 __syncthreads();
             }
-            if ((int)threadIdx.x < sb.n) {
-                bool nzf = false;
-#pragma unroll
-                for (int i = 0; i < 6; ++i) nzf |= (acc0[i] != 0.f) | (acc1[i] != 0.f);
-                if (nzf) soft_flush(t, im, ch.s, __ldg(sb.ent + threadIdx.x), acc0, acc1);
+            if (touched) {
+                flush_slots(S, t, im, ch.s, n, sb.ent);
+                __syncthreads();
             }
         } else {
             for (int k = ch.k0; k < ch.k1; ++k) {
                 load_need(t, im, k, tile, warp, lane, want, &S.need[0][warp]);
                 if (threadIdx.x == 0) S.taus[0] = t.sched_tau[im.sched_off + k];
+                S.pnz[0][myp] = 1.f;
+                S.nz[0][myp] = 0;
                 __syncthreads();
                 uint32_t anyn = 0u;
 #pragma unroll
                 for (int w = 0; w < SNW; ++w) anyn |= S.need[0][w];
-                __syncthreads();       // every warp has read need[] before the next sub-frame rewrites it
-                if (!anyn) continue;   // block-uniform
-                const bool mine = (S.need[0][warp] >> lane) & 1u;
-                float P = 1.f, Pnz = 1.f;
-                int nz = 0;
                 int base = 0, fpos = 0;
-                while (true) {   // pass 1 over all batches
-                    const int nb = sb.fb ? soft_fallback_fill(t, sb.rseg, S.taus[0], tc, SREC_S, fpos, S.sid, S.wsum)
-                                         : (base < sb.n ? min(SREC_S, sb.n - base) : 0);
+                while (anyn) {   // pass 1 over all batches
+                    const int nb = sb.fb ? soft_fallback_fill(t, sb.rseg, S.taus[0], tc, SREC_B9, fpos, S.sid, S.wsum)
+                                         : (base < sb.n ? min(SREC_B9, sb.n - base) : 0);
                     if (nb == 0) break;
                     const int nw = (nb + 31) >> 5;
                     for (int i = threadIdx.x; i < SNW * nw; i += NT) S.wm[i] = 0u;
+                    if (threadIdx.x == 0) S.head = 0;
                     __syncthreads();
-                    soft_stage_group(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm);
+                    soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
-                    if (mine) soft_product(S.rec, S.wm + warp * nw, nw, ul, vl, kexp, P, Pnz, nz);
+                    for (int it; (it = next_item(&S.head, SNW, lane)) >= 0;) {
+                        if ((S.need[0][it] >> lane) & 1u) {
+                            int p;
+                            float ul, vl, P = 1.f, Pnz = 1.f;
+                            int nz = 0;
+                            footprint_pixel(it, lane, tc, p, ul, vl);
+                            soft_product<false>(S.rec, S.wm + it * nw, nw, ul, vl, kexp, P, Pnz, nz, dummy);
+                            S.pnz[0][p] *= Pnz;
+                            S.nz[0][p] = (unsigned short)min((int)S.nz[0][p] + nz, 2);
+                        }
+                    }
                     base += nb;
                     __syncthreads();
                 }
-                if (mine) { S.pnz[0][myp] = Pnz; S.nz[0][myp] = nz; }
-                __syncthreads();
                 base = 0;
                 fpos = 0;
-                while (true) {   // pass 2: re-stage each batch
-                    const int nb = sb.fb ? soft_fallback_fill(t, sb.rseg, S.taus[0], tc, SREC_S, fpos, S.sid, S.wsum)
-                                         : (base < sb.n ? min(SREC_S, sb.n - base) : 0);
+                while (anyn) {   // pass 2: re-stage each batch
+                    const int nb = sb.fb ? soft_fallback_fill(t, sb.rseg, S.taus[0], tc, SREC_B9, fpos, S.sid, S.wsum)
+                                         : (base < sb.n ? min(SREC_B9, sb.n - base) : 0);
                     if (nb == 0) break;
                     const int nw = (nb + 31) >> 5;
                     for (int i = threadIdx.x; i < SNW * nw; i += NT) S.wm[i] = 0u;
+                    if (threadIdx.x == 0) S.head = 0;
                     __syncthreads();
-                    soft_stage_group(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm);
+                    soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
-                    soft_grad_group(S, t, im, ch.s, nb, 1, tc, sb.fb ? 0 : base, false, acc0, acc1,
-                                    sb.fb ? S.sid : sb.ent);
+                    for (int it; (it = next_item(&S.head, SNW, lane)) >= 0;) {
+                        if (!S.need[0][it]) continue;
+                        soft_grad_item(S, S.rec, S.wm + it * nw, nw, 0, it, lane, tc, kexp, c2);
+                    }
+                    __syncthreads();
+                    flush_slots(S, t, im, ch.s, nb, sb.fb ? S.sid : sb.ent + base);
                     base += nb;
                     __syncthreads();
                 }
+                __syncthreads();
             }
         }
     }
@@ -638,16 +731,22 @@ __global__ void __launch_bounds__(NT, 2) k9_soft_bwd(Tables t, const float *__re
 
 }  // namespace
 
-cudaError_t launch_soft_fwd(const Tables &t, float *out, cudaStream_t st)
+cudaError_t launch_soft_fwd(const Tables &t, float *out, unsigned long long *census, cudaStream_t st)
 {
     if (t.B == 0 || t.T == 0) return cudaSuccess;
     const size_t n = (size_t)t.B * t.H * t.W;
     cudaError_t e;
     if (t.F > 0) {
         const int smem = (int)sizeof(SoftFwdSmem);
-        e = cudaFuncSetAttribute(k8_soft_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        k8_soft_fwd<<<dim3(t.T, t.B, t.splits), NT, smem, st>>>(t);
+        if (census) {
+            e = cudaFuncSetAttribute(k8_soft_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+            k8_soft_fwd<true><<<dim3(t.T, t.B, t.splits), NT, smem, st>>>(t, census);
+        } else {
+            e = cudaFuncSetAttribute(k8_soft_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+            k8_soft_fwd<false><<<dim3(t.T, t.B, t.splits), NT, smem, st>>>(t, nullptr);
+        }
     } else {
         e = cudaMemsetAsync(t.spart, 0, sizeof(float) * n * t.splits, st);
         if (e != cudaSuccess) return e;
