@@ -31,9 +31,9 @@
 //             face order; each pixel's thread then sums 1 - P over the group's sub-frames in order
 //             (deterministic).
 //   K9 (bwd)  w^* frozen: dalpha/dA_j = prod_{l != j} (1 - A_l), dA/dd = -A/delta,
-//             dd/dv_i(tau) = -2 w^*_i (p - F(tau) w^*).  Pass 1 = K8's products (kept per pixel);
-//             pass 2 re-walks the same items, each lane forms its pixel's corner gradient for the
-//             face, a warp reduce-scatter (9 shuffles for 6 values) sums them over the footprint,
+//             dd/dv_i(tau) = -2 w^*_i (p - F(tau) w^*).  Per work item, pass 1 = K8's products (in
+//             registers); pass 2 re-walks the item's faces, each lane forms its pixel's corner
+//             gradient, a warp reduce-scatter (9 shuffles for 6 values) sums them over the footprint,
 //             and 12 lanes add the (1 - tau, tau) keyframe split into the face slot's shared
 //             accumulators, flushed with one vector RED per (corner, keyframe) per chunk.
 #include <algorithm>
@@ -523,6 +523,9 @@ __device__ __forceinline__ void flush_slots(SoftBwdSmem &S, const Tables &t, con
 // Pass 2 of one work item (sub-frame l, footprint w): for each masked face, every needing lane
 // forms its pixel's corner gradient; the warp reduce-scatters the 6 values (8 with padding: 9
 // shuffles) and the lanes holding the sums add the keyframe split into the slot accumulators.
+// FUSED: the products come from a pass over the same faces in this call (the whole bin is staged);
+// otherwise from S.pnz / S.nz (accumulated over the batches of a long bin).
+template <bool FUSED>
 __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *rec, const uint32_t *wm, int nw,
                                                int l, int w, int lane, const STile &tc, float kexp, float c2)
 {
@@ -530,8 +533,22 @@ __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *re
     int p;
     float ul, vl;
     footprint_pixel(w, lane, tc, p, ul, vl);
-    const float ga = mine ? S.ga[p] : 0.f, pz = mine ? S.pnz[l][p] : 0.f;
-    const int z = mine ? S.nz[l][p] : 2;
+    float pz = 0.f;
+    int z = 2;
+    if (mine) {
+        if (FUSED) {   // pass 1 of this footprint: the products, in face order, kept in registers
+            float P = 1.f;
+            unsigned long long dummy = 0;
+            pz = 1.f;
+            z = 0;
+            soft_product<false>(rec, wm, nw, ul, vl, kexp, P, pz, z, dummy);
+            z = min(z, 2);
+        } else {
+            pz = S.pnz[l][p];
+            z = S.nz[l][p];
+        }
+    }
+    const float ga = mine ? S.ga[p] : 0.f;
     const float tau = S.taus[l];
     // lane owning reduced value vi after the reduce-scatter: vi = 4 b4 + 2 b3 + b2 (lanes with b1 = b0 = 0)
     const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
@@ -641,24 +658,10 @@ __global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__re
                     touched = true;
                     soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
-                    for (int it; (it = next_item(&S.head, ng * SNW, lane)) >= 0;) {   // pass 1: products
-                        const int l = it / SNW, w = it - l * SNW;
-                        if ((S.need[l][w] >> lane) & 1u) {
-                            int p;
-                            float ul, vl, P = 1.f, Pnz = 1.f;
-                            int nz = 0;
-                            footprint_pixel(w, lane, tc, p, ul, vl);
-                            soft_product<false>(S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, ul, vl, kexp, P, Pnz, nz,
-                                                dummy);
-                            S.pnz[l][p] = Pnz;
-                            S.nz[l][p] = (unsigned short)min(nz, 2);
-                        }
-                    }
-                    __syncthreads();
-                    for (int it; (it = next_item(&S.head2, ng * SNW, lane)) >= 0;) {  // pass 2: gradients
+                    for (int it; (it = next_item(&S.head, ng * SNW, lane)) >= 0;) {   // products + gradients
                         const int l = it / SNW, w = it - l * SNW;
                         if (!S.need[l][w]) continue;
-                        soft_grad_item(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc, kexp, c2);
+                        soft_grad_item<true>(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc, kexp, c2);
                     }
                 }
                 __syncthreads();
@@ -716,7 +719,7 @@ __global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__re
                     __syncthreads();
                     for (int it; (it = next_item(&S.head, SNW, lane)) >= 0;) {
                         if (!S.need[0][it]) continue;
-                        soft_grad_item(S, S.rec, S.wm + it * nw, nw, 0, it, lane, tc, kexp, c2);
+                        soft_grad_item<false>(S, S.rec, S.wm + it * nw, nw, 0, it, lane, tc, kexp, c2);
                     }
                     __syncthreads();
                     flush_slots(S, t, im, ch.s, nb, sb.fb ? S.sid : sb.ent + base);
