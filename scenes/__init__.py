@@ -354,3 +354,20 @@ def random_mesh_scene(n_faces: int, seed: int, H: int = 16, W: int = 16, motion=
     motion = translate((0.8, 0.3, 0.2), N=5) if motion is None else motion
     return single_scene(verts, faces, rng.uniform(0, 1, (V, 3)), motion=motion, H=H, W=W,
                         seed=seed + 1, B=B)
+
+
+def cube(half: float = 0.5, centre=(0.0, 0.0, 0.0)):
+    """Closed axis-aligned cube (8 V / 12 F, outward-facing), for the voxel-IoU pins."""
+    c = np.asarray(centre, np.float64)
+    v = np.array([[x, y, z] for x in (-half, half) for y in (-half, half) for z in (-half, half)]) + c
+    f = [(0, 1, 3), (0, 3, 2), (4, 6, 7), (4, 7, 5), (0, 4, 5), (0, 5, 1),
+         (2, 3, 7), (2, 7, 6), (0, 2, 6), (0, 6, 4), (1, 5, 7), (1, 7, 3)]
+    return v, np.array(f, dtype=np.int32)
+
+
+def star(k: int = 6, radius: float = 1.0):
+    """Fan of k triangles around vertex 0 (ring vertices 1..k), for the Laplacian closed form."""
+    ring = [[radius * math.cos(2 * math.pi * i / k), radius * math.sin(2 * math.pi * i / k), 0.0] for i in range(k)]
+    v = np.array([[0.0, 0.0, 0.0]] + ring)
+    f = [(0, 1 + i, 1 + (i + 1) % k) for i in range(k)]
+    return v, np.array(f, dtype=np.int32)
