@@ -109,12 +109,12 @@ def smooth_loss(verts, faces):
     for a, b, c, d in interior_edges(faces):
         pa, pb, pc, pd = x[a], x[b], x[c], x[d]
         e = pb - pa
-        if float((e * e).sum()) == 0.0:
+        if float((e * e).sum().detach()) == 0.0:
             continue
         ee = (e * e).sum()
         u = (pc - pa) - ((pc - pa) * e).sum() / ee * e
         w = (pd - pa) - ((pd - pa) * e).sum() / ee * e
-        if float((u * u).sum()) == 0.0 or float((w * w).sum()) == 0.0:
+        if float((u * u).sum().detach()) == 0.0 or float((w * w).sum().detach()) == 0.0:
             continue                # degenerate face: edge skipped
         cs = _cos_dihedral(torch, pa, pb, pc, pd)
         loss = loss + (cs + 1.0) ** 2

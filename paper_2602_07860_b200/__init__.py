@@ -7,5 +7,6 @@ blur_render autograd op) -> dist.py (image / sub-frame sharding over torch.distr
 from . import _lib  # noqa: F401
 from ._lib import BlurError  # noqa: F401
 from .renderer import BlurRenderer, blur_render  # noqa: F401
+from .recover import Recovery  # noqa: F401
 
-__all__ = ["BlurRenderer", "blur_render", "BlurError"]
+__all__ = ["BlurRenderer", "blur_render", "BlurError", "Recovery"]

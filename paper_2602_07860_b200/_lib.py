@@ -25,7 +25,11 @@ STATUS_NAMES = {0: "BLUR_OK", 1: "BLUR_EINVAL", 2: "BLUR_EBEHIND", 3: "BLUR_ENOM
 
 EXPORTED = ["blur_workspace_bytes", "blur_render_fwd", "blur_render_bwd", "blur_l2_loss_grad",
             "blur_read_status", "blur_read_bins", "blur_read_soft_bins", "blur_ffma_probe", "blur_last_error",
-            "blur_abi_version"]
+            "blur_abi_version",
+            # include/blurrast_optim.h (NEXT-4 recovery step)
+            "blur_topology_bytes", "blur_topology_build", "blur_l1_loss_grad", "blur_laplacian_loss_grad",
+            "blur_smooth_loss_grad", "blur_adam_step", "blur_sum_sq_diff", "blur_voxel_scratch_bytes",
+            "blur_voxel_iou"]
 ABI_VERSION = 2
 
 
@@ -72,6 +76,18 @@ def load():
         lib.blur_read_soft_bins.argtypes = [P, P, P, P]
         lib.blur_ffma_probe.argtypes = [I, I, P, P, P]
         lib.blur_last_error.restype = C.c_char_p
+        F, D = C.c_float, C.c_double
+        lib.blur_topology_bytes.argtypes = [I, I, P]
+        lib.blur_topology_bytes.restype = SZ
+        lib.blur_topology_build.argtypes = [I, I, P, P, SZ, P]
+        lib.blur_l1_loss_grad.argtypes = [P, P, I, I, I, P, I, P, P, P]
+        lib.blur_laplacian_loss_grad.argtypes = [P, P, I, P, F, P, P, P]
+        lib.blur_smooth_loss_grad.argtypes = [P, I, P, F, P, P, P]
+        lib.blur_adam_step.argtypes = [P, P, P, P, C.c_int64, I, F, F, F, F, P]
+        lib.blur_sum_sq_diff.argtypes = [P, P, C.c_int64, P, P]
+        lib.blur_voxel_scratch_bytes.argtypes = [I]
+        lib.blur_voxel_scratch_bytes.restype = SZ
+        lib.blur_voxel_iou.argtypes = [P, I, P, I, P, I, P, I, I, P, SZ, P, P]
         lib.blur_abi_version.restype = I
         if lib.blur_abi_version() != ABI_VERSION:
             raise ImportError("libblurrast.so ABI %d != binding ABI %d: rebuild" % (lib.blur_abi_version(), ABI_VERSION))
@@ -251,3 +267,71 @@ def blur_last_error() -> str:
 
 def blur_abi_version() -> int:
     return int(load().blur_abi_version())
+
+
+# ------------------------------------------------------------------------- recovery step (blurrast_optim.h)
+
+def blur_topology_bytes(V, faces_np) -> int:
+    f = np.ascontiguousarray(np.asarray(faces_np, dtype=np.int32).reshape(-1, 3))
+    n = load().blur_topology_bytes(int(V), f.shape[0], _np_ptr(f))
+    if n == 0:
+        raise BlurError(BLUR_EINVAL, load().blur_last_error().decode())
+    return int(n)
+
+
+def blur_topology_build(V, faces_np, topo, stream=None):
+    import torch
+    f = np.ascontiguousarray(np.asarray(faces_np, dtype=np.int32).reshape(-1, 3))
+    return _check(load().blur_topology_build(int(V), f.shape[0], _np_ptr(f), _dev(topo, torch.uint8, "topo"),
+                                             topo.numel(), _stream(stream)))
+
+
+def blur_l1_loss_grad(out, target, loss, grad, image_mask=None, n_images=0, stream=None):
+    import torch
+    B, H, W = out.shape[0], out.shape[1], out.shape[2]
+    return _check(load().blur_l1_loss_grad(
+        _dev(out, torch.float32, "out"), _dev(target, torch.float32, "target"), B, H, W,
+        _dev(image_mask, torch.uint8, "image_mask"), int(n_images), _dev(loss, torch.float32, "loss"),
+        _dev(grad, torch.float32, "grad"), _stream(stream)))
+
+
+def blur_laplacian_loss_grad(verts, verts0, topo, weight, loss, grad_verts, stream=None):
+    import torch
+    return _check(load().blur_laplacian_loss_grad(
+        _dev(verts, torch.float32, "verts"), _dev(verts0, torch.float32, "verts0"), verts.shape[0],
+        _dev(topo, torch.uint8, "topo"), float(weight), _dev(loss, torch.float32, "loss"),
+        _dev(grad_verts, torch.float32, "grad_verts"), _stream(stream)))
+
+
+def blur_smooth_loss_grad(verts, topo, weight, loss, grad_verts, stream=None):
+    import torch
+    return _check(load().blur_smooth_loss_grad(
+        _dev(verts, torch.float32, "verts"), verts.shape[0], _dev(topo, torch.uint8, "topo"), float(weight),
+        _dev(loss, torch.float32, "loss"), _dev(grad_verts, torch.float32, "grad_verts"), _stream(stream)))
+
+
+def blur_adam_step(params, grads, m, v, step, lr=0.01, beta1=0.5, beta2=0.99, eps=1e-8, stream=None):
+    import torch
+    return _check(load().blur_adam_step(
+        _dev(params, torch.float32, "params"), _dev(grads, torch.float32, "grads"), _dev(m, torch.float32, "m"),
+        _dev(v, torch.float32, "v"), params.numel(), int(step), float(lr), float(beta1), float(beta2), float(eps),
+        _stream(stream)))
+
+
+def blur_sum_sq_diff(a, b, out, stream=None):
+    import torch
+    return _check(load().blur_sum_sq_diff(_dev(a, torch.float32, "a"), _dev(b, torch.float32, "b"), a.numel(),
+                                          _dev(out, torch.float64, "out"), _stream(stream)))
+
+
+def blur_voxel_scratch_bytes(res) -> int:
+    return int(load().blur_voxel_scratch_bytes(int(res)))
+
+
+def blur_voxel_iou(va, fa, vb, fb, res, scratch, counts, stream=None):
+    import torch
+    return _check(load().blur_voxel_iou(
+        _dev(va, torch.float32, "va"), va.shape[0], _dev(fa, torch.int32, "fa"), fa.shape[0],
+        _dev(vb, torch.float32, "vb"), vb.shape[0], _dev(fb, torch.int32, "fb"), fb.shape[0], int(res),
+        _dev(scratch, torch.uint8, "scratch"), scratch.numel(), _dev(counts, torch.int64, "counts"),
+        _stream(stream)))

@@ -422,6 +422,11 @@ int prepare(const float *verts, int V, const int32_t *faces, int F, const float 
 
 }  // namespace
 
+namespace br {
+void set_last_error(const std::string &msg) { g_err = msg; }
+void clear_last_error() { g_err.clear(); }
+}  // namespace br
+
 extern "C" {
 
 const char *blur_last_error(void) { return g_err.c_str(); }

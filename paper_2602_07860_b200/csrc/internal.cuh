@@ -132,7 +132,10 @@ __device__ __forceinline__ float box_lerp(float tau, float a, float b) { return 
 }  // namespace br
 
 // launchers (defined in the .cu files)
+#include <string>
 namespace br {
+void set_last_error(const std::string &msg);   // thread-local message of blur_last_error() (abi.cu)
+void clear_last_error();
 cudaError_t launch_setup(const Tables &t, const float *verts, const int *faces, const float *colors,
                          int maxS, cudaStream_t st);
 cudaError_t launch_binning(const Tables &t, const BinSet &bs, float dil, cudaStream_t st);

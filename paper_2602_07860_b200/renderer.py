@@ -78,6 +78,12 @@ class BlurRenderer:
             census.zero_()
         return self.forward(verts, colors, out, ids, ids_subframe, census, stream, events, soft_events)
 
+    def set_sub_range(self, sub_range):
+        """Per-image half-open sub-frame ranges for the next calls (None = all sub-frames).  The
+        workspace was sized for the ranges given at construction; narrower ranges (e.g. [0, 0) for the
+        views outside an optimisation batch) fit in it."""
+        self._sub = _lib.make_sub_range(sub_range)
+
     # -- forward / backward -------------------------------------------------------------
     def forward(self, verts: torch.Tensor, colors: torch.Tensor, out: Optional[torch.Tensor] = None,
                 ids: Optional[torch.Tensor] = None, ids_subframe: int = -1, census: Optional[torch.Tensor] = None,
