@@ -320,7 +320,9 @@ def main():
     # roofline of the dominant kernel (raster fwd K4 or raster bwd K6), this rank's launches
     nec, cov, cand, staged, soft_terms, soft_staged = units
     fw_flop = FLOP_PAIR * nec + FLOP_SHADE * cov + FLOP_SETUP * n_fsub
-    bw_flop = fw_flop + FLOP_BWD * cov
+    # K6 with the visibility buffer (BlurRenderer default) does not recompute the forward's tests
+    bw_flop = (FLOP_BWD * cov + FLOP_SETUP * n_fsub) if (rend is not None and rend.cache_flags) else \
+        fw_flop + FLOP_BWD * cov
     f_avg, b_avg = float(np.mean(fwd_ms)), float(np.mean(bwd_ms))
     kernels = [("k4_raster_fwd", fw_flop, f_avg), ("k6_raster_bwd", bw_flop, b_avg)]
     if soft:

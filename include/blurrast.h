@@ -100,6 +100,12 @@ typedef struct {
 /* Tuning / instrumentation (host struct; NULL = defaults). */
 #define BLUR_REUSE_SETUP 1   /* bwd: reuse keyframes, coefficients and bins that the preceding fwd
                                 call with identical arguments left in the same workspace */
+#define BLUR_CACHE_VISIBILITY 2   /* set on both the fwd and the bwd call: the fwd also leaves the
+                                winning bin slot of every (pixel, sub-frame) in the workspace (2 B each:
+                                sum_b N_b * H * W * 2 bytes, e.g. 0.84 GB for C4), and a bwd with
+                                BLUR_REUSE_SETUP reads it instead of recomputing the visibility (the
+                                result is identical; solver 0 only).  An index buffer, not sub-frame
+                                images: the blurred image is still accumulated in registers. */
 typedef struct {
     int32_t max_chunk;             /* G: max sub-frames sharing one tile bin (0 = automatic) */
     int32_t flags;                 /* BLUR_REUSE_SETUP */

@@ -25,16 +25,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile libblurrast.so (or `out`, with extra -D `defines`, for A/B variants)."""
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
-    tmp = LIB + ".tmp%d" % os.getpid()
+    tmp = target + ".tmp%d" % os.getpid()
     cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-           "-I", INCLUDE, "-o", tmp, *sources()]
+           "-I", INCLUDE, *["-D" + d for d in defines], "-o", tmp, *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     if os.environ.get("BR_DEBUG") == "1":
         cmd.insert(1, "-DBR_DEBUG")
     subprocess.check_call(cmd, cwd=CSRC)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target

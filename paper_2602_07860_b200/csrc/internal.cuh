@@ -93,6 +93,8 @@ struct Tables {          // device pointers into the workspace
     float rcut;          // NDC radius beyond which a face's term is dropped: sqrt(soft_cut * delta)
     int soft_exact;      // 1: Eq.12 (closest point on F(tau)) instead of Eq.13 (on F(X))
     uint32_t *covbits;   // [sum_b N_b][T][NWARP] coverage ballots per (sub-frame, tile, warp) or null
+    uint16_t *vis;       // [sum_b N_b][T][TW*TH] winning bin slot per (sub-frame, pixel), 0xFFFF none;
+                         // written by K4, read by K6 instead of recomputing visibility (or null)
     float *spart;        // [splits][B*H*W] soft alpha partial sums (K8)
     BinSet sb;           // soft bins (chunk boxes dilated by rcut)
 };

@@ -27,10 +27,29 @@
 namespace br {
 
 constexpr int NWARP = NT / 32;
-constexpr int SREC_F = 768;    // fwd: staged (tau, face) records per CTA (48 KB)
-constexpr int SREC_B = 512;    // bwd: staged records per CTA (32 KB); also the gather's slot limit
-constexpr int GMAX_F = 16;     // max sub-frames staged together
-constexpr int GMAX_B = 8;
+// tuning knobs (overridable with -D for A/B builds; defaults measured on C4, profiles/)
+#ifndef BR_SREC_F
+#define BR_SREC_F 768
+#endif
+#ifndef BR_SREC_B
+#define BR_SREC_B 384
+#endif
+#ifndef BR_GMAX_F
+#define BR_GMAX_F 16
+#endif
+#ifndef BR_GMAX_B
+#define BR_GMAX_B 8
+#endif
+#ifndef BR_K4_MINB
+#define BR_K4_MINB 4
+#endif
+#ifndef BR_K6_MINB
+#define BR_K6_MINB 4
+#endif
+constexpr int SREC_F = BR_SREC_F;   // fwd: staged (tau, face) records per CTA (64 B each)
+constexpr int SREC_B = BR_SREC_B;   // bwd: staged records per CTA; also the gather's slot limit
+constexpr int GMAX_F = BR_GMAX_F;   // max sub-frames staged together
+constexpr int GMAX_B = BR_GMAX_B;
 
 struct TileCtx {
     float uc, vc;     // NDC of the tile's reference pixel centre (TW/2, TH/2)
@@ -409,7 +428,7 @@ struct FwdSmem {
 };
 
 template <bool CENSUS, int MODE>
-__global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restrict__ out, int *__restrict__ ids,
+__global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float *__restrict__ out, int *__restrict__ ids,
                                                        int ids_k, unsigned long long *census)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -427,6 +446,7 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
     const float ul = (float)(lx - TW / 2) * tc.sx;
     const float vl = (float)(TH / 2 - ly) * tc.sy;
     const size_t pix = ((size_t)b * t.H + py) * t.W + px;
+    const int myp = ly * TW + lx;
     float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
     unsigned long long ncov = 0, ntest = 0, nshade = 0, nstage = 0;
 
@@ -456,6 +476,7 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
         if (!bc.fb && n <= SREC_F) {
             // grouped path: the whole bin staged for up to Gs sub-frames at once
             const int Gs = min(GMAX_F, SREC_F / n), nw = (n + 31) >> 5;
+            uint16_t *vis_out = (MODE == 0 && n <= SREC_B) ? t.vis : nullptr;
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
                 clear_words(S.wm, ng * NWARP * nw);
@@ -478,6 +499,9 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
                         if (CENSUS) nshade++;
                     }
                     if (ids && inimg && kg + l == ids_k) ids[pix] = fid;
+                    if (vis_out)   // visibility buffer for K6 (bins it takes the grouped path for)
+                        vis_out[((size_t)(im.cov_off + kg + l) * t.T + tile) * (TW * TH) + myp] =
+                            ebest >= 0 ? (uint16_t)ebest : (uint16_t)0xFFFF;
                     if (t.covbits) {   // soft path: which pixels of the warp are covered at this sub-frame
                         const unsigned m = __ballot_sync(0xffffffffu, ebest >= 0 || !inimg);
                         if (lane == 0) t.covbits[cov_word(t, im, kg + l, tile) + warp] = m;
@@ -550,6 +574,57 @@ __global__ void __launch_bounds__(NT, 4) k4_raster_fwd(Tables t, float *__restri
 // evaluates the closed form.  Face gradients accumulate in registers over the chunk's sub-frames
 // (slot == thread) and are flushed with one vector RED per (vertex, keyframe) at the chunk's end.
 
+// Record of a (face, segment) coefficient record at tau for this tile, written unconditionally (the
+// cached-visibility backward stages only faces that won a pixel in the forward, whose records the
+// forward built with the same arithmetic).
+__device__ __forceinline__ void stage_rec(const FaceRec &fr, float tau, const TileCtx &tc, TauRec &out)
+{
+    const float4 q6 = fr.q[6];
+    const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);
+    const float sg = D < 0.f ? -1.f : 1.f;
+    const float invD = 1.0f / fabsf(D);
+    float A[3], B[3], G[3];
+    const float *ef = reinterpret_cast<const float *>(fr.q);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float ox = ef[8 * i], oy = ef[8 * i + 1];
+        const float al = __fmaf_rn(tau, ef[8 * i + 3], ef[8 * i + 2]);
+        const float be = __fmaf_rn(tau, ef[8 * i + 5], ef[8 * i + 4]);
+        const float ga = __fmul_rn(tau, __fmaf_rn(tau, ef[8 * i + 7], ef[8 * i + 6]));
+        const float dx = __fsub_rn(tc.uc, ox), dy = __fsub_rn(tc.vc, oy);
+        const float gp = __fmaf_rn(al, dx, __fmaf_rn(be, dy, ga));
+        A[i] = al * sg;
+        B[i] = be * sg;
+        G[i] = gp * sg;
+    }
+    out.a[0] = A[0]; out.a[1] = A[1]; out.a[2] = A[2];
+    out.b[0] = B[0]; out.b[1] = B[1]; out.b[2] = B[2];
+    out.g[0] = G[0]; out.g[1] = G[1]; out.g[2] = G[2];
+    out.az = 0.f;       // depth plane unused by the gather
+    out.bz = 0.f;
+    out.cz = 0.f;
+    out.invD = invD;
+    out.fid = __float_as_int(q6.w);
+}
+
+// stage the won (face, sub-frame) pairs of bin slots [0, n) at the ng sub-frames: rec[l * n + j]
+__device__ __forceinline__ void stage_won(const BinCtx &bc, int n, const float *taus, int ng, const TileCtx &tc, int F,
+                                          const unsigned char *won, TauRec *rec)
+{
+    for (int p = threadIdx.x; p < n * ng; p += NT) {
+        const int j = p / ng, l = p - j * ng;
+        if (!won[l * n + j]) continue;
+        const int f = __ldg(bc.ent + j);
+        if ((unsigned)f >= (unsigned)F) {
+            atomicOr(bc.status, BLUR_ST_EINTERNAL);
+            continue;
+        }
+        FaceRec fr;
+        load_rec(bc.rseg + (size_t)f * REC_F4, fr);
+        stage_rec(fr, taus[l], tc, rec[l * n + j]);
+    }
+}
+
 template <int MODE>
 struct BwdSmem {
     TauRec rec[SREC_B];
@@ -565,6 +640,7 @@ struct BwdSmem {
     float4 g[TW * TH];        // dL/dI / N of the tile
     float taus[GMAX_B];
     int wsum[NWARP];
+    unsigned char won[SREC_B];   // cached visibility: (sub-frame, slot) pairs that won a pixel
 };
 
 // block-wide exclusive scan of cnt[0..nb) (nb <= 2 NT) into off[]; returns the total
@@ -748,7 +824,7 @@ __device__ __forceinline__ void bwd_gather(Sm &S, const TauRec *rec, const Table
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__restrict__ grad, float *__restrict__ dC)
+__global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const float *__restrict__ grad, float *__restrict__ dC)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BwdSmem<MODE> &S = *reinterpret_cast<BwdSmem<MODE> *>(smem_raw);
@@ -794,7 +870,27 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
         bc.fb = n > SORTCAP || o + n > t.cap;
         FaceAcc acc;
         acc_zero(acc);
-        if (!bc.fb && n <= SREC_B) {
+        if (MODE == 0 && t.vis && !bc.fb && n <= SREC_B) {
+            // visibility from the forward's buffer: stage only the (face, sub-frame) pairs that won
+            const int Gs = min(GMAX_B, SREC_B / n);
+            for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
+                const int ng = min(Gs, ch.k1 - kg);
+                for (int i = threadIdx.x; i < ng * n; i += NT) S.won[i] = 0;
+                if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
+                __syncthreads();
+                for (int l = 0; l < ng; ++l) {
+                    const uint16_t v = t.vis[((size_t)(im.cov_off + kg + l) * t.T + tile) * (TW * TH) + myp];
+                    const int e = (inimg && v != 0xFFFF) ? (int)v : -1;
+                    S.win[l][myp] = e;
+                    if (e >= 0) S.won[l * n + e] = 1;
+                }
+                __syncthreads();
+                stage_won(bc, n, S.taus, ng, tc, t.F, S.won, S.rec);
+                __syncthreads();
+                for (int l = 0; l < ng; ++l)
+                    bwd_gather(S, S.rec + l * n, t, im, ch.s, S.taus[l], 0, n, true, S.win[l][myp], myp, tc, acc, dC);
+            }
+        } else if (!bc.fb && n <= SREC_B) {
             const int Gs = min(GMAX_B, SREC_B / n), nw = (n + 31) >> 5;
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
@@ -849,7 +945,7 @@ __global__ void __launch_bounds__(NT, 3) k6_raster_bwd(Tables t, const float *__
                 }
             }
         }
-        if (!bc.fb && n <= SREC_B && (int)threadIdx.x < n) {
+        if (!bc.fb && n <= SREC_B && (int)threadIdx.x < n) {   // persistent slots (both grouped paths)
             bool nz = false;
 #pragma unroll
             for (int i = 0; i < 9; ++i) nz |= acc.c[i] != 0.f;

@@ -25,7 +25,7 @@ class BlurRenderer:
     def __init__(self, faces, motion: dict, cams, H: int, W: int, V: int, device="cuda",
                  sub_range=None, max_chunk: int = 0, bin_factor: float = 0.0, solver: int = 0,
                  delta: float = 0.0, soft_cut: float = 0.0, soft_exact: bool = False,
-                 soft_bin_factor: float = 0.0):
+                 soft_bin_factor: float = 0.0, cache_visibility: bool = True):
         _lib.load()
         self.device = torch.device(device)
         self.faces = torch.as_tensor(np.asarray(faces.cpu() if torch.is_tensor(faces) else faces),
@@ -45,11 +45,14 @@ class BlurRenderer:
         # soft background coverage (NEXT-1, Eq.10-15): delta > 0 enables it
         self.delta, self.soft_cut, self.soft_exact = float(delta), float(soft_cut), bool(soft_exact)
         self.soft_bin_factor = float(soft_bin_factor)
+        # K4 leaves the per-(pixel, sub-frame) winner slot for K6 (BLUR_CACHE_VISIBILITY)
+        self.cache_flags = _lib.BLUR_CACHE_VISIBILITY if (cache_visibility and self.solver == 0) else 0
         self.auto_bins = bin_factor == 0.0 or (self.delta > 0 and soft_bin_factor == 0.0)
         self._alloc(self.bin_factor, self.soft_bin_factor)
 
     def _cfg(self, flags=0, census=None, events=None, soft_events=None):
-        return _lib.make_config(self.max_chunk, flags, self.bin_factor, census, events, self.solver, self.delta,
+        return _lib.make_config(self.max_chunk, flags | self.cache_flags, self.bin_factor, census, events, self.solver,
+                                self.delta,
                                 self.soft_cut, self.soft_exact, self.soft_bin_factor, soft_events)
 
     def _alloc(self, factor: float, soft_factor: float = 0.0):

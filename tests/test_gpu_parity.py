@@ -23,12 +23,12 @@ def _torch():
     return torch
 
 
-def gpu_render(sc, ids_k=-1, sub_range=None, max_chunk=0, bin_factor=0.0, G=None, reuse=True):
+def gpu_render(sc, ids_k=-1, sub_range=None, max_chunk=0, bin_factor=0.0, G=None, reuse=True, cache=True):
     torch = _torch()
     from paper_2602_07860_b200 import BlurRenderer
     dev = torch.device("cuda:0")
     r = BlurRenderer(sc.faces, sc.motion, sc.cams, sc.H, sc.W, sc.V, device=dev, sub_range=sub_range,
-                     max_chunk=max_chunk, bin_factor=bin_factor)
+                     max_chunk=max_chunk, bin_factor=bin_factor, cache_visibility=cache)
     v = torch.tensor(np.asarray(sc.verts, np.float32), device=dev)
     c = torch.tensor(np.asarray(sc.colors, np.float32), device=dev)
     ids = torch.full((sc.B, sc.H, sc.W), -7, dtype=torch.int32, device=dev) if ids_k >= 0 else None
@@ -274,3 +274,17 @@ def test_naive_solvers_match_oracle(solver):
                         torch.tensor(G, dtype=torch.float32, device="cuda"), reuse_setup=True)
     rdv, rdc = oracle.render_bwd(sc, G)
     assert rel_l2(dv.cpu().numpy(), rdv) < TOL_GRAD and rel_l2(dc.cpu().numpy(), rdc) < TOL_GRAD
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_visibility_cache_equals_recompute(cfg):
+    """BLUR_CACHE_VISIBILITY (K6 reads K4's winner slots) gives the same image and gradients as
+    recomputing the visibility in K6 (and as a backward without the preceding forward)."""
+    sc = scenes.make(cfg).subset([0, 1])
+    G = np.random.default_rng(3).normal(size=(sc.B, sc.H, sc.W, 4)).astype(np.float32) * 1e-4
+    a = gpu_render(sc, G=G, cache=True)
+    b = gpu_render(sc, G=G, cache=False)
+    c = gpu_render(sc, G=G, cache=True, reuse=False)
+    assert np.array_equal(a["rgba"], b["rgba"])
+    for x in (b, c):
+        assert rel_l2(a["dv"], x["dv"]) < 1e-5 and rel_l2(a["dc"], x["dc"]) < 1e-5
