@@ -350,7 +350,11 @@ BinSet hard_bins(const Tables &t)
     b.entries = t.entries;
     b.cap = t.cap;
     b.binstat = t.binstat;
+#ifdef BR_SORT_HARD
     b.sortcap = SORTCAP;
+#else
+    b.sortcap = 0;      // not sorted: the raster z-buffer breaks depth ties by face index itself
+#endif
     return b;
 }
 

@@ -8,10 +8,11 @@
 //   K3a count  (chunk, face) -> atomic per (chunk, tile) counters
 //   K3b scan   exclusive prefix sum of the counters -> bin offsets
 //   K3c fill   (chunk, face) -> entries (unordered)
-//   K3d sort   one warp per bin: bitonic sort of the face ids in shared memory, so the raster
-//              kernels visit faces in index order (Z-buffer tie rule: lower index wins, Q7)
-// Bins longer than SORTCAP or beyond the entry capacity are left to the raster kernels' exact
-// fallback path (status bit BLUR_ST_EOVERFLOW).
+//   K3d sort   soft bins only: bitonic sort of the face ids (one warp per bin up to SORTCAP, one CTA
+//              per bin up to 4096), so that the soft product runs in face order (deterministic).
+//              The hard bins stay unsorted: the raster z-buffer breaks depth ties by face index (Q7).
+// Entries beyond the capacity are left to the raster kernels' exact fallback path (status bit
+// BLUR_ST_EOVERFLOW).
 #include <algorithm>
 #include <cstdio>
 
@@ -283,7 +284,7 @@ cudaError_t launch_binning(const Tables &t, const BinSet &bs, float dil, cudaStr
         k3_fill<<<grid, 256, 0, st>>>(t, bs, dil);
         int sb = (nbins + 7) / 8;
         if (sb > 148 * 16) sb = 148 * 16;
-        k3_sort<<<sb, 256, 0, st>>>(t, bs, nbins);
+        if (bs.sortcap > 0) k3_sort<<<sb, 256, 0, st>>>(t, bs, nbins);
         if (bs.sortcap > SORTCAP) k3_sort_big<<<std::min(nbins, 148 * 4), 512, 0, st>>>(t, bs, nbins);
     }
     return cudaGetLastError();

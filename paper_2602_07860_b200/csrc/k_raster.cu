@@ -15,9 +15,10 @@
 //   shade   fwd: w_i = N_i / |D|, I = sum w_i c_i (Eq.9), accumulated in registers over all
 //           sub-frames; the sub-frames never reach HBM.  Output (1/N) sum, written once.
 //           bwd: see the comment above k6_raster_bwd.
-// Bins that overflowed (or exceed SORTCAP) are regenerated exactly by scanning all faces in index
-// order (slow path); bins longer than the shared-memory record capacity are processed per
-// sub-frame in several batches.
+// Bins that overflowed are regenerated exactly by scanning all faces in index order (slow path); bins
+// longer than the shared-memory record capacity are processed per sub-frame in several batches.
+// The hard bins are not sorted: the z-buffer compares (depth, face index), which is independent of
+// the order the faces are visited in.
 #include <algorithm>
 #include <cstdio>
 
@@ -339,7 +340,7 @@ __device__ __forceinline__ void stage_group(const BinCtx &bc, int nb, int base, 
 
 template <bool CENSUS, int MODE>
 __device__ __forceinline__ void vis_mask(const TauRec *rec, const float4 *vtx, const uint32_t *wm, int nw,
-                                         int ebase, float ul, float vl, float &zbest, int &ebest,
+                                         int ebase, float ul, float vl, float &zbest, int &ebest, int &fbest,
                                          unsigned long long &ncov, unsigned long long &ntest, bool count)
 {
     for (int wd = 0; wd < nw; ++wd) {
@@ -374,7 +375,12 @@ __device__ __forceinline__ void vis_mask(const TauRec *rec, const float4 *vtx, c
                 cov = fminf(fminf(w0, w1), w2) >= 0.f && det != 0.f;
             }
             if (CENSUS && count) { ncov += cov; ntest += 1; }
-            if (cov && z < zbest) { zbest = z; ebest = ebase + j; }
+            // z-buffer on (depth, face index): strict < in depth, the lower face index on exact ties
+            // (Q7) -- order-independent, so the bins need not be sorted
+            if (cov && z <= zbest) {
+                const int fj = rw[k].fid;
+                if (z < zbest || fj < fbest) { zbest = z; ebest = ebase + j; fbest = fj; }
+            }
         }
     }
 }
@@ -472,7 +478,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
         bc.fcol = t.fcol;
         bc.ent = t.entries + o;
         bc.n = n;
-        bc.fb = n > SORTCAP || o + n > t.cap;
+        bc.fb = o + n > t.cap;
         if (!bc.fb && n <= SREC_F) {
             // grouped path: the whole bin staged for up to Gs sub-frames at once
             const int Gs = min(GMAX_F, SREC_F / n), nw = (n + 31) >> 5;
@@ -486,10 +492,10 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                 __syncthreads();
                 for (int l = 0; l < ng; ++l) {
                     float zbest = __int_as_float(0x7f800000);
-                    int ebest = -1;
+                    int ebest = -1, fbest = 0x7fffffff;
                     const TauRec *rl = S.rec + l * n;
                     vis_mask<CENSUS, MODE>(rl, S.vtx + 3 * l * n, S.wm + (l * NWARP + warp) * nw, nw, 0, ul, vl,
-                                           zbest, ebest, ncov, ntest, inimg);
+                                           zbest, ebest, fbest, ncov, ntest, inimg);
                     int fid = -1;
                     if (ebest >= 0) {
                         float pr, pg, pb;
@@ -514,7 +520,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
             for (int k = ch.k0; k < ch.k1; ++k) {
                 const float tau = t.sched_tau[sched_off + k];
                 float zbest = __int_as_float(0x7f800000);
-                int ebest = -1, bfid = -1;
+                int ebest = -1, bfid = -1, fbest = 0x7fffffff;
                 bool has = false;
                 float pr = 0.f, pg = 0.f, pb = 0.f;
                 int base = 0, fpos = 0;
@@ -527,11 +533,13 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                     __syncthreads();
                     stage_group<CENSUS, MODE>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, nstage);
                     __syncthreads();
-                    vis_mask<CENSUS, MODE>(S.rec, S.vtx, S.wm + warp * nw, nw, base, ul, vl, zbest, ebest, ncov, ntest, inimg);
+                    vis_mask<CENSUS, MODE>(S.rec, S.vtx, S.wm + warp * nw, nw, base, ul, vl, zbest, ebest, fbest, ncov,
+                                           ntest, inimg);
                     if (ebest >= base) {   // winner changed in this batch: shade now (Eq.9)
                         shade(S.rec[ebest - base], t.fcol, ul, vl, pr, pg, pb);
                         has = true;
                         bfid = S.rec[ebest - base].fid;
+                        fbest = bfid;      // ties against later batches compare face indices
                     }
                     base += nb;
                     __syncthreads();
@@ -867,7 +875,7 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
         bc.fcol = t.fcol;
         bc.ent = t.entries + o;
         bc.n = n;
-        bc.fb = n > SORTCAP || o + n > t.cap;
+        bc.fb = o + n > t.cap;
         FaceAcc acc;
         acc_zero(acc);
         if (MODE == 0 && t.vis && !bc.fb && n <= SREC_B) {
@@ -901,9 +909,9 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
                 __syncthreads();
                 for (int l = 0; l < ng; ++l) {       // visibility for the group (no barriers)
                     float zbest = __int_as_float(0x7f800000);
-                    int ebest = -1;
+                    int ebest = -1, fbest = 0x7fffffff;
                     vis_mask<false, MODE>(S.rec + l * n, S.vtx + 3 * l * n, S.wm + (l * NWARP + warp) * nw, nw, 0, ul,
-                                          vl, zbest, ebest, d0, d1, false);
+                                          vl, zbest, ebest, fbest, d0, d1, false);
                     S.win[l][myp] = inimg ? ebest : -1;
                 }
                 __syncthreads();
@@ -914,7 +922,7 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
             for (int k = ch.k0; k < ch.k1; ++k) {
                 const float tau = t.sched_tau[sched_off + k];
                 float zbest = __int_as_float(0x7f800000);
-                int ebest = -1;
+                int ebest = -1, fbest = 0x7fffffff;
                 int base = 0, fpos = 0;
                 if (threadIdx.x == 0) S.taus[0] = tau;
                 while (true) {                         // visibility over all batches
@@ -925,7 +933,9 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
                     __syncthreads();
                     stage_group<false, MODE>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, d2);
                     __syncthreads();
-                    vis_mask<false, MODE>(S.rec, S.vtx, S.wm + warp * nw, nw, base, ul, vl, zbest, ebest, d0, d1, false);
+                    vis_mask<false, MODE>(S.rec, S.vtx, S.wm + warp * nw, nw, base, ul, vl, zbest, ebest, fbest, d0, d1,
+                                          false);
+                    if (ebest >= base) fbest = S.rec[ebest - base].fid;
                     base += nb;
                     __syncthreads();
                 }
