@@ -288,3 +288,23 @@ def test_visibility_cache_equals_recompute(cfg):
     assert np.array_equal(a["rgba"], b["rgba"])
     for x in (b, c):
         assert rel_l2(a["dv"], x["dv"]) < 1e-5 and rel_l2(a["dc"], x["dc"]) < 1e-5
+
+
+def test_exact_depth_ties_lower_face_index_wins():
+    """Q7: coincident faces (duplicated vertices, different colours) tie exactly in depth at every
+    covered pixel; the lower face index must win, whatever order the (unsorted) bins visit them in."""
+    rng = np.random.default_rng(8)
+    base = scenes.random_mesh_scene(12, 21, H=40, W=40, motion=scenes.translate((0.5, 0.1, 0.0), N=6))
+    V = base.V
+    verts = np.concatenate([base.verts, base.verts]).astype(np.float32)
+    cols = np.concatenate([base.colors, rng.uniform(0, 1, base.colors.shape)]).astype(np.float32)
+    # interleave: the duplicate (second vertex copy) of face i gets index 2i, the original 2i + 1
+    faces = np.empty((2 * base.F, 3), np.int32)
+    faces[0::2] = base.faces + V
+    faces[1::2] = base.faces
+    sc = scenes.single_scene(verts, faces, cols, motion=scenes.translate((0.5, 0.1, 0.0), N=6), H=40, W=40)
+    r = check_parity(sc, ids_k=2, mode="brute")
+    got = gpu_render(sc, ids_k=2)
+    ids = got["ids"][0]
+    assert np.all((ids < 0) | (ids % 2 == 0))      # only the lower-index copies are visible
+    print(r)
