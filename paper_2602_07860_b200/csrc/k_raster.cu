@@ -333,9 +333,42 @@ __device__ __forceinline__ void stage_group(const BinCtx &bc, int nb, int base, 
             fm = stage_tau_naive<MODE>(bc, f, tau, tc, W, H, rec[l * nb + j], vtx + 3 * (l * nb + j));
         }
         if (CENSUS) nstage += fm != 0u;
-        const uint32_t bit = 0x80000000u >> (j & 31);          // bit-reversed: clz gives ascending slots
+        const uint32_t bit = 1u << (j & 31);
         for (uint32_t m = fm; m; m &= m - 1) atomicOr(wm + (l * NWARP + (__ffs(m) - 1)) * nw + (j >> 5), bit);
     }
+}
+
+// Visibility of one pixel over the faces of its warp's mask (any visiting order): z-buffer on
+// (depth, face index).  vis_mask_fast keeps strict < on depth only and reports whether an exact depth
+// tie occurred (the caller then re-runs vis_mask, which compares face indices) -- ties need exactly
+// equal float depths of two faces at a pixel centre, so the common loop stays short.
+template <bool CENSUS, int MODE>
+__device__ __forceinline__ bool vis_mask_fast(const TauRec *rec, const uint32_t *wm, int nw, float ul, float vl,
+                                              float &zbest, int &ebest, unsigned long long &ncov,
+                                              unsigned long long &ntest, bool count)
+{
+    float tief = 0.f;
+    for (int wd = 0; wd < nw; ++wd) {
+        uint32_t m = wm[wd];
+        const float4 *rw = reinterpret_cast<const float4 *>(rec + (wd << 5));
+        while (m) {
+            int k;
+            asm("bfind.u32 %0, %1;" : "=r"(k) : "r"(m));   // highest set bit (any order is fine)
+            m ^= 1u << k;
+            const float4 *rp = rw + 4 * k;
+            const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
+            const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
+            const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
+            const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
+            const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
+            const float emin = fminf(fminf(e0, e1), e2);
+            if (CENSUS && count) { ncov += emin >= 0.f; ntest += 1; }
+            // covered with z == zbest: an exact depth tie (kept in a float: one FSEL per test)
+            tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
+            if (emin >= 0.f && z < zbest) { zbest = z; ebest = (wd << 5) + k; }
+        }
+    }
+    return tief != 0.f;
 }
 
 template <bool CENSUS, int MODE>
@@ -347,8 +380,8 @@ __device__ __forceinline__ void vis_mask(const TauRec *rec, const float4 *vtx, c
         uint32_t m = wm[wd];
         const TauRec *rw = rec + (wd << 5);
         while (m) {
-            const int k = __clz(m);
-            m ^= 0x80000000u >> k;
+            const int k = 31 - __clz(m);
+            m ^= 1u << k;
             const int j = (wd << 5) + k;
             bool cov;
             float z;
@@ -494,8 +527,16 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                     float zbest = __int_as_float(0x7f800000);
                     int ebest = -1, fbest = 0x7fffffff;
                     const TauRec *rl = S.rec + l * n;
-                    vis_mask<CENSUS, MODE>(rl, S.vtx + 3 * l * n, S.wm + (l * NWARP + warp) * nw, nw, 0, ul, vl,
-                                           zbest, ebest, fbest, ncov, ntest, inimg);
+                    const uint32_t *wml = S.wm + (l * NWARP + warp) * nw;
+                    bool tie = true;
+                    if (MODE != 2) tie = vis_mask_fast<CENSUS, MODE>(rl, wml, nw, ul, vl, zbest, ebest, ncov, ntest, inimg);
+                    if (__any_sync(0xffffffffu, tie)) {   // exact depth tie somewhere in the warp: face indices decide
+                        unsigned long long d0 = 0, d1 = 0;
+                        zbest = __int_as_float(0x7f800000);
+                        ebest = -1;
+                        if (MODE != 2) vis_mask<false, MODE>(rl, S.vtx + 3 * l * n, wml, nw, 0, ul, vl, zbest, ebest, fbest, d0, d1, false);
+                        else vis_mask<CENSUS, MODE>(rl, S.vtx + 3 * l * n, wml, nw, 0, ul, vl, zbest, ebest, fbest, ncov, ntest, inimg);
+                    }
                     int fid = -1;
                     if (ebest >= 0) {
                         float pr, pg, pb;
@@ -910,8 +951,15 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
                 for (int l = 0; l < ng; ++l) {       // visibility for the group (no barriers)
                     float zbest = __int_as_float(0x7f800000);
                     int ebest = -1, fbest = 0x7fffffff;
-                    vis_mask<false, MODE>(S.rec + l * n, S.vtx + 3 * l * n, S.wm + (l * NWARP + warp) * nw, nw, 0, ul,
-                                          vl, zbest, ebest, fbest, d0, d1, false);
+                    const uint32_t *wml = S.wm + (l * NWARP + warp) * nw;
+                    bool tie = true;
+                    if (MODE != 2) tie = vis_mask_fast<false, MODE>(S.rec + l * n, wml, nw, ul, vl, zbest, ebest, d0, d1, false);
+                    if (__any_sync(0xffffffffu, tie)) {
+                        zbest = __int_as_float(0x7f800000);
+                        ebest = -1;
+                        vis_mask<false, MODE>(S.rec + l * n, S.vtx + 3 * l * n, wml, nw, 0, ul, vl, zbest, ebest, fbest,
+                                              d0, d1, false);
+                    }
                     S.win[l][myp] = inimg ? ebest : -1;
                 }
                 __syncthreads();
