@@ -90,6 +90,20 @@ __device__ __forceinline__ void load_rec(const float4 *__restrict__ r, FaceRec &
 }
 
 // max over the pixel centres of a local rect [x0..x1] x [y0..y1] of the edge function, >= -tol ?
+// (tol_i: per-record rounding allowance, see stage_tau)
+__device__ __forceinline__ bool rect_reaches_t(const float A[3], const float B[3], const float G[3], const float tol[3],
+                                               int x0, int x1, int y0, int y1, const TileCtx &tc)
+{
+    const float ulmin = (float)(x0 - TW / 2) * tc.sx, ulmax = (float)(x1 - TW / 2) * tc.sx;
+    const float vlmin = (float)(TH / 2 - y1) * tc.sy, vlmax = (float)(TH / 2 - y0) * tc.sy;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float m = G[i] + A[i] * (A[i] > 0.f ? ulmax : ulmin) + B[i] * (B[i] > 0.f ? vlmax : vlmin);
+        if (m < -tol[i]) return false;
+    }
+    return true;
+}
+
 __device__ __forceinline__ bool rect_reaches(const float A[3], const float B[3], const float G[3], int x0, int x1,
                                              int y0, int y1, const TileCtx &tc)
 {
@@ -107,17 +121,11 @@ __device__ __forceinline__ bool rect_reaches(const float A[3], const float B[3],
 
 // Evaluate a record at tau for this tile -> TauRec + the mask of warp footprints it can reach
 // (bit w = warp w's 8x4 footprint; 0 = the face cannot cover any pixel of the tile at tau).
-__device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, const TileCtx &tc, int W, int H,
-                                              TauRec &out)
+// D = det F(tau) (|D| > EPS_D) and the face's pixel box in the tile come from the caller's rejects.
+__device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, float D, int x0, int x1, int y0, int y1,
+                                              const TileCtx &tc, TauRec &out)
 {
     const float4 q6 = fr.q[6];
-    const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);   // a1 t^2 + a2 t + a3
-    if (!(fabsf(D) > EPS_D)) return 0u;                                 // Q8
-    const float4 b0 = fr.q[7], b1 = fr.q[8];
-    int x0, x1, y0, y1;
-    if (!tile_pixels(box_lerp(tau, b0.x, b1.x), box_lerp(tau, b0.y, b1.y), box_lerp(tau, b0.z, b1.z),
-                     box_lerp(tau, b0.w, b1.w), W, H, tc, x0, x1, y0, y1))
-        return 0u;
     const float sg = D < 0.f ? -1.f : 1.f;
     const float invD = 1.0f / fabsf(D);
     float A[3], B[3], G[3];
@@ -134,13 +142,18 @@ __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, cons
         B[i] = be * sg;
         G[i] = gp * sg;
     }
-    // warp footprints (8x4, arranged 2 x 4) reached by the box and the three edge half-planes
+    // warp footprints (8x4, arranged 2 x 4) reached by the box and the three edge half-planes; the
+    // rounding allowance is bounded once over the whole tile (|ul|, |vl| <= 8 pixels)
+    float tol[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        tol[i] = 1e-6f * (fabsf(A[i]) * (8.f * tc.sx) + fabsf(B[i]) * (8.f * tc.sy) + fabsf(G[i])) + 1e-30f;
     uint32_t fm = 0u;
     for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
         for (int wx = x0 >> 3; wx <= (x1 >> 3); ++wx) {
             const int rx0 = max(x0, wx * 8), rx1 = min(x1, wx * 8 + 7);
             const int ry0 = max(y0, wy * 4), ry1 = min(y1, wy * 4 + 3);
-            if (rect_reaches(A, B, G, rx0, rx1, ry0, ry1, tc)) fm |= 1u << (wy * 2 + wx);
+            if (rect_reaches_t(A, B, G, tol, rx0, rx1, ry0, ry1, tc)) fm |= 1u << (wy * 2 + wx);
         }
     if (!fm) return 0u;
     const float4 z0 = fr.q[9], z1 = fr.q[10];
@@ -315,20 +328,19 @@ __device__ __forceinline__ void stage_group(const BinCtx &bc, int nb, int base, 
         const float4 q6 = __ldg(r + 6);
         if (__float_as_int(q6.w) < 0) continue;               // skipped face (Q8, behind, bad index)
         const float tau = taus[l];
-        {   // cheap rejects before the full record is loaded: degenerate at tau, box off the tile
-            const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);
-            if (!(fabsf(D) > EPS_D)) continue;
-            const float4 b0 = __ldg(r + 7), b1 = __ldg(r + 8);
-            int x0, x1, y0, y1;
-            if (!tile_pixels(box_lerp(tau, b0.x, b1.x), box_lerp(tau, b0.y, b1.y), box_lerp(tau, b0.z, b1.z),
-                             box_lerp(tau, b0.w, b1.w), W, H, tc, x0, x1, y0, y1))
-                continue;
-        }
+        // cheap rejects before the full record is loaded: degenerate at tau (Q8), box off the tile
+        const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);   // a1 t^2 + a2 t + a3
+        if (!(fabsf(D) > EPS_D)) continue;
+        const float4 b0 = __ldg(r + 7), b1 = __ldg(r + 8);
+        int x0, x1, y0, y1;
+        if (!tile_pixels(box_lerp(tau, b0.x, b1.x), box_lerp(tau, b0.y, b1.y), box_lerp(tau, b0.z, b1.z),
+                         box_lerp(tau, b0.w, b1.w), W, H, tc, x0, x1, y0, y1))
+            continue;
         uint32_t fm;
         if (MODE == 0) {
             FaceRec fr;
             load_rec(r, fr);
-            fm = stage_tau(fr, tau, tc, W, H, rec[l * nb + j]);
+            fm = stage_tau(fr, tau, D, x0, x1, y0, y1, tc, rec[l * nb + j]);
         } else {
             fm = stage_tau_naive<MODE>(bc, f, tau, tc, W, H, rec[l * nb + j], vtx + 3 * (l * nb + j));
         }
