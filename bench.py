@@ -233,8 +233,8 @@ def main():
     stream = torch.cuda.current_stream()
 
     # census (outside timing): algorithmic unit counts of this rank's forward
-    census = torch.zeros(6, dtype=torch.int64, device=dev)
-    units = np.zeros(6)
+    census = torch.zeros(8, dtype=torch.int64, device=dev)
+    units = np.zeros(8)
     if rend is not None:
         rend.forward(verts, colors, census=census)
         units = census.cpu().numpy().astype(np.float64)
@@ -318,7 +318,7 @@ def main():
     value = sc.B / (ms_per_step / 1000.0)
 
     # roofline of the dominant kernel (raster fwd K4 or raster bwd K6), this rank's launches
-    nec, cov, cand, staged, soft_terms, soft_staged = units
+    nec, cov, cand, staged, soft_terms, soft_staged, soft_items, soft_iters = units
     fw_flop = FLOP_PAIR * nec + FLOP_SHADE * cov + FLOP_SETUP * n_fsub
     # K6 with the visibility buffer (BlurRenderer default) does not recompute the forward's tests
     bw_flop = (FLOP_BWD * cov + FLOP_SETUP * n_fsub) if (rend is not None and rend.cache_flags) else \
@@ -345,6 +345,7 @@ def main():
                 **({"soft_fwd_ms": float(np.mean(sf_ms)), "soft_bwd_ms": float(np.mean(sb_ms))} if soft else {}),
                 "executed_pair_tests_per_launch": cand, "necessary_pairs_per_launch": nec,
                 **({"soft_terms_per_launch": soft_terms, "soft_staged_records_per_launch": soft_staged,
+                    "soft_items_per_launch": soft_items, "soft_face_iterations_per_launch": soft_iters,
                     "kernels_ms": {k[0]: k[2] for k in kernels}} if soft else {})}
 
     # measured FFMA throughput (context for the derived peak)

@@ -47,7 +47,16 @@ namespace br {
 namespace {
 
 constexpr int SNW = NT / 32;     // warps per CTA
-constexpr int SREC_F8 = 512;     // K8: staged soft records per CTA (80 B each)
+#ifndef BR_SREC_F8
+#define BR_SREC_F8 512
+#endif
+#ifndef BR_K8_MINB
+#define BR_K8_MINB 4
+#endif
+#ifndef BR_K9_SPLIT
+#define BR_K9_SPLIT 1
+#endif
+constexpr int SREC_F8 = BR_SREC_F8;   // K8: staged soft records per CTA (80 B each)
 constexpr int SREC_B9 = 384;     // K9: staged soft records per CTA
 constexpr int GMAX_S = 8;        // sub-frames staged together
 constexpr int NPX = TW * TH;
@@ -372,7 +381,7 @@ struct SoftFwdSmem {
 };
 
 template <bool CENSUS>
-__global__ void __launch_bounds__(NT, 3) k8_soft_fwd(Tables t, unsigned long long *census)
+__global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned long long *census)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SoftFwdSmem &S = *reinterpret_cast<SoftFwdSmem *>(smem_raw);
@@ -386,7 +395,7 @@ __global__ void __launch_bounds__(NT, 3) k8_soft_fwd(Tables t, unsigned long lon
     const bool inimg = px < t.W && py < t.H;
     const float kexp = 1.0f / t.delta;
     float alpha = 0.f;
-    unsigned long long npair = 0, nstage = 0;
+    unsigned long long npair = 0, nstage = 0, nitem = 0, nface = 0;
 
     for (int c = im.chunk_begin + (int)blockIdx.z; c < im.chunk_end; c += t.splits) {
         const Chunk ch = t.chunks[c];
@@ -406,6 +415,10 @@ __global__ void __launch_bounds__(NT, 3) k8_soft_fwd(Tables t, unsigned long lon
                 __syncthreads();
                 for (int it; (it = next_item(&S.head, ng * SNW, lane)) >= 0;) {   // warp-uniform loop
                     const int l = it / SNW, w = it - l * SNW;
+                    if (CENSUS && lane == 0 && S.need[l][w]) {   // work items and their face iterations
+                        nitem++;
+                        for (int wd = 0; wd < nw; ++wd) nface += __popc(S.wm[(l * SNW + w) * nw + wd]);
+                    }
                     if ((S.need[l][w] >> lane) & 1u) {
                         int p;
                         float ul, vl, P = 1.f, Pnz = 1.f;
@@ -464,6 +477,8 @@ __global__ void __launch_bounds__(NT, 3) k8_soft_fwd(Tables t, unsigned long lon
     if (CENSUS) {
         atomicAdd(census + 4, npair);
         atomicAdd(census + 5, nstage);
+        atomicAdd(census + 6, nitem);
+        atomicAdd(census + 7, nface);
     }
 }
 
@@ -527,8 +542,10 @@ __device__ __forceinline__ void flush_slots(SoftBwdSmem &S, const Tables &t, con
 // otherwise from S.pnz / S.nz (accumulated over the batches of a long bin).
 template <bool FUSED>
 __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *rec, const uint32_t *wm, int nw,
-                                               int l, int w, int lane, const STile &tc, float kexp, float c2)
+                                               int l, int w, int lane, const STile &tc, float kexp, float c2,
+                                               int wd0 = 0, int wd1 = -1)
 {
+    if (wd1 < 0) wd1 = nw;
     const bool mine = (S.need[l][w] >> lane) & 1u;
     int p;
     float ul, vl;
@@ -552,7 +569,7 @@ __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *re
     const float tau = S.taus[l];
     // lane owning reduced value vi after the reduce-scatter: vi = 4 b4 + 2 b3 + b2 (lanes with b1 = b0 = 0)
     const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-    for (int wd = 0; wd < nw; ++wd) {
+    for (int wd = wd0; wd < wd1; ++wd) {
         uint32_t m = wm[wd];
         while (m) {
             const int k = __clz(m);
@@ -658,11 +675,35 @@ __global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__re
                     touched = true;
                     soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
+#if BR_K9_SPLIT
+                    for (int it; (it = next_item(&S.head, ng * SNW, lane)) >= 0;) {   // pass 1: products
+                        const int l = it / SNW, w = it - l * SNW;
+                        if ((S.need[l][w] >> lane) & 1u) {
+                            int p;
+                            float ul, vl, P = 1.f, Pnz = 1.f;
+                            int nz = 0;
+                            footprint_pixel(w, lane, tc, p, ul, vl);
+                            soft_product<false>(S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, ul, vl, kexp, P, Pnz, nz,
+                                                dummy);
+                            S.pnz[l][p] = Pnz;
+                            S.nz[l][p] = (unsigned short)min(nz, 2);
+                        }
+                    }
+                    __syncthreads();
+                    // pass 2: finer items (sub-frame, footprint, 32-face word) keep the tail short
+                    for (int it; (it = next_item(&S.head2, ng * SNW * nw, lane)) >= 0;) {
+                        const int wd = it % nw, lw = it / nw, l = lw / SNW, w = lw - l * SNW;
+                        if (!S.need[l][w] || !S.wm[(l * SNW + w) * nw + wd]) continue;
+                        soft_grad_item<false>(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc, kexp,
+                                              c2, wd, wd + 1);
+                    }
+#else
                     for (int it; (it = next_item(&S.head, ng * SNW, lane)) >= 0;) {   // products + gradients
                         const int l = it / SNW, w = it - l * SNW;
                         if (!S.need[l][w]) continue;
                         soft_grad_item<true>(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc, kexp, c2);
                     }
+#endif
                 }
                 __syncthreads();
             }
