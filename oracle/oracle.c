@@ -758,7 +758,8 @@ static void soft_accum(pixstate *ps, double A, double ambA)
     ps->P *= fac;
     if (fac == 0.0) ps->nz += 1;
     else ps->Pnz *= fac;
-    if (ambA > 0.0) { ps->amb_soft = 1; ps->delta += ambA; }   /* d alpha / d A_j <= 1 */
+    if (ambA > 0.0) ps->delta += ambA;          /* value-change bound: d alpha / d A_j <= 1 */
+    if (ambA > 1e-6) ps->amb_soft = 1;          /* gradient comparison: a tie that moves A by > 1e-6 (Q20) */
 }
 
 /* Pixel range whose soft term can be non-zero: the box of F(tau) grown by sqrt(760 delta) (beyond

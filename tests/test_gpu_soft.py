@@ -153,3 +153,29 @@ def test_soft_chunk_length_invariance(G):
     a = gpu_soft(sc, 1e-4, max_chunk=G)
     b = gpu_soft(sc, 1e-4, max_chunk=8)
     assert np.abs(a["rgba"] - b["rgba"]).max() < 1e-6
+
+
+def test_soft_c4_full_size_sampled_fwd_and_grad():
+    """C4 at full size (16 x 512^2, 20,480 faces, N = 100) with soft coverage, in the bench's launch
+    configuration: sampled silhouette-band pixels computed one by one by the oracle (all faces, all
+    sub-frames), and the gradient of a loss that reads only those pixels (alpha and RGB)."""
+    sc = scenes.make_c4()
+    delta = 1e-4
+    first = gpu_soft(sc, delta)
+    a = first["rgba"][..., 3]
+    rng = np.random.default_rng(9)
+    cand = np.argwhere((a > 1e-3) & (a < 0.99))
+    pick = cand[rng.choice(len(cand), size=min(64, len(cand)), replace=False)]
+    ref = oracle.render_fwd(sc, pixels=pick, eps_amb=1e-6, delta=delta)
+    ok = ~ref["amb_img"]
+    err = np.abs(first["rgba"][pick[:, 0], pick[:, 1], pick[:, 2]] - ref["rgba"])
+    assert ok.sum() > 0.8 * len(pick) and err[ok].max() < TOL_IMG, (ok.sum(), err[ok].max())
+    Gp = rng.normal(size=(len(pick), 4)) * (~ref["amb_win"])[:, None]
+    G = np.zeros((sc.B, sc.H, sc.W, 4), np.float32)
+    G[pick[:, 0], pick[:, 1], pick[:, 2]] = Gp
+    got = gpu_soft(sc, delta, G=G)
+    rdv, rdc = oracle.render_bwd(sc, Gp, pixels=pick, delta=delta)
+    print("sampled", len(pick), "alpha err", err[ok].max(), "grad px", int((~ref["amb_win"]).sum()), "dV rel",
+          rel_l2(got["dv"], rdv), "dC rel", rel_l2(got["dc"], rdc))
+    assert (~ref["amb_win"]).sum() > 0.5 * len(pick) and np.linalg.norm(rdv) > 0
+    assert rel_l2(got["dv"], rdv) < TOL_GRAD and rel_l2(got["dc"], rdc) < TOL_GRAD
