@@ -806,15 +806,28 @@ __device__ __forceinline__ void bwd_gather(Sm &S, const TauRec *rec, const Table
                                            const TileCtx &tc, FaceAcc &acc, float *dC)
 {
     const int tid = threadIdx.x, lane = tid & 31;
-    for (int j = tid; j < nb; j += NT) S.cnt[j] = 0;
-    __syncthreads();
+    // S.cnt[0..nb) is zero on entry (cleared at kernel start and by the previous gather's combine)
     const int e = ebest - base;
     const bool mine = ebest >= 0 && e >= 0 && e < nb;
     int rank = 0;
     if (mine) rank = atomicAdd(&S.cnt[e], 1);
     __syncthreads();
-    const int total = scan_counts(S, nb);
+    if ((tid >> 5) == 0) {   // one warp scans the <= SREC_B counts (no block barrier inside)
+        const int per = (nb + 31) >> 5, j0 = lane * per, j1 = min(nb, j0 + per);
+        int sum = 0;
+        for (int j = j0; j < j1; ++j) sum += S.cnt[j];
+        int x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        int run = x - sum;
+        for (int j = j0; j < j1; ++j) { S.off[j] = run; run += S.cnt[j]; }
+        if (lane == 31) S.wsum[0] = x;
+    }
     __syncthreads();
+    const int total = S.wsum[0];
     if (mine) {
         const int pos = S.off[e] + rank;
         S.key[pos] = e;
@@ -857,6 +870,7 @@ __device__ __forceinline__ void bwd_gather(Sm &S, const TauRec *rec, const Table
     for (int j = tid; j < nb; j += NT) {
         const int c = S.cnt[j];
         if (c == 0) continue;
+        S.cnt[j] = 0;                                  // ready for the next gather (see entry)
         const int st = S.off[j], en = st + c - 1;
         float m[9];
 #pragma unroll
@@ -911,6 +925,7 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
         }
         S.g[myp] = g;
     }
+    for (int j = threadIdx.x; j < SREC_B; j += NT) S.cnt[j] = 0;   // invariant of bwd_gather
     __syncthreads();
     unsigned long long d0 = 0, d1 = 0, d2 = 0;
 
