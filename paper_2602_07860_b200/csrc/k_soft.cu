@@ -413,7 +413,8 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
                 __syncthreads();
                 soft_stage_group<CENSUS>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, nstage);
                 __syncthreads();
-                for (int it; (it = next_item(&S.head, ng * SNW, lane)) >= 0;) {   // warp-uniform loop
+                for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+ nx = next_item(&S.head, ng * SNW, lane);   // warp-uniform loop
                     const int l = it / SNW, w = it - l * SNW;
                     if (CENSUS && lane == 0 && S.need[l][w]) {   // work items and their face iterations
                         nitem++;
@@ -454,7 +455,8 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
                     __syncthreads();
                     soft_stage_group<CENSUS>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, nstage);
                     __syncthreads();
-                    for (int it; (it = next_item(&S.head, SNW, lane)) >= 0;) {
+                    for (int it = next_item(&S.head, SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+ nx = next_item(&S.head, SNW, lane);
                         if ((S.need[0][it] >> lane) & 1u) {
                             int p;
                             float ul, vl, P = 1.f, Pnz = 1.f;
@@ -624,9 +626,10 @@ __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *re
             }
             s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
             s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
-            if ((lane & 3) == 0 && vi < 6 && s1 != 0.f) {
-                atomicAdd(&S.acc[j][vi], (1.f - tau) * s1);   // keyframe s
-                atomicAdd(&S.acc[j][6 + vi], tau * s1);       // keyframe s + 1
+            // all four lanes of a group hold the sum: lane 4g adds keyframe s, lane 4g+1 keyframe s+1
+            if ((lane & 2) == 0 && vi < 6 && s1 != 0.f) {
+                const bool k1 = lane & 1;
+                atomicAdd(&S.acc[j][(k1 ? 6 : 0) + vi], (k1 ? tau : 1.f - tau) * s1);
             }
         }
     }
@@ -676,7 +679,8 @@ __global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__re
                     soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
 #if BR_K9_SPLIT
-                    for (int it; (it = next_item(&S.head, ng * SNW, lane)) >= 0;) {   // pass 1: products
+                    for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+ nx = next_item(&S.head, ng * SNW, lane);   // pass 1: products
                         const int l = it / SNW, w = it - l * SNW;
                         if ((S.need[l][w] >> lane) & 1u) {
                             int p;
@@ -691,14 +695,16 @@ __global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__re
                     }
                     __syncthreads();
                     // pass 2: finer items (sub-frame, footprint, 32-face word) keep the tail short
-                    for (int it; (it = next_item(&S.head2, ng * SNW * nw, lane)) >= 0;) {
+                    for (int it = next_item(&S.head2, ng * SNW * nw, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+ nx = next_item(&S.head2, ng * SNW * nw, lane);
                         const int wd = it % nw, lw = it / nw, l = lw / SNW, w = lw - l * SNW;
                         if (!S.need[l][w] || !S.wm[(l * SNW + w) * nw + wd]) continue;
                         soft_grad_item<false>(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc, kexp,
                                               c2, wd, wd + 1);
                     }
 #else
-                    for (int it; (it = next_item(&S.head, ng * SNW, lane)) >= 0;) {   // products + gradients
+                    for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+ nx = next_item(&S.head, ng * SNW, lane);   // products + gradients
                         const int l = it / SNW, w = it - l * SNW;
                         if (!S.need[l][w]) continue;
                         soft_grad_item<true>(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc, kexp, c2);
@@ -732,7 +738,8 @@ __global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__re
                     __syncthreads();
                     soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
-                    for (int it; (it = next_item(&S.head, SNW, lane)) >= 0;) {
+                    for (int it = next_item(&S.head, SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+ nx = next_item(&S.head, SNW, lane);
                         if ((S.need[0][it] >> lane) & 1u) {
                             int p;
                             float ul, vl, P = 1.f, Pnz = 1.f;
@@ -758,7 +765,8 @@ __global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__re
                     __syncthreads();
                     soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
-                    for (int it; (it = next_item(&S.head, SNW, lane)) >= 0;) {
+                    for (int it = next_item(&S.head, SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+ nx = next_item(&S.head, SNW, lane);
                         if (!S.need[0][it]) continue;
                         soft_grad_item<false>(S, S.rec, S.wm + it * nw, nw, 0, it, lane, tc, kexp, c2);
                     }
