@@ -116,18 +116,16 @@ __device__ __forceinline__ bool grown_box(const float4 *__restrict__ r, float ta
 // Can any pixel centre of the local rect lie within rcut of the triangle (sign-normalised edge
 // functions e_i = A_i ul + B_i vl + G_i, positive inside)?  False only if the rect lies more than
 // rcut outside one edge line (then every point of it is farther than rcut from the triangle).
-__device__ __forceinline__ bool rect_near(const float A[3], const float B[3], const float G[3], int x0, int x1,
-                                          int y0, int y1, float rcut, const STile &tc)
+// thr_i = rcut |(A_i, B_i)| + rounding allowance (per record, bounded over the whole tile)
+__device__ __forceinline__ bool rect_near(const float A[3], const float B[3], const float G[3], const float thr[3],
+                                          int x0, int x1, int y0, int y1, const STile &tc)
 {
     const float ulmin = (float)(x0 - TW / 2) * tc.sx, ulmax = (float)(x1 - TW / 2) * tc.sx;
     const float vlmin = (float)(TH / 2 - y1) * tc.sy, vlmax = (float)(TH / 2 - y0) * tc.sy;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        const float m = G[i] + (A[i] > 0.f ? A[i] * ulmax : A[i] * ulmin) + (B[i] > 0.f ? B[i] * vlmax : B[i] * vlmin);
-        const float nrm = sqrtf(A[i] * A[i] + B[i] * B[i]);
-        const float tol = 1e-5f * (fabsf(A[i]) * fmaxf(-ulmin, ulmax) + fabsf(B[i]) * fmaxf(-vlmin, vlmax) +
-                                   fabsf(G[i])) + 1e-30f;
-        if (m < -(rcut * nrm) - tol) return false;
+        const float m = G[i] + A[i] * (A[i] > 0.f ? ulmax : ulmin) + B[i] * (B[i] > 0.f ? vlmax : vlmin);
+        if (m < -thr[i]) return false;
     }
     return true;
 }
@@ -213,6 +211,11 @@ __device__ __forceinline__ uint32_t soft_stage(const Tables &t, const float4 *__
         B[i] = be * sg;
         G[i] = gp * sg;
     }
+    float thr[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        thr[i] = t.rcut * sqrtf(A[i] * A[i] + B[i] * B[i]) +
+                 1e-5f * (fabsf(A[i]) * (8.f * tc.sx) + fabsf(B[i]) * (8.f * tc.sy) + fabsf(G[i])) + 1e-30f;
     uint32_t fm = 0u;
     for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
         for (int wx = x0 >> 3; wx <= (x1 >> 3); ++wx) {
@@ -220,7 +223,7 @@ __device__ __forceinline__ uint32_t soft_stage(const Tables &t, const float4 *__
             if (!need[w]) continue;
             const int rx0 = max(x0, wx * 8), rx1 = min(x1, wx * 8 + 7);
             const int ry0 = max(y0, wy * 4), ry1 = min(y1, wy * 4 + 3);
-            if (rect_near(A, B, G, rx0, rx1, ry0, ry1, t.rcut, tc)) fm |= 1u << w;
+            if (rect_near(A, B, G, thr, rx0, rx1, ry0, ry1, tc)) fm |= 1u << w;
         }
     if (!fm) return 0u;
     const float invD = 1.0f / fabsf(D);
