@@ -374,16 +374,24 @@ def main():
         h_out = torch.empty(6 * sc.V + 1, dtype=torch.float32).pin_memory()
         saved = step.targets
 
+        copy_stream = torch.cuda.Stream(device=dev)
+        tgt_ready = torch.cuda.Event()
+
         def e2e_step():
             d_verts.copy_(h_verts, non_blocking=True)
             d_cols.copy_(h_cols, non_blocking=True)
-            d_tgt.copy_(h_tgt, non_blocking=True)
+            # the observed images go up on a copy stream, overlapped with the forward pass; the
+            # copy waits for the previous step's use of the buffer, the loss waits for the copy
+            copy_stream.wait_stream(stream)
+            with torch.cuda.stream(copy_stream):
+                d_tgt.copy_(h_tgt, non_blocking=True)
+                tgt_ready.record(copy_stream)
             step.targets = d_tgt
             flat = one_step_public(d_verts, d_cols)
             h_out.copy_(flat, non_blocking=True)
 
         def one_step_public(v, c):
-            loss, dv, dc = step(v, c)
+            loss, dv, dc = step(v, c, targets_ready=tgt_ready)
             return torch.cat([dv.reshape(-1), dc.reshape(-1), loss])
 
         for _ in range(2):

@@ -92,10 +92,14 @@ class ShardedStep:
                 if rank in ranks:
                     self.groups.append((self.images.index(b), g))
 
-    def __call__(self, verts: torch.Tensor, colors: torch.Tensor):
+    def __call__(self, verts: torch.Tensor, colors: torch.Tensor, targets_ready=None):
+        """targets_ready: optional CUDA event after which self.targets is valid (a loader copying the
+        next observed images on another stream overlaps that copy with the forward pass)."""
         V = verts.shape[0]
         if self.renderer is not None:
             out = self.renderer.forward(verts, colors)
+            if targets_ready is not None:
+                torch.cuda.current_stream().wait_event(targets_ready)
             for slot, g in self.groups:                               # partial images -> full image
                 part = out[slot].contiguous()
                 dist.all_reduce(part, group=g)
