@@ -30,7 +30,7 @@ namespace br {
 constexpr int NWARP = NT / 32;
 // tuning knobs (overridable with -D for A/B builds; defaults measured on C4, profiles/)
 #ifndef BR_SREC_F
-#define BR_SREC_F 768
+#define BR_SREC_F 512
 #endif
 #ifndef BR_SREC_B
 #define BR_SREC_B 384
