@@ -7,15 +7,19 @@ namespace br {
 
 // K7: dL/dP0[v] = sum_b sum_s R_s^T Rc^T J(Q)^T dkey[b][s][v]; A34 Jacobian
 // J = [[1/(z ta), 0, -x_ndc/z], [0, 1/(z ta), -y_ndc/z]] (Q = view coords, x_ndc = Qx/(z ta)).
-// One thread per vertex, deterministic loop over (b, s); fp64 accumulation.
+// One warp per vertex: the lanes take the (image, keyframe) terms round-robin in fp64 and a fixed
+// shuffle tree sums them (deterministic; C4 has ~120 keyframe terms per vertex, so a thread per
+// vertex left most SMs idle).
 __global__ void __launch_bounds__(256) k7_vertex_chain(Tables t, float *__restrict__ gv)
 {
-    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (v >= t.V) return;
     double acc[3] = {0.0, 0.0, 0.0};
+    int q = 0;   // running index of the (image, keyframe) term
     for (int b = 0; b < t.B; ++b) {
         const ImgInfo &im = t.imgs[b];
-        for (int s = 0; s <= im.S; ++s) {
+        for (int s = 0; s <= im.S; ++s, ++q) {
+            if ((q & 31) != lane) continue;
             const size_t o = (size_t)im.key_off + (size_t)s * t.V + v;
             const float2 g = t.dkey[o];
             if (g.x == 0.f && g.y == 0.f) continue;
@@ -30,15 +34,21 @@ __global__ void __launch_bounds__(256) k7_vertex_chain(Tables t, float *__restri
             for (int i = 0; i < 3; ++i) acc[i] += pr.R[i] * dP[0] + pr.R[3 + i] * dP[1] + pr.R[6 + i] * dP[2];
         }
     }
-    gv[3 * v] = (float)acc[0];
-    gv[3 * v + 1] = (float)acc[1];
-    gv[3 * v + 2] = (float)acc[2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    if (lane == 0) {
+        gv[3 * v] = (float)acc[0];
+        gv[3 * v + 1] = (float)acc[1];
+        gv[3 * v + 2] = (float)acc[2];
+    }
 }
 
 cudaError_t launch_vertex_chain(const Tables &t, float *gv, cudaStream_t st)
 {
     if (t.V == 0) return cudaSuccess;
-    k7_vertex_chain<<<(t.V + 255) / 256, 256, 0, st>>>(t, gv);
+    k7_vertex_chain<<<(t.V + 7) / 8, 256, 0, st>>>(t, gv);
     return cudaGetLastError();
 }
 
