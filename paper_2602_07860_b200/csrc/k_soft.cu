@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
                 soft_stage_group<CENSUS>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, nstage);
                 __syncthreads();
                 for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
- nx = next_item(&S.head, ng * SNW, lane);   // warp-uniform loop
+                    nx = next_item(&S.head, ng * SNW, lane);
                     const int l = it / SNW, w = it - l * SNW;
                     if (CENSUS && lane == 0 && S.need[l][w]) {   // work items and their face iterations
                         nitem++;
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
                     soft_stage_group<CENSUS>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, nstage);
                     __syncthreads();
                     for (int it = next_item(&S.head, SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
- nx = next_item(&S.head, SNW, lane);
+                        nx = next_item(&S.head, SNW, lane);
                         if ((S.need[0][it] >> lane) & 1u) {
                             int p;
                             float ul, vl, P = 1.f, Pnz = 1.f;
@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__re
                     __syncthreads();
 #if BR_K9_SPLIT
                     for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
- nx = next_item(&S.head, ng * SNW, lane);   // pass 1: products
+                        nx = next_item(&S.head, ng * SNW, lane);
                         const int l = it / SNW, w = it - l * SNW;
                         if ((S.need[l][w] >> lane) & 1u) {
                             int p;
@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__re
                     __syncthreads();
                     // pass 2: finer items (sub-frame, footprint, 32-face word) keep the tail short
                     for (int it = next_item(&S.head2, ng * SNW * nw, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
- nx = next_item(&S.head2, ng * SNW * nw, lane);
+                        nx = next_item(&S.head2, ng * SNW * nw, lane);
                         const int wd = it % nw, lw = it / nw, l = lw / SNW, w = lw - l * SNW;
                         if (!S.need[l][w] || !S.wm[(l * SNW + w) * nw + wd]) continue;
                         soft_grad_item<false>(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc, kexp,
@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__re
                     }
 #else
                     for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
- nx = next_item(&S.head, ng * SNW, lane);   // products + gradients
+                        nx = next_item(&S.head, ng * SNW, lane);
                         const int l = it / SNW, w = it - l * SNW;
                         if (!S.need[l][w]) continue;
                         soft_grad_item<true>(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc, kexp, c2);
@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__re
                     soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
                     for (int it = next_item(&S.head, SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
- nx = next_item(&S.head, SNW, lane);
+                        nx = next_item(&S.head, SNW, lane);
                         if ((S.need[0][it] >> lane) & 1u) {
                             int p;
                             float ul, vl, P = 1.f, Pnz = 1.f;
@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__re
                     soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
                     for (int it = next_item(&S.head, SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
- nx = next_item(&S.head, SNW, lane);
+                        nx = next_item(&S.head, SNW, lane);
                         if (!S.need[0][it]) continue;
                         soft_grad_item<false>(S, S.rec, S.wm + it * nw, nw, 0, it, lane, tc, kexp, c2);
                     }
