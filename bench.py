@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the oracle sample")
+    p.add_argument("--graph", action="store_true",
+                   help="replay the step as a CUDA graph (launch-bound configs C1-C3; 1 GPU, no sub-frame split)")
     p.add_argument("--delta", type=float, default=0.0,
                    help="soft background coverage bandwidth (NEXT-1, Eq.10-15; the paper uses 1e-4); 0 = hard path")
     return p.parse_args()
@@ -273,8 +275,20 @@ def main():
             dist.all_reduce(flat)
         return flat
 
+    graph = None
+    if args.graph:
+        if rend is None or step.groups or world > 1:
+            raise SystemExit("--graph needs 1 GPU and no sub-frame split")
+        graph = rend.capture_step(verts, colors, step.targets, n_norm=step.n_norm)
+
+    def timed_step(ev_f=None, ev_b=None, ev_sf=None, ev_sb=None):
+        if graph is None:
+            return one_step(ev_f, ev_b, ev_sf, ev_sb)
+        loss, dv, dc, _ = graph.replay()
+        return loss
+
     for _ in range(max(3, args.warmup)):
-        one_step()
+        timed_step()
     torch.cuda.synchronize()
     if rend is not None:
         st = rend.status()
@@ -298,7 +312,7 @@ def main():
     for i in range(K):
         flush_buf.zero_()                                       # L2 flush between timed steps
         ev_s[i].record(stream)
-        one_step(evf[i], evb[i], evsf[i], evsb[i])
+        timed_step(evf[i], evb[i], evsf[i], evsb[i])
         ev_e[i].record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -306,6 +320,11 @@ def main():
     clk = clocks.stop()
     step_ms = [ev_s[i].elapsed_time(ev_e[i]) for i in range(K)]
     tot_ms = float(sum(step_ms))
+    if graph is not None:   # kernel events are not part of the graph: time the kernels in eager steps
+        for i in range(K):
+            flush_buf.zero_()
+            one_step(evf[i], evb[i], evsf[i], evsb[i])
+        torch.cuda.synchronize()
     fwd_ms = [evf[i][0].elapsed_time(evf[i][1]) for i in range(K)] if rend is not None else [0.0]
     bwd_ms = [evb[i][0].elapsed_time(evb[i][1]) for i in range(K)] if rend is not None else [0.0]
     sf_ms = [evsf[i][0].elapsed_time(evsf[i][1]) for i in range(K)] if soft and rend is not None else [0.0]
@@ -428,7 +447,8 @@ def main():
                            "segments": sorted({int(x) for x in sc.motion["n_seg"]}),
                            **({"delta": args.delta, "coverage": "soft (Eq.10-15)"} if soft else {}),
                            "parallelism": "image-sharded x%d" % world + ("" if not step.groups else " + subframe split"),
-                           "l2": "flushed (256 MB write) before every timed step"},
+                           "l2": "flushed (256 MB write) before every timed step",
+                           **({"cuda_graph": True} if graph is not None else {})},
                 "barycentric_evals_per_s": {"executed": cand * world / (ms_per_step / 1000.0),
                                             "necessary": nec * world / (ms_per_step / 1000.0),
                                             "note": "per-rank census x ranks (rank 0's counts)"},

@@ -100,6 +100,10 @@ typedef struct {
 /* Tuning / instrumentation (host struct; NULL = defaults). */
 #define BLUR_REUSE_SETUP 1   /* bwd: reuse keyframes, coefficients and bins that the preceding fwd
                                 call with identical arguments left in the same workspace */
+#define BLUR_TABLES_RESIDENT 4   /* fwd: the workspace already holds the host-side tables (schedule,
+                                poses, chunks) of a previous call with identical arguments; skip their
+                                upload.  With it a fwd/bwd pair issues device work only, so it can be
+                                captured in a CUDA graph and replayed (BlurRenderer.capture_step). */
 #define BLUR_CACHE_VISIBILITY 2   /* set on both the fwd and the bwd call: the fwd also leaves the
                                 winning bin slot of every (pixel, sub-frame) in the workspace (2 B each:
                                 sum_b N_b * H * W * 2 bytes, e.g. 0.84 GB for C4), and a bwd with

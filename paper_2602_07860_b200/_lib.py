@@ -21,6 +21,7 @@ BLUR_OK, BLUR_EINVAL, BLUR_EBEHIND, BLUR_ENOMEM, BLUR_ECUDA, BLUR_EOVERFLOW = ra
 BLUR_ST_EINVAL, BLUR_ST_EBEHIND, BLUR_ST_EOVERFLOW, BLUR_ST_EINTERNAL = 1, 2, 4, 8
 BLUR_REUSE_SETUP = 1
 BLUR_CACHE_VISIBILITY = 2
+BLUR_TABLES_RESIDENT = 4
 STATUS_NAMES = {0: "BLUR_OK", 1: "BLUR_EINVAL", 2: "BLUR_EBEHIND", 3: "BLUR_ENOMEM", 4: "BLUR_ECUDA",
                 5: "BLUR_EOVERFLOW"}
 

@@ -422,8 +422,10 @@ int prepare(const float *verts, int V, const int32_t *faces, int F, const float 
     if (!do_setup) return BLUR_OK;
     r = cuda_check(cudaMemsetAsync(t.status, 0, sizeof(int), st), "status clear");
     if (r) return r;
-    r = upload_tables(P, ws, st);
-    if (r) return r;
+    if (!(cfg && (cfg->flags & BLUR_TABLES_RESIDENT))) {   // host tables (pageable copy): not capturable
+        r = upload_tables(P, ws, st);
+        if (r) return r;
+    }
     r = cuda_check(launch_setup(t, verts, faces, colors, P.maxS, st), "setup kernels");
     if (r) return r;
     r = cuda_check(launch_binning(t, hard_bins(t), 0.f, st), "binning kernels");

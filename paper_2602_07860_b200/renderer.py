@@ -126,6 +126,27 @@ class BlurRenderer:
     def status(self) -> int:
         return _lib.blur_read_status(self.ws)
 
+    def capture_step(self, verts: torch.Tensor, colors: torch.Tensor, target: torch.Tensor, n_norm: int = 0):
+        """CUDA-graph form of step() for launch-bound configurations (C1-C3: tens of microseconds of
+        kernels per step).  One eager step sizes the workspace and leaves the host tables on the
+        device; the graph then replays fwd -> L2 -> bwd on the given buffers (update them in place
+        between replays).  Returns a StepGraph; its replay() enqueues the step on the current stream."""
+        self.step(verts, colors, target, n_norm)             # eager: bins sized, tables resident
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                out = torch.empty((self.B, self.H, self.W, 4), dtype=torch.float32, device=self.device)
+                cfg = self._cfg(_lib.BLUR_TABLES_RESIDENT)
+                _lib.blur_render_fwd(verts, self.faces, colors, self._motions, self._cams, self.B, self.H, self.W,
+                                     out, self.ws, sub_range=self._sub, cfg=cfg, stream=s)
+                loss, grad = self.l2_loss_grad(out, target, n_norm=n_norm, stream=s)
+                dv, dc = self.backward(verts, colors, grad, reuse_setup=True, stream=s)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        return StepGraph(g, loss, dv, dc, out)
+
     def step(self, verts, colors, target, n_norm: int = 0):
         """One inverse-rendering step: fwd -> L2 loss -> bwd (setup reused).  Device tensors in,
         (loss [1], dverts, dcolors, out) device tensors out."""
@@ -133,6 +154,18 @@ class BlurRenderer:
         loss, g = self.l2_loss_grad(out, target, n_norm=n_norm)
         dv, dc = self.backward(verts, colors, g, reuse_setup=True)
         return loss, dv, dc, out
+
+
+class StepGraph:
+    """A captured fwd -> L2 -> bwd step (BlurRenderer.capture_step): replay() re-runs it on the buffers
+    it was captured with; loss, dv, dc, out are the graph's output tensors."""
+
+    def __init__(self, graph, loss, dv, dc, out):
+        self.graph, self.loss, self.dv, self.dc, self.out = graph, loss, dv, dc, out
+
+    def replay(self):
+        self.graph.replay()
+        return self.loss, self.dv, self.dc, self.out
 
 
 class _BlurFn(torch.autograd.Function):
