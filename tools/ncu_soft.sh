@@ -1,7 +1,7 @@
 # ncu --set full of the soft kernels (C3, one launch each), after a plain run of the same command
 set -x
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_soft.py -x -q 2>&1 | tail -3
+
 CMD="python bench.py --config C3 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --delta 1e-4"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k8_soft_fwd|k9_soft_bwd" -s 2 -c 2 \
