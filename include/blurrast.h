@@ -73,7 +73,9 @@ typedef enum { BLUR_SCHED_GLOBAL_INCLUSIVE = 0, BLUR_SCHED_PAPER_SEGMENTED = 1 }
  *  BLUR_PARABOLIC: P(t) = c + R(vec, angle t)(P0 - c) + (s, -4 s^2 + 0.5, s), s = 0.5 - t
  *                  (composite rotation + parabolic translation, A35-A37; the paper's
  *                  case is vec = +y, angle = pi, c = 0).  Not linear in t: use several segments.
- *  n_subframes N >= 1; n_segments S >= 1 (linear segments); sched_rule as Q1:
+ *  n_subframes N >= 1; n_segments S >= 1 (linear segments), or 0 for the automatic
+ *  count: 1 for translation / static, ceil(12 |angle| / 2 pi - 1e-6) for rotation / parabolic (12 per
+ *  full turn; Q24); sched_rule as Q1:
  *   GLOBAL_INCLUSIVE: t_k = k/(N-1) (N=1: 0.5), s_k = min(floor(t_k S), S-1), tau_k = t_k S - s_k;
  *   PAPER_SEGMENTED:  S | N, K = N/S, s_k = k div K, tau_k = (k mod K)/(K-1) (K=1: 0.5). */
 typedef struct {

@@ -42,6 +42,7 @@
  * pixel arithmetic and the face order are unchanged, so the two modes are
  * bit-identical; pinned by tests/test_oracle_pins.py).
  */
+#define _GNU_SOURCE
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -122,6 +123,21 @@ int om_schedule(int N, int S, int rule, int *s_out, double *tau_out)
         tau_out[k] = (double)(num - s * (N - 1)) / (double)(N - 1);
     }
     return 0;
+}
+
+/* Segment count of image b (Q24): n_seg as given, or for n_seg == 0 the paper's segmentation rule --
+ * one linear segment for translation / static, ceil(12 turns - 1e-6) for rotation (12 per full turn,
+ * P:L277; the 1e-6 keeps an fp32 angle of a whole number of turns from adding a segment), at least one. */
+int om_segments(const om_scene *sc, int b)
+{
+    int S = sc->n_seg[b];
+    if (S != 0) return S;
+    if (sc->kind[b] == OM_ROTATE || sc->kind[b] == OM_PARABOLIC) {
+        double turns = fabs(sc->angle[b]) / (2.0 * M_PI);
+        int s12 = (int)ceil(12.0 * turns - 1e-6);   /* float angles of whole turns stay whole */
+        return s12 < 1 ? 1 : s12;
+    }
+    return 1;
 }
 
 /* --------------------------------------------------------------- pose + projection */
@@ -209,7 +225,7 @@ static void cam_frame(const double *cam, double Rc[9])
  * Optionally returns the view coordinates Q (for the backward chain). */
 int om_keyframes(const om_scene *sc, int b, double *key, unsigned char *valid, double *Qout)
 {
-    int S = sc->n_seg[b], V = sc->V;
+    int S = om_segments(sc, b), V = sc->V;
     const double *cam = sc->cams + 11 * b;
     double Rc[9];
     cam_frame(cam, Rc);
@@ -454,7 +470,7 @@ static int img_init(const om_scene *sc, int b, img_state *st)
 {
     memset(st, 0, sizeof(*st));
     st->N = sc->n_sub[b];
-    st->S = sc->n_seg[b];
+    st->S = om_segments(sc, b);
     st->k0 = sc->sub_range ? sc->sub_range[2 * b] : 0;
     st->k1 = sc->sub_range ? sc->sub_range[2 * b + 1] : st->N;
     st->sk = (int *)malloc(sizeof(int) * (size_t)st->N);

@@ -15,7 +15,7 @@ _lock = threading.Lock()
 _lib = None
 
 __all__ = ["build", "lib", "schedule", "keyframes", "bary_textbook", "fast_coeffs", "fast_eval",
-           "render_fwd", "render_bwd", "num_threads", "closest_w", "soft_pair"]
+           "render_fwd", "render_bwd", "num_threads", "closest_w", "soft_pair", "segments"]
 
 
 def build(force: bool = False) -> str:
@@ -57,6 +57,7 @@ def lib():
             _lib.om_render_fwd.argtypes = [P, P, P, P, C.c_int, P, P, P, P, P]
             _lib.om_render_bwd.argtypes = [P, P, P, P, P, P]
             _lib.om_num_threads.argtypes = [C.c_int]
+            _lib.om_segments.argtypes = [P, C.c_int]
             _lib.om_closest_w.argtypes = [P, P, C.c_double, C.c_double, P, P, P, P, P]
             _lib.om_soft_pair.argtypes = [P, P, P, P, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int,
                                           C.c_double, P, P, P, P, P]
@@ -114,10 +115,16 @@ def schedule(N: int, S: int, rule: int = 0):
     return s, t
 
 
+def segments(sc, b: int = 0) -> int:
+    """Segment count of image b (n_seg, or the automatic rule for n_seg == 0; Q24)."""
+    pk = _Pack(sc)
+    return int(lib().om_segments(C.byref(pk.s), b))
+
+
 def keyframes(sc, b: int = 0):
     """(S+1, V, 3) NDC x, y and view z; (S+1, V) valid; (S+1, V, 3) view coordinates."""
     pk = _Pack(sc)
-    S = int(sc.motion["n_seg"][b])
+    S = segments(sc, b)
     key = np.zeros((S + 1, sc.V, 3))
     valid = np.zeros((S + 1, sc.V), np.uint8)
     Q = np.zeros((S + 1, sc.V, 3))
@@ -193,7 +200,8 @@ def render_bwd(sc, grad_rgba, mode="binned", threads=0, sub_range=None, pixels=N
     g = _d(grad_rgba)
     dv = np.zeros((sc.V, 3))
     dc = np.zeros((sc.V, 3))
-    nkey = int(sum((int(S) + 1) * sc.V * 2 for S in sc.motion["n_seg"]))
+    Ss = [segments(sc, b) for b in range(sc.B)]
+    nkey = int(sum((S + 1) * sc.V * 2 for S in Ss))
     dk = np.zeros(nkey) if want_dkey else None
     r = lib().om_render_bwd(C.byref(pk.s), C.byref(o), _p(g), _p(dv), _p(dc), _p(dk))
     if r < 0:
@@ -201,7 +209,7 @@ def render_bwd(sc, grad_rgba, mode="binned", threads=0, sub_range=None, pixels=N
     if not want_dkey:
         return dv, dc
     out, off = [], 0
-    for S in sc.motion["n_seg"]:
+    for S in Ss:
         n = (int(S) + 1) * sc.V * 2
         out.append(dk[off:off + n].reshape(int(S) + 1, sc.V, 2))
         off += n

@@ -135,7 +135,13 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
     long long rec_off = 0;
     for (int b = 0; b < B; ++b) {
         const blur_motion &mo = m[b];
-        const int N = mo.n_subframes, S = mo.n_segments;
+        const int N = mo.n_subframes;
+        int S = mo.n_segments;
+        if (S == 0) {   // automatic (Q24): 1 for translation / static, 12 per full turn for rotation
+            S = 1;
+            if (mo.kind == BLUR_ROTATE || mo.kind == BLUR_PARABOLIC)
+                S = std::max(1, (int)std::ceil(12.0 * (std::fabs((double)mo.angle) / (2.0 * M_PI)) - 1e-6));
+        }
         if (mo.kind < 0 || mo.kind > 3) return fail(BLUR_EINVAL, "motion kind must be 0, 1, 2 or 3");
         if (N < 1) return fail(BLUR_EINVAL, "n_subframes must be >= 1");
         if (S < 1) return fail(BLUR_EINVAL, "n_segments must be >= 1");

@@ -54,7 +54,7 @@ def test_workspace_query_and_validation(lib):
     n2 = _lib.blur_workspace_bytes(sc.V, sc.F, sc.B, 64, 64, m, c, cfg=_lib.make_config(max_chunk=1))
     assert n2 >= n           # more chunks -> more bins
     bad = {k: v.copy() for k, v in sc.motion.items()}
-    bad["n_seg"][0] = 0
+    bad["n_seg"][0] = -1
     with pytest.raises(_lib.BlurError) as e:
         _lib.blur_workspace_bytes(sc.V, sc.F, 1, 64, 64, _lib.make_motions(bad), c)
     assert "n_segments" in str(e.value)

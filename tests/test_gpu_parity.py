@@ -334,3 +334,10 @@ def test_cuda_graph_step_matches_eager(cfg):
         assert abs(float(loss) - float(l2)) <= 1e-6 * abs(float(l2))
         assert rel_l2(dv.cpu().numpy(), dv2.cpu().numpy()) < 1e-5
         assert rel_l2(dc.cpu().numpy(), dc2.cpu().numpy()) < 1e-5
+
+
+def test_automatic_segment_count_parity():
+    """n_segments = 0 (Q24) resolves to the same segmentation on the GPU as in the oracle."""
+    sc = scenes.random_mesh_scene(20, 31, H=40, W=40, motion=scenes.rotate((0.1, 1, 0.2), 3.0, N=13, S=0))
+    r = check_parity(sc, ids_k=6, mode="brute")
+    print(r)

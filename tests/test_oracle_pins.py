@@ -570,3 +570,20 @@ def test_segmentation_converges_to_exact_pose():
 def dataclasses_replace_motion(sc, motion):
     import dataclasses
     return dataclasses.replace(sc, motion=scenes.motion_arrays([motion] * sc.B))
+
+
+def test_automatic_segment_count_rule():
+    """Q24 (n_seg = 0): one segment for translation, 12 per full turn for rotation."""
+    import dataclasses
+    sc = scenes.random_mesh_scene(3, 4, motion=scenes.rotate((0, 1, 0), 2 * math.pi * 1.5, N=10, S=0))
+    assert oracle.segments(sc) == 18
+    sc2 = scenes.random_mesh_scene(3, 4, motion=scenes.translate((1, 0, 0), N=10, S=0))
+    assert oracle.segments(sc2) == 1
+    sc3 = scenes.random_mesh_scene(3, 4, motion=scenes.rotate((0, 1, 0), 0.3, N=10, S=0))
+    assert oracle.segments(sc3) == 1
+    # rendering with S = 0 equals rendering with the resolved count
+    m = dict(sc.motion)
+    m["n_seg"] = np.array([18], np.int32)
+    a = oracle.render_fwd(sc)["rgba"]
+    b = oracle.render_fwd(dataclasses.replace(sc, motion=m))["rgba"]
+    assert np.array_equal(a, b)
