@@ -42,7 +42,7 @@ constexpr int NWARP = NT / 32;
 #define BR_GMAX_B 8
 #endif
 #ifndef BR_K4_MINB
-#define BR_K4_MINB 4
+#define BR_K4_MINB 5
 #endif
 #ifndef BR_K6_MINB
 #define BR_K6_MINB 4
