@@ -48,16 +48,22 @@ namespace {
 
 constexpr int SNW = NT / 32;     // warps per CTA
 #ifndef BR_SREC_F8
-#define BR_SREC_F8 512
+#define BR_SREC_F8 384
 #endif
 #ifndef BR_K8_MINB
-#define BR_K8_MINB 4
+#define BR_K8_MINB 5
 #endif
 #ifndef BR_K9_SPLIT
 #define BR_K9_SPLIT 1
 #endif
 constexpr int SREC_F8 = BR_SREC_F8;   // K8: staged soft records per CTA (80 B each)
-constexpr int SREC_B9 = 384;     // K9: staged soft records per CTA
+#ifndef BR_SREC_B9
+#define BR_SREC_B9 384
+#endif
+#ifndef BR_K9_MINB
+#define BR_K9_MINB 3
+#endif
+constexpr int SREC_B9 = BR_SREC_B9;   // K9: staged soft records per CTA
 constexpr int GMAX_S = 8;        // sub-frames staged together
 constexpr int NPX = TW * TH;
 
@@ -638,7 +644,7 @@ __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *re
     }
 }
 
-__global__ void __launch_bounds__(NT, 3) k9_soft_bwd(Tables t, const float *__restrict__ grad)
+__global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const float *__restrict__ grad)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SoftBwdSmem &S = *reinterpret_cast<SoftBwdSmem *>(smem_raw);
