@@ -90,6 +90,7 @@ struct Plan {
     size_t o_cov = 0, o_spart = 0, o_scnt = 0, o_soff = 0, o_sbsum = 0, o_sent = 0;
     bool vis = false;      // BLUR_CACHE_VISIBILITY: K4 leaves the winning bin slot per (pixel, sub-frame)
     size_t o_vis = 0;
+    size_t o_spz = 0;      // soft products K8 -> K9 (BLUR_CACHE_VISIBILITY with delta > 0)
     size_t total = 0;
 };
 
@@ -299,6 +300,7 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
     P.vis = cfg && (cfg->flags & BLUR_CACHE_VISIBILITY) && (!cfg || cfg->solver == 0);
     if (P.vis) {
         P.o_vis = o; o = align256(o + 2 * (size_t)P.n_sub * P.T * TW * TH);
+        if (P.soft) { P.o_spz = o; o = align256(o + 4 * (size_t)P.n_sub * P.T * TW * TH); }
     }
     P.total = o;
     return BLUR_OK;
@@ -344,6 +346,7 @@ Tables make_tables(const Plan &P, void *ws)
         t.sb.sortcap = 4096;
     }
     if (P.vis) t.vis = (uint16_t *)(w + P.o_vis);
+    if (P.vis && P.soft) t.spz = (float *)(w + P.o_spz);
     return t;
 }
 
@@ -516,7 +519,10 @@ int blur_render_bwd(const float *verts, int V, const int32_t *faces, int F, cons
         r = cuda_check(cudaMemsetAsync(t.dkey, 0, 8 * (size_t)P.n_key, st), "dkey clear");
         if (r) return r;
     }
-    if (!reuse) t.vis = nullptr;   // the visibility buffer is only valid right after the forward
+    if (!reuse) {   // the visibility and soft-product buffers are only valid right after the forward
+        t.vis = nullptr;
+        t.spz = nullptr;
+    }
     if (P.soft && !reuse) {   // coverage of every (pixel, sub-frame) for the soft term (no image written)
         r = cuda_check(launch_raster_fwd(t, nullptr, nullptr, -1, nullptr, st), "coverage pass");
         if (r) return r;

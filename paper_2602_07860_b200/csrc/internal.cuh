@@ -96,6 +96,9 @@ struct Tables {          // device pointers into the workspace
     uint16_t *vis;       // [sum_b N_b][T][TW*TH] winning bin slot per (sub-frame, pixel), 0xFFFF none;
                          // written by K4, read by K6 instead of recomputing visibility (or null)
     float *spart;        // [splits][B*H*W] soft alpha partial sums (K8)
+    float *spz;          // [sum_b N_b][T][TW*TH] soft products per (sub-frame, pixel) left by K8 for K9
+                         // (prod of the non-zero factors 1 - A; negative: one zero factor, NaN: two or
+                         // more; written where K8 needs the pixel) or null
     BinSet sb;           // soft bins (chunk boxes dilated by rcut)
 };
 

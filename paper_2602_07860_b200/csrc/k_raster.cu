@@ -28,6 +28,14 @@
 namespace br {
 
 constexpr int NWARP = NT / 32;
+#ifndef BR_HALF
+#define BR_HALF 0
+#endif
+// Culling footprints: BR_HALF = 1 -> 4x4 pixel blocks (16 per tile, two per warp: the left and right
+// halves of its 8x4 pixels iterate their own face masks), 0 -> the warps' 8x4 blocks.
+constexpr int FPW_SH = BR_HALF ? 2 : 3, FPW = 1 << FPW_SH;   // footprint width (pixels); height 4
+constexpr int NFP = (TW / FPW) * (TH / 4);    // footprints (mask sets) per sub-frame
+__device__ __forceinline__ int fp_of(int warp, int lane) { return BR_HALF ? warp * 2 + ((lane >> 2) & 1) : warp; }
 // tuning knobs (overridable with -D for A/B builds; defaults measured on C4, profiles/)
 #ifndef BR_SREC_F
 #define BR_SREC_F 512
@@ -120,7 +128,7 @@ __device__ __forceinline__ bool rect_reaches(const float A[3], const float B[3],
 }
 
 // Evaluate a record at tau for this tile -> TauRec + the mask of warp footprints it can reach
-// (bit w = warp w's 8x4 footprint; 0 = the face cannot cover any pixel of the tile at tau).
+// (bit w = culling footprint w, see FPW; 0 = the face cannot cover any pixel of the tile at tau).
 // D = det F(tau) (|D| > EPS_D) and the face's pixel box in the tile come from the caller's rejects.
 __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, float D, int x0, int x1, int y0, int y1,
                                               const TileCtx &tc, TauRec &out)
@@ -142,7 +150,7 @@ __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, floa
         B[i] = be * sg;
         G[i] = gp * sg;
     }
-    // warp footprints (8x4, arranged 2 x 4) reached by the box and the three edge half-planes; the
+    // culling footprints (FPW x 4) reached by the box and the three edge half-planes; the
     // rounding allowance is bounded once over the whole tile (|ul|, |vl| <= 8 pixels)
     float tol[3];
 #pragma unroll
@@ -150,10 +158,10 @@ __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, floa
         tol[i] = 1e-6f * (fabsf(A[i]) * (8.f * tc.sx) + fabsf(B[i]) * (8.f * tc.sy) + fabsf(G[i])) + 1e-30f;
     uint32_t fm = 0u;
     for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
-        for (int wx = x0 >> 3; wx <= (x1 >> 3); ++wx) {
-            const int rx0 = max(x0, wx * 8), rx1 = min(x1, wx * 8 + 7);
+        for (int wx = x0 >> FPW_SH; wx <= (x1 >> FPW_SH); ++wx) {
+            const int rx0 = max(x0, wx * FPW), rx1 = min(x1, wx * FPW + FPW - 1);
             const int ry0 = max(y0, wy * 4), ry1 = min(y1, wy * 4 + 3);
-            if (rect_reaches_t(A, B, G, tol, rx0, rx1, ry0, ry1, tc)) fm |= 1u << (wy * 2 + wx);
+            if (rect_reaches_t(A, B, G, tol, rx0, rx1, ry0, ry1, tc)) fm |= 1u << (wy * (TW / FPW) + wx);
         }
     if (!fm) return 0u;
     const float4 z0 = fr.q[9], z1 = fr.q[10];
@@ -279,10 +287,10 @@ __device__ __forceinline__ uint32_t stage_tau_naive(const BinCtx &bc, int f, flo
     }
     uint32_t fm = 0u;
     for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
-        for (int wx = x0 >> 3; wx <= (x1 >> 3); ++wx) {
-            const int rx0 = max(x0, wx * 8), rx1 = min(x1, wx * 8 + 7);
+        for (int wx = x0 >> FPW_SH; wx <= (x1 >> FPW_SH); ++wx) {
+            const int rx0 = max(x0, wx * FPW), rx1 = min(x1, wx * FPW + FPW - 1);
             const int ry0 = max(y0, wy * 4), ry1 = min(y1, wy * 4 + 3);
-            if (rect_reaches(A, B, G, rx0, rx1, ry0, ry1, tc)) fm |= 1u << (wy * 2 + wx);
+            if (rect_reaches(A, B, G, rx0, rx1, ry0, ry1, tc)) fm |= 1u << (wy * (TW / FPW) + wx);
         }
     if (!fm) return 0u;
     out.a[0] = A[0]; out.a[1] = A[1]; out.a[2] = A[2];
@@ -303,7 +311,7 @@ __device__ __forceinline__ uint32_t stage_tau_naive(const BinCtx &bc, int f, flo
 }
 
 // Stage faces [base, base+nb) of the bin (or sid[] in fallback mode) at the ng sub-frames
-// taus[0..ng): records rec[l*nb + j], masks wm[(l*NWARP + w)*nw + j/32].  Masks must be clear.
+// taus[0..ng): records rec[l*nb + j], masks wm[(l*NFP + w)*nw + j/32].  Masks must be clear.
 // Work is spread over (face, sub-frame) pairs, face-major, so the lanes that share a face load its
 // record with broadcast loads.
 template <bool CENSUS, int MODE>
@@ -346,7 +354,7 @@ __device__ __forceinline__ void stage_group(const BinCtx &bc, int nb, int base, 
         }
         if (CENSUS) nstage += fm != 0u;
         const uint32_t bit = 1u << (j & 31);
-        for (uint32_t m = fm; m; m &= m - 1) atomicOr(wm + (l * NWARP + (__ffs(m) - 1)) * nw + (j >> 5), bit);
+        for (uint32_t m = fm; m; m &= m - 1) atomicOr(wm + (l * NFP + (__ffs(m) - 1)) * nw + (j >> 5), bit);
     }
 }
 
@@ -472,7 +480,7 @@ template <int MODE>
 struct FwdSmem {
     TauRec rec[SREC_F];
     float4 vtx[MODE == 2 ? 3 * SREC_F : 1];   // solver 2: lerped vertices per staged record
-    uint32_t wm[NWARP * (SREC_F / 32 + GMAX_F)];
+    uint32_t wm[NFP * (SREC_F / 32 + GMAX_F)];
     int sid[SREC_F];
     float taus[GMAX_F];
     int wsum[NWARP];
@@ -530,7 +538,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
             uint16_t *vis_out = (MODE == 0 && n <= SREC_B) ? t.vis : nullptr;
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
-                clear_words(S.wm, ng * NWARP * nw);
+                clear_words(S.wm, ng * NFP * nw);
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();
                 stage_group<CENSUS, MODE>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, nstage);
@@ -539,7 +547,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                     float zbest = __int_as_float(0x7f800000);
                     int ebest = -1, fbest = 0x7fffffff;
                     const TauRec *rl = S.rec + l * n;
-                    const uint32_t *wml = S.wm + (l * NWARP + warp) * nw;
+                    const uint32_t *wml = S.wm + (l * NFP + fp_of(warp, lane)) * nw;
                     bool tie = true;
                     if (MODE != 2) tie = vis_mask_fast<CENSUS, MODE>(rl, wml, nw, ul, vl, zbest, ebest, ncov, ntest, inimg);
                     if (__any_sync(0xffffffffu, tie)) {   // exact depth tie somewhere in the warp: face indices decide
@@ -582,11 +590,11 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                     const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SREC_F, base, fpos, S.sid, S.wsum);
                     if (nb == 0) break;
                     const int nw = (nb + 31) >> 5;
-                    clear_words(S.wm, NWARP * nw);
+                    clear_words(S.wm, NFP * nw);
                     __syncthreads();
                     stage_group<CENSUS, MODE>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, nstage);
                     __syncthreads();
-                    vis_mask<CENSUS, MODE>(S.rec, S.vtx, S.wm + warp * nw, nw, base, ul, vl, zbest, ebest, fbest, ncov,
+                    vis_mask<CENSUS, MODE>(S.rec, S.vtx, S.wm + fp_of(warp, lane) * nw, nw, base, ul, vl, zbest, ebest, fbest, ncov,
                                            ntest, inimg);
                     if (ebest >= base) {   // winner changed in this batch: shade now (Eq.9)
                         shade(S.rec[ebest - base], t.fcol, ul, vl, pr, pg, pb);
@@ -690,7 +698,7 @@ template <int MODE>
 struct BwdSmem {
     TauRec rec[SREC_B];
     float4 vtx[MODE == 2 ? 3 * SREC_B : 1];
-    uint32_t wm[NWARP * (SREC_B / 32 + GMAX_B)];
+    uint32_t wm[NFP * (SREC_B / 32 + GMAX_B)];
     int sid[SREC_B];
     int win[GMAX_B][TW * TH]; // winning slot per (sub-frame of the group, pixel)
     int cnt[SREC_B];          // won-pixel count per staged slot
@@ -970,7 +978,7 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
             const int Gs = min(GMAX_B, SREC_B / n), nw = (n + 31) >> 5;
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
-                clear_words(S.wm, ng * NWARP * nw);
+                clear_words(S.wm, ng * NFP * nw);
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();
                 stage_group<false, MODE>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, d2);
@@ -978,7 +986,7 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
                 for (int l = 0; l < ng; ++l) {       // visibility for the group (no barriers)
                     float zbest = __int_as_float(0x7f800000);
                     int ebest = -1, fbest = 0x7fffffff;
-                    const uint32_t *wml = S.wm + (l * NWARP + warp) * nw;
+                    const uint32_t *wml = S.wm + (l * NFP + fp_of(warp, lane)) * nw;
                     bool tie = true;
                     if (MODE != 2) tie = vis_mask_fast<false, MODE>(S.rec + l * n, wml, nw, ul, vl, zbest, ebest, d0, d1, false);
                     if (__any_sync(0xffffffffu, tie)) {
@@ -1004,11 +1012,11 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
                     const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SREC_B, base, fpos, S.sid, S.wsum);
                     if (nb == 0) break;
                     const int nw = (nb + 31) >> 5;
-                    clear_words(S.wm, NWARP * nw);
+                    clear_words(S.wm, NFP * nw);
                     __syncthreads();
                     stage_group<false, MODE>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, d2);
                     __syncthreads();
-                    vis_mask<false, MODE>(S.rec, S.vtx, S.wm + warp * nw, nw, base, ul, vl, zbest, ebest, fbest, d0, d1,
+                    vis_mask<false, MODE>(S.rec, S.vtx, S.wm + fp_of(warp, lane) * nw, nw, base, ul, vl, zbest, ebest, fbest, d0, d1,
                                           false);
                     if (ebest >= base) fbest = S.rec[ebest - base].fid;
                     base += nb;
@@ -1021,7 +1029,7 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
                     const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SREC_B, base, fpos, S.sid, S.wsum);
                     if (nb == 0) break;
                     const int nw = (nb + 31) >> 5;
-                    clear_words(S.wm, NWARP * nw);
+                    clear_words(S.wm, NFP * nw);
                     __syncthreads();
                     stage_group<false, MODE>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, d2);
                     __syncthreads();

@@ -437,6 +437,9 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
                         soft_product<CENSUS>(S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, ul, vl, kexp, P, Pnz, nz,
                                              npair);
                         S.om[l][p] = 1.f - P;
+                        if (t.spz)   // the backward's dalpha/dA factors (K9 skips its product pass)
+                            t.spz[((size_t)(im.cov_off + kg + l) * t.T + tile) * NPX + p] =
+                                nz == 0 ? Pnz : (nz == 1 ? -Pnz : __int_as_float(0x7fffffff));
                     }
                 }
                 __syncthreads();
@@ -554,7 +557,7 @@ __device__ __forceinline__ void flush_slots(SoftBwdSmem &S, const Tables &t, con
 template <bool FUSED>
 __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *rec, const uint32_t *wm, int nw,
                                                int l, int w, int lane, const STile &tc, float kexp, float c2,
-                                               int wd0 = 0, int wd1 = -1)
+                                               int wd0 = 0, int wd1 = -1, const float *pzc = nullptr)
 {
     if (wd1 < 0) wd1 = nw;
     const bool mine = (S.need[l][w] >> lane) & 1u;
@@ -571,6 +574,11 @@ __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *re
             z = 0;
             soft_product<false>(rec, wm, nw, ul, vl, kexp, P, pz, z, dummy);
             z = min(z, 2);
+        } else if (pzc) {   // K8's products of this (sub-frame, pixel)
+            const float e = pzc[p];
+            const unsigned u = __float_as_uint(e);
+            z = (u & 0x7fffffffu) > 0x7f800000u ? 2 : (int)(u >> 31);
+            pz = fabsf(e);
         } else {
             pz = S.pnz[l][p];
             z = S.nz[l][p];
@@ -688,7 +696,8 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
                     soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
 #if BR_K9_SPLIT
-                    for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+                    const bool cached = t.spz && n <= SREC_F8;   // K8 took its grouped path for this bin
+                    for (int it = cached ? -1 : next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {
                         nx = next_item(&S.head, ng * SNW, lane);
                         const int l = it / SNW, w = it - l * SNW;
                         if ((S.need[l][w] >> lane) & 1u) {
@@ -702,14 +711,16 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
                             S.nz[l][p] = (unsigned short)min(nz, 2);
                         }
                     }
-                    __syncthreads();
+                    if (!cached) __syncthreads();   // block-uniform
                     // pass 2: finer items (sub-frame, footprint, 32-face word) keep the tail short
                     for (int it = next_item(&S.head2, ng * SNW * nw, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
                         nx = next_item(&S.head2, ng * SNW * nw, lane);
                         const int wd = it % nw, lw = it / nw, l = lw / SNW, w = lw - l * SNW;
                         if (!S.need[l][w] || !S.wm[(l * SNW + w) * nw + wd]) continue;
                         soft_grad_item<false>(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc, kexp,
-                                              c2, wd, wd + 1);
+                                              c2, wd, wd + 1,
+                                              cached ? t.spz + ((size_t)(im.cov_off + kg + l) * t.T + tile) * NPX
+                                                     : nullptr);
                     }
 #else
                     for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched

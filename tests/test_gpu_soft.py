@@ -20,13 +20,13 @@ TOL_GRAD = 1e-3
 
 
 def gpu_soft(sc, delta, G=None, reuse=True, sub_range=None, soft_exact=False, soft_cut=0.0, max_chunk=0,
-             soft_bin_factor=0.0, ids_k=-1):
+             soft_bin_factor=0.0, ids_k=-1, cache=True):
     import torch
     from paper_2602_07860_b200 import BlurRenderer
     dev = torch.device("cuda:0")
     r = BlurRenderer(sc.faces, sc.motion, sc.cams, sc.H, sc.W, sc.V, device=dev, sub_range=sub_range,
                      max_chunk=max_chunk, delta=delta, soft_exact=soft_exact, soft_cut=soft_cut,
-                     soft_bin_factor=soft_bin_factor)
+                     soft_bin_factor=soft_bin_factor, cache_visibility=cache)
     v = torch.tensor(np.asarray(sc.verts, np.float32), device=dev)
     c = torch.tensor(np.asarray(sc.colors, np.float32), device=dev)
     ids = torch.full((sc.B, sc.H, sc.W), -7, dtype=torch.int32, device=dev) if ids_k >= 0 else None
@@ -132,6 +132,18 @@ def test_soft_backward_without_reuse_and_delta_zero():
     h = gpu_soft(sc, 0.0, G=G)
     assert np.array_equal(h["rgba"][..., :3], a["rgba"][..., :3])
     assert np.all(a["rgba"][..., 3] >= h["rgba"][..., 3])
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_soft_product_cache_equals_recompute(cfg):
+    """BLUR_CACHE_VISIBILITY with delta > 0: K9 reads the products K8 left per (sub-frame, pixel)
+    instead of recomputing them; same gradients as the recomputing backward."""
+    sc = scenes.make(cfg).subset([0, 1])
+    G = np.random.default_rng(5).normal(size=(sc.B, sc.H, sc.W, 4)).astype(np.float32) * 1e-4
+    a = gpu_soft(sc, 1e-4, G=G, cache=True)
+    b = gpu_soft(sc, 1e-4, G=G, cache=False)
+    assert np.array_equal(a["rgba"], b["rgba"])
+    assert rel_l2(a["dv"], b["dv"]) < 1e-6 and rel_l2(a["dc"], b["dc"]) < 1e-6
 
 
 def test_soft_overflow_fallback_and_cut():
