@@ -111,7 +111,11 @@ typedef struct {
                                 sum_b N_b * H * W * 2 bytes, e.g. 0.84 GB for C4), and a bwd with
                                 BLUR_REUSE_SETUP reads it instead of recomputing the visibility (the
                                 result is identical; solver 0 only).  An index buffer, not sub-frame
-                                images: the blurred image is still accumulated in registers. */
+                                images: the blurred image is still accumulated in registers.  With
+                                delta > 0 the soft forward (K8) also leaves, per background (pixel,
+                                sub-frame), the product of the factors 1 - A_j (Eq.15; 4 B each) that
+                                the soft backward (K9) needs for dalpha/dA_j, instead of recomputing
+                                them. */
 typedef struct {
     int32_t max_chunk;             /* G: max sub-frames sharing one tile bin (0 = automatic) */
     int32_t flags;                 /* BLUR_REUSE_SETUP */

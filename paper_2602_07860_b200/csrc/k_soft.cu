@@ -53,6 +53,9 @@ constexpr int SNW = NT / 32;     // warps per CTA
 #ifndef BR_K8_MINB
 #define BR_K8_MINB 5
 #endif
+#ifndef BR_K9_T
+#define BR_K9_T 1          // K9 pass 2 with cached products: face-per-lane (soft_grad_faces)
+#endif
 #ifndef BR_K9_SPLIT
 #define BR_K9_SPLIT 1
 #endif
@@ -652,6 +655,102 @@ __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *re
     }
 }
 
+#ifdef BR_K9_STATS
+__device__ unsigned long long br_k9_stats[8];
+#endif
+
+// position (0..31) of the r-th (0-based) set bit of x, counted from the least significant bit
+__device__ __forceinline__ int nth_set_bit(uint32_t x, int r)
+{
+    int pos = 0;
+#pragma unroll
+    for (int s = 16; s; s >>= 1) {
+        const int c = __popc(x & ((1u << s) - 1u));
+        if (r >= c) { r -= c; x >>= s; pos += s; }
+    }
+    return pos;
+}
+
+// Pass 2 with K8's cached products, transposed: the lanes are faces -- batch b of 32 of the faces
+// in the item's mask, compacted -- with the record in registers, and loop over the footprint's
+// pixels (their gradient factor and products broadcast by shuffles), so each lane sums its own
+// face's corner gradients over the pixels in registers: no cross-lane reduction per (pixel, face)
+// term, one set of shared atomics per (face, item).
+__device__ __forceinline__ void soft_grad_faces(SoftBwdSmem &S, const SoftRec *rec, const uint32_t *wm, int nw,
+                                                int b, int l, int w, int lane, const STile &tc, float kexp, float c2,
+                                                const float *pzc)
+{
+    // compaction: inclusive scan of the words' face counts (nw <= 32)
+    const uint32_t myw = lane < nw ? wm[lane] : 0u;
+    int incl = __popc(myw);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if ((b << 5) >= total) return;                                      // warp-uniform
+    const int idx = (b << 5) + lane;
+    const bool has = idx < total;
+    int wi = 0;                                                         // word holding face idx
+    for (int j = 0; j < nw; ++j) wi += __shfl_sync(0xffffffffu, incl, j) <= idx;
+    const uint32_t wv = __shfl_sync(0xffffffffu, myw, wi & 31);
+    const int ex = __shfl_sync(0xffffffffu, incl, wi & 31) - __popc(wv);
+    const int slot = (wi << 5) + nth_set_bit(__brev(wv), idx - ex);    // bit 31 - k = slot 32 wi + k
+    int p;
+    float ulp, vlp;
+    footprint_pixel(w, lane, tc, p, ulp, vlp);
+    float cp = 0.f, pzp = 0.f;
+    int zp = 2;
+    if ((S.need[l][w] >> lane) & 1u) {
+        const float e = pzc[p];
+        const unsigned u = __float_as_uint(e);
+        zp = (u & 0x7fffffffu) > 0x7f800000u ? 2 : (int)(u >> 31);
+        pzp = fabsf(e);
+        cp = S.ga[p] * c2;
+    }
+    unsigned act = __ballot_sync(0xffffffffu, zp < 2 && cp != 0.f);   // pixels with a non-zero factor
+    SoftRec r;
+    if (has) r = rec[slot];
+    float g[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    while (act) {
+        const int q = __ffs(act) - 1;
+        act &= act - 1;
+        const float ul = __shfl_sync(0xffffffffu, ulp, q), vl = __shfl_sync(0xffffffffu, vlp, q);
+        const float cq = __shfl_sync(0xffffffffu, cp, q), pzq = __shfl_sync(0xffffffffu, pzp, q);
+        const int zq = __shfl_sync(0xffffffffu, zp, q);
+        if (!has) continue;
+        const SoftHit h = soft_eval(r, ul, vl);
+        const float A = __expf(-h.d * kexp);
+        const float fac = 1.0f - A;
+        // dalpha/dA_j = prod_{l != j} (1 - A_l)
+        const float dadA = zq == 0 ? __fdividef(pzq, fac) : (fac == 0.f ? pzq : 0.f);
+        // dL/dv_i(tau) = G_a dalpha/dA (A / delta) 2 w^*_i F(tau) Delta
+        const float cc = cq * dadA * A;
+        const float4 q4 = r.q[4];
+        const float gx = cc * __fmaf_rn(h.d1, q4.x, h.d2 * q4.z);
+        const float gy = cc * __fmaf_rn(h.d1, q4.y, h.d2 * q4.w);
+        const float wa = 1.f - h.t, wb = h.t;
+        // corners (e, e + 1 mod 3) of the chosen edge get weights (1 - t, t)
+        const float w0 = h.e == 0 ? wa : (h.e == 2 ? wb : 0.f);
+        const float w1 = h.e == 1 ? wa : (h.e == 0 ? wb : 0.f);
+        const float w2 = h.e == 2 ? wa : (h.e == 1 ? wb : 0.f);
+        g[0] = __fmaf_rn(w0, gx, g[0]); g[1] = __fmaf_rn(w0, gy, g[1]);
+        g[2] = __fmaf_rn(w1, gx, g[2]); g[3] = __fmaf_rn(w1, gy, g[3]);
+        g[4] = __fmaf_rn(w2, gx, g[4]); g[5] = __fmaf_rn(w2, gy, g[5]);
+    }
+    if (has) {
+        const float tau = S.taus[l];
+        float *a = S.acc[slot];
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+            if (g[i] != 0.f) {
+                atomicAdd(a + i, (1.f - tau) * g[i]);   // keyframe s
+                atomicAdd(a + 6 + i, tau * g[i]);       // keyframe s + 1
+            }
+    }
+}
+
 __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const float *__restrict__ grad)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -693,6 +792,9 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
                     for (int w = 0; w < SNW; ++w) anyn |= S.need[l][w];
                 if (anyn) {   // block-uniform
                     touched = true;
+#ifdef BR_K9_STATS
+                    if (threadIdx.x == 0) { atomicAdd(&br_k9_stats[0], 1ull); atomicAdd(&br_k9_stats[1], (unsigned long long)n); }
+#endif
                     soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
 #if BR_K9_SPLIT
@@ -716,11 +818,19 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
                     for (int it = next_item(&S.head2, ng * SNW * nw, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
                         nx = next_item(&S.head2, ng * SNW * nw, lane);
                         const int wd = it % nw, lw = it / nw, l = lw / SNW, w = lw - l * SNW;
-                        if (!S.need[l][w] || !S.wm[(l * SNW + w) * nw + wd]) continue;
-                        soft_grad_item<false>(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc, kexp,
-                                              c2, wd, wd + 1,
-                                              cached ? t.spz + ((size_t)(im.cov_off + kg + l) * t.T + tile) * NPX
-                                                     : nullptr);
+                        const uint32_t m = (cached && BR_K9_T) ? 1u : S.wm[(l * SNW + w) * nw + wd];
+#ifdef BR_K9_STATS
+                        if (lane == 0 && m && S.need[l][w]) { atomicAdd(&br_k9_stats[2], 1ull); atomicAdd(&br_k9_stats[3], (unsigned long long)__popc(m)); atomicAdd(&br_k9_stats[4], (unsigned long long)__popc(S.need[l][w])); }
+#endif
+                        if (!S.need[l][w] || !m) continue;
+                        if (cached && BR_K9_T)
+                            soft_grad_faces(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, wd, l, w, lane, tc, kexp, c2,
+                                            t.spz + ((size_t)(im.cov_off + kg + l) * t.T + tile) * NPX);
+                        else
+                            soft_grad_item<false>(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc,
+                                                  kexp, c2, wd, wd + 1,
+                                                  cached ? t.spz + ((size_t)(im.cov_off + kg + l) * t.T + tile) * NPX
+                                                         : nullptr);
                     }
 #else
                     for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
@@ -748,6 +858,9 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
 #pragma unroll
                 for (int w = 0; w < SNW; ++w) anyn |= S.need[0][w];
                 int base = 0, fpos = 0;
+#ifdef BR_K9_STATS
+                if (anyn && threadIdx.x == 0) { atomicAdd(&br_k9_stats[5], 1ull); atomicAdd(&br_k9_stats[6], (unsigned long long)sb.n); atomicAdd(&br_k9_stats[7], (unsigned long long)sb.fb); }
+#endif
                 while (anyn) {   // pass 1 over all batches
                     const int nb = sb.fb ? soft_fallback_fill(t, sb.rseg, S.taus[0], tc, SREC_B9, fpos, S.sid, S.wsum)
                                          : (base < sb.n ? min(SREC_B9, sb.n - base) : 0);
@@ -839,3 +952,14 @@ cudaError_t launch_soft_bwd(const Tables &t, const float *grad, cudaStream_t st)
 }
 
 }  // namespace br
+
+#ifdef BR_K9_STATS
+extern "C" int blur_debug_k9_stats(unsigned long long *out)
+{
+    cudaDeviceSynchronize();
+    const cudaError_t e = cudaMemcpyFromSymbol(out, br::br_k9_stats, sizeof(unsigned long long) * 8);
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(br::br_k9_stats, z, sizeof(z));
+    return (int)e;
+}
+#endif
