@@ -40,7 +40,7 @@ FLOP_PAIR, FLOP_SHADE, FLOP_SETUP, FLOP_BWD = 18.0, 25.0, 30.0, 100.0
 # the backward (pass 1 the same, pass 2 the same + 16 for the gradient and its keyframe split)
 FLOP_SOFT_FWD, FLOP_SOFT_BWD = 54.0, 124.0
 LAUNCHES_FWD, LAUNCHES_LOSS, LAUNCHES_BWD = 9, 1, 2
-LAUNCHES_SOFT_FWD, LAUNCHES_SOFT_BWD = 9, 1     # soft bins (7) + K8 + reduce; K9
+LAUNCHES_SOFT_FWD, LAUNCHES_SOFT_BWD = 9, 2     # soft bins (7) + K8 + reduce; K9C (cached products) + K9
 
 
 def parse():

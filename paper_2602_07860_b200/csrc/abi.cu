@@ -10,6 +10,10 @@
 #include "internal.cuh"
 #include "../../include/blurrast.h"
 
+#ifndef BR_SOFT_SPLITS
+#define BR_SOFT_SPLITS 8   // soft kernels: up to 8 CTAs per (image, tile), each taking every 8th chunk
+#endif
+
 using namespace br;
 
 namespace {
@@ -72,7 +76,7 @@ void rodrigues(const double ax_in[3], double th, double R[9])
 }
 
 struct Plan {
-    int B = 0, V = 0, F = 0, H = 0, W = 0, TX = 0, TY = 0, T = 0, NC = 0, maxS = 1, splits = 1;
+    int B = 0, V = 0, F = 0, H = 0, W = 0, TX = 0, TY = 0, T = 0, NC = 0, maxS = 1, splits = 1, ssplits = 1;
     std::vector<ImgInfo> imgs;
     std::vector<Chunk> chunks;
     std::vector<int> sched_s;
@@ -247,6 +251,7 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
             if (sp > 32) sp = 32;
             P.splits = (int)std::max(1LL, sp);
         }
+        P.ssplits = std::max(P.splits, std::min(maxc, BR_SOFT_SPLITS));
     }
     P.n_key = key_off;
     P.n_rec = rec_off;
@@ -291,7 +296,7 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
     P.o_part = o; o = align256(o + (P.splits > 1 ? 16 * (size_t)P.splits * B * H * W : 0));
     if (P.soft) {
         P.o_cov = o; o = align256(o + 4 * (size_t)P.n_sub * P.T * (NT / 32));
-        P.o_spart = o; o = align256(o + 4 * (size_t)P.splits * B * H * W);
+        P.o_spart = o; o = align256(o + 4 * (size_t)P.ssplits * B * H * W);
         P.o_scnt = o; o = align256(o + 4 * P.nbins);
         P.o_soff = o; o = align256(o + 8 * (P.nbins + 1));
         P.o_sbsum = o; o = align256(o + 8 * ((P.nbins + 1023) / 1024 + 1));
@@ -329,6 +334,7 @@ Tables make_tables(const Plan &P, void *ws)
     t.dkey = (float2 *)(w + P.o_dkey);
     t.NC = P.NC; t.T = P.T; t.TX = P.TX; t.TY = P.TY;
     t.splits = P.splits;
+    t.ssplits = P.ssplits;
     t.part = (float4 *)(w + P.o_part);
     t.B = P.B; t.V = P.V; t.F = P.F; t.H = P.H; t.W = P.W;
     if (P.soft) {

@@ -87,6 +87,8 @@ struct Tables {          // device pointers into the workspace
     int B, V, F, H, W;
     int solver;          // 0 fast (Eq.8 coefficients), 1 naive per-frame setup, 2 naive per-pixel solve
     int splits;          // CTAs sharing one (image, tile) by sub-frame chunks (small launches)
+    int ssplits;         // the same for the soft kernels K8/K9 (>= splits: their silhouette tiles
+                         // are heavy, so splitting them shortens the launch's tail)
     float4 *part;        // splits > 1: per-split partial images [splits][B*H*W]
     // soft background coverage (NEXT-1; delta > 0)
     float delta;         // Eq.10 bandwidth (NDC^2)

@@ -53,8 +53,8 @@ constexpr int SNW = NT / 32;     // warps per CTA
 #ifndef BR_K8_MINB
 #define BR_K8_MINB 5
 #endif
-#ifndef BR_K9_T
-#define BR_K9_T 1          // K9 pass 2 with cached products: face-per-lane (soft_grad_faces)
+#ifndef BR_K9C_MINB
+#define BR_K9C_MINB 4      // K9C (cached products) CTAs per SM
 #endif
 #ifndef BR_K9_SPLIT
 #define BR_K9_SPLIT 1
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
     float alpha = 0.f;
     unsigned long long npair = 0, nstage = 0, nitem = 0, nface = 0;
 
-    for (int c = im.chunk_begin + (int)blockIdx.z; c < im.chunk_end; c += t.splits) {
+    for (int c = im.chunk_begin + (int)blockIdx.z; c < im.chunk_end; c += t.ssplits) {
         const Chunk ch = t.chunks[c];
         SoftBin sb;
         soft_bin(t, im, ch, c, tile, sb);
@@ -540,7 +540,8 @@ __device__ __forceinline__ void soft_flush(const Tables &t, const ImgInfo &im, i
 }
 
 // flush and clear the slot accumulators [0, nb)
-__device__ __forceinline__ void flush_slots(SoftBwdSmem &S, const Tables &t, const ImgInfo &im, int s, int nb,
+template <class Sm>
+__device__ __forceinline__ void flush_slots(Sm &S, const Tables &t, const ImgInfo &im, int s, int nb,
                                             const int *fid_of)
 {
     for (int j = threadIdx.x; j < nb; j += NT) {
@@ -560,7 +561,7 @@ __device__ __forceinline__ void flush_slots(SoftBwdSmem &S, const Tables &t, con
 template <bool FUSED>
 __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *rec, const uint32_t *wm, int nw,
                                                int l, int w, int lane, const STile &tc, float kexp, float c2,
-                                               int wd0 = 0, int wd1 = -1, const float *pzc = nullptr)
+                                               int wd0 = 0, int wd1 = -1)
 {
     if (wd1 < 0) wd1 = nw;
     const bool mine = (S.need[l][w] >> lane) & 1u;
@@ -577,11 +578,6 @@ __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *re
             z = 0;
             soft_product<false>(rec, wm, nw, ul, vl, kexp, P, pz, z, dummy);
             z = min(z, 2);
-        } else if (pzc) {   // K8's products of this (sub-frame, pixel)
-            const float e = pzc[p];
-            const unsigned u = __float_as_uint(e);
-            z = (u & 0x7fffffffu) > 0x7f800000u ? 2 : (int)(u >> 31);
-            pz = fabsf(e);
         } else {
             pz = S.pnz[l][p];
             z = S.nz[l][p];
@@ -655,10 +651,6 @@ __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *re
     }
 }
 
-#ifdef BR_K9_STATS
-__device__ unsigned long long br_k9_stats[8];
-#endif
-
 // position (0..31) of the r-th (0-based) set bit of x, counted from the least significant bit
 __device__ __forceinline__ int nth_set_bit(uint32_t x, int r)
 {
@@ -676,7 +668,8 @@ __device__ __forceinline__ int nth_set_bit(uint32_t x, int r)
 // pixels (their gradient factor and products broadcast by shuffles), so each lane sums its own
 // face's corner gradients over the pixels in registers: no cross-lane reduction per (pixel, face)
 // term, one set of shared atomics per (face, item).
-__device__ __forceinline__ void soft_grad_faces(SoftBwdSmem &S, const SoftRec *rec, const uint32_t *wm, int nw,
+template <class Sm>
+__device__ __forceinline__ void soft_grad_faces(Sm &S, const SoftRec *rec, const uint32_t *wm, int nw,
                                                 int b, int l, int w, int lane, const STile &tc, float kexp, float c2,
                                                 const float *pzc)
 {
@@ -751,6 +744,81 @@ __device__ __forceinline__ void soft_grad_faces(SoftBwdSmem &S, const SoftRec *r
     }
 }
 
+// bins whose products K8 cached (its grouped path) and that K9C's record stage holds
+__device__ __forceinline__ bool k9c_bin(const SoftBin &sb) { return !sb.fb && sb.n <= SREC_B9 && sb.n <= SREC_F8; }
+
+struct SoftBwdCSmem {
+    SoftRec rec[SREC_B9];
+    uint32_t wm[GMAX_S * SNW * (SREC_B9 / 32 + 1)];
+    uint32_t need[GMAX_S][SNW];
+    float ga[NPX];
+    float acc[SREC_B9][12];    // per bin slot: d/d keyframe s (corners x, y), then keyframe s+1
+    float taus[GMAX_S];
+    int head2;
+};
+
+// K9C: the soft backward of the bins whose dalpha/dA products K8 left in t.spz (BLUR_CACHE_VISIBILITY):
+// per group of sub-frames, stage the records, then work items (sub-frame, footprint, batch of 32
+// faces) through soft_grad_faces.  Launched before K9, which takes every other bin.
+__global__ void __launch_bounds__(NT, BR_K9C_MINB) k9c_soft_bwd(Tables t, const float *__restrict__ grad)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SoftBwdCSmem &S = *reinterpret_cast<SoftBwdCSmem *>(smem_raw);
+    const int b = blockIdx.y, tile = blockIdx.x;
+    const ImgInfo &im = t.imgs[b];
+    STile tc;
+    stile(t, tile, tc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+    const int px = tc.px0 + lx, py = tc.py0 + ly, myp = ly * TW + lx;
+    const bool inimg = px < t.W && py < t.H;
+    const float kexp = 1.0f / t.delta, c2 = 2.0f / t.delta;
+    const float ga = inimg ? __ldg(grad + 4 * (((size_t)b * t.H + py) * t.W + px) + 3) / (float)im.N : 0.f;
+    S.ga[myp] = ga;
+    const bool want = inimg && ga != 0.f;
+    for (int i = threadIdx.x; i < SREC_B9 * 12; i += NT) (&S.acc[0][0])[i] = 0.f;
+    unsigned long long dummy = 0;
+    __syncthreads();
+
+    for (int c = im.chunk_begin + (int)blockIdx.z; c < im.chunk_end; c += t.ssplits) {
+        const Chunk ch = t.chunks[c];
+        SoftBin sb;
+        soft_bin(t, im, ch, c, tile, sb);
+        if (sb.n == 0 || !k9c_bin(sb)) continue;
+        const int n = sb.n, Gs = min(GMAX_S, SREC_B9 / n), nw = (n + 31) >> 5;
+        bool touched = false;
+        for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
+            const int ng = min(Gs, ch.k1 - kg);
+            for (int l = 0; l < ng; ++l) load_need(t, im, kg + l, tile, warp, lane, want, &S.need[l][warp]);
+            for (int i = threadIdx.x; i < ng * SNW * nw; i += NT) S.wm[i] = 0u;
+            if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[im.sched_off + kg + threadIdx.x];
+            if (threadIdx.x == 0) S.head2 = 0;
+            __syncthreads();
+            uint32_t anyn = 0u;
+            for (int l = 0; l < ng; ++l)
+#pragma unroll
+                for (int w = 0; w < SNW; ++w) anyn |= S.need[l][w];
+            if (anyn) {   // block-uniform
+                touched = true;
+                soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, nullptr, S.rec, S.wm, dummy);
+                __syncthreads();
+                for (int it = next_item(&S.head2, ng * SNW * nw, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+                    nx = next_item(&S.head2, ng * SNW * nw, lane);
+                    const int bt = it % nw, lw = it / nw, l = lw / SNW, w = lw - l * SNW;
+                    if (!S.need[l][w]) continue;
+                    soft_grad_faces(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, bt, l, w, lane, tc, kexp, c2,
+                                    t.spz + ((size_t)(im.cov_off + kg + l) * t.T + tile) * NPX);
+                }
+            }
+            __syncthreads();
+        }
+        if (touched) {
+            flush_slots(S, t, im, ch.s, n, sb.ent);
+            __syncthreads();
+        }
+    }
+}
+
 __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const float *__restrict__ grad)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -771,11 +839,11 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
     unsigned long long dummy = 0;
     __syncthreads();
 
-    for (int c = im.chunk_begin + (int)blockIdx.z; c < im.chunk_end; c += t.splits) {
+    for (int c = im.chunk_begin + (int)blockIdx.z; c < im.chunk_end; c += t.ssplits) {
         const Chunk ch = t.chunks[c];
         SoftBin sb;
         soft_bin(t, im, ch, c, tile, sb);
-        if (sb.n == 0) continue;
+        if (sb.n == 0 || (t.spz && k9c_bin(sb))) continue;   // empty, or K9C's
         if (!sb.fb && sb.n <= SREC_B9) {
             const int n = sb.n, Gs = min(GMAX_S, SREC_B9 / n), nw = (n + 31) >> 5;
             bool touched = false;
@@ -792,14 +860,10 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
                     for (int w = 0; w < SNW; ++w) anyn |= S.need[l][w];
                 if (anyn) {   // block-uniform
                     touched = true;
-#ifdef BR_K9_STATS
-                    if (threadIdx.x == 0) { atomicAdd(&br_k9_stats[0], 1ull); atomicAdd(&br_k9_stats[1], (unsigned long long)n); }
-#endif
                     soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, dummy);
                     __syncthreads();
 #if BR_K9_SPLIT
-                    const bool cached = t.spz && n <= SREC_F8;   // K8 took its grouped path for this bin
-                    for (int it = cached ? -1 : next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {
+                    for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
                         nx = next_item(&S.head, ng * SNW, lane);
                         const int l = it / SNW, w = it - l * SNW;
                         if ((S.need[l][w] >> lane) & 1u) {
@@ -813,24 +877,14 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
                             S.nz[l][p] = (unsigned short)min(nz, 2);
                         }
                     }
-                    if (!cached) __syncthreads();   // block-uniform
+                    __syncthreads();
                     // pass 2: finer items (sub-frame, footprint, 32-face word) keep the tail short
                     for (int it = next_item(&S.head2, ng * SNW * nw, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
                         nx = next_item(&S.head2, ng * SNW * nw, lane);
                         const int wd = it % nw, lw = it / nw, l = lw / SNW, w = lw - l * SNW;
-                        const uint32_t m = (cached && BR_K9_T) ? 1u : S.wm[(l * SNW + w) * nw + wd];
-#ifdef BR_K9_STATS
-                        if (lane == 0 && m && S.need[l][w]) { atomicAdd(&br_k9_stats[2], 1ull); atomicAdd(&br_k9_stats[3], (unsigned long long)__popc(m)); atomicAdd(&br_k9_stats[4], (unsigned long long)__popc(S.need[l][w])); }
-#endif
-                        if (!S.need[l][w] || !m) continue;
-                        if (cached && BR_K9_T)
-                            soft_grad_faces(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, wd, l, w, lane, tc, kexp, c2,
-                                            t.spz + ((size_t)(im.cov_off + kg + l) * t.T + tile) * NPX);
-                        else
-                            soft_grad_item<false>(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc,
-                                                  kexp, c2, wd, wd + 1,
-                                                  cached ? t.spz + ((size_t)(im.cov_off + kg + l) * t.T + tile) * NPX
-                                                         : nullptr);
+                        if (!S.need[l][w] || !S.wm[(l * SNW + w) * nw + wd]) continue;
+                        soft_grad_item<false>(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, l, w, lane, tc, kexp,
+                                              c2, wd, wd + 1);
                     }
 #else
                     for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
@@ -858,9 +912,6 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
 #pragma unroll
                 for (int w = 0; w < SNW; ++w) anyn |= S.need[0][w];
                 int base = 0, fpos = 0;
-#ifdef BR_K9_STATS
-                if (anyn && threadIdx.x == 0) { atomicAdd(&br_k9_stats[5], 1ull); atomicAdd(&br_k9_stats[6], (unsigned long long)sb.n); atomicAdd(&br_k9_stats[7], (unsigned long long)sb.fb); }
-#endif
                 while (anyn) {   // pass 1 over all batches
                     const int nb = sb.fb ? soft_fallback_fill(t, sb.rseg, S.taus[0], tc, SREC_B9, fpos, S.sid, S.wsum)
                                          : (base < sb.n ? min(SREC_B9, sb.n - base) : 0);
@@ -926,40 +977,37 @@ cudaError_t launch_soft_fwd(const Tables &t, float *out, unsigned long long *cen
         if (census) {
             e = cudaFuncSetAttribute(k8_soft_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e != cudaSuccess) return e;
-            k8_soft_fwd<true><<<dim3(t.T, t.B, t.splits), NT, smem, st>>>(t, census);
+            k8_soft_fwd<true><<<dim3(t.T, t.B, t.ssplits), NT, smem, st>>>(t, census);
         } else {
             e = cudaFuncSetAttribute(k8_soft_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e != cudaSuccess) return e;
-            k8_soft_fwd<false><<<dim3(t.T, t.B, t.splits), NT, smem, st>>>(t, nullptr);
+            k8_soft_fwd<false><<<dim3(t.T, t.B, t.ssplits), NT, smem, st>>>(t, nullptr);
         }
     } else {
-        e = cudaMemsetAsync(t.spart, 0, sizeof(float) * n * t.splits, st);
+        e = cudaMemsetAsync(t.spart, 0, sizeof(float) * n * t.ssplits, st);
         if (e != cudaSuccess) return e;
     }
     const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 16);
-    k8_soft_reduce<<<blocks, 256, 0, st>>>(t.spart, reinterpret_cast<float4 *>(out), n, t.splits);
+    k8_soft_reduce<<<blocks, 256, 0, st>>>(t.spart, reinterpret_cast<float4 *>(out), n, t.ssplits);
     return cudaGetLastError();
 }
 
 cudaError_t launch_soft_bwd(const Tables &t, const float *grad, cudaStream_t st)
 {
     if (t.B == 0 || t.T == 0 || t.F == 0) return cudaSuccess;
+    cudaError_t e;
+    if (t.spz) {   // bins with K8's cached products first (K9C), then K9 for the rest
+        const int smc = (int)sizeof(SoftBwdCSmem);
+        e = cudaFuncSetAttribute(k9c_soft_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smc);
+        if (e != cudaSuccess) return e;
+        k9c_soft_bwd<<<dim3(t.T, t.B, t.ssplits), NT, smc, st>>>(t, grad);
+    }
     const int smem = (int)sizeof(SoftBwdSmem);
-    cudaError_t e = cudaFuncSetAttribute(k9_soft_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = cudaFuncSetAttribute(k9_soft_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    k9_soft_bwd<<<dim3(t.T, t.B, t.splits), NT, smem, st>>>(t, grad);
+    k9_soft_bwd<<<dim3(t.T, t.B, t.ssplits), NT, smem, st>>>(t, grad);
     return cudaGetLastError();
 }
 
 }  // namespace br
 
-#ifdef BR_K9_STATS
-extern "C" int blur_debug_k9_stats(unsigned long long *out)
-{
-    cudaDeviceSynchronize();
-    const cudaError_t e = cudaMemcpyFromSymbol(out, br::br_k9_stats, sizeof(unsigned long long) * 8);
-    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyToSymbol(br::br_k9_stats, z, sizeof(z));
-    return (int)e;
-}
-#endif
