@@ -10,6 +10,9 @@
 #include "internal.cuh"
 #include "../../include/blurrast.h"
 
+#ifndef BR_HARD_SPLITS
+#define BR_HARD_SPLITS 2   // hard raster: at least 2 CTAs per (image, tile) when it has 2+ chunks (C4 -1%)
+#endif
 #ifndef BR_SOFT_SPLITS
 #define BR_SOFT_SPLITS 8   // soft kernels: up to 8 CTAs per (image, tile), each taking every 8th chunk
 #endif
@@ -238,13 +241,14 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
         im.chunk_end = (int)P.chunks.size();
     }
     P.NC = (int)P.chunks.size();
-    // small launches (few tiles x images) split each tile's sub-frame chunks over several CTAs so
-    // that the grid fills the 148 SMs; partial images are reduced in a fixed order (deterministic)
+    // each tile's sub-frame chunks are split over BR_HARD_SPLITS CTAs (more for small launches, few
+    // tiles x images, so that the grid fills the 148 SMs); partial images are reduced in a fixed
+    // order (deterministic).  The soft kernels split further (their silhouette tiles are heavy).
     {
         int maxc = 1;
         for (const ImgInfo &im : P.imgs) maxc = std::max(maxc, im.chunk_end - im.chunk_begin);
         const long long ctas = (long long)P.T * B, target = 148LL * 8;
-        P.splits = 1;
+        P.splits = std::min(maxc, BR_HARD_SPLITS);
         if (ctas > 0 && ctas < target) {
             long long sp = (target + ctas - 1) / ctas;
             if (sp > maxc) sp = maxc;

@@ -1,6 +1,4 @@
 # scratch A/B driver (edited per experiment)
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_soft.py tests/test_gpu_parity.py tests/test_gpu_optim.py -m gpu -x -q 2>&1 | tail -3
-for c in C4 C3 C2; do
-timeout 600 python bench.py --config $c --delta 1e-4 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$c soft', round(d['ms_per_step'],3), r['kernels_ms'])"
-done
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 600 python bench.py 2>&1 | tail -1 > gpurun_out/bench_now.json; cut -c1-400 gpurun_out/bench_now.json
