@@ -700,8 +700,8 @@ struct BwdSmem {
     float4 vtx[MODE == 2 ? 3 * SREC_B : 1];
     uint32_t wm[NFP * (SREC_B / 32 + GMAX_B)];
     int sid[SREC_B];
-    int win[GMAX_B][TW * TH]; // winning slot per (sub-frame of the group, pixel)
-    int cnt[SREC_B];          // won-pixel count per staged slot
+    short win[GMAX_B][TW * TH];   // winning slot per (sub-frame of the group, pixel), -1 none
+    int cnt[SREC_B];          // won-pixel count per staged slot (key)
     int off[SREC_B];          // exclusive prefix of cnt
     int key[TW * TH];         // sorted won pixels: slot
     int pix[TW * TH];         //                    pixel
@@ -965,7 +965,7 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
                 for (int l = 0; l < ng; ++l) {
                     const uint16_t v = t.vis[((size_t)(im.cov_off + kg + l) * t.T + tile) * (TW * TH) + myp];
                     const int e = (inimg && v != 0xFFFF) ? (int)v : -1;
-                    S.win[l][myp] = e;
+                    S.win[l][myp] = (short)e;
                     if (e >= 0) S.won[l * n + e] = 1;
                 }
                 __syncthreads();
@@ -995,7 +995,7 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
                         vis_mask<false, MODE>(S.rec + l * n, S.vtx + 3 * l * n, wml, nw, 0, ul, vl, zbest, ebest, fbest,
                                               d0, d1, false);
                     }
-                    S.win[l][myp] = inimg ? ebest : -1;
+                    S.win[l][myp] = (short)(inimg ? ebest : -1);
                 }
                 __syncthreads();
                 for (int l = 0; l < ng; ++l)

@@ -1,4 +1,4 @@
 # scratch A/B driver (edited per experiment)
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 600 python bench.py 2>&1 | tail -1 > gpurun_out/bench_now.json; cut -c1-400 gpurun_out/bench_now.json
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_soft.py -m gpu -x -q 2>&1 | tail -3
+CONFIGS="C4 C3 C2" bash tools/ab_variants.sh
