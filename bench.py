@@ -37,8 +37,9 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 FLOP_PAIR, FLOP_SHADE, FLOP_SETUP, FLOP_BWD = 18.0, 25.0, 30.0, 100.0
 # soft background coverage (NEXT-1): flop per evaluated (pixel, face, sub-frame) term in the forward
 # (w1, w2: 8; three projections + quadratic forms: 3 x 12; Eq.14 form + exp + product: 10) and in
-# the backward (pass 1 the same, pass 2 the same + 16 for the gradient and its keyframe split)
-FLOP_SOFT_FWD, FLOP_SOFT_BWD = 54.0, 124.0
+# the backward (pass 1 the same, pass 2 the same + 16 for the gradient and its keyframe split; with
+# the visibility cache K9 reads K8's products and runs pass 2 only: 70)
+FLOP_SOFT_FWD, FLOP_SOFT_BWD, FLOP_SOFT_BWD_CACHED = 54.0, 124.0, 70.0
 LAUNCHES_FWD, LAUNCHES_LOSS, LAUNCHES_BWD = 9, 1, 2
 LAUNCHES_SOFT_FWD, LAUNCHES_SOFT_BWD = 9, 2     # soft bins (7) + K8 + reduce; K9C (cached products) + K9
 
@@ -346,7 +347,8 @@ def main():
     kernels = [("k4_raster_fwd", fw_flop, f_avg), ("k6_raster_bwd", bw_flop, b_avg)]
     if soft:
         kernels += [("k8_soft_fwd", FLOP_SOFT_FWD * soft_terms, float(np.mean(sf_ms))),
-                    ("k9_soft_bwd", FLOP_SOFT_BWD * soft_terms, float(np.mean(sb_ms)))]
+                    ("k9_soft_bwd", (FLOP_SOFT_BWD_CACHED if (rend is not None and rend.cache_flags) else FLOP_SOFT_BWD) * soft_terms,
+                     float(np.mean(sb_ms)))]
     kname, flop, dur = max(kernels, key=lambda k: k[2])
     achieved = flop / (dur / 1000.0) / 1e12 if dur > 0 else 0.0
     traffic = None
