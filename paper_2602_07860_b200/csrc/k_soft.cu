@@ -455,6 +455,8 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
                 load_need(t, im, k, tile, warp, lane, inimg, &S.need[0][warp]);
                 if (threadIdx.x == 0) S.taus[0] = t.sched_tau[im.sched_off + k];
                 S.om[0][myp] = 1.f;
+                S.om[1][myp] = 1.f;                                   // prod of the non-zero factors
+                reinterpret_cast<int *>(S.om[2])[myp] = 0;           // zero factors
                 __syncthreads();
                 uint32_t anyn = 0u;
 #pragma unroll
@@ -479,12 +481,22 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
                             footprint_pixel(it, lane, tc, p, ul, vl);
                             soft_product<CENSUS>(S.rec, S.wm + it * nw, nw, ul, vl, kexp, P, Pnz, nz, npair);
                             S.om[0][p] *= P;
+                            S.om[1][p] *= Pnz;
+                            reinterpret_cast<int *>(S.om[2])[p] += nz;
                         }
                     }
                     base += nb;
                     __syncthreads();
                 }
-                if ((S.need[0][warp] >> lane) & 1u) alpha += 1.f - S.om[0][myp];
+                if ((S.need[0][warp] >> lane) & 1u) {
+                    alpha += 1.f - S.om[0][myp];
+                    if (t.spz) {   // the backward's dalpha/dA factors, as in the grouped path
+                        const int nz = reinterpret_cast<const int *>(S.om[2])[myp];
+                        const float pnz = S.om[1][myp];
+                        t.spz[((size_t)(im.cov_off + k) * t.T + tile) * NPX + myp] =
+                            nz == 0 ? pnz : (nz == 1 ? -pnz : __int_as_float(0x7fffffff));
+                    }
+                }
                 __syncthreads();
             }
         }
@@ -912,6 +924,31 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
 #pragma unroll
                 for (int w = 0; w < SNW; ++w) anyn |= S.need[0][w];
                 int base = 0, fpos = 0;
+                if (t.spz) {   // K8 left the products: one pass, batch by batch
+                    const float *pzc = t.spz + ((size_t)(im.cov_off + k) * t.T + tile) * NPX;
+                    while (anyn) {
+                        const int nb = sb.fb ? soft_fallback_fill(t, sb.rseg, S.taus[0], tc, SREC_B9, fpos, S.sid, S.wsum)
+                                             : (base < sb.n ? min(SREC_B9, sb.n - base) : 0);
+                        if (nb == 0) break;
+                        const int nw = (nb + 31) >> 5;
+                        for (int i = threadIdx.x; i < SNW * nw; i += NT) S.wm[i] = 0u;
+                        if (threadIdx.x == 0) S.head2 = 0;
+                        __syncthreads();
+                        soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy);
+                        __syncthreads();
+                        for (int it = next_item(&S.head2, SNW * nw, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+                            nx = next_item(&S.head2, SNW * nw, lane);
+                            const int bt = it % nw, w = it / nw;
+                            if (!S.need[0][w]) continue;
+                            soft_grad_faces(S, S.rec, S.wm + w * nw, nw, bt, 0, w, lane, tc, kexp, c2, pzc);
+                        }
+                        __syncthreads();
+                        flush_slots(S, t, im, ch.s, nb, sb.fb ? S.sid : sb.ent + base);
+                        base += nb;
+                        __syncthreads();
+                    }
+                    anyn = 0u;
+                }
                 while (anyn) {   // pass 1 over all batches
                     const int nb = sb.fb ? soft_fallback_fill(t, sb.rseg, S.taus[0], tc, SREC_B9, fpos, S.sid, S.wsum)
                                          : (base < sb.n ? min(SREC_B9, sb.n - base) : 0);

@@ -13,3 +13,8 @@ $CMD1 > gpurun_out/plain1.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k4_raster_fwd|k6_raster_bwd" -s 3 -c 2 \
     -o gpurun_out/prof_c4 $CMD1 > gpurun_out/ncu_full.log 2>&1
 echo full=$?
+bash tools/ncu_soft.sh > gpurun_out/ncu_soft_driver.log 2>&1
+echo soft_full=$?
+for c in C1 C2; do
+  timeout 600 python bench.py --config $c --graph --steps 50 --no-cpu-baseline > gpurun_out/bench_${c}_graph.json 2> gpurun_out/bench_${c}_graph.err; echo graph_$c=$?
+done

@@ -42,7 +42,8 @@ METRICS = [
     ("smem bank conflicts", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", 1),
     ("DRAM read (MB)", "dram__bytes_read.sum", 1e-6),
     ("DRAM write (MB)", "dram__bytes_write.sum", 1e-6),
-    ("warp instructions", "sm__inst_executed.sum", 1),
+    ("warp instructions", "smsp__inst_executed.sum", 1),
+    ("SM active / elapsed cycles", "ACTIVE_FRAC", 1),
 ]
 
 
@@ -61,6 +62,14 @@ def full(rep):
         if m is None:
             vals = ["%s, %s" % (d.get("launch__occupancy_limit_registers", "?"), d.get("launch__occupancy_limit_shared_mem", "?"))
                     for _, d, _ in kern]
+        elif m == "ACTIVE_FRAC":   # launch tail: SMs without a resident warp
+            vals = []
+            for _, d, _ in kern:
+                try:
+                    vals.append("%.3f" % (float(d["sm__cycles_active.avg"].replace(",", "")) /
+                                          float(d["sm__cycles_elapsed.avg"].replace(",", ""))))
+                except (KeyError, ValueError):
+                    vals.append("-")
         else:
             vals = []
             for _, d, u in kern:

@@ -38,7 +38,11 @@ HISTORY = """| change | fwd ms | bwd ms | step ms | images/s |
 | hard bins unsorted, (depth, face index) z-buffer | 9.1 | 8.1 | 18.4 | 871 |
 | short visibility loop (bfind, exact-tie re-run), one-time edge tolerance, reject reuse | 8.7 | 7.8 | 17.7 | 903 |
 | (tried) per-entry sub-frame ranges from the binning | 8.7 | 7.8 | 18.0 | 889 |
-| K6 one-warp count scan, K7 warp per vertex, e2e copy overlap | 8.7 | 7.7 | 17.6 | 908 |"""
+| K6 one-warp count scan, K7 warp per vertex, e2e copy overlap | 8.7 | 7.7 | 17.6 | 908 |
+| K4 at 5 CTAs/SM (48 registers), K8 at 5 CTAs/SM | 8.3 | 7.7 | 17.2 | 930 |
+| (tried) face-parallel K4 with 32-bit shared min (two box walks) | 22.8 | 7.7 | 31.7 | - |
+| (tried) 4x4 culling footprints; K6 gather per group of sub-frames | 8.3 | 7.7-8.6 | 17.2-17.9 | - |
+| 2 CTAs per (image, tile) by chunk | 8.2 | 7.7 | 17.05 | 938 |"""
 
 
 def main():
@@ -48,6 +52,11 @@ def main():
     rep = os.path.join(OUT, "prof_c4.ncu-rep")
     tab_l = sp.launches(launches)
     tab_f = sp.full(rep)
+    srep = os.path.join(OUT, "prof_soft.ncu-rep")
+    tab_s = sp.full(srep) if os.path.exists(srep) else "(no soft capture)"
+    if os.path.exists(srep):
+        open(os.path.join(PROF, "r1_ncu_details_soft_C3.csv"), "w").write(
+            sh(["ncu", "-i", srep, "--page", "details", "--csv"]))
     k4l = sh([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep, "k4", "10"])
     k6l = sh([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep, "k6", "10"])
     # raw copies
@@ -137,9 +146,17 @@ Top source lines by warp-stall samples (`tools/ncu_lines.py`):
 
 {HISTORY}
 
-Soft coverage (NEXT-1) on C4, delta 1e-4: first version K8 40 / K9 106 ms (178 ms/step); barycentric
-closest point, work queue, pixel-parallel backward with warp reduce-scatter, 4 CTAs/SM for K8, split
-K9 items: K8 {r(s4)['kernels_ms']['k8_soft_fwd']:.1f} / K9 {r(s4)['kernels_ms']['k9_soft_bwd']:.1f} ms ({s4['ms_per_step']:.1f} ms/step).
+## Soft coverage (NEXT-1): `ncu --set full` of K8, K9C, K9 (C3, delta 1e-4, one launch each)
+
+{tab_s}
+
+"SM active / elapsed" below 1 is the launch tail (SMs with no resident warp); it motivated the soft
+splits (up to 8 CTAs per (image, tile)).  K9 here handles only the bins longer than the record stage.
+
+History on C4, delta 1e-4: first version K8 40 / K9 106 ms (178 ms/step); barycentric closest point,
+work queue, pixel-parallel backward with warp reduce-scatter, 4 CTAs/SM for K8, split K9 items:
+K8 23.7 / K9 71.1 ms (120.5 ms/step); product cache K8 -> K9: K9 58.8; face-per-lane K9C over
+compacted masks: 48.8; soft splits: 36.6; products cached for the long bins too (K9 one pass): K8 {r(s4)['kernels_ms']['k8_soft_fwd']:.1f} / K9C + K9 {r(s4)['kernels_ms']['k9_soft_bwd']:.1f} ms ({s4['ms_per_step']:.1f} ms/step).
 """
     open(os.path.join(PROF, "r1_summary.md"), "w").write(md)
     print("wrote profiles/r1_summary.md")
