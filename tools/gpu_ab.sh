@@ -1,7 +1,5 @@
-# scratch A/B driver (edited per experiment)
+# scratch driver (edited per experiment)
 mkdir -p gpurun_out
-for v in variants/lib_*.so; do
-for c in C4 C3; do
-BLURRAST_LIB=$PWD/$v timeout 600 python bench.py --config $c --delta 1e-4 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$v $c soft', round(d['ms_per_step'],3), r['kernels_ms'])"
-done
-done
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 900 python studies/recovery.py > gpurun_out/recovery.log 2> gpurun_out/recovery.err; echo recovery=$?
+cp studies/recovery_r1.md gpurun_out/recovery_r1.md 2>/dev/null; tail -12 gpurun_out/recovery.log
