@@ -93,6 +93,76 @@ __global__ void __launch_bounds__(256) k3_fill(Tables t, BinSet bs, float dil)
     if (ovf) atomicOr(t.status, BLUR_ST_EOVERFLOW);
 }
 
+// Shared-memory variants (images with <= K3_SMEM_TILES tiles): a CTA takes K3_FPB faces of one
+// chunk and counts their tiles in a shared histogram, so that the global atomics are one per
+// (CTA, touched tile) instead of one per (face, tile) entry; the fill reserves each touched tile's
+// range with one global atomic and places the entries with shared cursors.
+constexpr int K3_FPB = 1024;
+constexpr int K3_SMEM_TILES = 4096;
+
+__global__ void __launch_bounds__(256) k3_count_s(Tables t, BinSet bs, float dil)
+{
+    extern __shared__ int hist[];   // [T]
+    const int c = blockIdx.y, T = t.T;
+    for (int i = threadIdx.x; i < T; i += 256) hist[i] = 0;
+    __syncthreads();
+    const Chunk ch = t.chunks[c];
+    const ImgInfo &im = t.imgs[ch.b];
+    const int f1 = min(t.F, (int)(blockIdx.x + 1) * K3_FPB);
+    for (int f = blockIdx.x * K3_FPB + threadIdx.x; f < f1; f += 256) {
+        const float4 *r = t.rec + (size_t)(im.rec_off + (long long)ch.s * t.F + f) * REC_F4;
+        int tx0, tx1, ty0, ty1;
+        if (!swept_tiles(t, r, ch.tmin, ch.tmax, dil, tx0, tx1, ty0, ty1)) continue;
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(hist + ty * t.TX + tx, 1);
+    }
+    __syncthreads();
+    int *cnt = bs.cnt + (size_t)c * T;
+    for (int i = threadIdx.x; i < T; i += 256)
+        if (hist[i]) atomicAdd(cnt + i, hist[i]);
+}
+
+__global__ void __launch_bounds__(256) k3_fill_s(Tables t, BinSet bs, float dil)
+{
+    extern __shared__ long long sbase[];   // [T] global start of this CTA's range per tile, then [T] ints
+    const int c = blockIdx.y, T = t.T;
+    int *hist = reinterpret_cast<int *>(sbase + T);
+    for (int i = threadIdx.x; i < T; i += 256) hist[i] = 0;
+    __syncthreads();
+    const Chunk ch = t.chunks[c];
+    const ImgInfo &im = t.imgs[ch.b];
+    const int f1 = min(t.F, (int)(blockIdx.x + 1) * K3_FPB);
+    for (int f = blockIdx.x * K3_FPB + threadIdx.x; f < f1; f += 256) {
+        const float4 *r = t.rec + (size_t)(im.rec_off + (long long)ch.s * t.F + f) * REC_F4;
+        int tx0, tx1, ty0, ty1;
+        if (!swept_tiles(t, r, ch.tmin, ch.tmax, dil, tx0, tx1, ty0, ty1)) continue;
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(hist + ty * t.TX + tx, 1);
+    }
+    __syncthreads();
+    const size_t base = (size_t)c * T;
+    for (int i = threadIdx.x; i < T; i += 256) {
+        const int h = hist[i];
+        if (h) sbase[i] = bs.off[base + i] + atomicAdd(bs.cnt + base + i, h);
+        hist[i] = 0;
+    }
+    __syncthreads();
+    bool ovf = false;
+    for (int f = blockIdx.x * K3_FPB + threadIdx.x; f < f1; f += 256) {
+        const float4 *r = t.rec + (size_t)(im.rec_off + (long long)ch.s * t.F + f) * REC_F4;
+        int tx0, tx1, ty0, ty1;
+        if (!swept_tiles(t, r, ch.tmin, ch.tmax, dil, tx0, tx1, ty0, ty1)) continue;
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) {
+                const int ti = ty * t.TX + tx;
+                const long long pos = sbase[ti] + atomicAdd(hist + ti, 1);
+                if (pos < bs.cap) bs.entries[pos] = f;
+                else ovf = true;
+            }
+    }
+    if (ovf) atomicOr(t.status, BLUR_ST_EOVERFLOW);
+}
+
 // ---- exclusive scan of cnt[0..n) into off[0..n], off[n] = total (3 kernels, 1024 per block)
 __device__ __forceinline__ int block_excl_scan_1024(int v[4], int *sm)
 {
@@ -269,9 +339,15 @@ cudaError_t launch_binning(const Tables &t, const BinSet &bs, float dil, cudaStr
     if (nbins == 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(bs.cnt, 0, sizeof(int) * (size_t)nbins, st);
     if (e != cudaSuccess) return e;
+    const bool shm = t.T <= K3_SMEM_TILES;
     if (t.F > 0) {
-        dim3 grid((t.F + 255) / 256, t.NC);
-        k3_count<<<grid, 256, 0, st>>>(t, bs, dil);
+        if (shm) {
+            dim3 grid((t.F + K3_FPB - 1) / K3_FPB, t.NC);
+            k3_count_s<<<grid, 256, sizeof(int) * t.T, st>>>(t, bs, dil);
+        } else {
+            dim3 grid((t.F + 255) / 256, t.NC);
+            k3_count<<<grid, 256, 0, st>>>(t, bs, dil);
+        }
     }
     const int nb = (nbins + 1023) / 1024;
     k3_scan_blocks<<<nb, 256, 0, st>>>(bs.cnt, bs.off, bs.bsum, nbins);
@@ -280,8 +356,16 @@ cudaError_t launch_binning(const Tables &t, const BinSet &bs, float dil, cudaStr
     e = cudaMemsetAsync(bs.cnt, 0, sizeof(int) * (size_t)nbins, st);
     if (e != cudaSuccess) return e;
     if (t.F > 0) {
-        dim3 grid((t.F + 255) / 256, t.NC);
-        k3_fill<<<grid, 256, 0, st>>>(t, bs, dil);
+        if (shm) {
+            const size_t smem = (sizeof(long long) + sizeof(int)) * t.T;
+            e = cudaFuncSetAttribute(k3_fill_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            dim3 grid((t.F + K3_FPB - 1) / K3_FPB, t.NC);
+            k3_fill_s<<<grid, 256, smem, st>>>(t, bs, dil);
+        } else {
+            dim3 grid((t.F + 255) / 256, t.NC);
+            k3_fill<<<grid, 256, 0, st>>>(t, bs, dil);
+        }
         int sb = (nbins + 7) / 8;
         if (sb > 148 * 16) sb = 148 * 16;
         if (bs.sortcap > 0) k3_sort<<<sb, 256, 0, st>>>(t, bs, nbins);
