@@ -73,6 +73,14 @@ def check_parity(sc, ids_k=0, mode="binned", max_chunk=0, sub_range=None, grad=T
     return out
 
 
+def test_large_image_global_binning_path():
+    """Images with more than 4096 tiles take K3's global-atomic count/fill (the shared-histogram
+    variants need the tile counters in shared memory): 1100 x 1040 pixels = 69 x 65 tiles."""
+    sc = scenes.random_mesh_scene(40, 17, H=1040, W=1100, motion=scenes.translate((0.6, -0.2, 0.1), N=3))
+    r = check_parity(sc, ids_k=1)
+    print(r)
+
+
 def test_c1_full_brute():
     r = check_parity(scenes.make_c1(), ids_k=3, mode="brute")
     print(r)
