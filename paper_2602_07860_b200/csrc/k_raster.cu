@@ -41,13 +41,13 @@ __device__ __forceinline__ int fp_of(int warp, int lane) { return BR_HALF ? warp
 #define BR_SREC_F 512
 #endif
 #ifndef BR_SREC_B
-#define BR_SREC_B 384
+#define BR_SREC_B 256
 #endif
 #ifndef BR_GMAX_F
 #define BR_GMAX_F 16
 #endif
 #ifndef BR_GMAX_B
-#define BR_GMAX_B 8
+#define BR_GMAX_B 4
 #endif
 #ifndef BR_K4_MINB
 #define BR_K4_MINB 5

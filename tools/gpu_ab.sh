@@ -1,5 +1,4 @@
-# scratch A/B driver (edited per experiment)
+# scratch driver (edited per experiment)
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-CONFIGS="C4 C3 C2" bash tools/ab_variants.sh
-CONFIGS="C4" bash tools/ab_variants.sh
+timeout 600 python bench.py 2>&1 | tail -1 | cut -c1-300
