@@ -1,4 +1,3 @@
-# scratch driver (edited per experiment)
+# scratch A/B driver (edited per experiment)
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 600 python bench.py 2>&1 | tail -1 | cut -c1-300
+CONFIGS="C4 C3" bash tools/ab_variants.sh
