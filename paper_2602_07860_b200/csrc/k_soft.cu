@@ -765,8 +765,9 @@ struct SoftBwdCSmem {
     uint32_t need[GMAX_S][SNW];
     float ga[NPX];
     float acc[SREC_B9][12];    // per bin slot: d/d keyframe s (corners x, y), then keyframe s+1
+    unsigned short items[GMAX_S * SNW * (SREC_B9 / 32)];   // non-empty work items: (l * SNW + w) << 4 | batch
     float taus[GMAX_S];
-    int head2;
+    int head2, nitems;
 };
 
 // K9C: the soft backward of the bins whose dalpha/dA products K8 left in t.spz (BLUR_CACHE_VISIBILITY):
@@ -804,7 +805,7 @@ __global__ void __launch_bounds__(NT, BR_K9C_MINB) k9c_soft_bwd(Tables t, const 
             for (int l = 0; l < ng; ++l) load_need(t, im, kg + l, tile, warp, lane, want, &S.need[l][warp]);
             for (int i = threadIdx.x; i < ng * SNW * nw; i += NT) S.wm[i] = 0u;
             if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[im.sched_off + kg + threadIdx.x];
-            if (threadIdx.x == 0) S.head2 = 0;
+            if (threadIdx.x == 0) { S.head2 = 0; S.nitems = 0; }
             __syncthreads();
             uint32_t anyn = 0u;
             for (int l = 0; l < ng; ++l)
@@ -814,11 +815,22 @@ __global__ void __launch_bounds__(NT, BR_K9C_MINB) k9c_soft_bwd(Tables t, const 
                 touched = true;
                 soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, nullptr, S.rec, S.wm, dummy);
                 __syncthreads();
-                for (int it = next_item(&S.head2, ng * SNW * nw, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
-                    nx = next_item(&S.head2, ng * SNW * nw, lane);
-                    const int bt = it % nw, lw = it / nw, l = lw / SNW, w = lw - l * SNW;
-                    if (!S.need[l][w]) continue;
-                    soft_grad_faces(S, S.rec + l * n, S.wm + (l * SNW + w) * nw, nw, bt, l, w, lane, tc, kexp, c2,
+                // list the non-empty items (sub-frame, footprint, batch of 32 masked faces)
+                for (int lw = warp; lw < ng * SNW; lw += SNW) {
+                    if (!S.need[0][lw]) continue;   // need[l][w] == need[0][lw]
+                    const unsigned cnt = lane < nw ? __popc(S.wm[lw * nw + lane]) : 0u;
+                    const int nb = (int)((__reduce_add_sync(0xffffffffu, cnt) + 31u) >> 5);
+                    int base = 0;
+                    if (lane == 0 && nb) base = atomicAdd(&S.nitems, nb);
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (lane < nb) S.items[base + lane] = (unsigned short)((lw << 4) | lane);
+                }
+                __syncthreads();
+                const int nit = S.nitems;
+                for (int it = next_item(&S.head2, nit, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+                    nx = next_item(&S.head2, nit, lane);
+                    const int v = S.items[it], lw = v >> 4, l = lw / SNW, w = lw - l * SNW;
+                    soft_grad_faces(S, S.rec + l * n, S.wm + lw * nw, nw, v & 15, l, w, lane, tc, kexp, c2,
                                     t.spz + ((size_t)(im.cov_off + kg + l) * t.T + tile) * NPX);
                 }
             }
