@@ -535,7 +535,8 @@ struct SoftBwdSmem {
     int sid[SREC_B9];
     float taus[GMAX_S];
     int wsum[SNW];
-    int head, head2;
+    unsigned short items[SNW * (SREC_B9 / 32)];   // long path: non-empty items w << 4 | batch
+    int head, head2, nitems;
 };
 
 __device__ __forceinline__ void soft_flush(const Tables &t, const ImgInfo &im, int s, int f, const float *a)
@@ -944,15 +945,24 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
                         if (nb == 0) break;
                         const int nw = (nb + 31) >> 5;
                         for (int i = threadIdx.x; i < SNW * nw; i += NT) S.wm[i] = 0u;
-                        if (threadIdx.x == 0) S.head2 = 0;
+                        if (threadIdx.x == 0) { S.head2 = 0; S.nitems = 0; }
                         __syncthreads();
                         soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy);
                         __syncthreads();
-                        for (int it = next_item(&S.head2, SNW * nw, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
-                            nx = next_item(&S.head2, SNW * nw, lane);
-                            const int bt = it % nw, w = it / nw;
-                            if (!S.need[0][w]) continue;
-                            soft_grad_faces(S, S.rec, S.wm + w * nw, nw, bt, 0, w, lane, tc, kexp, c2, pzc);
+                        if (S.need[0][warp]) {   // this warp lists its footprint's non-empty batches
+                            const unsigned cnt = lane < nw ? __popc(S.wm[warp * nw + lane]) : 0u;
+                            const int nbt = (int)((__reduce_add_sync(0xffffffffu, cnt) + 31u) >> 5);
+                            int b0 = 0;
+                            if (lane == 0 && nbt) b0 = atomicAdd(&S.nitems, nbt);
+                            b0 = __shfl_sync(0xffffffffu, b0, 0);
+                            if (lane < nbt) S.items[b0 + lane] = (unsigned short)((warp << 4) | lane);
+                        }
+                        __syncthreads();
+                        const int nit = S.nitems;
+                        for (int it = next_item(&S.head2, nit, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+                            nx = next_item(&S.head2, nit, lane);
+                            const int v = S.items[it], w = v >> 4;
+                            soft_grad_faces(S, S.rec, S.wm + w * nw, nw, v & 15, 0, w, lane, tc, kexp, c2, pzc);
                         }
                         __syncthreads();
                         flush_slots(S, t, im, ch.s, nb, sb.fb ? S.sid : sb.ent + base);
