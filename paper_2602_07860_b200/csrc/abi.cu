@@ -13,6 +13,9 @@
 #ifndef BR_HARD_SPLITS
 #define BR_HARD_SPLITS 2   // hard raster: at least 2 CTAs per (image, tile) when it has 2+ chunks (C4 -1%)
 #endif
+#ifndef BR_K8_CUT
+#define BR_K8_CUT 18.f     // K8's cut in units of delta (see rcut_f)
+#endif
 #ifndef BR_SOFT_SPLITS
 #define BR_SOFT_SPLITS 8   // soft kernels: up to 8 CTAs per (image, tile), each taking every 8th chunk
 #endif
@@ -91,7 +94,7 @@ struct Plan {
     size_t o_key = 0, o_rec = 0, o_fcol = 0, o_cnt = 0, o_off = 0, o_bsum = 0, o_ent = 0, o_dkey = 0, o_part = 0;
     // soft background coverage (NEXT-1)
     bool soft = false;
-    float delta = 0.f, rcut = 0.f;
+    float delta = 0.f, rcut = 0.f, rcut_f = 0.f;
     int soft_exact = 0;
     long long scap = 0, n_sub = 0;
     size_t o_cov = 0, o_spart = 0, o_scnt = 0, o_soff = 0, o_sbsum = 0, o_sent = 0;
@@ -268,6 +271,9 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
         P.soft = true;
         P.delta = cfg->delta;
         P.rcut = (float)std::sqrt((double)kc * (double)cfg->delta) + 2.0f * BBOX_PAD;
+        // K8's own radius: a face at d >= 18 delta from a pixel has A = exp(-d / delta) < 2^-25, so
+        // its factor 1 - A rounds to exactly 1.0f and dropping it leaves the products bit-identical
+        P.rcut_f = (float)std::sqrt((double)std::min(kc, BR_K8_CUT) * (double)cfg->delta) + 2.0f * BBOX_PAD;
         P.soft_exact = cfg->soft_exact ? 1 : 0;
         const double sf = cfg->soft_bin_factor > 0.f ? cfg->soft_bin_factor : 12.0;
         double sc = sf * (double)P.NC * (double)F + 16.0 * (double)P.T;
@@ -344,6 +350,7 @@ Tables make_tables(const Plan &P, void *ws)
     if (P.soft) {
         t.delta = P.delta;
         t.rcut = P.rcut;
+        t.rcut_f = P.rcut_f;
         t.soft_exact = P.soft_exact;
         t.covbits = (uint32_t *)(w + P.o_cov);
         t.spart = (float *)(w + P.o_spart);

@@ -93,6 +93,7 @@ struct Tables {          // device pointers into the workspace
     // soft background coverage (NEXT-1; delta > 0)
     float delta;         // Eq.10 bandwidth (NDC^2)
     float rcut;          // NDC radius beyond which a face's term is dropped: sqrt(soft_cut * delta)
+    float rcut_f;        // the forward's radius sqrt(min(soft_cut, 18) delta): farther factors are 1.0f
     int soft_exact;      // 1: Eq.12 (closest point on F(tau)) instead of Eq.13 (on F(X))
     uint32_t *covbits;   // [sum_b N_b][T][NWARP] coverage ballots per (sub-frame, tile, warp) or null
     uint16_t *vis;       // [sum_b N_b][T][TW*TH] winning bin slot per (sub-frame, pixel), 0xFFFF none;

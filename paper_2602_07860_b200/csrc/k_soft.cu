@@ -71,10 +71,11 @@ constexpr int GMAX_S = 8;        // sub-frames staged together
 constexpr int NPX = TW * TH;
 
 struct __align__(16) SoftRec {
-    // q0: a1 b1 g1 a2 | q1: b2 g2 k01 r01 | q2: c1 c2 k20 r20 | q3: E1x E1y E2x E2y of F(X)
+    // q0: a1 b1 g1 a2 | q1: b2 g2 v0x r01 | q2: c1 c2 v0y r20 | q3: E1x E1y E2x E2y of F(X)
     // q4: E1x E1y E2x E2y of F(tau)
     //   w_i = a_i ul + b_i vl + g_i (i = 1, 2; fast solver at tau, tile-local pixel coordinates)
-    //   t01 = sat(k01 w1 + r01 w2), t12 = sat(c1 (w1 - 1) + c2 w2), t20 = sat(k20 (1 - w2) - r20 w1)
+    //   t01 = sat(w1 + r01 w2), t12 = sat(c1 (w1 - 1) + c2 w2), t20 = sat((1 - w2) - r20 w1); a zero-length
+    //   edge of F(X) has r = NaN, which sat() flushes to t = 0 (Q19); (v0x, v0y) = v0 of F(tau), tile-local
     float4 q[5];
 };
 
@@ -198,14 +199,14 @@ __device__ __forceinline__ void soft_bin(const Tables &t, const ImgInfo &im, con
 __device__ __forceinline__ uint32_t soft_stage(const Tables &t, const float4 *__restrict__ r,
                                                const float4 *__restrict__ key0, const float4 *__restrict__ key1,
                                                int f, float tau, const STile &tc, const uint32_t *need,
-                                               SoftRec &out)
+                                               float rcut, SoftRec &out)
 {
     const float4 q6 = __ldg(r + 6);
     if (__float_as_int(q6.w) < 0) return 0u;                             // skipped face
     const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);   // det F(tau) (Eq.8 a-coefficients)
     if (!(fabsf(D) > EPS_D)) return 0u;                                 // Q8
     int x0, x1, y0, y1;
-    if (!grown_box(r, tau, t.rcut, t.W, t.H, tc, x0, x1, y0, y1)) return 0u;
+    if (!grown_box(r, tau, rcut, t.W, t.H, tc, x0, x1, y0, y1)) return 0u;
     const float sg = D < 0.f ? -1.f : 1.f;
     float A[3], B[3], G[3];
 #pragma unroll
@@ -223,7 +224,7 @@ __device__ __forceinline__ uint32_t soft_stage(const Tables &t, const float4 *__
     float thr[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
-        thr[i] = t.rcut * sqrtf(A[i] * A[i] + B[i] * B[i]) +
+        thr[i] = rcut * sqrtf(A[i] * A[i] + B[i] * B[i]) +
                  1e-5f * (fabsf(A[i]) * (8.f * tc.sx) + fabsf(B[i]) * (8.f * tc.sy) + fabsf(G[i])) + 1e-30f;
     uint32_t fm = 0u;
     for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
@@ -253,22 +254,22 @@ __device__ __forceinline__ uint32_t soft_stage(const Tables &t, const float4 *__
     const float e3x = xX[2] - xX[1], e3y = yX[2] - yX[1];
     const float g11 = e1x * e1x + e1y * e1y, g22 = e2x * e2x + e2y * e2y, g12 = e1x * e2x + e1y * e2y;
     const float l12 = e3x * e3x + e3y * e3y;
-    const float k01 = g11 > 0.f ? 1.f : 0.f, r01 = g11 > 0.f ? g12 / g11 : 0.f;
-    const float k20 = g22 > 0.f ? 1.f : 0.f, r20 = g22 > 0.f ? g12 / g22 : 0.f;
+    const float r01 = g11 > 0.f ? g12 / g11 : __int_as_float(0x7fffffff);
+    const float r20 = g22 > 0.f ? g12 / g22 : __int_as_float(0x7fffffff);
     const float c1 = l12 > 0.f ? (e1x * e3x + e1y * e3y) / l12 : 0.f;
     const float c2 = l12 > 0.f ? (e2x * e3x + e2y * e3y) / l12 : 0.f;
     out.q[0] = make_float4(A[1] * invD, B[1] * invD, G[1] * invD, A[2] * invD);
-    out.q[1] = make_float4(B[2] * invD, G[2] * invD, k01, r01);
-    out.q[2] = make_float4(c1, c2, k20, r20);
+    out.q[1] = make_float4(B[2] * invD, G[2] * invD, __fsub_rn(xT[0], tc.uc), r01);
+    out.q[2] = make_float4(c1, c2, __fsub_rn(yT[0], tc.vc), r20);
     out.q[3] = make_float4(e1x, e1y, e2x, e2y);
     out.q[4] = make_float4(xT[1] - xT[0], yT[1] - yT[0], xT[2] - xT[0], yT[2] - yT[0]);   // F(tau)
     return fm;
 }
 
 // One (pixel, face, tau) term: d (Eq.14), the chosen edge e (corners e, (e+1)%3) with parameter t,
-// and the residual Delta = w - w^* in the (E1, E2) basis.
+// and the residual r = p - F(tau) w^* (Eq.14's vector).
 struct SoftHit {
-    float d, t, d1, d2;
+    float d, t, rx, ry;
     int e;
 };
 
@@ -285,25 +286,29 @@ __device__ __forceinline__ SoftHit soft_eval(const SoftRec &r, float ul, float v
     const float w1 = __fmaf_rn(q0.x, ul, __fmaf_rn(q0.y, vl, q0.z));   // w(tau), Eq.8
     const float w2 = __fmaf_rn(q0.w, ul, __fmaf_rn(q1.x, vl, q1.y));
     SoftHit h;
+    // the closest point of p' = F(X) w on F(X) (A17-A18): residual Delta = w - w^* in the (E1, E2) basis
     // edge v0v1: w^* = (1 - t, t, 0)
-    float tt = __saturatef(__fmaf_rn(w1, q1.z, w2 * q1.w));
-    float d1 = w1 - tt, d2 = w2;
-    float best = resid2(d1, d2, q3);
-    h.t = tt; h.d1 = d1; h.d2 = d2; h.e = 0;
+    float tt = __saturatef(__fmaf_rn(w2, q1.w, w1));
+    float best = resid2(w1 - tt, w2, q3);
+    h.t = tt; h.e = 0;
     // edge v1v2: w^* = (0, 1 - t, t)
     const float w1m = w1 - 1.f;
     tt = __saturatef(__fmaf_rn(w1m, q2.x, w2 * q2.y));
-    d1 = w1m + tt; d2 = w2 - tt;
-    float qq = resid2(d1, d2, q3);
-    if (qq < best) { best = qq; h.t = tt; h.d1 = d1; h.d2 = d2; h.e = 1; }
+    float qq = resid2(w1m + tt, w2 - tt, q3);
+    if (qq < best) { best = qq; h.t = tt; h.e = 1; }
     // edge v2v0: w^* = (t, 0, 1 - t)
     const float w2m = w2 - 1.f;
-    tt = __saturatef(__fmaf_rn(-w1, q2.w, -w2m * q2.z));
-    d1 = w1; d2 = w2m + tt;
-    qq = resid2(d1, d2, q3);
-    if (qq < best) { h.t = tt; h.d1 = d1; h.d2 = d2; h.e = 2; }
-    // Eq.14: || F(tau) Delta ||^2
-    h.d = resid2(h.d1, h.d2, r.q[4]);
+    tt = __saturatef(__fmaf_rn(-w1, q2.w, -w2m));
+    qq = resid2(w1, w2m + tt, q3);
+    if (qq < best) { h.t = tt; h.e = 2; }
+    // Eq.14: d = || p - F(tau) w^* ||^2, formed from the pixel itself (F(tau) Delta equals it, but for a
+    // far pixel of a sliver face w is ill-conditioned and F(tau) w no longer reproduces p in fp32)
+    const float4 q4 = r.q[4];
+    const float ws1 = h.e == 0 ? h.t : (h.e == 1 ? 1.f - h.t : 0.f);
+    const float ws2 = h.e == 0 ? 0.f : (h.e == 1 ? h.t : 1.f - h.t);
+    h.rx = __fsub_rn(ul, q1.z) - __fmaf_rn(ws1, q4.x, ws2 * q4.z);
+    h.ry = __fsub_rn(vl, q2.z) - __fmaf_rn(ws1, q4.y, ws2 * q4.w);
+    h.d = __fmaf_rn(h.rx, h.rx, h.ry * h.ry);
     return h;
 }
 
@@ -312,7 +317,7 @@ __device__ __forceinline__ SoftHit soft_eval(const SoftRec &r, float ul, float v
 template <bool CENSUS>
 __device__ __forceinline__ void soft_stage_group(const Tables &t, const SoftBin &sb, int nb, int base, const float *taus,
                                                  int ng, const STile &tc, const uint32_t (*need)[SNW], const int *sid,
-                                                 SoftRec *rec, uint32_t *wm, unsigned long long &nstage)
+                                                 SoftRec *rec, uint32_t *wm, unsigned long long &nstage, float rcut)
 {
     const int nw = (nb + 31) >> 5;
     for (int p = threadIdx.x; p < nb * ng; p += NT) {
@@ -327,7 +332,7 @@ __device__ __forceinline__ void soft_stage_group(const Tables &t, const SoftBin 
             continue;
         }
         const uint32_t fm = soft_stage(t, sb.rseg + (size_t)f * REC_F4, sb.key0, sb.key1, f, taus[l], tc, need[l],
-                                       rec[l * nb + j]);
+                                       rcut, rec[l * nb + j]);
         if (CENSUS) nstage += fm != 0u;
         const uint32_t bit = 0x80000000u >> (j & 31);
         for (uint32_t m = fm; m; m &= m - 1) atomicOr(wm + (l * SNW + (__ffs(m) - 1)) * nw + (j >> 5), bit);
@@ -423,7 +428,7 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[im.sched_off + kg + threadIdx.x];
                 if (threadIdx.x == 0) S.head = 0;
                 __syncthreads();
-                soft_stage_group<CENSUS>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, nstage);
+                soft_stage_group<CENSUS>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, nstage, t.rcut_f);
                 __syncthreads();
                 for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
                     nx = next_item(&S.head, ng * SNW, lane);
@@ -470,7 +475,7 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
                     for (int i = threadIdx.x; i < SNW * nw; i += NT) S.wm[i] = 0u;
                     if (threadIdx.x == 0) S.head = 0;
                     __syncthreads();
-                    soft_stage_group<CENSUS>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, nstage);
+                    soft_stage_group<CENSUS>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, nstage, t.rcut_f);
                     __syncthreads();
                     for (int it = next_item(&S.head, SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
                         nx = next_item(&S.head, SNW, lane);
@@ -616,12 +621,11 @@ __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *re
                 const float A = __expf(-h.d * kexp);
                 const float fac = 1.0f - A;
                 const float dadA = z == 0 ? pz / fac : (fac == 0.f ? pz : 0.f);
-                // dL/dv_i(tau) = G_a dalpha/dA (A / delta) 2 w^*_i (p - F(tau) w^*), p - F(tau) w^* = F(tau) Delta
+                // dL/dv_i(tau) = G_a dalpha/dA (A / delta) 2 w^*_i (p - F(tau) w^*)
                 const float cc = ga * dadA * A * c2;
                 if (cc != 0.f) {
-                    const float4 q4 = r.q[4];
-                    const float gx = cc * __fmaf_rn(h.d1, q4.x, h.d2 * q4.z);
-                    const float gy = cc * __fmaf_rn(h.d1, q4.y, h.d2 * q4.w);
+                    const float gx = cc * h.rx;
+                    const float gy = cc * h.ry;
                     const int ia = h.e, ib = h.e == 2 ? 0 : h.e + 1;
                     const float wa = 1.f - h.t, wb = h.t;
 #pragma unroll
@@ -731,11 +735,10 @@ __device__ __forceinline__ void soft_grad_faces(Sm &S, const SoftRec *rec, const
         const float fac = 1.0f - A;
         // dalpha/dA_j = prod_{l != j} (1 - A_l)
         const float dadA = zq == 0 ? __fdividef(pzq, fac) : (fac == 0.f ? pzq : 0.f);
-        // dL/dv_i(tau) = G_a dalpha/dA (A / delta) 2 w^*_i F(tau) Delta
+        // dL/dv_i(tau) = G_a dalpha/dA (A / delta) 2 w^*_i (p - F(tau) w^*)
         const float cc = cq * dadA * A;
-        const float4 q4 = r.q[4];
-        const float gx = cc * __fmaf_rn(h.d1, q4.x, h.d2 * q4.z);
-        const float gy = cc * __fmaf_rn(h.d1, q4.y, h.d2 * q4.w);
+        const float gx = cc * h.rx;
+        const float gy = cc * h.ry;
         const float wa = 1.f - h.t, wb = h.t;
         // corners (e, e + 1 mod 3) of the chosen edge get weights (1 - t, t)
         const float w0 = h.e == 0 ? wa : (h.e == 2 ? wb : 0.f);
@@ -814,7 +817,7 @@ __global__ void __launch_bounds__(NT, BR_K9C_MINB) k9c_soft_bwd(Tables t, const 
                 for (int w = 0; w < SNW; ++w) anyn |= S.need[l][w];
             if (anyn) {   // block-uniform
                 touched = true;
-                soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, nullptr, S.rec, S.wm, dummy);
+                soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, nullptr, S.rec, S.wm, dummy, t.rcut);
                 __syncthreads();
                 // list the non-empty items (sub-frame, footprint, batch of 32 masked faces)
                 for (int lw = warp; lw < ng * SNW; lw += SNW) {
@@ -885,7 +888,7 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
                     for (int w = 0; w < SNW; ++w) anyn |= S.need[l][w];
                 if (anyn) {   // block-uniform
                     touched = true;
-                    soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, dummy);
+                    soft_stage_group<false>(t, sb, n, 0, S.taus, ng, tc, S.need, S.sid, S.rec, S.wm, dummy, t.rcut);
                     __syncthreads();
 #if BR_K9_SPLIT
                     for (int it = next_item(&S.head, ng * SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
@@ -947,7 +950,7 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
                         for (int i = threadIdx.x; i < SNW * nw; i += NT) S.wm[i] = 0u;
                         if (threadIdx.x == 0) { S.head2 = 0; S.nitems = 0; }
                         __syncthreads();
-                        soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy);
+                        soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy, t.rcut);
                         __syncthreads();
                         if (S.need[0][warp]) {   // this warp lists its footprint's non-empty batches
                             const unsigned cnt = lane < nw ? __popc(S.wm[warp * nw + lane]) : 0u;
@@ -979,7 +982,7 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
                     for (int i = threadIdx.x; i < SNW * nw; i += NT) S.wm[i] = 0u;
                     if (threadIdx.x == 0) S.head = 0;
                     __syncthreads();
-                    soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy);
+                    soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy, t.rcut);
                     __syncthreads();
                     for (int it = next_item(&S.head, SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
                         nx = next_item(&S.head, SNW, lane);
@@ -1006,7 +1009,7 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
                     for (int i = threadIdx.x; i < SNW * nw; i += NT) S.wm[i] = 0u;
                     if (threadIdx.x == 0) S.head = 0;
                     __syncthreads();
-                    soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy);
+                    soft_stage_group<false>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, dummy, t.rcut);
                     __syncthreads();
                     for (int it = next_item(&S.head, SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
                         nx = next_item(&S.head, SNW, lane);

@@ -120,6 +120,21 @@ def test_soft_c3_sampled_pixels_full_size():
     assert ok.sum() > 0.8 * len(pick) and err[ok].max() < TOL_IMG
 
 
+def test_soft_far_sliver_window_c3():
+    """Regression pin: on C3 view 0 around pixel (260, 98) a sliver face about 2.5 delta^(1/2) away
+    had its Eq.14 distance formed as F(tau) Delta from ill-conditioned barycentrics, and fp32 lost
+    it (alpha off by 2e-4).  The kernels now form p - F(tau) w^* from the pixel itself."""
+    sc = scenes.make_c3()
+    got = gpu_soft(sc, 1e-4)
+    ys, xs = np.meshgrid(np.arange(254, 268), np.arange(90, 108), indexing="ij")
+    pick = np.stack([np.zeros(ys.size, int), ys.ravel(), xs.ravel()], 1)
+    ref = oracle.render_fwd(sc, pixels=pick, eps_amb=1e-6, delta=1e-4)
+    ok = ~ref["amb_img"]
+    err = np.abs(got["rgba"][pick[:, 0], pick[:, 1], pick[:, 2]] - ref["rgba"])
+    print("window", len(pick), "max err", err[ok].max(), "flagged", int((~ok).sum()))
+    assert ok.sum() > 0.8 * len(pick) and err[ok].max() < TOL_IMG
+
+
 def test_soft_backward_without_reuse_and_delta_zero():
     """The backward recomputes coverage when the forward's workspace is not reused; delta = 0 is
     the hard path exactly."""
