@@ -36,7 +36,7 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 # backward's extra work per covered (pixel, sub-frame)
 FLOP_PAIR, FLOP_SHADE, FLOP_SETUP, FLOP_BWD = 18.0, 25.0, 30.0, 100.0
 # soft background coverage (NEXT-1): flop per evaluated (pixel, face, sub-frame) term (census [4]: the
-# terms K8 evaluates, within 18 delta; K9 evaluates those within 24 delta, so its fraction is understated)
+# terms K8 evaluates, within 18 delta: the default cut-off of both kernels)
 # in the forward
 # (w1, w2: 8; three projections + quadratic forms: 3 x 12; Eq.14 form + exp + product: 10) and in
 # the backward (pass 1 the same, pass 2 the same + 16 for the gradient and its keyframe split; with

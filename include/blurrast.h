@@ -144,7 +144,8 @@ typedef struct {
      * Needs solver 0.  delta = 0: hard coverage only (alpha = coverage, the delta -> 0 limit). */
     float delta;
     float soft_cut;                /* faces with d > soft_cut * delta are dropped (their term is below
-                                      exp(-soft_cut)); 0 = default 24 (Q21) */
+                                      exp(-soft_cut)); 0 = default 18: beyond it the forward's fp32
+                                      factor 1 - A is exactly 1 (Q21) */
     int32_t soft_exact;            /* 1: Eq.12 (closest point on F(tau) itself) instead of Eq.13 */
     float soft_bin_factor;         /* soft-bin entry capacity per (chunk, face) (0 = default 12); see
                                       blur_read_soft_bins */

@@ -266,7 +266,7 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
     if (cfg && cfg->delta != 0.f) {
         if (!(cfg->delta > 0.f) || !std::isfinite(cfg->delta)) return fail(BLUR_EINVAL, "delta must be >= 0 and finite");
         if (cfg->solver != 0) return fail(BLUR_EINVAL, "soft coverage (delta > 0) needs solver 0");
-        const float kc = cfg->soft_cut > 0.f ? cfg->soft_cut : 24.f;
+        const float kc = cfg->soft_cut > 0.f ? cfg->soft_cut : 18.f;
         if (!std::isfinite(kc)) return fail(BLUR_EINVAL, "soft_cut must be finite");
         P.soft = true;
         P.delta = cfg->delta;

@@ -4,8 +4,9 @@ vs the fp64 oracle on the same seeded inputs.
 Bars as for the hard path (BASELINE north_star): blurred RGBA within 1e-4 max-abs on the pixels the
 oracle does not flag (Q16 coverage ambiguity, Q20 closest-edge ties), vertex gradients within 1e-3
 relative L2 with the same upstream G on both sides (zeroed at flagged pixels, Q18).  The oracle
-sums every face (no cut-off); the GPU drops faces with d > 24 delta (Q21): that changes alpha by at
-most (faces dropped) x exp(-24) < 1e-9 here.
+sums every face (no cut-off); the GPU drops faces with d > 18 delta (Q21): there A < 2^-25, so the
+forward's fp32 factors 1 - A are exactly 1 and the image is unchanged; the backward's dropped terms
+are below exp(-18) relative.
 """
 import numpy as np
 import pytest
