@@ -12,43 +12,50 @@ namespace br {
 // vertex left most SMs idle).
 __global__ void __launch_bounds__(256) k7_vertex_chain(Tables t, float *__restrict__ gv)
 {
-    const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (v >= t.V) return;
+    // CTA = 32 vertices (lanes, so the dkey / key loads of one (image, keyframe) are coalesced) x 8 warps
+    // sharing the (image, keyframe) terms round-robin; the warps' fp64 partials are summed in a fixed
+    // order (deterministic)
+    __shared__ double part[8][3][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int v = blockIdx.x * 32 + lane;
     double acc[3] = {0.0, 0.0, 0.0};
-    int q = 0;   // running index of the (image, keyframe) term
-    for (int b = 0; b < t.B; ++b) {
-        const ImgInfo &im = t.imgs[b];
-        for (int s = 0; s <= im.S; ++s, ++q) {
-            if ((q & 31) != lane) continue;
-            const size_t o = (size_t)im.key_off + (size_t)s * t.V + v;
-            const float2 g = t.dkey[o];
-            if (g.x == 0.f && g.y == 0.f) continue;
-            const float4 kq = t.key[o];
-            const double z = kq.z, iz = 1.0 / (z * im.tan_half);
-            const double dQ[3] = {g.x * iz, g.y * iz, -((double)g.x * kq.x + (double)g.y * kq.y) / z};
-            double dP[3];
+    if (v < t.V) {
+        int q = 0;   // running index of the (image, keyframe) term
+        for (int b = 0; b < t.B; ++b) {
+            const ImgInfo &im = t.imgs[b];
+            const double itan = 1.0 / im.tan_half;
+            for (int s = 0; s <= im.S; ++s, ++q) {
+                if ((q & 7) != warp) continue;
+                const size_t o = (size_t)im.key_off + (size_t)s * t.V + v;
+                const float2 g = t.dkey[o];
+                if (g.x == 0.f && g.y == 0.f) continue;
+                const float4 kq = t.key[o];
+                const double rz = 1.0 / (double)kq.z, iz = rz * itan;
+                const double dQ[3] = {g.x * iz, g.y * iz, -((double)g.x * kq.x + (double)g.y * kq.y) * rz};
+                double dP[3];
 #pragma unroll
-            for (int i = 0; i < 3; ++i) dP[i] = im.Rc[i] * dQ[0] + im.Rc[3 + i] * dQ[1] + im.Rc[6 + i] * dQ[2];
-            const PoseRec &pr = t.poses[im.pose_off + s];
+                for (int i = 0; i < 3; ++i) dP[i] = im.Rc[i] * dQ[0] + im.Rc[3 + i] * dQ[1] + im.Rc[6 + i] * dQ[2];
+                const PoseRec &pr = t.poses[im.pose_off + s];
 #pragma unroll
-            for (int i = 0; i < 3; ++i) acc[i] += pr.R[i] * dP[0] + pr.R[3 + i] * dP[1] + pr.R[6 + i] * dP[2];
+                for (int i = 0; i < 3; ++i) acc[i] += pr.R[i] * dP[0] + pr.R[3 + i] * dP[1] + pr.R[6 + i] * dP[2];
+            }
         }
     }
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 3; ++i) part[warp][i][lane] = acc[i];
+    __syncthreads();
+    if (warp < 3 && v < t.V) {   // warp i sums component i over the 8 warps in order
+        double a = 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
-    if (lane == 0) {
-        gv[3 * v] = (float)acc[0];
-        gv[3 * v + 1] = (float)acc[1];
-        gv[3 * v + 2] = (float)acc[2];
+        for (int w = 0; w < 8; ++w) a += part[w][warp][lane];
+        gv[3 * v + warp] = (float)a;
     }
 }
 
 cudaError_t launch_vertex_chain(const Tables &t, float *gv, cudaStream_t st)
 {
     if (t.V == 0) return cudaSuccess;
-    k7_vertex_chain<<<(t.V + 7) / 8, 256, 0, st>>>(t, gv);
+    k7_vertex_chain<<<(t.V + 31) / 32, 256, 0, st>>>(t, gv);
     return cudaGetLastError();
 }
 
