@@ -53,16 +53,12 @@ __device__ __forceinline__ double xcross(double ax, double ay, double bx, double
     return __fma_rn(ax, by, -__dmul_rn(ay, bx));
 }
 
-__global__ void __launch_bounds__(256) k2_face_setup(Tables t, const int *__restrict__ faces,
-                                                     const float *__restrict__ colors)
+// One (image, segment, face) record into out[0..REC_F4) (registers); skipped faces get q6.w = -1.
+__device__ __forceinline__ void face_setup(const Tables &t, const ImgInfo &im, int b, int s, int f,
+                                           const int *__restrict__ faces, const float *__restrict__ colors,
+                                           float4 *out)
 {
-    const int b = blockIdx.y;
-    const ImgInfo &im = t.imgs[b];
-    const int F = t.F, V = t.V;
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= im.S * F) return;
-    const int s = idx / F, f = idx - s * F;
-    float4 *out = t.rec + (size_t)(im.rec_off + idx) * REC_F4;
+    const int V = t.V;
     int vid[3] = {faces[3 * f], faces[3 * f + 1], faces[3 * f + 2]};
     const bool oob = vid[0] < 0 || vid[0] >= V || vid[1] < 0 || vid[1] >= V || vid[2] < 0 || vid[2] >= V;
     if (b == 0 && s == 0) {   // per-face colour/index table (image independent)
@@ -136,6 +132,33 @@ __global__ void __launch_bounds__(256) k2_face_setup(Tables t, const int *__rest
                          fmaxf(fmaxf(p1[0].y, p1[1].y), p1[2].y) + BBOX_PAD);
     out[9] = make_float4(p0[0].z, p0[1].z, p0[2].z, 0.f);
     out[10] = make_float4(p1[0].z, p1[1].z, p1[2].z, 0.f);
+}
+
+// K2: thread per (segment, face) of image blockIdx.y; each warp stages its 32 consecutive records in
+// shared memory and stores them as one contiguous run (coalesced, instead of 176-B strided stores)
+__global__ void __launch_bounds__(256) k2_face_setup(Tables t, const int *__restrict__ faces,
+                                                     const float *__restrict__ colors)
+{
+    __shared__ float4 st[8][32 * REC_F4];
+    const int b = blockIdx.y;
+    const ImgInfo &im = t.imgs[b];
+    const int F = t.F, n = im.S * F;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int base = blockIdx.x * blockDim.x + warp * 32, idx = base + lane;
+    if (base >= n) return;   // warp-uniform
+    float4 r[REC_F4];
+#pragma unroll
+    for (int q = 0; q < REC_F4; ++q) r[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (idx < n) {
+        const int s = idx / F, f = idx - s * F;
+        face_setup(t, im, b, s, f, faces, colors, r);
+    }
+#pragma unroll
+    for (int q = 0; q < REC_F4; ++q) st[warp][lane * REC_F4 + q] = r[q];
+    __syncwarp();
+    const int cnt = min(32, n - base) * REC_F4;
+    float4 *out = t.rec + (size_t)(im.rec_off + base) * REC_F4;
+    for (int k = lane; k < cnt; k += 32) out[k] = st[warp][k];
 }
 
 cudaError_t launch_setup(const Tables &t, const float *verts, const int *faces, const float *colors,
