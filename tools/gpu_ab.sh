@@ -1,4 +1,5 @@
-# scratch driver
+# scratch driver: re-run the studies with the current kernels
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for i in 1 2; do timeout 600 python bench.py --no-e2e --no-cpu-baseline 2>&1 | tail -1 | cut -c1-200; done
+for s in ablation segmentation soft_approx; do
+  timeout 1200 python studies/$s.py > gpurun_out/study_$s.md 2> gpurun_out/study_$s.err; echo $s=$?
+done
