@@ -28,6 +28,9 @@
 namespace br {
 
 constexpr int NWARP = NT / 32;
+#ifndef BR_K4_SACC
+#define BR_K4_SACC 1       // K4 keeps the pixel sums in shared memory (frees 4 registers in the hot loop)
+#endif
 #ifndef BR_HALF
 #define BR_HALF 0
 #endif
@@ -484,6 +487,9 @@ struct FwdSmem {
     int sid[SREC_F];
     float taus[GMAX_F];
     int wsum[NWARP];
+#if BR_K4_SACC
+    float4 acc[TW * TH];   // per-pixel (r, g, b, a) sums over the sub-frames (thread-private slot)
+#endif
 };
 
 template <bool CENSUS, int MODE>
@@ -506,7 +512,13 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
     const float vl = (float)(TH / 2 - ly) * tc.sy;
     const size_t pix = ((size_t)b * t.H + py) * t.W + px;
     const int myp = ly * TW + lx;
+#if BR_K4_SACC
+    S.acc[myp] = make_float4(0.f, 0.f, 0.f, 0.f);
+#define K4_ACC(pr, pg, pb) do { float4 a_ = S.acc[myp]; a_.x += (pr); a_.y += (pg); a_.z += (pb); a_.w += 1.f; S.acc[myp] = a_; } while (0)
+#else
     float ar = 0.f, ag = 0.f, ab = 0.f, aa = 0.f;
+#define K4_ACC(pr, pg, pb) do { ar += (pr); ag += (pg); ab += (pb); aa += 1.f; } while (0)
+#endif
     unsigned long long ncov = 0, ntest = 0, nshade = 0, nstage = 0;
 
     for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
@@ -561,7 +573,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                     if (ebest >= 0) {
                         float pr, pg, pb;
                         shade(rl[ebest], t.fcol, ul, vl, pr, pg, pb);      // Eq.9
-                        ar += pr; ag += pg; ab += pb; aa += 1.f;
+                        K4_ACC(pr, pg, pb);
                         fid = rl[ebest].fid;
                         if (CENSUS) nshade++;
                     }
@@ -605,7 +617,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                     base += nb;
                     __syncthreads();
                 }
-                if (has) { ar += pr; ag += pg; ab += pb; aa += 1.f; if (CENSUS) nshade++; }
+                if (has) { K4_ACC(pr, pg, pb); if (CENSUS) nshade++; }
                 if (ids && inimg && k == ids_k) ids[pix] = has ? bfid : -1;
                 if (t.covbits) {
                     const unsigned m = __ballot_sync(0xffffffffu, has || !inimg);
@@ -616,7 +628,12 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
     }
     if (inimg && out) {   // out == null: coverage-only pass (soft backward without a preceding forward)
         const float inv = 1.0f / (float)N;
+#if BR_K4_SACC
+        const float4 a = S.acc[myp];
+        const float4 v = make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
+#else
         const float4 v = make_float4(ar * inv, ag * inv, ab * inv, aa * inv);
+#endif
         if (t.splits == 1) reinterpret_cast<float4 *>(out)[pix] = v;
         else t.part[(size_t)blockIdx.z * ((size_t)t.B * t.H * t.W) + pix] = v;
     }

@@ -1,5 +1,3 @@
-# scratch driver: re-run the studies with the current kernels
+# scratch A/B driver (edited per experiment)
 mkdir -p gpurun_out
-for s in ablation segmentation soft_approx; do
-  timeout 1200 python studies/$s.py > gpurun_out/study_$s.md 2> gpurun_out/study_$s.err; echo $s=$?
-done
+CONFIGS="C4 C3" bash tools/ab_variants.sh
