@@ -42,7 +42,14 @@ HISTORY = """| change | fwd ms | bwd ms | step ms | images/s |
 | K4 at 5 CTAs/SM (48 registers), K8 at 5 CTAs/SM | 8.3 | 7.7 | 17.2 | 930 |
 | (tried) face-parallel K4 with 32-bit shared min (two box walks) | 22.8 | 7.7 | 31.7 | - |
 | (tried) 4x4 culling footprints; K6 gather per group of sub-frames | 8.3 | 7.7-8.6 | 17.2-17.9 | - |
-| 2 CTAs per (image, tile) by chunk | 8.2 | 7.7 | 17.05 | 938 |"""
+| 2 CTAs per (image, tile) by chunk | 8.2 | 7.7 | 17.05 | 938 |
+| K3 count/fill with shared-memory tile histograms | 8.17 | 7.61 | 16.66 | 960 |
+| K6 record stage 256, groups of 4 sub-frames | 8.16 | 7.15 | 16.18 | 989 |
+| K7 coalesced CTA of 32 vertices; K2 warp-staged record stores; K4 sums in shared memory | 8.14 | 7.15 | 15.98 | 1001 |"""
+
+
+import csv  # noqa: E402
+import io  # noqa: E402
 
 
 def main():
@@ -52,6 +59,16 @@ def main():
     rep = os.path.join(OUT, "prof_c4.ncu-rep")
     tab_l = sp.launches(launches)
     tab_f = sp.full(rep)
+    k4_inst, k4_issue = 7.0e9, 70.0
+    try:
+        rawk = list(csv.reader(io.StringIO(sh(["ncu", "-i", rep, "--page", "raw", "--csv"]))))
+        for r_ in rawk[2:]:
+            d_ = dict(zip(rawk[0], r_))
+            if "k4_raster_fwd" in d_["Kernel Name"]:
+                k4_inst = float(d_["smsp__inst_executed.sum"].replace(",", ""))
+                k4_issue = float(d_["smsp__issue_active.avg.pct_of_peak_sustained_active"].replace(",", ""))
+    except (KeyError, ValueError, IndexError):
+        pass
     srep = os.path.join(OUT, "prof_soft.ncu-rep")
     tab_s = sp.full(srep) if os.path.exists(srep) else "(no soft capture)"
     if os.path.exists(srep):
@@ -64,8 +81,6 @@ def main():
     open(os.path.join(PROF, "r1_ncu_details_raster_C4.csv"), "w").write(
         sh(["ncu", "-i", rep, "--page", "details", "--csv"]))
     raw = sh(["ncu", "-i", rep, "--page", "raw", "--csv"])
-    import csv
-    import io
     rows = list(csv.reader(io.StringIO(raw)))
     hdr = rows[0]
     traffic = {}
@@ -115,11 +130,11 @@ Measured FFMA probe: {c4['ffma_measured_tflops']:.1f} TFLOP/s (derived peak 74.4
 
 C4 forward census per launch: {rc['executed_pair_tests_per_launch']:.3e} executed (pixel, face, sub-frame) tests,
 {rc['necessary_pairs_per_launch']:.3e} covered pairs, {rc['covered_pixel_subframes_per_launch']:.3e} covered (pixel, sub-frame),
-{rc['staged_records_per_launch']:.3e} staged (face, sub-frame, tile) records.  K4 executes ~{7.6e9 / rc['staged_records_per_launch']:.0f} warp
-instructions per staged record (visibility ~38%, staging ~25%).  The fraction counts only SURVEY 8(d)'s
+{rc['staged_records_per_launch']:.3e} staged (face, sub-frame, tile) records.  K4 executes ~{k4_inst / rc['staged_records_per_launch']:.0f} warp
+instructions per staged record (visibility ~40%, staging ~25%).  The fraction counts only SURVEY 8(d)'s
 algorithmic flops (18 per covered pair, 25 per shade, 30 per face set-up), while the kernel tests
 {rc['executed_pair_tests_per_launch'] / rc['necessary_pairs_per_launch']:.1f} candidates per covered pair (8x4 warp footprints vs ~10-pixel faces); issue
-utilisation (66% for K4) is the better efficiency indicator.
+utilisation ({k4_issue:.0f}% for K4) is the better efficiency indicator.
 
 ## Launch list (ncu `gpu__time_duration.sum`, `--clock-control none`; `python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline`)
 
