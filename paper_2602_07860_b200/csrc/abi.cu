@@ -454,9 +454,8 @@ int prepare(const float *verts, int V, const int32_t *faces, int F, const float 
     }
     r = cuda_check(launch_setup(t, verts, faces, colors, P.maxS, st), "setup kernels");
     if (r) return r;
-    r = cuda_check(launch_binning(t, hard_bins(t), 0.f, st), "binning kernels");
-    if (r || !P.soft) return r;
-    return cuda_check(launch_binning(t, t.sb, P.rcut, st), "soft binning kernels");
+    // (the soft bins are built after K4: their sort skips the tiles K4 found fully covered)
+    return cuda_check(launch_binning(t, hard_bins(t), 0.f, st), "binning kernels");
 }
 
 }  // namespace
@@ -504,6 +503,8 @@ int blur_render_fwd(const float *verts, int V, const int32_t *faces, int F, cons
     }
     if (cfg && cfg->raster_events[1]) cudaEventRecord((cudaEvent_t)cfg->raster_events[1], st);
     if (P.soft) {   // NEXT-1: background alpha of the uncovered (pixel, sub-frame) pairs K4 recorded
+        r = cuda_check(launch_binning(t, t.sb, P.rcut, st), "soft binning kernels");
+        if (r) return r;
         if (cfg->soft_events[0]) cudaEventRecord((cudaEvent_t)cfg->soft_events[0], st);
         r = cuda_check(launch_soft_fwd(t, out_rgba, cfg->census, st), "soft fwd");
         if (r) return r;
@@ -542,6 +543,8 @@ int blur_render_bwd(const float *verts, int V, const int32_t *faces, int F, cons
     }
     if (P.soft && !reuse) {   // coverage of every (pixel, sub-frame) for the soft term (no image written)
         r = cuda_check(launch_raster_fwd(t, nullptr, nullptr, -1, nullptr, st), "coverage pass");
+        if (r) return r;
+        r = cuda_check(launch_binning(t, t.sb, P.rcut, st), "soft binning kernels");
         if (r) return r;
     }
     if (cfg && cfg->raster_events[0]) cudaEventRecord((cudaEvent_t)cfg->raster_events[0], st);

@@ -255,6 +255,24 @@ __global__ void __launch_bounds__(256) k3_scan_add(long long *off, const long lo
 }
 
 // ---- per-bin bitonic sort (one warp per bin)
+// soft bins: true if every pixel of the bin's tile is covered at every sub-frame of its chunk (K4's
+// coverage ballots; out-of-image pixels count as covered) -- no soft term is ever evaluated for it,
+// so it need not be sorted.  Warp-uniform.
+__device__ __forceinline__ bool bin_fully_covered(const Tables &t, int bi, int lane)
+{
+    if (!t.covbits) return false;
+    const int c = bi / t.T, tile = bi - c * t.T;
+    const Chunk ch = t.chunks[c];
+    const ImgInfo &im = t.imgs[ch.b];
+    const int nw = (ch.k1 - ch.k0) * (NT / 32);
+    bool all = true;
+    for (int i = lane; i < nw; i += 32) {
+        const int k = ch.k0 + i / (NT / 32), w = i % (NT / 32);
+        all &= t.covbits[cov_word(t, im, k, tile) + w] == 0xFFFFFFFFu;
+    }
+    return __all_sync(0xffffffffu, all);
+}
+
 __global__ void __launch_bounds__(256) k3_sort(Tables t, BinSet bs, int nbins)
 {
     __shared__ int sm[8][SORTCAP];
@@ -264,6 +282,7 @@ __global__ void __launch_bounds__(256) k3_sort(Tables t, BinSet bs, int nbins)
         const long long o = bs.off[bi];
         const int n = (int)(bs.off[bi + 1] - o);
         if (n <= 1 || n > SORTCAP || o + n > bs.cap) continue;
+        if (bin_fully_covered(t, bi, lane)) continue;
         int n2 = 32;
         while (n2 < n) n2 <<= 1;
         for (int i = lane; i < n2; i += 32) s[i] = i < n ? bs.entries[o + i] : 0x7fffffff;
@@ -306,6 +325,17 @@ __global__ void __launch_bounds__(512) k3_sort_big(Tables t, BinSet bs, int nbin
         const long long o = bs.off[bi];
         const int n = (int)(bs.off[bi + 1] - o);
         if (n <= SORTCAP || n > bs.sortcap || o + n > bs.cap) continue;   // block-uniform
+        {
+            __shared__ int cov;
+            if (threadIdx.x < 32) {
+                const bool fc = bin_fully_covered(t, bi, threadIdx.x);
+                if (threadIdx.x == 0) cov = fc;
+            }
+            __syncthreads();
+            const bool skip = cov;
+            __syncthreads();
+            if (skip) continue;
+        }
         int n2 = 2 * SORTCAP;
         while (n2 < n) n2 <<= 1;
         if (threadIdx.x == 0) bad = 0;
