@@ -89,3 +89,39 @@ def test_closest_weights_are_convex_and_no_farther_than_vertices_or_midpoints(xs
     cands = [np.array([x[i], y[i]]) for i in range(3)]
     cands += [0.5 * (cands[i] + cands[(i + 1) % 3]) for i in range(3)]
     assert all(d2 <= np.sum((p - c) ** 2) + 1e-12 for c in cands)
+
+
+def _seg_dist2(px, py, ax, ay, bx, by):
+    """Squared distance from a point to a segment (textbook clamp of the projection)."""
+    dx, dy = bx - ax, by - ay
+    L = dx * dx + dy * dy
+    t = 0.0 if L == 0 else min(1.0, max(0.0, ((px - ax) * dx + (py - ay) * dy) / L))
+    qx, qy = ax + t * dx - px, ay + t * dy - py
+    return qx * qx + qy * qy
+
+
+@settings(**SETTINGS)
+@given(st.lists(coord, min_size=12, max_size=12), st.floats(0, 1), st.floats(-2, 2), st.floats(-2, 2))
+def test_soft_distance_bounds_true_distance(xs, tau, u, v):
+    """Eq.14's d = |p - F(tau) w*|^2 with w* convex (A17-A18 on F(X)), so F(tau) w* lies on the
+    triangle: d >= dist(p, F(tau))^2, with equality for the exact variant (Eq.12).  This is what lets
+    the GPU drop faces farther than sqrt(kappa delta) from a pixel (Q21)."""
+    X0, Y0, _ = _tri(xs[:6])
+    X1, Y1, _ = _tri(xs[6:])
+    Xt, Yt = (1 - tau) * X0 + tau * X1, (1 - tau) * Y0 + tau * Y1
+    det = (Xt[1] - Xt[0]) * (Yt[2] - Yt[0]) - (Yt[1] - Yt[0]) * (Xt[2] - Xt[0])
+    if abs(det) < 1e-3:
+        return
+    w, _ = oracle.bary_textbook(Xt, Yt, u, v)
+    if w.min() >= 0:
+        return                                          # inside F(tau): not a background term
+    true2 = min(_seg_dist2(u, v, Xt[i], Yt[i], Xt[(i + 1) % 3], Yt[(i + 1) % 3]) for i in range(3))
+    for exact in (False, True):
+        r = oracle.soft_pair(X0, Y0, X1, Y1, tau, u, v, 1e-4, exact=exact)
+        assert r is not None
+        wh = r["what"]
+        assert np.all(wh >= -1e-12) and abs(wh.sum() - 1) < 1e-9
+        assert abs(r["d"] - ((r["pstar"][0] - u) ** 2 + (r["pstar"][1] - v) ** 2)) <= 1e-9 * max(1.0, r["d"])
+        assert r["d"] >= true2 * (1 - 1e-9) - 1e-12
+        if exact:
+            assert abs(r["d"] - true2) <= 1e-9 * max(1.0, true2) + 1e-12
