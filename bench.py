@@ -368,6 +368,9 @@ def main():
                 **({"soft_fwd_ms": float(np.mean(sf_ms)), "soft_bwd_ms": float(np.mean(sb_ms))} if soft else {}),
                 "executed_pair_tests_per_launch": cand, "necessary_pairs_per_launch": nec,
                 "covered_pixel_subframes_per_launch": cov, "staged_records_per_launch": staged,
+                # every timed kernel: algorithmic TFLOP/s (same per-unit figures) and fraction of the peak
+                "kernels_frac": {k[0]: (k[1] / (k[2] / 1000.0) / 1e12 / FP32_PEAK_TFLOPS if k[2] > 0 else 0.0)
+                                 for k in kernels},
                 **({"soft_terms_per_launch": soft_terms, "soft_staged_records_per_launch": soft_staged,
                     "soft_items_per_launch": soft_items, "soft_face_iterations_per_launch": soft_iters,
                     "kernels_ms": {k[0]: k[2] for k in kernels}} if soft else {})}

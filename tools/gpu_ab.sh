@@ -1,6 +1,3 @@
-# scratch driver
+# scratch A/B driver (edited per experiment)
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for c in C4 C3 C2; do
-timeout 600 python bench.py --config $c --delta 1e-4 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; k=r['kernels_ms']; print('$c soft', round(d['ms_per_step'],3), 'k8 %.2f k9 %.2f' % (k['k8_soft_fwd'], k['k9_soft_bwd']))"
-done
+CONFIGS="C4 C3 C5" bash tools/ab_variants.sh
