@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
     const bool inimg = px < t.W && py < t.H;
     const float ul = (float)(lx - TW / 2) * tc.sx;
     const float vl = (float)(TH / 2 - ly) * tc.sy;
-    const size_t pix = ((size_t)b * t.H + py) * t.W + px;
+#define PIX (((size_t)b * t.H + py) * t.W + px)   // (recomputed where used: keeps registers free)
     const int myp = ly * TW + lx;
 #if BR_K4_SACC
     S.acc[myp] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
         const long long o = t.off[bi];
         const int n = (int)(t.off[bi + 1] - o);
         if (n == 0) {
-            if (ids && inimg && ids_k >= ch.k0 && ids_k < ch.k1) ids[pix] = -1;
+            if (ids && inimg && ids_k >= ch.k0 && ids_k < ch.k1) ids[PIX] = -1;
             if (t.covbits) {
                 const unsigned m = __ballot_sync(0xffffffffu, !inimg);
                 if (lane == 0)
@@ -555,6 +555,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                 __syncthreads();
                 stage_group<CENSUS, MODE>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, nstage);
                 __syncthreads();
+                // visibility-buffer row of this pixel at sub-frame kg, advanced by one sub-frame per l
+                uint16_t *vrow = vis_out ? vis_out + ((size_t)(im.cov_off + kg) * t.T + tile) * (TW * TH) + myp : nullptr;
+                const int l_ids = (ids && inimg) ? ids_k - kg : -1;
                 for (int l = 0; l < ng; ++l) {
                     float zbest = __int_as_float(0x7f800000);
                     int ebest = -1, fbest = 0x7fffffff;
@@ -577,10 +580,11 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                         fid = rl[ebest].fid;
                         if (CENSUS) nshade++;
                     }
-                    if (ids && inimg && kg + l == ids_k) ids[pix] = fid;
-                    if (vis_out)   // visibility buffer for K6 (bins it takes the grouped path for)
-                        vis_out[((size_t)(im.cov_off + kg + l) * t.T + tile) * (TW * TH) + myp] =
-                            ebest >= 0 ? (uint16_t)ebest : (uint16_t)0xFFFF;
+                    if (l == l_ids) ids[PIX] = fid;
+                    if (vrow) {   // visibility buffer for K6 (bins it takes the grouped path for)
+                        *vrow = ebest >= 0 ? (uint16_t)ebest : (uint16_t)0xFFFF;
+                        vrow += (size_t)t.T * (TW * TH);
+                    }
                     if (t.covbits) {   // soft path: which pixels of the warp are covered at this sub-frame
                         const unsigned m = __ballot_sync(0xffffffffu, ebest >= 0 || !inimg);
                         if (lane == 0) t.covbits[cov_word(t, im, kg + l, tile) + warp] = m;
@@ -618,7 +622,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                     __syncthreads();
                 }
                 if (has) { K4_ACC(pr, pg, pb); if (CENSUS) nshade++; }
-                if (ids && inimg && k == ids_k) ids[pix] = has ? bfid : -1;
+                if (ids && inimg && k == ids_k) ids[PIX] = has ? bfid : -1;
                 if (t.covbits) {
                     const unsigned m = __ballot_sync(0xffffffffu, has || !inimg);
                     if (lane == 0) t.covbits[cov_word(t, im, k, tile) + warp] = m;
@@ -634,9 +638,10 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
 #else
         const float4 v = make_float4(ar * inv, ag * inv, ab * inv, aa * inv);
 #endif
-        if (t.splits == 1) reinterpret_cast<float4 *>(out)[pix] = v;
-        else t.part[(size_t)blockIdx.z * ((size_t)t.B * t.H * t.W) + pix] = v;
+        if (t.splits == 1) reinterpret_cast<float4 *>(out)[PIX] = v;
+        else t.part[(size_t)blockIdx.z * ((size_t)t.B * t.H * t.W) + PIX] = v;
     }
+#undef PIX
     if (CENSUS) {
         atomicAdd(census + 0, ncov);
         atomicAdd(census + 1, inimg ? nshade : 0ull);

@@ -1,3 +1,5 @@
 # scratch A/B driver (edited per experiment)
 mkdir -p gpurun_out
-CONFIGS="C4 C3 C5" bash tools/ab_variants.sh
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q 2>&1 | tail -2
+CONFIGS="C4 C3" bash tools/ab_variants.sh
+CONFIGS="C4" bash tools/ab_variants.sh
