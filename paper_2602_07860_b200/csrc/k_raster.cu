@@ -984,8 +984,9 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
                 for (int i = threadIdx.x; i < ng * n; i += NT) S.won[i] = 0;
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();
-                for (int l = 0; l < ng; ++l) {
-                    const uint16_t v = t.vis[((size_t)(im.cov_off + kg + l) * t.T + tile) * (TW * TH) + myp];
+                const uint16_t *vrow = t.vis + ((size_t)(im.cov_off + kg) * t.T + tile) * (TW * TH) + myp;
+                for (int l = 0; l < ng; ++l, vrow += (size_t)t.T * (TW * TH)) {
+                    const uint16_t v = *vrow;
                     const int e = (inimg && v != 0xFFFF) ? (int)v : -1;
                     S.win[l][myp] = (short)e;
                     if (e >= 0) S.won[l * n + e] = 1;
