@@ -158,4 +158,8 @@ cudaError_t launch_split_reduce(const Tables &t, float *out, cudaStream_t st);
 cudaError_t launch_l2(const float *out, const float *tgt, long long n, long long n_norm, float *loss,
                       float *grad, cudaStream_t st);
 cudaError_t launch_ffma_probe(int ctas, int iters, float *sink, cudaStream_t st);
+// p / ng for the (face, sub-frame) pair loops without an integer division: p < 2^13 and ng <= 16,
+// so (p + 0.5) / ng in fp32 (relative error < 1e-6) is never within rounding of an integer
+__device__ __forceinline__ int div_small(int p, float inv_ng) { return __float2int_rz(((float)p + 0.5f) * inv_ng); }
+
 }  // namespace br

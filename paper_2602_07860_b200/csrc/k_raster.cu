@@ -324,8 +324,9 @@ __device__ __forceinline__ void stage_group(const BinCtx &bc, int nb, int base, 
 {
     const int nw = (nb + 31) >> 5;
     const int npair = nb * ng;
+    const float inv_ng = 1.0f / (float)ng;
     for (int p = threadIdx.x; p < npair; p += NT) {
-        const int j = p / ng, l = p - j * ng;
+        const int j = div_small(p, inv_ng), l = p - j * ng;
         const int f = bc.fb ? sid[j] : __ldg(bc.ent + base + j);
         if ((unsigned)f >= (unsigned)F) {     // never expected: bins hold valid face ids
 #ifdef BR_DEBUG
@@ -702,8 +703,9 @@ __device__ __forceinline__ void stage_rec(const FaceRec &fr, float tau, const Ti
 __device__ __forceinline__ void stage_won(const BinCtx &bc, int n, const float *taus, int ng, const TileCtx &tc, int F,
                                           const unsigned char *won, TauRec *rec)
 {
+    const float inv_ng = 1.0f / (float)ng;
     for (int p = threadIdx.x; p < n * ng; p += NT) {
-        const int j = p / ng, l = p - j * ng;
+        const int j = div_small(p, inv_ng), l = p - j * ng;
         if (!won[l * n + j]) continue;
         const int f = __ldg(bc.ent + j);
         if ((unsigned)f >= (unsigned)F) {

@@ -320,8 +320,9 @@ __device__ __forceinline__ void soft_stage_group(const Tables &t, const SoftBin 
                                                  SoftRec *rec, uint32_t *wm, unsigned long long &nstage, float rcut)
 {
     const int nw = (nb + 31) >> 5;
+    const float inv_ng = 1.0f / (float)ng;
     for (int p = threadIdx.x; p < nb * ng; p += NT) {
-        const int j = p / ng, l = p - j * ng;
+        const int j = div_small(p, inv_ng), l = p - j * ng;
         uint32_t any = 0u;
 #pragma unroll
         for (int w = 0; w < SNW; ++w) any |= need[l][w];

@@ -339,7 +339,8 @@ def test_cuda_graph_step_matches_eager(cfg):
         l2, dv2, dc2, out2 = r2.step(v.clone(), c, tgt)
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy(), out2.cpu().numpy())
-        assert abs(float(loss) - float(l2)) <= 1e-6 * abs(float(l2))
+        # the L2 loss sums the CTAs' partials with float atomics: its last bits depend on their order
+        assert abs(float(loss) - float(l2)) <= 1e-5 * abs(float(l2))
         assert rel_l2(dv.cpu().numpy(), dv2.cpu().numpy()) < 1e-5
         assert rel_l2(dc.cpu().numpy(), dc2.cpu().numpy()) < 1e-5
 
