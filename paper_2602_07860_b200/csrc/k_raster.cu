@@ -372,9 +372,12 @@ __device__ __forceinline__ bool vis_mask_fast(const TauRec *rec, const uint32_t 
                                               unsigned long long &ntest, bool count)
 {
     float tief = 0.f;
-    for (int wd = 0; wd < nw; ++wd) {
-        uint32_t m = wm[wd];
-        const float4 *rw = reinterpret_cast<const float4 *>(rec + (wd << 5));
+    // words walked by pointer with a countdown (a `wd < nw` bound or an end pointer was re-derived
+    // from the bin length at every word under register pressure)
+    const uint32_t *wp = wm;
+    const float4 *rw = reinterpret_cast<const float4 *>(rec);
+    for (int wbase = 0, left = nw; left > 0; --left, ++wp, rw += 4 * 32, wbase += 32) {
+        uint32_t m = *wp;
         while (m) {
             int k;
             asm("bfind.u32 %0, %1;" : "=r"(k) : "r"(m));   // highest set bit (any order is fine)
@@ -389,7 +392,7 @@ __device__ __forceinline__ bool vis_mask_fast(const TauRec *rec, const uint32_t 
             if (CENSUS && count) { ncov += emin >= 0.f; ntest += 1; }
             // covered with z == zbest: an exact depth tie (kept in a float: one FSEL per test)
             tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
-            if (emin >= 0.f && z < zbest) { zbest = z; ebest = (wd << 5) + k; }
+            if (emin >= 0.f && z < zbest) { zbest = z; ebest = wbase + k; }
         }
     }
     return tief != 0.f;
@@ -491,6 +494,8 @@ struct FwdSmem {
 #if BR_K4_SACC
     float4 acc[TW * TH];   // per-pixel (r, g, b, a) sums over the sub-frames (thread-private slot)
 #endif
+    float2 uv[NT];         // the thread's pixel (ul, vl): reloaded at each visibility pass instead of being
+                           // re-derived from the thread index under register pressure
 };
 
 template <bool CENSUS, int MODE>
@@ -513,6 +518,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
     const float vl = (float)(TH / 2 - ly) * tc.sy;
 #define PIX (((size_t)b * t.H + py) * t.W + px)   // (recomputed where used: keeps registers free)
     const int myp = ly * TW + lx;
+    S.uv[threadIdx.x] = make_float2(ul, vl);
 #if BR_K4_SACC
     S.acc[myp] = make_float4(0.f, 0.f, 0.f, 0.f);
 #define K4_ACC(pr, pg, pb) do { float4 a_ = S.acc[myp]; a_.x += (pr); a_.y += (pg); a_.z += (pb); a_.w += 1.f; S.acc[myp] = a_; } while (0)
@@ -565,7 +571,10 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                     const TauRec *rl = S.rec + l * n;
                     const uint32_t *wml = S.wm + (l * NFP + fp_of(warp, lane)) * nw;
                     bool tie = true;
-                    if (MODE != 2) tie = vis_mask_fast<CENSUS, MODE>(rl, wml, nw, ul, vl, zbest, ebest, ncov, ntest, inimg);
+                    if (MODE != 2) {
+                        const float2 uv = S.uv[threadIdx.x];
+                        tie = vis_mask_fast<CENSUS, MODE>(rl, wml, nw, uv.x, uv.y, zbest, ebest, ncov, ntest, inimg);
+                    }
                     if (__any_sync(0xffffffffu, tie)) {   // exact depth tie somewhere in the warp: face indices decide
                         unsigned long long d0 = 0, d1 = 0;
                         zbest = __int_as_float(0x7f800000);
