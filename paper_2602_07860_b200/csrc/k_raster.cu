@@ -133,6 +133,7 @@ __device__ __forceinline__ bool rect_reaches(const float A[3], const float B[3],
 // Evaluate a record at tau for this tile -> TauRec + the mask of warp footprints it can reach
 // (bit w = culling footprint w, see FPW; 0 = the face cannot cover any pixel of the tile at tau).
 // D = det F(tau) (|D| > EPS_D) and the face's pixel box in the tile come from the caller's rejects.
+template <bool GRID>
 __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, float D, int x0, int x1, int y0, int y1,
                                               const TileCtx &tc, TauRec &out)
 {
@@ -159,13 +160,40 @@ __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, floa
 #pragma unroll
     for (int i = 0; i < 3; ++i)
         tol[i] = 1e-6f * (fabsf(A[i]) * (8.f * tc.sx) + fabsf(B[i]) * (8.f * tc.sy) + fabsf(G[i])) + 1e-30f;
+    // the max of e_i over a footprint rect (clipped to the box) sits at the corner along (A_i, B_i): a
+    // column term A_i u per footprint column of the box, a row term G_i + B_i v + tol_i per row, and the
+    // footprint is reached iff every edge has column + row term >= 0
     uint32_t fm = 0u;
-    for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
-        for (int wx = x0 >> FPW_SH; wx <= (x1 >> FPW_SH); ++wx) {
-            const int rx0 = max(x0, wx * FPW), rx1 = min(x1, wx * FPW + FPW - 1);
-            const int ry0 = max(y0, wy * 4), ry1 = min(y1, wy * 4 + 3);
-            if (rect_reaches_t(A, B, G, tol, rx0, rx1, ry0, ry1, tc)) fm |= 1u << (wy * (TW / FPW) + wx);
-        }
+    if (!GRID) {   // per footprint (K6's copy: keeps that kernel's register allocation)
+        for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
+            for (int wx = x0 >> FPW_SH; wx <= (x1 >> FPW_SH); ++wx) {
+                const int rx0 = max(x0, wx * FPW), rx1 = min(x1, wx * FPW + FPW - 1);
+                const int ry0 = max(y0, wy * 4), ry1 = min(y1, wy * 4 + 3);
+                if (rect_reaches_t(A, B, G, tol, rx0, rx1, ry0, ry1, tc)) fm |= 1u << (wy * (TW / FPW) + wx);
+            }
+    } else {
+    const int wx0 = x0 >> FPW_SH, ncol = (x1 >> FPW_SH) - wx0 + 1;
+    float cu[TW / FPW][3];
+#pragma unroll
+    for (int c = 0; c < TW / FPW; ++c) {
+        const int wx = min(wx0 + c, TW / FPW - 1);
+        const float ulmin = (float)(max(x0, wx * FPW) - TW / 2) * tc.sx;
+        const float ulmax = (float)(min(x1, wx * FPW + FPW - 1) - TW / 2) * tc.sx;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) cu[c][i] = A[i] * (A[i] > 0.f ? ulmax : ulmin);
+    }
+    for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy) {
+        const float vlmin = (float)(TH / 2 - min(y1, wy * 4 + 3)) * tc.sy;
+        const float vlmax = (float)(TH / 2 - max(y0, wy * 4)) * tc.sy;
+        float rv[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) rv[i] = G[i] + B[i] * (B[i] > 0.f ? vlmax : vlmin) + tol[i];
+#pragma unroll
+        for (int c = 0; c < TW / FPW; ++c)
+            if (c < ncol && rv[0] + cu[c][0] >= 0.f && rv[1] + cu[c][1] >= 0.f && rv[2] + cu[c][2] >= 0.f)
+                fm |= 1u << (wy * (TW / FPW) + wx0 + c);
+    }
+    }
     if (!fm) return 0u;
     const float4 z0 = fr.q[9], z1 = fr.q[10];
     const float za = __fmaf_rn(tau, z1.x - z0.x, z0.x);
@@ -317,7 +345,7 @@ __device__ __forceinline__ uint32_t stage_tau_naive(const BinCtx &bc, int f, flo
 // taus[0..ng): records rec[l*nb + j], masks wm[(l*NFP + w)*nw + j/32].  Masks must be clear.
 // Work is spread over (face, sub-frame) pairs, face-major, so the lanes that share a face load its
 // record with broadcast loads.
-template <bool CENSUS, int MODE>
+template <bool CENSUS, int MODE, bool GRID = false>
 __device__ __forceinline__ void stage_group(const BinCtx &bc, int nb, int base, const float *taus, int ng,
                                             const TileCtx &tc, int W, int H, int F, const int *sid, TauRec *rec,
                                             float4 *vtx, uint32_t *wm, unsigned long long &nstage)
@@ -352,7 +380,7 @@ __device__ __forceinline__ void stage_group(const BinCtx &bc, int nb, int base, 
         if (MODE == 0) {
             FaceRec fr;
             load_rec(r, fr);
-            fm = stage_tau(fr, tau, D, x0, x1, y0, y1, tc, rec[l * nb + j]);
+            fm = stage_tau<GRID>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * nb + j]);
         } else {
             fm = stage_tau_naive<MODE>(bc, f, tau, tc, W, H, rec[l * nb + j], vtx + 3 * (l * nb + j));
         }
@@ -560,7 +588,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                 clear_words(S.wm, ng * NFP * nw);
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();
-                stage_group<CENSUS, MODE>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, nstage);
+                stage_group<CENSUS, MODE, true>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, nstage);
                 __syncthreads();
                 // visibility-buffer row of this pixel at sub-frame kg, advanced by one sub-frame per l
                 uint16_t *vrow = vis_out ? vis_out + ((size_t)(im.cov_off + kg) * t.T + tile) * (TW * TH) + myp : nullptr;
@@ -618,7 +646,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                     const int nw = (nb + 31) >> 5;
                     clear_words(S.wm, NFP * nw);
                     __syncthreads();
-                    stage_group<CENSUS, MODE>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, nstage);
+                    stage_group<CENSUS, MODE, true>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, nstage);
                     __syncthreads();
                     vis_mask<CENSUS, MODE>(S.rec, S.vtx, S.wm + fp_of(warp, lane) * nw, nw, base, ul, vl, zbest, ebest, fbest, ncov,
                                            ntest, inimg);
