@@ -770,7 +770,11 @@ struct BwdSmem {
     float4 g[TW * TH];        // dL/dI / N of the tile
     float taus[GMAX_B];
     int wsum[NWARP];
-    unsigned char won[SREC_B];   // cached visibility: (sub-frame, slot) pairs that won a pixel
+    union {
+        unsigned char won[SREC_B];   // cached visibility: (sub-frame, slot) pairs that won a pixel
+        uint32_t won4[SREC_B / 4];   //   (cleared by words)
+    };
+    int pxinfo[NT];                  // the thread's pixel: myp | in-image << 8 (reloaded rather than re-derived)
 };
 
 // block-wide exclusive scan of cnt[0..nb) (nb <= 2 NT) into off[]; returns the total
@@ -995,6 +999,7 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
         S.g[myp] = g;
     }
     for (int j = threadIdx.x; j < SREC_B; j += NT) S.cnt[j] = 0;   // invariant of bwd_gather
+    S.pxinfo[threadIdx.x] = myp | (inimg ? 0x100 : 0);
     __syncthreads();
     unsigned long long d0 = 0, d1 = 0, d2 = 0;
 
@@ -1020,21 +1025,24 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
             const int Gs = min(GMAX_B, SREC_B / n);
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
-                for (int i = threadIdx.x; i < ng * n; i += NT) S.won[i] = 0;
+                for (int i = threadIdx.x; i < ((ng * n + 3) >> 2); i += NT) S.won4[i] = 0u;
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();
-                const uint16_t *vrow = t.vis + ((size_t)(im.cov_off + kg) * t.T + tile) * (TW * TH) + myp;
+                const int pi = S.pxinfo[threadIdx.x], mp = pi & 0xFF;
+                const uint16_t *vrow = t.vis + ((size_t)(im.cov_off + kg) * t.T + tile) * (TW * TH) + mp;
                 for (int l = 0; l < ng; ++l, vrow += (size_t)t.T * (TW * TH)) {
                     const uint16_t v = *vrow;
-                    const int e = (inimg && v != 0xFFFF) ? (int)v : -1;
-                    S.win[l][myp] = (short)e;
+                    const int e = ((pi & 0x100) && v != 0xFFFF) ? (int)v : -1;
+                    S.win[l][mp] = (short)e;
                     if (e >= 0) S.won[l * n + e] = 1;
                 }
                 __syncthreads();
                 stage_won(bc, n, S.taus, ng, tc, t.F, S.won, S.rec);
                 __syncthreads();
-                for (int l = 0; l < ng; ++l)
-                    bwd_gather(S, S.rec + l * n, t, im, ch.s, S.taus[l], 0, n, true, S.win[l][myp], myp, tc, acc, dC);
+                for (int l = 0; l < ng; ++l) {
+                    const int mq = S.pxinfo[threadIdx.x] & 0xFF;
+                    bwd_gather(S, S.rec + l * n, t, im, ch.s, S.taus[l], 0, n, true, S.win[l][mq], mq, tc, acc, dC);
+                }
             }
         } else if (!bc.fb && n <= SREC_B) {
             const int Gs = min(GMAX_B, SREC_B / n), nw = (n + 31) >> 5;
