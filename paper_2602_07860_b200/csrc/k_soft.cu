@@ -346,12 +346,13 @@ template <bool CENSUS>
 __device__ __forceinline__ void soft_product(const SoftRec *rec, const uint32_t *wm, int nw, float ul, float vl,
                                              float kexp, float &P, float &Pnz, int &nz, unsigned long long &npair)
 {
-    for (int wd = 0; wd < nw; ++wd) {
-        uint32_t m = wm[wd];
+    // words by pointer with a countdown (keeps the bound from being re-derived per word)
+    for (int left = nw; left > 0; --left, ++wm, rec += 32) {
+        uint32_t m = *wm;
         while (m) {
             const int k = __clz(m);
             m ^= 0x80000000u >> k;
-            const SoftHit h = soft_eval(rec[(wd << 5) + k], ul, vl);
+            const SoftHit h = soft_eval(rec[k], ul, vl);
             const float A = __expf(-h.d * kexp);                     // Eq.10 with the exp kernel (A20)
             const float fac = 1.0f - A;
             P *= fac;                                                // Eq.15
@@ -794,7 +795,7 @@ __global__ void __launch_bounds__(NT, BR_K9C_MINB) k9c_soft_bwd(Tables t, const 
     const float ga = inimg ? __ldg(grad + 4 * (((size_t)b * t.H + py) * t.W + px) + 3) / (float)im.N : 0.f;
     S.ga[myp] = ga;
     const bool want = inimg && ga != 0.f;
-    for (int i = threadIdx.x; i < SREC_B9 * 12; i += NT) (&S.acc[0][0])[i] = 0.f;
+    for (int i = threadIdx.x; i < SREC_B9 * 3; i += NT) reinterpret_cast<float4 *>(&S.acc[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     unsigned long long dummy = 0;
     __syncthreads();
 
@@ -864,7 +865,7 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
     const float ga = inimg ? __ldg(grad + 4 * (((size_t)b * t.H + py) * t.W + px) + 3) / (float)im.N : 0.f;
     S.ga[myp] = ga;
     const bool want = inimg && ga != 0.f;
-    for (int i = threadIdx.x; i < SREC_B9 * 12; i += NT) (&S.acc[0][0])[i] = 0.f;
+    for (int i = threadIdx.x; i < SREC_B9 * 3; i += NT) reinterpret_cast<float4 *>(&S.acc[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     unsigned long long dummy = 0;
     __syncthreads();
 
