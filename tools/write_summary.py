@@ -45,7 +45,10 @@ HISTORY = """| change | fwd ms | bwd ms | step ms | images/s |
 | 2 CTAs per (image, tile) by chunk | 8.2 | 7.7 | 17.05 | 938 |
 | K3 count/fill with shared-memory tile histograms | 8.17 | 7.61 | 16.66 | 960 |
 | K6 record stage 256, groups of 4 sub-frames | 8.16 | 7.15 | 16.18 | 989 |
-| K7 coalesced CTA of 32 vertices; K2 warp-staged record stores; K4 sums in shared memory | 8.14 | 7.15 | 15.98 | 1001 |"""
+| K7 coalesced CTA of 32 vertices; K2 warp-staged record stores; K4 sums in shared memory | 8.14 | 7.15 | 15.98 | 1001 |
+| K4/K6 register pressure: row pointers, no integer division in the stage loops | 8.03 | 7.09 | 15.75 | 1016 |
+| K4 vis loop word countdown, (ul, vl) reloaded from shared memory (no per-word rematerialisation) | 7.48 | 7.09 | 15.24 | 1050 |
+| K4 footprint reach from per-column / per-row edge terms; K6 pixel info from shared memory | 7.10 | 7.01 | 14.78 | 1082 |"""
 
 
 import csv  # noqa: E402
