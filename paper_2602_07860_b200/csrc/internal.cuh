@@ -162,4 +162,8 @@ cudaError_t launch_ffma_probe(int ctas, int iters, float *sink, cudaStream_t st)
 // so (p + 0.5) / ng in fp32 (relative error < 1e-6) is never within rounding of an integer
 __device__ __forceinline__ int div_small(int p, float inv_ng) { return __float2int_rz(((float)p + 0.5f) * inv_ng); }
 
+// floor(cap / n) for 1 <= n <= cap <= 4096 without an integer division: cap / n is either an integer
+// (exact in fp32) or at least 1 / n below the next one, far more than __fdividef's 2-ulp error
+__device__ __forceinline__ int group_div(int cap, int n) { return (int)__fdividef((float)cap, (float)n); }
+
 }  // namespace br

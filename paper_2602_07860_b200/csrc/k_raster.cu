@@ -737,13 +737,14 @@ __device__ __forceinline__ void stage_rec(const FaceRec &fr, float tau, const Ti
 }
 
 // stage the won (face, sub-frame) pairs of bin slots [0, n) at the ng sub-frames: rec[l * n + j]
+// (won[l * n + j] == stamp marks them: no clearing between groups)
 __device__ __forceinline__ void stage_won(const BinCtx &bc, int n, const float *taus, int ng, const TileCtx &tc, int F,
-                                          const unsigned char *won, TauRec *rec)
+                                          const unsigned int *won, unsigned int stamp, TauRec *rec)
 {
     const float inv_ng = 1.0f / (float)ng;
     for (int p = threadIdx.x; p < n * ng; p += NT) {
         const int j = div_small(p, inv_ng), l = p - j * ng;
-        if (!won[l * n + j]) continue;
+        if (won[l * n + j] != stamp) continue;
         const int f = __ldg(bc.ent + j);
         if ((unsigned)f >= (unsigned)F) {
             atomicOr(bc.status, BLUR_ST_EINTERNAL);
@@ -770,10 +771,7 @@ struct BwdSmem {
     float4 g[TW * TH];        // dL/dI / N of the tile
     float taus[GMAX_B];
     int wsum[NWARP];
-    union {
-        unsigned char won[SREC_B];   // cached visibility: (sub-frame, slot) pairs that won a pixel
-        uint32_t won4[SREC_B / 4];   //   (cleared by words)
-    };
+    unsigned int won[SREC_B];   // cached visibility: group stamp of the (sub-frame, slot) pairs that won a pixel
     int pxinfo[NT];                  // the thread's pixel: myp | in-image << 8 (reloaded rather than re-derived)
 };
 
@@ -1000,6 +998,8 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
     }
     for (int j = threadIdx.x; j < SREC_B; j += NT) S.cnt[j] = 0;   // invariant of bwd_gather
     S.pxinfo[threadIdx.x] = myp | (inimg ? 0x100 : 0);
+    for (int j = threadIdx.x; j < SREC_B; j += NT) S.won[j] = 0xFFFFFFFFu;
+    unsigned int stamp = 0;   // group counter of the cached path (won flags)
     __syncthreads();
     unsigned long long d0 = 0, d1 = 0, d2 = 0;
 
@@ -1022,10 +1022,10 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
         acc_zero(acc);
         if (MODE == 0 && t.vis && !bc.fb && n <= SREC_B) {
             // visibility from the forward's buffer: stage only the (face, sub-frame) pairs that won
-            const int Gs = min(GMAX_B, SREC_B / n);
+            const int Gs = min(GMAX_B, group_div(SREC_B, n));
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
-                for (int i = threadIdx.x; i < ((ng * n + 3) >> 2); i += NT) S.won4[i] = 0u;
+                ++stamp;
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();
                 const int pi = S.pxinfo[threadIdx.x], mp = pi & 0xFF;
@@ -1034,10 +1034,10 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
                     const uint16_t v = *vrow;
                     const int e = ((pi & 0x100) && v != 0xFFFF) ? (int)v : -1;
                     S.win[l][mp] = (short)e;
-                    if (e >= 0) S.won[l * n + e] = 1;
+                    if (e >= 0) S.won[l * n + e] = stamp;
                 }
                 __syncthreads();
-                stage_won(bc, n, S.taus, ng, tc, t.F, S.won, S.rec);
+                stage_won(bc, n, S.taus, ng, tc, t.F, S.won, stamp, S.rec);
                 __syncthreads();
                 for (int l = 0; l < ng; ++l) {
                     const int mq = S.pxinfo[threadIdx.x] & 0xFF;
@@ -1045,7 +1045,7 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
                 }
             }
         } else if (!bc.fb && n <= SREC_B) {
-            const int Gs = min(GMAX_B, SREC_B / n), nw = (n + 31) >> 5;
+            const int Gs = min(GMAX_B, group_div(SREC_B, n)), nw = (n + 31) >> 5;
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
                 clear_words(S.wm, ng * NFP * nw);

@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
         soft_bin(t, im, ch, c, tile, sb);
         if (sb.n == 0) continue;   // no face within rcut of the tile during the chunk: every P = 1
         if (!sb.fb && sb.n <= SREC_F8) {
-            const int n = sb.n, Gs = min(GMAX_S, SREC_F8 / n), nw = (n + 31) >> 5;
+            const int n = sb.n, Gs = min(GMAX_S, group_div(SREC_F8, n)), nw = (n + 31) >> 5;
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
                 for (int l = 0; l < ng; ++l) load_need(t, im, kg + l, tile, warp, lane, inimg, &S.need[l][warp]);
@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(NT, BR_K9C_MINB) k9c_soft_bwd(Tables t, const 
         SoftBin sb;
         soft_bin(t, im, ch, c, tile, sb);
         if (sb.n == 0 || !k9c_bin(sb)) continue;
-        const int n = sb.n, Gs = min(GMAX_S, SREC_B9 / n), nw = (n + 31) >> 5;
+        const int n = sb.n, Gs = min(GMAX_S, group_div(SREC_B9, n)), nw = (n + 31) >> 5;
         bool touched = false;
         for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
             const int ng = min(Gs, ch.k1 - kg);
@@ -875,7 +875,7 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
         soft_bin(t, im, ch, c, tile, sb);
         if (sb.n == 0 || (t.spz && k9c_bin(sb))) continue;   // empty, or K9C's
         if (!sb.fb && sb.n <= SREC_B9) {
-            const int n = sb.n, Gs = min(GMAX_S, SREC_B9 / n), nw = (n + 31) >> 5;
+            const int n = sb.n, Gs = min(GMAX_S, group_div(SREC_B9, n)), nw = (n + 31) >> 5;
             bool touched = false;
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
