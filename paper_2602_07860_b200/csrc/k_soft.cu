@@ -266,6 +266,16 @@ __device__ __forceinline__ uint32_t soft_stage(const Tables &t, const float4 *__
     return fm;
 }
 
+// A = exp(-d / delta) (Eq.10, A20) as 2^(d kexp) with kexp = -log2(e) / delta, flushing results below
+// 2^-126 to 0 (d > 87 delta, far past the cut-off): one multiply and one MUFU.EX2
+__device__ __forceinline__ float soft_kexp(float delta) { return -1.4426950408889634f / delta; }
+__device__ __forceinline__ float soft_A(float d, float kexp)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d * kexp));
+    return y;
+}
+
 // One (pixel, face, tau) term: d (Eq.14), the chosen edge e (corners e, (e+1)%3) with parameter t,
 // and the residual r = p - F(tau) w^* (Eq.14's vector).
 struct SoftHit {
@@ -353,7 +363,7 @@ __device__ __forceinline__ void soft_product(const SoftRec *rec, const uint32_t 
             const int k = __clz(m);
             m ^= 0x80000000u >> k;
             const SoftHit h = soft_eval(rec[k], ul, vl);
-            const float A = __expf(-h.d * kexp);                     // Eq.10 with the exp kernel (A20)
+            const float A = soft_A(h.d, kexp);                       // Eq.10 with the exp kernel (A20)
             const float fac = 1.0f - A;
             P *= fac;                                                // Eq.15
             if (fac == 0.f) nz++;
@@ -412,7 +422,7 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
     const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
     const int px = tc.px0 + lx, py = tc.py0 + ly, myp = ly * TW + lx;
     const bool inimg = px < t.W && py < t.H;
-    const float kexp = 1.0f / t.delta;
+    const float kexp = soft_kexp(t.delta);
     float alpha = 0.f;
     unsigned long long npair = 0, nstage = 0, nitem = 0, nface = 0;
 
@@ -620,7 +630,7 @@ __device__ __forceinline__ void soft_grad_item(SoftBwdSmem &S, const SoftRec *re
             if (mine && z < 2) {
                 const SoftRec &r = rec[j];
                 const SoftHit h = soft_eval(r, ul, vl);
-                const float A = __expf(-h.d * kexp);
+                const float A = soft_A(h.d, kexp);
                 const float fac = 1.0f - A;
                 const float dadA = z == 0 ? pz / fac : (fac == 0.f ? pz : 0.f);
                 // dL/dv_i(tau) = G_a dalpha/dA (A / delta) 2 w^*_i (p - F(tau) w^*)
@@ -733,7 +743,7 @@ __device__ __forceinline__ void soft_grad_faces(Sm &S, const SoftRec *rec, const
         const int zq = __shfl_sync(0xffffffffu, zp, q);
         if (!has) continue;
         const SoftHit h = soft_eval(r, ul, vl);
-        const float A = __expf(-h.d * kexp);
+        const float A = soft_A(h.d, kexp);
         const float fac = 1.0f - A;
         // dalpha/dA_j = prod_{l != j} (1 - A_l)
         const float dadA = zq == 0 ? __fdividef(pzq, fac) : (fac == 0.f ? pzq : 0.f);
@@ -791,7 +801,7 @@ __global__ void __launch_bounds__(NT, BR_K9C_MINB) k9c_soft_bwd(Tables t, const 
     const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
     const int px = tc.px0 + lx, py = tc.py0 + ly, myp = ly * TW + lx;
     const bool inimg = px < t.W && py < t.H;
-    const float kexp = 1.0f / t.delta, c2 = 2.0f / t.delta;
+    const float kexp = soft_kexp(t.delta), c2 = 2.0f / t.delta;
     const float ga = inimg ? __ldg(grad + 4 * (((size_t)b * t.H + py) * t.W + px) + 3) / (float)im.N : 0.f;
     S.ga[myp] = ga;
     const bool want = inimg && ga != 0.f;
@@ -861,7 +871,7 @@ __global__ void __launch_bounds__(NT, BR_K9_MINB) k9_soft_bwd(Tables t, const fl
     const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
     const int px = tc.px0 + lx, py = tc.py0 + ly, myp = ly * TW + lx;
     const bool inimg = px < t.W && py < t.H;
-    const float kexp = 1.0f / t.delta, c2 = 2.0f / t.delta;
+    const float kexp = soft_kexp(t.delta), c2 = 2.0f / t.delta;
     const float ga = inimg ? __ldg(grad + 4 * (((size_t)b * t.H + py) * t.W + px) + 3) / (float)im.N : 0.f;
     S.ga[myp] = ga;
     const bool want = inimg && ga != 0.f;
