@@ -365,12 +365,12 @@ __device__ __forceinline__ void soft_product(const SoftRec *rec, const uint32_t 
             const SoftHit h = soft_eval(rec[k], ul, vl);
             const float A = soft_A(h.d, kexp);                       // Eq.10 with the exp kernel (A20)
             const float fac = 1.0f - A;
-            P *= fac;                                                // Eq.15
-            if (fac == 0.f) nz++;
+            if (fac == 0.f) nz++;                                    // Eq.15, zero factors counted apart
             else Pnz *= fac;
             if (CENSUS) npair++;
         }
     }
+    P = nz ? 0.f : Pnz;   // the full product (callers start from P = Pnz = 1, nz = 0): bit-identical
 }
 
 __device__ __forceinline__ void load_need(const Tables &t, const ImgInfo &im, int k, int tile, int warp, int lane,
