@@ -722,16 +722,14 @@ __device__ __forceinline__ void soft_grad_faces(Sm &S, const SoftRec *rec, const
     int p;
     float ulp, vlp;
     footprint_pixel(w, lane, tc, p, ulp, vlp);
-    float cp = 0.f, pzp = 0.f;
-    int zp = 2;
+    float cp = 0.f, ep = 0.f;
+    bool ok = false;
     if ((S.need[l][w] >> lane) & 1u) {
-        const float e = pzc[p];
-        const unsigned u = __float_as_uint(e);
-        zp = (u & 0x7fffffffu) > 0x7f800000u ? 2 : (int)(u >> 31);
-        pzp = fabsf(e);
+        ep = pzc[p];                    // K8's encoding: |ep| the non-zero product, sign = one zero factor
+        ok = (__float_as_uint(ep) & 0x7fffffffu) <= 0x7f800000u;   // NaN: two or more zero factors
         cp = S.ga[p] * c2;
     }
-    unsigned act = __ballot_sync(0xffffffffu, zp < 2 && cp != 0.f);   // pixels with a non-zero factor
+    unsigned act = __ballot_sync(0xffffffffu, ok && cp != 0.f);   // pixels with a non-zero factor
     SoftRec r;
     if (has) r = rec[slot];
     float g[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -739,14 +737,17 @@ __device__ __forceinline__ void soft_grad_faces(Sm &S, const SoftRec *rec, const
         const int q = __ffs(act) - 1;
         act &= act - 1;
         const float ul = __shfl_sync(0xffffffffu, ulp, q), vl = __shfl_sync(0xffffffffu, vlp, q);
-        const float cq = __shfl_sync(0xffffffffu, cp, q), pzq = __shfl_sync(0xffffffffu, pzp, q);
-        const int zq = __shfl_sync(0xffffffffu, zp, q);
+        const float cq = __shfl_sync(0xffffffffu, cp, q), eq = __shfl_sync(0xffffffffu, ep, q);
         if (!has) continue;
         const SoftHit h = soft_eval(r, ul, vl);
         const float A = soft_A(h.d, kexp);
         const float fac = 1.0f - A;
-        // dalpha/dA_j = prod_{l != j} (1 - A_l)
-        const float dadA = zq == 0 ? __fdividef(pzq, fac) : (fac == 0.f ? pzq : 0.f);
+        // dalpha/dA_j = prod_{l != j} (1 - A_l): the non-zero product over fac_j (fac_j > 0 then), or with
+        // one zero factor the product itself at that face
+        const float pzq = fabsf(eq);
+        float rf;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"(fac));
+        const float dadA = !signbit(eq) ? pzq * rf : (fac == 0.f ? pzq : 0.f);
         // dL/dv_i(tau) = G_a dalpha/dA (A / delta) 2 w^*_i (p - F(tau) w^*)
         const float cc = cq * dadA * A;
         const float gx = cc * h.rx;
