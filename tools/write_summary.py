@@ -48,7 +48,8 @@ HISTORY = """| change | fwd ms | bwd ms | step ms | images/s |
 | K7 coalesced CTA of 32 vertices; K2 warp-staged record stores; K4 sums in shared memory | 8.14 | 7.15 | 15.98 | 1001 |
 | K4/K6 register pressure: row pointers, no integer division in the stage loops | 8.03 | 7.09 | 15.75 | 1016 |
 | K4 vis loop word countdown, (ul, vl) reloaded from shared memory (no per-word rematerialisation) | 7.48 | 7.09 | 15.24 | 1050 |
-| K4 footprint reach from per-column / per-row edge terms; K6 pixel info from shared memory | 7.10 | 7.01 | 14.78 | 1082 |"""
+| K4 footprint reach from per-column / per-row edge terms; K6 pixel info from shared memory | 7.10 | 7.01 | 14.78 | 1082 |
+| K6 won flags as group stamps; group sizes without integer division | 7.09 | 6.90 | 14.67 | 1091 |"""
 
 
 import csv  # noqa: E402
@@ -174,7 +175,8 @@ splits (up to 8 CTAs per (image, tile)).  K9 here handles only the bins longer t
 History on C4, delta 1e-4: first version K8 40 / K9 106 ms (178 ms/step); barycentric closest point,
 work queue, pixel-parallel backward with warp reduce-scatter, 4 CTAs/SM for K8, split K9 items:
 K8 23.7 / K9 71.1 ms (120.5 ms/step); product cache K8 -> K9: K9 58.8; face-per-lane K9C over
-compacted masks: 48.8; soft splits: 36.6; products cached for the long bins too (K9 one pass): K8 {r(s4)['kernels_ms']['k8_soft_fwd']:.1f} / K9C + K9 {r(s4)['kernels_ms']['k9_soft_bwd']:.1f} ms ({s4['ms_per_step']:.1f} ms/step).
+compacted masks: 48.8; soft splits: 36.6; products cached for the long bins too (K9 one pass): 25.9;
+cut-off 18 delta, Eq.14 from the pixel, sorted bins only where needed, ex2 and register-pressure work: K8 {r(s4)['kernels_ms']['k8_soft_fwd']:.1f} / K9C + K9 {r(s4)['kernels_ms']['k9_soft_bwd']:.1f} ms ({s4['ms_per_step']:.1f} ms/step).
 """
     open(os.path.join(PROF, "r1_summary.md"), "w").write(md)
     print("wrote profiles/r1_summary.md")
