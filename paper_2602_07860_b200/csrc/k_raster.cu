@@ -41,7 +41,7 @@ constexpr int NFP = (TW / FPW) * (TH / 4);    // footprints (mask sets) per sub-
 __device__ __forceinline__ int fp_of(int warp, int lane) { return BR_HALF ? warp * 2 + ((lane >> 2) & 1) : warp; }
 // tuning knobs (overridable with -D for A/B builds; defaults measured on C4, profiles/)
 #ifndef BR_SREC_F
-#define BR_SREC_F 512
+#define BR_SREC_F 448
 #endif
 #ifndef BR_SREC_B
 #define BR_SREC_B 256
