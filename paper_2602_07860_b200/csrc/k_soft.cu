@@ -48,7 +48,7 @@ namespace {
 
 constexpr int SNW = NT / 32;     // warps per CTA
 #ifndef BR_SREC_F8
-#define BR_SREC_F8 384
+#define BR_SREC_F8 320
 #endif
 #ifndef BR_K8_MINB
 #define BR_K8_MINB 5
@@ -773,8 +773,8 @@ __device__ __forceinline__ void soft_grad_faces(Sm &S, const SoftRec *rec, const
     }
 }
 
-// bins whose products K8 cached (its grouped path) and that K9C's record stage holds
-__device__ __forceinline__ bool k9c_bin(const SoftBin &sb) { return !sb.fb && sb.n <= SREC_B9 && sb.n <= SREC_F8; }
+// bins K9C takes: K8 cached their products (grouped or per-sub-frame path) and K9C's record stage holds them
+__device__ __forceinline__ bool k9c_bin(const SoftBin &sb) { return !sb.fb && sb.n <= SREC_B9; }
 
 struct SoftBwdCSmem {
     SoftRec rec[SREC_B9];
