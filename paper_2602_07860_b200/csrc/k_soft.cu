@@ -489,18 +489,38 @@ __global__ void __launch_bounds__(NT, BR_K8_MINB) k8_soft_fwd(Tables t, unsigned
                     __syncthreads();
                     soft_stage_group<CENSUS>(t, sb, nb, base, S.taus, 1, tc, S.need, S.sid, S.rec, S.wm, nstage, t.rcut_f);
                     __syncthreads();
-                    for (int it = next_item(&S.head, SNW, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
-                        nx = next_item(&S.head, SNW, lane);
-                        if ((S.need[0][it] >> lane) & 1u) {
+                    // items (footprint, part of the words): a long bin gives one footprint's warp a
+                    // whole batch otherwise; the parts' products (om rows 3.., sign / NaN = one / more
+                    // zero factors) are folded into the pixel's running product in part order
+                    const int LP = min(GMAX_S - 3, nw);
+                    for (int it = next_item(&S.head, SNW * LP, lane), nx = 0; it >= 0; it = nx) {   // next item prefetched
+                        nx = next_item(&S.head, SNW * LP, lane);
+                        const int part = it % LP, w = it / LP;
+                        if ((S.need[0][w] >> lane) & 1u) {
                             int p;
                             float ul, vl, P = 1.f, Pnz = 1.f;
                             int nz = 0;
-                            footprint_pixel(it, lane, tc, p, ul, vl);
-                            soft_product<CENSUS>(S.rec, S.wm + it * nw, nw, ul, vl, kexp, P, Pnz, nz, npair);
-                            S.om[0][p] *= P;
-                            S.om[1][p] *= Pnz;
-                            reinterpret_cast<int *>(S.om[2])[p] += nz;
+                            footprint_pixel(w, lane, tc, p, ul, vl);
+                            const int wd0 = part * nw / LP, wd1 = (part + 1) * nw / LP;
+                            soft_product<CENSUS>(S.rec + (wd0 << 5), S.wm + w * nw + wd0, wd1 - wd0, ul, vl, kexp, P, Pnz,
+                                                 nz, npair);
+                            S.om[3 + part][p] = nz == 0 ? Pnz : (nz == 1 ? -Pnz : __int_as_float(0x7fffffff));
                         }
+                    }
+                    __syncthreads();
+                    if ((S.need[0][warp] >> lane) & 1u) {
+                        float pnz = S.om[1][myp];
+                        int nz = reinterpret_cast<const int *>(S.om[2])[myp];
+                        for (int part = 0; part < LP; ++part) {
+                            const float e = S.om[3 + part][myp];
+                            const unsigned u = __float_as_uint(e);
+                            nz += (u & 0x7fffffffu) > 0x7f800000u ? 2 : (int)(u >> 31);
+                            pnz *= fabsf(e);
+                        }
+                        nz = min(nz, 2);
+                        S.om[1][myp] = pnz;
+                        reinterpret_cast<int *>(S.om[2])[myp] = nz;
+                        S.om[0][myp] = nz ? 0.f : pnz;
                     }
                     base += nb;
                     __syncthreads();
