@@ -162,6 +162,15 @@ def test_soft_product_cache_equals_recompute(cfg):
     assert rel_l2(a["dv"], b["dv"]) < 1e-6 and rel_l2(a["dc"], b["dc"]) < 1e-6
 
 
+def test_soft_forward_is_deterministic():
+    """The soft forward is bit-reproducible (sorted soft bins, products in face order, split partials
+    summed in a fixed order)."""
+    sc = scenes.make_c3().subset([0, 5])
+    a = gpu_soft(sc, 1e-4)
+    b = gpu_soft(sc, 1e-4)
+    assert np.array_equal(a["rgba"], b["rgba"])
+
+
 def test_soft_overflow_fallback_and_cut():
     """A tiny soft-bin capacity forces the exact fallback scan (same result); a larger cut-off
     changes alpha by at most the dropped terms."""
