@@ -48,7 +48,7 @@ namespace {
 
 constexpr int SNW = NT / 32;     // warps per CTA
 #ifndef BR_SREC_F8
-#define BR_SREC_F8 320
+#define BR_SREC_F8 224
 #endif
 #ifndef BR_K8_MINB
 #define BR_K8_MINB 5
