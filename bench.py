@@ -50,7 +50,7 @@ def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
-    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--config", default="C4")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--split", type=int, default=0, help="sub-frame ranges per image (0 = auto)")
