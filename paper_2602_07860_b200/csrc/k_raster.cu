@@ -921,10 +921,14 @@ __device__ __forceinline__ void bwd_gather(Sm &S, const TauRec *rec, const Table
             m[3] = ul * g.x; m[4] = ul * g.y; m[5] = ul * g.z;
             m[6] = vl * g.x; m[7] = vl * g.y; m[8] = vl * g.z;
         }
+        // run heads (a lane whose key differs from the previous lane's) once, then each step adds the
+        // value d lanes up iff that lane is still in this lane's run: lane - d >= run start
+        const int kprev = __shfl_up_sync(0xffffffffu, key, 1);
+        const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || kprev != key);
+        const int run = lane - (31 - __clz(heads & (0xffffffffu >> (31 - lane))));   // lanes before this one in the run
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const int ku = __shfl_up_sync(0xffffffffu, key, d);
-            const bool take = lane >= d && ku == key;
+            const bool take = run >= d;
 #pragma unroll
             for (int q = 0; q < 9; ++q) {
                 const float v = __shfl_up_sync(0xffffffffu, m[q], d);
