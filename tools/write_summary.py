@@ -50,7 +50,8 @@ HISTORY = """| change | fwd ms | bwd ms | step ms | images/s |
 | K4 vis loop word countdown, (ul, vl) reloaded from shared memory (no per-word rematerialisation) | 7.48 | 7.09 | 15.24 | 1050 |
 | K4 footprint reach from per-column / per-row edge terms; K6 pixel info from shared memory | 7.10 | 7.01 | 14.78 | 1082 |
 | K6 won flags as group stamps; group sizes without integer division | 7.09 | 6.90 | 14.67 | 1091 |
-| K4 record stage 448 (re-tuned) | 7.06 | 6.90 | 14.63 | 1094 |"""
+| K4 record stage 448 (re-tuned) | 7.06 | 6.90 | 14.63 | 1094 |
+| K6 segmented scan with run heads from one ballot | 7.06 | 6.83 | 14.57 | 1098 |"""
 
 
 import csv  # noqa: E402
