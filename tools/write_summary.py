@@ -122,8 +122,9 @@ def main():
 
 Numbers from `tools/profile_round.sh` (+ the `--graph` lines), one gpurun call on a fresh box; this
 file is regenerated by `tools/write_summary.py`.  Raw files: `r1_launches_C4.csv` (ncu launch list),
-`r1_ncu_details_raster_C4.csv` (ncu --set full details of K4 and K6), `traffic.json` (DRAM bytes per
-launch, reported by bench.py as `roofline.traffic`).
+`r1_ncu_details_raster_C4.csv` (ncu --set full details of K4 and K6), `r1_ncu_details_soft_C3.csv`
+(the same for K8, K9C, K9 on C3), `traffic.json` (DRAM bytes per launch, reported by bench.py as
+`roofline.traffic`).
 
 ## Bench lines
 
