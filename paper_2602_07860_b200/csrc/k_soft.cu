@@ -51,7 +51,7 @@ constexpr int SNW = NT / 32;     // warps per CTA
 #define BR_SREC_F8 224
 #endif
 #ifndef BR_K8_MINB
-#define BR_K8_MINB 5
+#define BR_K8_MINB 6
 #endif
 #ifndef BR_K9C_MINB
 #define BR_K9C_MINB 4      // K9C (cached products) CTAs per SM
