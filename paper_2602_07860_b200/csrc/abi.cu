@@ -101,8 +101,11 @@ struct Plan {
     bool vis = false;      // BLUR_CACHE_VISIBILITY: K4 leaves the winning bin slot per (pixel, sub-frame)
     size_t o_vis = 0;
     size_t o_spz = 0;      // soft products K8 -> K9 (BLUR_CACHE_VISIBILITY with delta > 0)
+    bool spz_on = false;
     size_t total = 0;
 };
+
+bool legacy_env();
 
 int auto_chunk(const blur_motion &m, const blur_camera &c, int H, int W)
 {
@@ -135,6 +138,7 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
 {
     if (V < 0 || F < 0 || B < 0) return fail(BLUR_EINVAL, "V, F, B must be >= 0");
     if (F > 0 && V == 0) return fail(BLUR_EINVAL, "faces given but V == 0");
+    if (F > 4000000) return fail(BLUR_EINVAL, "F > 4,000,000 (the raster z-buffer key holds 22 bits of face index)");
     if (H < 1 || W < 1 || H > 32768 || W > 32768) return fail(BLUR_EINVAL, "H, W must be in [1, 32768]");
     if (B > 0 && !m) return fail(BLUR_EINVAL, "motions is NULL");
     P.B = B; P.V = V; P.F = F; P.H = H; P.W = W;
@@ -312,11 +316,13 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
         P.o_sbsum = o; o = align256(o + 8 * ((P.nbins + 1023) / 1024 + 1));
         P.o_sent = o; o = align256(o + 4 * (size_t)P.scap);
     }
-    P.vis = cfg && (cfg->flags & BLUR_CACHE_VISIBILITY) && (!cfg || cfg->solver == 0);
-    if (P.vis) {
-        P.o_vis = o; o = align256(o + 2 * (size_t)P.n_sub * P.T * TW * TH);
-        if (P.soft) { P.o_spz = o; o = align256(o + 4 * (size_t)P.n_sub * P.T * TW * TH); }
-    }
+    // BLUR_CACHE_VISIBILITY: the soft product cache K8 -> K9 (NEXT-1); the hard path's per-(pixel,
+    // sub-frame) winner buffer only for round 1's legacy kernels (the span raster recomputes winners)
+    const bool cache = cfg && (cfg->flags & BLUR_CACHE_VISIBILITY) && cfg->solver == 0;
+    P.vis = cache && legacy_env();
+    P.spz_on = cache && P.soft;
+    if (P.vis) { P.o_vis = o; o = align256(o + 2 * (size_t)P.n_sub * P.T * TW * TH); }
+    if (P.spz_on) { P.o_spz = o; o = align256(o + 4 * (size_t)P.n_sub * P.T * TW * TH); }
     P.total = o;
     return BLUR_OK;
 }
@@ -363,7 +369,8 @@ Tables make_tables(const Plan &P, void *ws)
         t.sb.sortcap = 4096;
     }
     if (P.vis) t.vis = (uint16_t *)(w + P.o_vis);
-    if (P.vis && P.soft) t.spz = (float *)(w + P.o_spz);
+    if (P.spz_on) t.spz = (float *)(w + P.o_spz);
+    t.legacy = legacy_env() ? 1 : 0;
     return t;
 }
 
@@ -404,6 +411,14 @@ int cuda_check(cudaError_t e, const char *what)
 {
     if (e != cudaSuccess) return fail(BLUR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
     return BLUR_OK;
+}
+
+// Raster kernels of the fast solver: BLURRAST_RASTER=span selects k_span.cu's span raster (A/B while it
+// is tuned), otherwise round 1's footprint-mask kernels (k_raster.cu)
+bool legacy_env()
+{
+    const char *s = std::getenv("BLURRAST_RASTER");
+    return !(s && std::strcmp(s, "span") == 0);
 }
 
 bool check_env()

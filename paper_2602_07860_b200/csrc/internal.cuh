@@ -86,6 +86,7 @@ struct Tables {          // device pointers into the workspace
     int NC, T, TX, TY;
     int B, V, F, H, W;
     int solver;          // 0 fast (Eq.8 coefficients), 1 naive per-frame setup, 2 naive per-pixel solve
+    int legacy;          // 1: the fast solver also takes k_raster.cu's footprint-mask kernels (A/B only)
     int splits;          // CTAs sharing one (image, tile) by sub-frame chunks (small launches)
     int ssplits;         // the same for the soft kernels K8/K9 (>= splits: their silhouette tiles
                          // are heavy, so splitting them shortens the launch's tail)
@@ -153,6 +154,12 @@ cudaError_t launch_raster_fwd(const Tables &t, float *out, int *ids, int ids_k,
                               unsigned long long *census, cudaStream_t st);
 cudaError_t launch_raster_bwd(const Tables &t, const float *grad_rgba, float *grad_colors,
                               cudaStream_t st);
+// round-1 footprint-mask raster kernels (k_raster.cu): the naive solvers of the NEXT-2 ablation, and the
+// fast solver when Tables::legacy is set (A/B)
+cudaError_t launch_raster_fwd_legacy(const Tables &t, float *out, int *ids, int ids_k,
+                                     unsigned long long *census, cudaStream_t st);
+cudaError_t launch_raster_bwd_legacy(const Tables &t, const float *grad_rgba, float *grad_colors,
+                                     cudaStream_t st);
 cudaError_t launch_vertex_chain(const Tables &t, float *grad_verts, cudaStream_t st);
 cudaError_t launch_split_reduce(const Tables &t, float *out, cudaStream_t st);
 cudaError_t launch_l2(const float *out, const float *tgt, long long n, long long n_norm, float *loss,
