@@ -931,6 +931,226 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
     }
 }
 
+// ------------------------------------------------------------------ backward without the visibility buffer
+//
+// k6_raster_bwd_fx recomputes the visibility with the forward's own stage + per-warp mask walk (the
+// winners are never stored in HBM), and reduces the nine moments of every staged (face,
+// sub-frame) record in fixed point: each pixel adds q = round(g * 2^e) and q * (x - TW/2), q * (TH/2 - y)
+// (g = dL/dI / N per channel; 2^e a power of two per tile with max |q| <= 2^19, so every sum of the
+// 256 pixels stays below 2^31) to its winner's slot with native 32-bit shared-memory atomics.  Integer
+// sums are exact and independent of the order the pixels arrive in (deterministic); the one rounding per
+// pixel is below 2^-20 of the tile's largest |g|.  The moments convert back (m0 = M0 2^-e, mu = Mu 2^-e sx,
+// mv = Mv 2^-e sy) and the closed form of face_grad gives each record's gradient; the slot's thread adds
+// it over the chunk's sub-frames, split (1 - tau, tau) onto the keyframes (Eq.5-6).
+
+template <int MODE>
+struct BwdFxSmem {
+    TauRec rec[SREC_B];
+    float4 vtx[MODE == 2 ? 3 * SREC_B : 1];
+    uint32_t wm[NFP * (SREC_B / 32 + GMAX_B)];
+    int sid[SREC_B];
+    int imom[SREC_B][10];    // fixed-point moments M0 (rgb), Mu (rgb), Mv (rgb) and the won count per record
+    int4 qg[TW * TH];        // the tile's fixed-point pixel gradients q (rgb)
+    float taus[GMAX_B];
+    int wsum[NWARP];
+    float red[NWARP];
+};
+
+// add the pixel's fixed-point moment terms to its winning record's slot
+__device__ __forceinline__ void add_moments(int *m, int4 q, int dx, int dy)
+{
+    atomicAdd(m + 0, q.x); atomicAdd(m + 1, q.y); atomicAdd(m + 2, q.z);
+    atomicAdd(m + 3, q.x * dx); atomicAdd(m + 4, q.y * dx); atomicAdd(m + 5, q.z * dx);
+    atomicAdd(m + 6, q.x * dy); atomicAdd(m + 7, q.y * dy); atomicAdd(m + 8, q.z * dy);
+    atomicAdd(m + 9, 1);
+}
+
+// read, clear and convert the fixed-point moments of one record (returns the won count)
+__device__ __forceinline__ int take_moments(int *m, float inv, float sx, float sy, float f[9])
+{
+    const int cnt = m[9];
+    if (cnt == 0) return 0;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        f[q] = (float)m[q] * inv;
+        f[3 + q] = (float)m[3 + q] * inv * sx;
+        f[6 + q] = (float)m[6 + q] * inv * sy;
+    }
+#pragma unroll
+    for (int q = 0; q < 10; ++q) m[q] = 0;
+    return cnt;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd_fx(Tables t, const float *__restrict__ grad,
+                                                                  float *__restrict__ dC)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BwdFxSmem<MODE> &S = *reinterpret_cast<BwdFxSmem<MODE> *>(smem_raw);
+    const int b = blockIdx.y, tile = blockIdx.x;
+    const ImgInfo &im = t.imgs[b];
+    const int N = im.N, c_begin = im.chunk_begin, c_end = im.chunk_end, sched_off = im.sched_off;
+    const long long rec_off = im.rec_off;
+    TileCtx tc;
+    tile_ctx(t, tile, tc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+    const int px = tc.px0 + lx, py = tc.py0 + ly;
+    const bool inimg = px < t.W && py < t.H;
+    const float ul = (float)(lx - TW / 2) * tc.sx;
+    const float vl = (float)(TH / 2 - ly) * tc.sy;
+    const int myp = ly * TW + lx;
+    // the tile's pixel gradients in fixed point: scale 2^e with max |g| 2^e < 2^19
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (inimg) {
+        g = __ldg(reinterpret_cast<const float4 *>(grad) + ((size_t)b * t.H + py) * t.W + px);
+        const float inv = 1.0f / (float)N;   // dI/dI_k = 1/N (uniform mean)
+        g.x *= inv; g.y *= inv; g.z *= inv;
+    }
+    float gm = fmaxf(fmaxf(fabsf(g.x), fabsf(g.y)), fabsf(g.z));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    if (lane == 0) S.red[warp] = gm;
+    for (int j = threadIdx.x; j < SREC_B * 10; j += NT) (&S.imom[0][0])[j] = 0;
+    __syncthreads();
+    gm = 0.f;
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) gm = fmaxf(gm, S.red[w]);
+    int ex = 0;
+    if (gm > 0.f) frexpf(gm, &ex);                 // gm = m 2^ex, m in [0.5, 1)
+    ex = min(max(ex, -100), 100);
+    const float scale = ldexpf(1.0f, 19 - ex), inv_scale = ldexpf(1.0f, ex - 19);
+    S.qg[myp] = make_int4(__float2int_rn(g.x * scale), __float2int_rn(g.y * scale), __float2int_rn(g.z * scale), 0);
+    const int dx = lx - TW / 2, dy = TH / 2 - ly;
+    unsigned long long d0 = 0, d1 = 0, d2 = 0;
+    __syncthreads();
+
+    for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
+        const Chunk ch = t.chunks[c];
+        const size_t bi = (size_t)c * t.T + tile;
+        const long long o = t.off[bi];
+        const int n = (int)(t.off[bi + 1] - o);
+        if (n == 0) continue;
+        BinCtx bc;
+        bc.status = t.status;
+        bc.rseg = t.rec + (size_t)(rec_off + (long long)ch.s * t.F) * REC_F4;
+        bc.key0 = t.key + im.key_off + (size_t)ch.s * t.V;
+        bc.key1 = bc.key0 + t.V;
+        bc.fcol = t.fcol;
+        bc.ent = t.entries + o;
+        bc.n = n;
+        bc.fb = o + n > t.cap;
+        if (!bc.fb && n <= SREC_B) {
+            const int Gs = min(GMAX_B, group_div(SREC_B, n)), nw = (n + 31) >> 5;
+            FaceAcc acc;
+            acc_zero(acc);
+            for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
+                const int ng = min(Gs, ch.k1 - kg);
+                clear_words(S.wm, ng * NFP * nw);
+                if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
+                __syncthreads();
+                stage_group<false, MODE, true>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, d2);
+                __syncthreads();
+                const int4 q = S.qg[myp];
+                for (int l = 0; l < ng; ++l) {       // visibility, then the pixel's moments (no barriers)
+                    float zbest = __int_as_float(0x7f800000);
+                    int ebest = -1, fbest = 0x7fffffff;
+                    const uint32_t *wml = S.wm + (l * NFP + fp_of(warp, lane)) * nw;
+                    bool tie = true;
+                    if (MODE != 2) tie = vis_mask_fast<false, MODE>(S.rec + l * n, wml, nw, ul, vl, zbest, ebest, d0, d1, false);
+                    if (__any_sync(0xffffffffu, tie)) {
+                        zbest = __int_as_float(0x7f800000);
+                        ebest = -1;
+                        vis_mask<false, MODE>(S.rec + l * n, S.vtx + 3 * l * n, wml, nw, 0, ul, vl, zbest, ebest, fbest,
+                                              d0, d1, false);
+                    }
+                    if (inimg && ebest >= 0) add_moments(S.imom[l * n + ebest], q, dx, dy);
+                }
+                __syncthreads();
+                for (int j = threadIdx.x; j < n; j += NT) {   // one thread per bin slot
+                    for (int l = 0; l < ng; ++l) {
+                        float m[9];
+                        if (take_moments(S.imom[l * n + j], inv_scale, tc.sx, tc.sy, m) == 0) continue;
+                        float dv[6], dcl[9];
+                        face_grad(S.rec[l * n + j], m, t.fcol, dv, dcl);
+                        const float tau = S.taus[l];
+                        if (j == (int)threadIdx.x) {
+#pragma unroll
+                            for (int i = 0; i < 6; ++i) {
+                                acc.k0[i] = __fmaf_rn(1.f - tau, dv[i], acc.k0[i]);
+                                acc.k1[i] = __fmaf_rn(tau, dv[i], acc.k1[i]);
+                            }
+#pragma unroll
+                            for (int i = 0; i < 9; ++i) acc.c[i] += dcl[i];
+                        } else {
+                            float a0[6], a1[6];
+#pragma unroll
+                            for (int i = 0; i < 6; ++i) { a0[i] = (1.f - tau) * dv[i]; a1[i] = tau * dv[i]; }
+                            flush(t, im, ch.s, S.rec[l * n + j].fid, a0, a1, dcl, dC);
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            if ((int)threadIdx.x < n) {   // persistent slot of this thread
+                bool nz = false;
+#pragma unroll
+                for (int i = 0; i < 9; ++i) nz |= acc.c[i] != 0.f;
+#pragma unroll
+                for (int i = 0; i < 6; ++i) nz |= (acc.k0[i] != 0.f) | (acc.k1[i] != 0.f);
+                if (nz) flush(t, im, ch.s, __ldg(bc.ent + threadIdx.x), acc.k0, acc.k1, acc.c, dC);
+            }
+        } else {
+            for (int k = ch.k0; k < ch.k1; ++k) {
+                const float tau = t.sched_tau[sched_off + k];
+                float zbest = __int_as_float(0x7f800000);
+                int ebest = -1, fbest = 0x7fffffff;
+                int base = 0, fpos = 0;
+                if (threadIdx.x == 0) S.taus[0] = tau;
+                while (true) {                         // visibility over all batches
+                    const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SREC_B, base, fpos, S.sid, S.wsum);
+                    if (nb == 0) break;
+                    const int nw = (nb + 31) >> 5;
+                    clear_words(S.wm, NFP * nw);
+                    __syncthreads();
+                    stage_group<false, MODE, true>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, d2);
+                    __syncthreads();
+                    vis_mask<false, MODE>(S.rec, S.vtx, S.wm + fp_of(warp, lane) * nw, nw, base, ul, vl, zbest, ebest, fbest, d0, d1,
+                                          false);
+                    if (ebest >= base) fbest = S.rec[ebest - base].fid;
+                    base += nb;
+                    __syncthreads();
+                }
+                if (!inimg) ebest = -1;
+                base = 0;
+                fpos = 0;
+                while (true) {                         // re-stage each batch, moments and gradients of its winners
+                    const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SREC_B, base, fpos, S.sid, S.wsum);
+                    if (nb == 0) break;
+                    const int nw = (nb + 31) >> 5;
+                    clear_words(S.wm, NFP * nw);
+                    __syncthreads();
+                    stage_group<false, MODE, true>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, d2);
+                    __syncthreads();
+                    if (ebest >= base && ebest < base + nb) add_moments(S.imom[ebest - base], S.qg[myp], dx, dy);
+                    __syncthreads();
+                    for (int j = threadIdx.x; j < nb; j += NT) {
+                        float m[9];
+                        if (take_moments(S.imom[j], inv_scale, tc.sx, tc.sy, m) == 0) continue;
+                        float dv[6], dcl[9], a0[6], a1[6];
+                        face_grad(S.rec[j], m, t.fcol, dv, dcl);
+#pragma unroll
+                        for (int i = 0; i < 6; ++i) { a0[i] = (1.f - tau) * dv[i]; a1[i] = tau * dv[i]; }
+                        flush(t, im, ch.s, S.rec[j].fid, a0, a1, dcl, dC);
+                    }
+                    base += nb;
+                    __syncthreads();
+                }
+            }
+        }
+    }
+}
+
 template <bool CENSUS, int MODE>
 static cudaError_t launch_fwd_t(const Tables &t, float *out, int *ids, int ids_k, unsigned long long *census,
                                 cudaStream_t st)
@@ -947,6 +1167,13 @@ template <int MODE>
 static cudaError_t launch_bwd_t(const Tables &t, const float *grad, float *dC, cudaStream_t st)
 {
     dim3 grid(t.T, t.B, t.splits);
+    if (!t.vis) {   // no visibility buffer: recompute, fixed-point moments
+        const int smem = (int)sizeof(BwdFxSmem<MODE>);
+        cudaError_t e = cudaFuncSetAttribute(k6_raster_bwd_fx<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        k6_raster_bwd_fx<MODE><<<grid, NT, smem, st>>>(t, grad, dC);
+        return cudaGetLastError();
+    }
     const int smem = (int)sizeof(BwdSmem<MODE>);
     cudaError_t e = cudaFuncSetAttribute(k6_raster_bwd<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;

@@ -57,23 +57,19 @@ static_assert(SP_SREC_F <= 1024 && SP_SREC_B <= 1024, "slot field of the z-buffe
 constexpr unsigned long long ZB_EMPTY = ~0ull;
 constexpr float SPAN_DLT = 1.0f / 1024.0f;   // px: boundaries closer than this to a pixel centre are re-tested
 
-struct __align__(16) SpanRec {   // a (face, sub-frame) record for this tile, 64 B
-    float a[3], b[3], g[3];      // sign-normalised edge functions e_i = a_i ul + b_i vl + g_i (tile-local)
-    float invD;                  // 1 / |det F(tau)|
-    int fid;
+struct __align__(16) SpanRec {   // a (face, sub-frame) record for this tile, 80 B
+    float b[3], g[3];            // sign-normalised edge functions e_i = a_i ul + b_i vl + g_i (tile-local)
+    float k[3];                  // -1 / (a_i sx) (0 where a_i = 0): edge i bounds a row at x = TW/2 + k_i R_i(v)
     int box;                     // x0 | x1 << 4 | y0 << 8 | y1 << 12 (tile-local pixel box) | l << 16 (sub-frame
-                                 // layer) | first run << 20; -1: no record
+                                 // layer); -1: no record
     float az, bz, cz;            // depth plane z = fma(az, ul, fma(bz, vl, cz)) (Q6)
     unsigned tag;                // z-buffer key low word: fid << 10 | slot j
+    float invD;                  // 1 / |det F(tau)|
+    int fid;
+    float a[3];
+    float pad;
 };
 static_assert(SP_GMAX <= 16, "layer field of SpanRec::box is 4 bits");
-static_assert(SP_SREC_F * TH <= 4096 && SP_SREC_B * TH <= 4096, "run index field of SpanRec::box is 12 bits");
-// a run: the exact covered pixels [lo, hi] of row y of record r: r << 12 | y << 8 | lo << 4 | hi (lo > hi: none)
-__device__ __forceinline__ unsigned run_word(int r, int y, int lo, int hi)
-{
-    return lo <= hi ? ((unsigned)r << 12) | ((unsigned)y << 8) | ((unsigned)lo << 4) | (unsigned)hi
-                    : ((unsigned)r << 12) | ((unsigned)y << 8) | 0x10u;   // lo = 1, hi = 0
-}
 
 // order-preserving map of a float onto uint32 (for the depth half of the z-buffer key)
 __device__ __forceinline__ unsigned zord(float z)
@@ -102,48 +98,34 @@ __device__ __forceinline__ bool cov_at(const float A[3], const float R[3], int x
 
 // Exact covered range of row y (tile-local x within [x0, x1]; lo > hi: none).
 //
-// Every edge function e_i(x) = fma(A_i, ul(x), R_i) of the row is monotone in x (a correctly rounded fma
-// of an increasing ul(x)), so the covered pixels form one interval, bounded below by the edges with
-// A_i > 0 and above by those with A_i < 0; an edge's boundary is x* = TW/2 - R_i / (A_i sx).  The record
-// carries these boundaries as lines in y (fast form, accurate to < 3e-4 px) -- or, for SLOW records (an
-// edge steeper than 500 px per row, |A_i sx| underflowing, three same-side edges), the row evaluates them
-// from R_i and k_i = -1/(A_i sx) -- and a range end that lies within SPAN_DLT of a pixel centre is
-// re-tested with the per-pixel arithmetic itself, scanning inward.  The result is exactly the set of
-// pixels of the row that pass cov_at.  Returns the number of exact tests taken (census).
-__device__ __forceinline__ int row_range(const float ln[8], bool slow, const SpanRec &Rec, int y, int x0, int x1,
-                                         const TileCtx &tc, int &lo, int &hi)
+// Every edge function e_i(x) = fma(A_i, ul(x), R_i) of the row (R_i = fma(B_i, vl, G_i)) is monotone in x
+// (a correctly rounded fma of an increasing ul(x)), so the covered pixels form one interval, bounded below
+// by the edges with A_i > 0 (k_i < 0) and above by those with A_i < 0 (k_i > 0); an edge's boundary is
+// x* = TW/2 + k_i R_i, k_i = -1 / (A_i sx).  Evaluated from the row's exact R_i it carries an error of a few
+// ulp of |x* - TW/2|, i.e. < 1e-5 px wherever the boundary is inside the tile (edges with A_i = 0 restrict
+// the record's rows instead, span_setup).  A range end within SPAN_DLT of a boundary is re-tested with the
+// per-pixel arithmetic itself, scanning inward, so the result is exactly the set of pixels of the row
+// that pass cov_at.  Returns the number of exact tests taken (census).
+__device__ __forceinline__ int row_range(const SpanRec &Rec, int y, int x0, int x1, const TileCtx &tc, int &lo,
+                                         int &hi)
 {
-    float L, U;
-    bool force = false;
-    if (!slow) {
-        const float yf = (float)y;
-        L = fmaxf(fmaf(ln[1], yf, ln[0]), fmaf(ln[3], yf, ln[2]));
-        U = fminf(fmaf(ln[5], yf, ln[4]), fmaf(ln[7], yf, ln[6]));
-    } else {   // per-edge boundaries from the row's exact R_i
-        const float vl = (float)(TH / 2 - y) * tc.sy;
-        L = -1000.5f;
-        U = 1000.5f;
+    const float vl = (float)(TH / 2 - y) * tc.sy;
+    float L = -100.5f, U = 116.5f;
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const float A = Rec.a[i], R = __fmaf_rn(Rec.b[i], vl, Rec.g[i]);
-            const float as = A * tc.sx;
-            if (fabsf(as) >= 1e-30f) {
-                const float t = fminf(fmaxf(fmaf(R, -__frcp_rn(as), (float)(TW / 2)), -100.5f), 116.5f);
-                if (A > 0.f) L = fmaxf(L, t); else U = fminf(U, t);
-            } else if (A != 0.f) {
-                force = true;                  // no usable bound: the ends are scanned inward exactly
-            } else if (R < 0.f) {
-                U = -1000.5f;                  // e_i = R_i < 0 on the whole row
-            }
-        }
+    for (int i = 0; i < 3; ++i) {
+        const float R = __fmaf_rn(Rec.b[i], vl, Rec.g[i]);
+        const float t = fmaf(R, Rec.k[i], (float)(TW / 2));
+        L = Rec.k[i] < 0.f ? fmaxf(L, t) : L;
+        U = Rec.k[i] > 0.f ? fminf(U, t) : U;
     }
+    L = fminf(L, 116.5f);
+    U = fmaxf(U, -100.5f);
     const float cl = ceilf(L - SPAN_DLT), ch = floorf(U + SPAN_DLT);
     lo = max((int)cl, x0);
     hi = min((int)ch, x1);
     int nt = 0;
-    if (lo <= hi && (force || cl <= L + SPAN_DLT || ch >= U - SPAN_DLT)) {
+    if (lo <= hi && (cl <= L + SPAN_DLT || ch >= U - SPAN_DLT)) {
         // a range end within SPAN_DLT of a boundary: move the ends inward with the exact test
-        const float vl = (float)(TH / 2 - y) * tc.sy;
         const float A[3] = {Rec.a[0], Rec.a[1], Rec.a[2]};
         const float R[3] = {__fmaf_rn(Rec.b[0], vl, Rec.g[0]), __fmaf_rn(Rec.b[1], vl, Rec.g[1]),
                             __fmaf_rn(Rec.b[2], vl, Rec.g[2])};
@@ -185,49 +167,35 @@ __device__ __forceinline__ void eval_tau(const FaceRec &fr, float tau, float D, 
     cz = __fmaf_rn(__fmaf_rn(G[1], dzb, G[2] * dzc), invD, za);
 }
 
-// Boundary lines of the record (see row_range) and the exact row range of the edges with A_i == 0
-// (e_i = R_i does not depend on x: rows with R_i < 0 are dropped from [y0, y1]).  Returns false when no
-// row is left.  slow: the lines are not used (see row_range).
-__device__ __forceinline__ bool span_lines(const float A[3], const float B[3], const float G[3], const TileCtx &tc,
-                                           int &y0, int &y1, float ln[8], bool &slow)
+// The row bounds of the record (see row_range): k_i = -1/(A_i sx), clamped to +-1e30 (finite even where
+// A_i sx underflows; the boundary of an edge with A_i ~ 0 lies far off the tile unless R_i ~ 0, and then
+// at TW/2, where it is), 0 for A_i = 0.  An edge with A_i = 0 has e_i = R_i on the whole row: rows with
+// R_i < 0 are dropped from [y0, y1] (R_i is monotone in the row).  Returns false when no row is left.
+__device__ __forceinline__ bool span_setup(const float A[3], const float B[3], const float G[3], const TileCtx &tc,
+                                           int &y0, int &y1, float K[3])
 {
-    int nl = 0, nu = 0;
-    slow = false;
-    float l0 = -1000.5f, l1 = 0.f, l2 = -1000.5f, l3 = 0.f, u0 = 1000.5f, u1 = 0.f, u2 = 1000.5f, u3 = 0.f;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
+        const float as = A[i] * tc.sx;
+        K[i] = as != 0.f ? fminf(fmaxf(-__frcp_rn(as), -1e30f), 1e30f) : 0.f;
         if (A[i] == 0.f) {
             while (y0 <= y1 && __fmaf_rn(B[i], (float)(TH / 2 - y0) * tc.sy, G[i]) < 0.f) ++y0;
             while (y0 <= y1 && __fmaf_rn(B[i], (float)(TH / 2 - y1) * tc.sy, G[i]) < 0.f) --y1;
-            continue;
-        }
-        // x*(y) = TW/2 - (B_i vl(y) + G_i) / (A_i sx), vl(y) = (TH/2 - y) sy: each term carries a few ulp
-        // of relative error, so lines with |T0| + 16 |TY| < 500 px are accurate to < 3e-4 px (< SPAN_DLT)
-        const float as = A[i] * tc.sx;
-        const float k = -__frcp_rn(as);
-        const float bs = B[i] * tc.sy;
-        const float f0 = fmaf(k, fmaf(bs, (float)(TH / 2), G[i]), (float)(TW / 2)), f1 = -k * bs;
-        if (!(fabsf(f0) + 16.f * fabsf(f1) < 500.f) || !(fabsf(as) >= 1e-30f)) slow = true;
-        if (A[i] > 0.f) {
-            if (nl == 0) { l0 = f0; l1 = f1; } else if (nl == 1) { l2 = f0; l3 = f1; } else slow = true;
-            ++nl;
-        } else {
-            if (nu == 0) { u0 = f0; u1 = f1; } else if (nu == 1) { u2 = f0; u3 = f1; } else slow = true;
-            ++nu;
         }
     }
-    ln[0] = l0; ln[1] = l1; ln[2] = l2; ln[3] = l3; ln[4] = u0; ln[5] = u1; ln[6] = u2; ln[7] = u3;
     return y0 <= y1;
 }
 
 __device__ __forceinline__ void store_rec(SpanRec &o, const float A[3], const float B[3], const float G[3], float invD,
-                                          int fid, int box, float az, float bz, float cz, unsigned tag)
+                                          int fid, int box, const float K[3], float az, float bz, float cz,
+                                          unsigned tag)
 {
     float4 *q = reinterpret_cast<float4 *>(&o);
-    q[0] = make_float4(A[0], A[1], A[2], B[0]);
-    q[1] = make_float4(B[1], B[2], G[0], G[1]);
-    q[2] = make_float4(G[2], invD, __int_as_float(fid), __int_as_float(box));
-    q[3] = make_float4(az, bz, cz, __uint_as_float(tag));
+    q[0] = make_float4(B[0], B[1], B[2], G[0]);
+    q[1] = make_float4(G[1], G[2], K[0], K[1]);
+    q[2] = make_float4(K[2], __int_as_float(box), az, bz);
+    q[3] = make_float4(cz, __uint_as_float(tag), invD, __int_as_float(fid));
+    q[4] = make_float4(A[0], A[1], A[2], 0.f);
 }
 
 struct WalkCount {
@@ -235,30 +203,26 @@ struct WalkCount {
 };
 
 // Stage the bin faces [base, base+nb) (or sid[] on the fallback path) at the ng sub-frames taus[0..ng):
-// one thread per (face j, sub-frame l) pair builds the record rec[l * nb + j] and the exact covered
-// range of every row of its pixel box (row_range), written as run words to runs[] (one slot per box row,
-// reserved with one shared atomic per warp).  Pairs without coverage get box = -1.  Work is spread
-// face-major, so lanes sharing a face load its (face, segment) record with broadcast loads.
+// one thread per (face j, sub-frame l) pair builds the record rec[l * nb + j] (edge functions, boundary
+// lines, depth plane) and appends one unit (record << 4 | row) per row of its pixel box to units[]
+// (one shared atomic per warp).  Pairs without coverage get box = -1.  Work is spread face-major, so
+// lanes sharing a face load its (face, segment) record with broadcast loads.
 template <bool CENSUS>
-__device__ __forceinline__ void stage_runs(const BinCtx &bc, int nb, int base, const float *taus, int ng,
-                                           const TileCtx &tc, int W, int H, int F, const int *sid, SpanRec *rec,
-                                           unsigned *runs, int *nruns, WalkCount &wc)
+__device__ __forceinline__ void stage_units(const BinCtx &bc, int nb, int base, const float *taus, int ng,
+                                            const TileCtx &tc, int W, int H, int F, const int *sid, SpanRec *rec,
+                                            uint16_t *units, int *nunits, WalkCount &wc)
 {
     const int lane = threadIdx.x & 31;
     const float inv_ng = 1.0f / (float)ng;
     const int npair = nb * ng;
     for (int p0 = 0; p0 < npair; p0 += NT) {   // block-uniform trip count: the warp scan below is convergent
         const int p = p0 + threadIdx.x;
-        int rows = 0, y0 = 0, r = 0, x0 = 0, x1 = -1, y1 = -1;
-        bool slow = false;
-        float ln[8];
-        SpanRec *out = nullptr;
-        int box = 0;
+        int rows = 0, y0 = 0, r = 0;
         if (p < npair) {
             const int j = div_small(p, inv_ng), l = p - j * ng;
             r = l * nb + j;
-            out = rec + r;
-            out->box = -1;
+            SpanRec &out = rec[r];
+            out.box = -1;
             const int f = bc.fb ? sid[j] : __ldg(bc.ent + base + j);
             if ((unsigned)f >= (unsigned)F) {     // never expected: bins hold valid face ids
                 atomicOr(bc.status, BLUR_ST_EINTERNAL);
@@ -267,6 +231,7 @@ __device__ __forceinline__ void stage_runs(const BinCtx &bc, int nb, int base, c
                 const float4 q6 = __ldg(rp + 6);
                 const float tau = taus[l];
                 const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);   // det F(tau), A8
+                int x0 = 0, x1 = -1, y1 = -1;
                 bool ok = __float_as_int(q6.w) >= 0 && fabsf(D) > EPS_D;          // skipped face; Q8
                 if (ok) {
                     const float4 b0 = __ldg(rp + 7), b1 = __ldg(rp + 8);
@@ -276,12 +241,12 @@ __device__ __forceinline__ void stage_runs(const BinCtx &bc, int nb, int base, c
                 if (ok) {
                     FaceRec fr;
                     load_rec(rp, fr);
-                    float A[3], B[3], G[3], invD, az, bz, cz;
+                    float A[3], B[3], G[3], invD, az, bz, cz, K[3];
                     eval_tau(fr, tau, D, tc, A, B, G, invD, az, bz, cz);
-                    if (span_lines(A, B, G, tc, y0, y1, ln, slow)) {
+                    if (span_setup(A, B, G, tc, y0, y1, K)) {
                         const int fid = __float_as_int(q6.w);
-                        box = x0 | (x1 << 4) | (y0 << 8) | (y1 << 12) | (l << 16);
-                        store_rec(*out, A, B, G, invD, fid, box, az, bz, cz, ((unsigned)fid << 10) | (unsigned)j);
+                        store_rec(out, A, B, G, invD, fid, x0 | (x1 << 4) | (y0 << 8) | (y1 << 12) | (l << 16), K, az,
+                                  bz, cz, ((unsigned)fid << 10) | (unsigned)j);
                         rows = y1 - y0 + 1;
                         if (CENSUS) wc.rec++;
                     }
@@ -296,47 +261,42 @@ __device__ __forceinline__ void stage_runs(const BinCtx &bc, int nb, int base, c
         }
         const int tot = __shfl_sync(0xffffffffu, incl, 31);
         int b0 = 0;
-        if (lane == 31 && tot > 0) b0 = atomicAdd(nruns, tot);
+        if (lane == 31 && tot > 0) b0 = atomicAdd(nunits, tot);
         b0 = __shfl_sync(0xffffffffu, b0, 31) + incl - rows;
-        if (rows > 0) out->box = box | (b0 << 20);
-        for (int k = 0; k < rows; ++k) {
-            int lo, hi;
-            const int nt = row_range(ln, slow, *out, y0 + k, x0, x1, tc, lo, hi);
-            if (CENSUS) { wc.test += nt; wc.frag += hi >= lo ? hi - lo + 1 : 0; }
-            runs[b0 + k] = run_word(r, y0 + k, lo, hi);
-        }
+        for (int k = 0; k < rows; ++k) units[b0 + k] = (uint16_t)((r << 4) | (y0 + k));
     }
 }
 
-// Walk the runs[0..nr): the covered pixels of each warp's 32 runs are spread evenly over its lanes
-// (rounds of 32 pixels: each lane finds the run its pixel belongs to from the runs' start positions in
-// the round and takes the run's data by shuffles), and every covered pixel offers its key
-// (order(depth) << 32 | fid << 10 | slot j) to the z-buffer layer of the record's sub-frame (64-bit
-// shared CAS min).  win: 32 ints per warp.
-__device__ __forceinline__ void walk_runs(const SpanRec *rec, const unsigned *runs, int nr, const TileCtx &tc,
-                                          unsigned long long *zb, int *wwin)
+// Walk the units[0..nu): one thread per (record, row) finds the row's exact covered range (row_range);
+// the covered pixels of each warp's 32 units are then spread evenly over its lanes (rounds of 32 pixels:
+// each lane finds the unit its pixel belongs to from the units' start positions in the round and takes
+// the unit's data by shuffles), and every covered pixel offers its key (order(depth) << 32 | fid << 10 |
+// slot j) to the z-buffer layer of the record's sub-frame (64-bit shared CAS min).  win: 32 ints per warp.
+template <bool CENSUS>
+__device__ __forceinline__ void walk_units(const SpanRec *rec, const uint16_t *units, int nu, const TileCtx &tc,
+                                           unsigned long long *zb, int *wwin, WalkCount &wc)
 {
     const int lane = threadIdx.x & 31;
     int *win = wwin + (threadIdx.x >> 5) * 32;
-    for (int u0 = 0; u0 < nr; u0 += NT) {   // block-uniform trip count (the warp collectives are convergent)
+    for (int u0 = 0; u0 < nu; u0 += NT) {   // block-uniform trip count (the warp collectives are convergent)
         const int u = u0 + (int)threadIdx.x;
         int lo = 0, cnt = 0, zoff = 0;
         float az = 0.f, rz = 0.f;
         unsigned tag = 0;
-        if (u < nr) {
-            const unsigned w = runs[u];
-            lo = (w >> 4) & 15;
-            cnt = max((int)(w & 15) - lo + 1, 0);
-            if (cnt > 0) {
-                const int r = (int)(w >> 12), y = (int)((w >> 8) & 15);
-                const SpanRec &R = rec[r];
-                const float4 zq = reinterpret_cast<const float4 *>(&R)[3];
-                const float vl = (float)(TH / 2 - y) * tc.sy;
-                az = zq.x;
-                rz = __fmaf_rn(zq.y, vl, zq.z);
-                tag = __float_as_uint(zq.w);
-                zoff = ((R.box >> 16) & 15) * (TW * TH) + y * TW;
-            }
+        if (u < nu) {
+            const unsigned e = units[u];
+            const int r = (int)(e >> 4), y = (int)(e & 15u);
+            const SpanRec &R = rec[r];
+            const int box = R.box;
+            int hi;
+            const int nt = row_range(R, y, box & 15, (box >> 4) & 15, tc, lo, hi);
+            cnt = hi >= lo ? hi - lo + 1 : 0;
+            if (CENSUS) { wc.test += nt; wc.frag += cnt; }
+            const float vl = (float)(TH / 2 - y) * tc.sy;
+            az = R.az;
+            rz = __fmaf_rn(R.bz, vl, R.cz);
+            tag = R.tag;
+            zoff = ((box >> 16) & 15) * (TW * TH) + y * TW;
         }
         int incl = cnt;
 #pragma unroll
@@ -347,8 +307,8 @@ __device__ __forceinline__ void walk_runs(const SpanRec *rec, const unsigned *ru
         const int tot = __shfl_sync(0xffffffffu, incl, 31);
         const int excl = incl - cnt;
         for (int f0 = 0; f0 < tot; f0 += 32) {
-            // runs starting in this round mark their start position; the other pixels of the round belong
-            // to the last run started before it (the carried one)
+            // units starting in this round mark their start position; the other pixels of the round belong
+            // to the last unit started before it (the carried one)
             const bool st = cnt > 0 && excl >= f0 && excl < f0 + 32;
             if (st) win[excl - f0] = lane;
             const unsigned P = __reduce_or_sync(0xffffffffu, st ? 1u << (excl - f0) : 0u);
@@ -375,12 +335,12 @@ __device__ __forceinline__ void walk_runs(const SpanRec *rec, const unsigned *ru
 struct SpFwdSmem {
     SpanRec rec[SP_SREC_F];
     unsigned long long zb[SP_GMAX][TW * TH];
-    unsigned runs[SP_SREC_F * TH];   // covered row ranges of the group's records (run_word)
+    uint16_t units[SP_SREC_F * TH];   // (record, row) work items of the group: record << 4 | row
     int sid[SP_SREC_F];
     float taus[SP_GMAX];
     int wsum[NWARP];
-    int nruns;
-    int win[NWARP * 32];   // walk_runs: per-warp owner windows
+    int nunits;
+    int win[NWARP * 32];   // walk_units: per-warp owner windows
     float4 acc[TW * TH];   // per-pixel (r, g, b, a) sums over the sub-frames (thread-private slot)
 };
 
@@ -405,9 +365,9 @@ __global__ void __launch_bounds__(NT, BR_SP_MINB_F) k4s_raster_fwd(Tables t, flo
 #define PIX (((size_t)b * t.H + py) * t.W + px)
     for (int l = 0; l < SP_GMAX; ++l) S.zb[l][threadIdx.x] = ZB_EMPTY;
     S.acc[myp] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (threadIdx.x == 0) S.nruns = 0;
+    if (threadIdx.x == 0) S.nunits = 0;
     WalkCount wc;
-    unsigned long long nshade = 0;
+    unsigned long long nshade = 0, ngroup = 0, npairs = 0, nsub = 0;
     __syncthreads();
 
     for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
@@ -437,13 +397,14 @@ __global__ void __launch_bounds__(NT, BR_SP_MINB_F) k4s_raster_fwd(Tables t, flo
             const int Gs = min(SP_GMAX, group_div(SP_SREC_F, n));
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
+                if (CENSUS) { ngroup++; npairs += n * ng; nsub += ng; }
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();
-                stage_runs<CENSUS>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.runs, &S.nruns, wc);
+                stage_units<CENSUS>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.units, &S.nunits, wc);
                 __syncthreads();
-                walk_runs(S.rec, S.runs, S.nruns, tc, &S.zb[0][0], S.win);
+                walk_units<CENSUS>(S.rec, S.units, S.nunits, tc, &S.zb[0][0], S.win, wc);
                 __syncthreads();
-                if (threadIdx.x == 0) S.nruns = 0;
+                if (threadIdx.x == 0) S.nunits = 0;
                 const float ul = (float)(lx - TW / 2) * tc.sx, vl = (float)(TH / 2 - ly) * tc.sy;
                 for (int l = 0; l < ng; ++l) {
                     const unsigned long long key = S.zb[l][myp];
@@ -481,11 +442,11 @@ __global__ void __launch_bounds__(NT, BR_SP_MINB_F) k4s_raster_fwd(Tables t, flo
                     const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SP_SREC_F, base, fpos, S.sid, S.wsum);
                     if (nb == 0) break;
                     __syncthreads();
-                    stage_runs<CENSUS>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.runs, &S.nruns, wc);
+                    stage_units<CENSUS>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.units, &S.nunits, wc);
                     __syncthreads();
-                    walk_runs(S.rec, S.runs, S.nruns, tc, &S.zb[0][0], S.win);
+                    walk_units<CENSUS>(S.rec, S.units, S.nunits, tc, &S.zb[0][0], S.win, wc);
                     __syncthreads();
-                    if (threadIdx.x == 0) S.nruns = 0;
+                    if (threadIdx.x == 0) S.nunits = 0;
                     const unsigned long long key = S.zb[0][myp];
                     if (key != prev) {   // the winner changed in this batch: shade it now (Eq.9)
                         const SpanRec &r = S.rec[(int)(key & 1023u)];
@@ -526,12 +487,17 @@ __global__ void __launch_bounds__(NT, BR_SP_MINB_F) k4s_raster_fwd(Tables t, flo
         atomicAdd(census + 1, nshade);
         atomicAdd(census + 2, wc.frag + wc.test);
         atomicAdd(census + 3, wc.rec);
+        if (threadIdx.x == 0) {   // grouped-path shape (diagnostics): groups, (face, sub-frame) pairs, sub-frames
+            atomicAdd(census + 5, ngroup);
+            atomicAdd(census + 6, npairs);
+            atomicAdd(census + 7, nsub);
+        }
     }
 }
 
 // ------------------------------------------------------------------ backward
 //
-// The z-buffer is rebuilt exactly as in the forward (stage_runs + walk_runs).  Then one thread per
+// The z-buffer is rebuilt exactly as in the forward (stage_units + walk_units).  Then one thread per
 // record (face j, sub-frame l) walks the record's rows again and sums the nine moments m = sum over its
 // won pixels of g (1, u, v), g = dL/dI / N (the pixel's key names this face and slot), into the
 // record's own shared slot (its boundary lines are not needed any more).  The face's gradient is linear
@@ -545,34 +511,32 @@ __global__ void __launch_bounds__(NT, BR_SP_MINB_F) k4s_raster_fwd(Tables t, flo
 struct SpBwdSmem {
     SpanRec rec[SP_SREC_B];
     unsigned long long zb[SP_GMAX_B][TW * TH];
-    unsigned runs[SP_SREC_B * TH];
+    uint16_t units[SP_SREC_B * TH];
     float mom[SP_SREC_B][10];   // per record: the nine moments of its won pixels and their count
     float4 g[TW * TH];          // dL/dI / N of the tile
     int sid[SP_SREC_B];
     float taus[SP_GMAX_B];
     int wsum[NWARP];
-    int nruns;
+    int nunits;
     int win[NWARP * 32];
 };
 
 // moments of the pixels record r won (key low word == tag, or with by_fid (batched path: slots repeat
-// across batches) key low word >> 10 == fid) over its runs, into mom[r]; returns the count
-__device__ __forceinline__ int rec_moments(const SpanRec &R, const unsigned *runs, bool by_fid,
-                                           const unsigned long long *zl, const float4 *g, const TileCtx &tc,
-                                           float *mo)
+// across batches) key low word >> 10 == fid) over its rows, into mo[0..9]; returns the count
+__device__ __forceinline__ int rec_moments(const SpanRec &R, bool by_fid, const unsigned long long *zl,
+                                           const float4 *g, const TileCtx &tc, float *mo)
 {
     const int box = R.box;
-    const int nrow = ((box >> 12) & 15) - ((box >> 8) & 15) + 1;
-    const unsigned *rw = runs + ((unsigned)box >> 20);
+    const int x0 = box & 15, x1 = (box >> 4) & 15, y0 = (box >> 8) & 15, y1 = (box >> 12) & 15;
     const unsigned tag = R.tag, fid = (unsigned)R.fid;
     float m[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) m[q] = 0.f;
     int cnt = 0;
     const unsigned *zw = reinterpret_cast<const unsigned *>(zl);
-    for (int k = 0; k < nrow; ++k) {
-        const unsigned w = rw[k];
-        const int y = (w >> 8) & 15, lo = (w >> 4) & 15, hi = w & 15;
+    for (int y = y0; y <= y1; ++y) {
+        int lo, hi;
+        row_range(R, y, x0, x1, tc, lo, hi);
         const float vl = (float)(TH / 2 - y) * tc.sy;
         for (int x = lo; x <= hi; ++x) {
             const int p = y * TW + x;
@@ -617,7 +581,7 @@ __global__ void __launch_bounds__(NT, BR_SP_MINB_B) k6s_raster_bwd(Tables t, con
         S.g[ly * TW + lx] = g;
     }
     for (int l = 0; l < SP_GMAX_B; ++l) S.zb[l][threadIdx.x] = ZB_EMPTY;
-    if (threadIdx.x == 0) S.nruns = 0;
+    if (threadIdx.x == 0) S.nunits = 0;
     __syncthreads();
     WalkCount wc;
 
@@ -643,17 +607,17 @@ __global__ void __launch_bounds__(NT, BR_SP_MINB_B) k6s_raster_bwd(Tables t, con
                 const int ng = min(Gs, ch.k1 - kg);
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();
-                stage_runs<false>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.runs, &S.nruns, wc);
+                stage_units<false>(bc, n, 0, S.taus, ng, tc, t.W, t.H, t.F, S.sid, S.rec, S.units, &S.nunits, wc);
                 __syncthreads();
-                walk_runs(S.rec, S.runs, S.nruns, tc, &S.zb[0][0], S.win);
+                walk_units<false>(S.rec, S.units, S.nunits, tc, &S.zb[0][0], S.win, wc);
                 __syncthreads();
                 for (int r = threadIdx.x; r < n * ng; r += NT) {   // moments, one thread per record
                     const SpanRec &R = S.rec[r];
                     if (R.box < 0) { S.mom[r][9] = 0.f; continue; }
-                    rec_moments(R, S.runs, false, &S.zb[(R.box >> 16) & 15][0], S.g, tc, S.mom[r]);
+                    rec_moments(R, false, &S.zb[(R.box >> 16) & 15][0], S.g, tc, S.mom[r]);
                 }
                 __syncthreads();
-                if (threadIdx.x == 0) S.nruns = 0;
+                if (threadIdx.x == 0) S.nunits = 0;
                 for (int l = 0; l < ng; ++l) S.zb[l][threadIdx.x] = ZB_EMPTY;
                 for (int j = threadIdx.x; j < n; j += NT) {        // gradients, one thread per bin face
                     for (int l = 0; l < ng; ++l) {
@@ -698,11 +662,11 @@ __global__ void __launch_bounds__(NT, BR_SP_MINB_B) k6s_raster_bwd(Tables t, con
                     const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SP_SREC_B, base, fpos, S.sid, S.wsum);
                     if (nb == 0) break;
                     __syncthreads();
-                    stage_runs<false>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.runs, &S.nruns, wc);
+                    stage_units<false>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.units, &S.nunits, wc);
                     __syncthreads();
-                    walk_runs(S.rec, S.runs, S.nruns, tc, &S.zb[0][0], S.win);
+                    walk_units<false>(S.rec, S.units, S.nunits, tc, &S.zb[0][0], S.win, wc);
                     __syncthreads();
-                    if (threadIdx.x == 0) S.nruns = 0;
+                    if (threadIdx.x == 0) S.nunits = 0;
                     base += nb;
                 }
                 base = 0;
@@ -711,13 +675,13 @@ __global__ void __launch_bounds__(NT, BR_SP_MINB_B) k6s_raster_bwd(Tables t, con
                     const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SP_SREC_B, base, fpos, S.sid, S.wsum);
                     if (nb == 0) break;
                     __syncthreads();
-                    stage_runs<false>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.runs, &S.nruns, wc);
+                    stage_units<false>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.units, &S.nunits, wc);
                     __syncthreads();
-                    if (threadIdx.x == 0) S.nruns = 0;
+                    if (threadIdx.x == 0) S.nunits = 0;
                     for (int j = threadIdx.x; j < nb; j += NT) {
                         const SpanRec &R = S.rec[j];
                         if (R.box < 0) continue;
-                        if (rec_moments(R, S.runs, true, &S.zb[0][0], S.g, tc, S.mom[j]) == 0) continue;
+                        if (rec_moments(R, true, &S.zb[0][0], S.g, tc, S.mom[j]) == 0) continue;
                         float dv[6], dc[9], a0[6], a1[6];
                         face_grad(R, S.mom[j], t.fcol, dv, dc);
 #pragma unroll

@@ -23,7 +23,7 @@ def _torch():
     return torch
 
 
-def gpu_render(sc, ids_k=-1, sub_range=None, max_chunk=0, bin_factor=0.0, G=None, reuse=True, cache=True):
+def gpu_render(sc, ids_k=-1, sub_range=None, max_chunk=0, bin_factor=0.0, G=None, reuse=True, cache=False):
     torch = _torch()
     from paper_2602_07860_b200 import BlurRenderer
     dev = torch.device("cuda:0")
@@ -286,8 +286,10 @@ def test_naive_solvers_match_oracle(solver):
 
 @pytest.mark.parametrize("cfg", ["C2", "C3"])
 def test_visibility_cache_equals_recompute(cfg):
-    """BLUR_CACHE_VISIBILITY (K6 reads K4's winner slots) gives the same image and gradients as
-    recomputing the visibility in K6 (and as a backward without the preceding forward)."""
+    """BLUR_CACHE_VISIBILITY (K6 reads K4's winner slots, float moments) gives the same image and
+    gradients as recomputing the visibility in K6 (k6_raster_bwd_fx: fixed-point moments, one rounding of
+    2^-20 of the tile's largest |g| per pixel, amplified by the closed form's cancellation for faces far
+    from the tile centre: ~1e-4 relative) and as a backward without the preceding forward."""
     sc = scenes.make(cfg).subset([0, 1])
     G = np.random.default_rng(3).normal(size=(sc.B, sc.H, sc.W, 4)).astype(np.float32) * 1e-4
     a = gpu_render(sc, G=G, cache=True)
@@ -295,7 +297,9 @@ def test_visibility_cache_equals_recompute(cfg):
     c = gpu_render(sc, G=G, cache=True, reuse=False)
     assert np.array_equal(a["rgba"], b["rgba"])
     for x in (b, c):
-        assert rel_l2(a["dv"], x["dv"]) < 1e-5 and rel_l2(a["dc"], x["dc"]) < 1e-5
+        ev, ec = rel_l2(x["dv"], a["dv"]), rel_l2(x["dc"], a["dc"])
+        print(cfg, "dV %.2e dC %.2e" % (ev, ec))
+        assert ev < 3e-4 and ec < 3e-4
 
 
 def test_exact_depth_ties_lower_face_index_wins():
