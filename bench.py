@@ -46,6 +46,15 @@ LAUNCHES_FWD, LAUNCHES_LOSS, LAUNCHES_BWD = 9, 1, 2
 LAUNCHES_SOFT_FWD, LAUNCHES_SOFT_BWD = 9, 2     # soft bins (7) + K8 + reduce; K9C (cached products) + K9
 
 
+def _free_port() -> int:
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    p = so.getsockname()[1]
+    so.close()
+    return p
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -58,6 +67,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the oracle sample")
+    p.add_argument("--ref-images", type=int, default=2, help="--impl reference: images per timed step")
     p.add_argument("--graph", action="store_true",
                    help="replay the step as a CUDA graph (launch-bound configs C1-C3; 1 GPU, no sub-frame split)")
     p.add_argument("--delta", type=float, default=0.0,
@@ -178,38 +188,81 @@ def cpu_baseline(sc, target_seconds: float, delta: float = 0.0):
             "seconds": t}
 
 
-def run_reference(args, rank, world):
+def workload_config(sc, args, world, split_groups=False, graph=False):
+    """The `config` object of the JSON line (both arms)."""
+    soft = args.delta > 0
+    return {"workload": sc.name, "images": sc.B, "H": sc.H, "W": sc.W, "faces": sc.F, "vertices": sc.V,
+            "subframes": int(sc.motion["n_sub"][0]), "segments": sorted({int(x) for x in sc.motion["n_seg"]}),
+            **({"delta": args.delta, "coverage": "soft (Eq.10-15)"} if soft else {}),
+            "parallelism": "image-sharded x%d" % world + (" + subframe split" if split_groups else ""),
+            "l2": "flushed (256 MB write) before every timed step",
+            **({"cuda_graph": True} if graph else {})}
+
+
+def run_reference(args, rank, world, out_json):
+    """The reference arm: the fp64 CPU oracle as it stands (binned, all host cores), one bounded sample
+    of the workload per step -- `sample_images` whole images (translational and rotational views in
+    turn), fwd + bwd, all sub-frames -- timed step by step.  ms_per_step is the measured time of one
+    such step; value = images processed / time."""
     if rank != 0:
         return
+    import oracle
     import scenes
     sc = scenes.make(args.config)
-    vals = []
-    for _ in range(args.warmup + args.steps):
-        vals.append(cpu_baseline(sc, max(2.0, args.cpu_seconds / max(1, args.steps)), args.delta))
-    cb = vals[-1]
-    timed = vals[args.warmup:]
-    v = len(timed) / sum(1.0 / x["value"] for x in timed)
+    cores = oracle.num_threads(0)
+    order = []
+    lo, hi = 0, sc.B - 1
+    while lo <= hi:                       # 0, B-1, 1, B-2, ... (both motion kinds)
+        order.append(lo)
+        if hi != lo:
+            order.append(hi)
+        lo, hi = lo + 1, hi - 1
+    m = max(1, min(sc.B, args.ref_images))
+    N = int(sc.motion["n_sub"][0])
+    times, pos = [], 0
+    for it in range(args.warmup + args.steps):
+        imgs = sorted(order[(pos + i) % len(order)] for i in range(m))
+        pos += m
+        sub = sc.subset(imgs)
+        t0 = time.perf_counter()
+        fw = oracle.render_fwd(sub, delta=args.delta)
+        G = 2.0 * (fw["rgba"] - (sub.target if sub.target is not None else 0.0)) / fw["rgba"].size
+        oracle.render_bwd(sub, G, delta=args.delta)
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    v = m * len(times) / tot
+    sample = ("fp64 oracle (binned%s) fwd+bwd of %d of the %d images of %s per step (all %d sub-frames), %d "
+              "timed steps: %.1f s on %d threads" % (", soft delta=%g" % args.delta if args.delta > 0 else "", m,
+                                                    sc.B, sc.name, N, len(times), tot, cores))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v * sc.B,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": sc.name, "images": sc.B, "H": sc.H, "W": sc.W,
-                                            "faces": sc.F, "subframes": int(sc.motion["n_sub"][0]),
-                                            **({"delta": args.delta} if args.delta > 0 else {})},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "oracle",
-                             "sample": cb["sample"]},
+            "data": "synthetic", "config": workload_config(sc, args, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=out_json, flush=True)
 
 
 # ------------------------------------------------------------------ main (ours)
 
+def _stdout_to_stderr():
+    """Route file descriptor 1 to stderr for the run (NCCL and CUDA libraries print banners on stdout)
+    and return a writer for the real stdout, which receives the one JSON line."""
+    real = os.dup(1)
+    sys.stdout.flush()
+    os.dup2(2, 1)
+    return os.fdopen(real, "w")
+
+
 def main():
     args = parse()
+    out_json = _stdout_to_stderr()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        run_reference(args, rank, world, out_json)
         return
     import torch
     import torch.distributed as dist
@@ -221,8 +274,15 @@ def main():
     assert torch.cuda.is_available(), "bench.py needs CUDA"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    # NCCL at every world size (a 1-rank group at N = 1): the timed step is the same product path,
+    # ShardedStep with its [dV || dC || loss] all-reduce, on one GPU and on eight
+    os.environ.setdefault("NCCL_DEBUG", "WARN")     # no version banner on stdout (one JSON line)
+    if world == 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+    dist.init_process_group("nccl", device_id=dev)
     sc = scenes.make(args.config)
     target = make_target(sc, dev, args.delta)
     verts = torch.tensor(sc.verts, device=dev)
@@ -233,7 +293,8 @@ def main():
         return BlurRenderer(s.faces, s.motion, s.cams, s.H, s.W, s.V, device=dev, sub_range=sub_range,
                             max_chunk=args.max_chunk, delta=args.delta)
 
-    step = ShardedStep(sc.motion["n_sub"], target, make_renderer, rank, world, split=args.split, device=dev)
+    step = ShardedStep(sc.motion["n_sub"], target, make_renderer, rank, world, split=args.split, device=dev,
+                       reduce=True)
     rend = step.renderer
     stream = torch.cuda.current_stream()
 
@@ -255,28 +316,9 @@ def main():
     flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
 
     def one_step(ev_f=None, ev_b=None, ev_sf=None, ev_sb=None):
-        if rend is None:
-            return step(verts, colors)
-        out = rend.forward(verts, colors, events=ev_f, soft_events=ev_sf)
-        for slot, g in step.groups:
-            part = out[slot].contiguous()
-            dist.all_reduce(part, group=g)
-            out[slot].copy_(part)
-        if all(u.k0 == 0 for u in step.mine):
-            loss, grads = rend.l2_loss_grad(out, step.targets, n_norm=step.n_norm)
-        else:
-            loss = torch.zeros(1, device=dev)
-            grads = torch.empty_like(out)
-            for i in range(len(step.images)):
-                li, gi = rend.l2_loss_grad(out[i:i + 1].contiguous(), step.targets[i:i + 1].contiguous(),
-                                           n_norm=step.n_norm)
-                loss += li * step.loss_mask[i]
-                grads[i].copy_(gi[0])
-        dv, dc = rend.backward(verts, colors, grads, reuse_setup=True, events=ev_b, soft_events=ev_sb)
-        flat = torch.cat([dv.reshape(-1), dc.reshape(-1), loss])
-        if world > 1:
-            dist.all_reduce(flat)
-        return flat
+        ev = {"fwd": ev_f, "bwd": ev_b, "soft_fwd": ev_sf, "soft_bwd": ev_sb} if ev_f is not None else None
+        loss, dv, dc = step(verts, colors, events=ev)
+        return loss
 
     graph = None
     if args.graph:
@@ -307,8 +349,7 @@ def main():
     evsf = [evpair() if soft else None for _ in range(K)]
     evsb = [evpair() if soft else None for _ in range(K)]
     clocks = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
+    dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)
@@ -318,8 +359,7 @@ def main():
         timed_step(evf[i], evb[i], evsf[i], evsb[i])
         ev_e[i].record(stream)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    dist.barrier()
     clk = clocks.stop()
     step_ms = [ev_s[i].elapsed_time(ev_e[i]) for i in range(K)]
     tot_ms = float(sum(step_ms))
@@ -333,8 +373,7 @@ def main():
     sf_ms = [evsf[i][0].elapsed_time(evsf[i][1]) for i in range(K)] if soft and rend is not None else [0.0]
     sb_ms = [evsb[i][0].elapsed_time(evsb[i][1]) for i in range(K)] if soft and rend is not None else [0.0]
     t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot_max = float(t.item())
     ms_per_step = tot_max / K
     value = sc.B / (ms_per_step / 1000.0)
@@ -353,15 +392,36 @@ def main():
                      float(np.mean(sb_ms)))]
     kname, flop, dur = max(kernels, key=lambda k: k[2])
     achieved = flop / (dur / 1000.0) / 1e12 if dur > 0 else 0.0
-    traffic = None
+    traffic, prof = None, {}
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(sc.name, {}).get(kname)
+            prof = json.load(open(tp)).get(sc.name, {})
+            traffic = prof.get(kname)
         except Exception:
-            traffic = None
+            traffic, prof = None, {}
+    hbm_peak, hbm_src = 6546.2, "MEASURED_PEAKS.json hbm_gbs (round 1 copy of the file)"
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        pass
+    # HBM side of the same kernel: the DRAM bytes ncu measured per launch over its live duration, and
+    # the algorithmic bytes (16 B/px written by the forward, 48 B/px read+written by loss
+    # and backward)
+    n_px = float(len(step.images)) * sc.H * sc.W
+    alg_bytes = (16.0 if kname.startswith(("k4", "k8")) else 48.0) * n_px
+    hbm = {"dram_bytes_per_launch": traffic, "algorithmic_bytes_per_launch": alg_bytes, "peak_gbs": hbm_peak,
+           "peak_source": hbm_src,
+           "achieved_gbs": (traffic / (dur / 1000.0) / 1e9) if (traffic and dur > 0) else None}
+    hbm["frac"] = hbm["achieved_gbs"] / hbm_peak if hbm["achieved_gbs"] else None
+    weff = prof.get("warp_efficiency", {}).get(kname)
     roofline = {"bound": "alu", "kernel": kname, "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
+                "hbm_frac": hbm["frac"], "hbm": hbm,
+                # active lanes per executed warp instruction / 32 (ncu, profiles/traffic.json): the whole
+                # kernel and its coverage-test loop
+                "warp_efficiency": weff,
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md nominal "
                                "SM count and clocks.max.sm)",
                 "fwd_raster_ms": f_avg, "bwd_raster_ms": b_avg,
@@ -424,8 +484,7 @@ def main():
         for _ in range(2):
             e2e_step()
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(K):
@@ -433,8 +492,7 @@ def main():
         b.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
         step.targets = saved
         e2e = {"value": sc.B / (float(te.item()) / K / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": int(h_verts.numel() * 4 + h_cols.numel() * 4 + h_tgt.numel() * 4),
@@ -450,13 +508,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": sc.name, "images": sc.B, "H": sc.H, "W": sc.W, "faces": sc.F,
-                           "vertices": sc.V, "subframes": n_sub,
-                           "segments": sorted({int(x) for x in sc.motion["n_seg"]}),
-                           **({"delta": args.delta, "coverage": "soft (Eq.10-15)"} if soft else {}),
-                           "parallelism": "image-sharded x%d" % world + ("" if not step.groups else " + subframe split"),
-                           "l2": "flushed (256 MB write) before every timed step",
-                           **({"cuda_graph": True} if graph is not None else {})},
+                "config": workload_config(sc, args, world, bool(step.groups), graph is not None),
                 "barycentric_evals_per_s": {"executed": cand * world / (ms_per_step / 1000.0),
                                             "necessary": nec * world / (ms_per_step / 1000.0),
                                             "note": "per-rank census x ranks (rank 0's counts)"},
@@ -464,10 +516,9 @@ def main():
                 "gpu_launches": (LAUNCHES_FWD + LAUNCHES_LOSS + LAUNCHES_BWD +
                                  (LAUNCHES_SOFT_FWD + LAUNCHES_SOFT_BWD if soft else 0)) * K,
                 "e2e": e2e, "cpu_baseline": cb}
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+        print(json.dumps(line), file=out_json, flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

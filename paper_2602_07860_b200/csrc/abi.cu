@@ -248,6 +248,8 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
         im.chunk_end = (int)P.chunks.size();
     }
     P.NC = (int)P.chunks.size();
+    if (P.NC > 65535)   // K3 launches one grid row per chunk (gridDim.y <= 65535)
+        return fail(BLUR_EINVAL, "more than 65535 sub-frame chunks in the batch (reduce B x N or raise max_chunk)");
     // each tile's sub-frame chunks are split over BR_HARD_SPLITS CTAs (more for small launches, few
     // tiles x images, so that the grid fills the 148 SMs); partial images are reduced in a fixed
     // order (deterministic).  The soft kernels split further (their silhouette tiles are heavy).

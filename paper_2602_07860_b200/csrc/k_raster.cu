@@ -954,6 +954,7 @@ struct BwdFxSmem {
     float taus[GMAX_B];
     int wsum[NWARP];
     float red[NWARP];
+    unsigned int won[SREC_B];   // cached visibility: group stamp of the (sub-frame, slot) pairs that won a pixel
 };
 
 // add the pixel's fixed-point moment terms to its winning record's slot
@@ -1023,6 +1024,8 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd_fx(Tables t, con
     S.qg[myp] = make_int4(__float2int_rn(g.x * scale), __float2int_rn(g.y * scale), __float2int_rn(g.z * scale), 0);
     const int dx = lx - TW / 2, dy = TH / 2 - ly;
     unsigned long long d0 = 0, d1 = 0, d2 = 0;
+    for (int j = threadIdx.x; j < SREC_B; j += NT) S.won[j] = 0xFFFFFFFFu;
+    unsigned int stamp = 0;   // group counter of the cached path (won flags)
     __syncthreads();
 
     for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
@@ -1040,7 +1043,62 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd_fx(Tables t, con
         bc.ent = t.entries + o;
         bc.n = n;
         bc.fb = o + n > t.cap;
-        if (!bc.fb && n <= SREC_B) {
+        if (MODE == 0 && t.vis && !bc.fb && n <= SREC_B) {
+            // visibility from the forward's buffer (BLUR_CACHE_VISIBILITY): the pixels add their moments
+            // to the slots they name, only the (face, sub-frame) pairs that won are staged
+            const int Gs = min(GMAX_B, group_div(SREC_B, n));
+            FaceAcc acc;
+            acc_zero(acc);
+            for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
+                const int ng = min(Gs, ch.k1 - kg);
+                ++stamp;
+                if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
+                const uint16_t *vrow = t.vis + ((size_t)(im.cov_off + kg) * t.T + tile) * (TW * TH) + myp;
+                const int4 q = S.qg[myp];
+                for (int l = 0; l < ng; ++l, vrow += (size_t)t.T * (TW * TH)) {
+                    const uint16_t v = *vrow;
+                    if (inimg && v != 0xFFFF) {
+                        S.won[l * n + v] = stamp;
+                        add_moments(S.imom[l * n + v], q, dx, dy);
+                    }
+                }
+                __syncthreads();
+                stage_won(bc, n, S.taus, ng, tc, t.F, S.won, stamp, S.rec);
+                __syncthreads();
+                for (int j = threadIdx.x; j < n; j += NT) {   // one thread per bin slot
+                    for (int l = 0; l < ng; ++l) {
+                        float m[9];
+                        if (take_moments(S.imom[l * n + j], inv_scale, tc.sx, tc.sy, m) == 0) continue;
+                        float dv[6], dcl[9];
+                        face_grad(S.rec[l * n + j], m, t.fcol, dv, dcl);
+                        const float tau = S.taus[l];
+                        if (j == (int)threadIdx.x) {
+#pragma unroll
+                            for (int i = 0; i < 6; ++i) {
+                                acc.k0[i] = __fmaf_rn(1.f - tau, dv[i], acc.k0[i]);
+                                acc.k1[i] = __fmaf_rn(tau, dv[i], acc.k1[i]);
+                            }
+#pragma unroll
+                            for (int i = 0; i < 9; ++i) acc.c[i] += dcl[i];
+                        } else {
+                            float a0[6], a1[6];
+#pragma unroll
+                            for (int i = 0; i < 6; ++i) { a0[i] = (1.f - tau) * dv[i]; a1[i] = tau * dv[i]; }
+                            flush(t, im, ch.s, S.rec[l * n + j].fid, a0, a1, dcl, dC);
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            if ((int)threadIdx.x < n) {
+                bool nz = false;
+#pragma unroll
+                for (int i = 0; i < 9; ++i) nz |= acc.c[i] != 0.f;
+#pragma unroll
+                for (int i = 0; i < 6; ++i) nz |= (acc.k0[i] != 0.f) | (acc.k1[i] != 0.f);
+                if (nz) flush(t, im, ch.s, __ldg(bc.ent + threadIdx.x), acc.k0, acc.k1, acc.c, dC);
+            }
+        } else if (!bc.fb && n <= SREC_B) {
             const int Gs = min(GMAX_B, group_div(SREC_B, n)), nw = (n + 31) >> 5;
             FaceAcc acc;
             acc_zero(acc);
@@ -1167,7 +1225,11 @@ template <int MODE>
 static cudaError_t launch_bwd_t(const Tables &t, const float *grad, float *dC, cudaStream_t st)
 {
     dim3 grid(t.T, t.B, t.splits);
-    if (!t.vis) {   // no visibility buffer: recompute, fixed-point moments
+#ifdef BR_K6_SORT
+    if (!t.vis) {   // round 1's counting-sort gather for the cached path (A/B builds)
+#else
+    if (true) {     // fixed-point moments (k6_raster_bwd_fx), visibility cached or recomputed
+#endif
         const int smem = (int)sizeof(BwdFxSmem<MODE>);
         cudaError_t e = cudaFuncSetAttribute(k6_raster_bwd_fx<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;

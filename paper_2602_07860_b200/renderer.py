@@ -22,10 +22,14 @@ class BlurRenderer:
     sub_range: optional int [B,2] half-open sub-frame ranges (sub-frame sharding).
     """
 
+    # BLUR_CACHE_VISIBILITY budget: the per-(pixel, sub-frame) winner index (2 B, +4 B of soft products)
+    # is kept between the forward and the backward only when it fits (C4: 0.84 GB; C5: 34 GB -> off)
+    CACHE_BUDGET_BYTES = 1 << 30
+
     def __init__(self, faces, motion: dict, cams, H: int, W: int, V: int, device="cuda",
                  sub_range=None, max_chunk: int = 0, bin_factor: float = 0.0, solver: int = 0,
                  delta: float = 0.0, soft_cut: float = 0.0, soft_exact: bool = False,
-                 soft_bin_factor: float = 0.0, cache_visibility: bool = True):
+                 soft_bin_factor: float = 0.0, cache_visibility: Optional[bool] = None):
         _lib.load()
         self.device = torch.device(device)
         self.faces = torch.as_tensor(np.asarray(faces.cpu() if torch.is_tensor(faces) else faces),
@@ -39,18 +43,30 @@ class BlurRenderer:
         self._motions = _lib.make_motions(motion)
         self._cams = _lib.make_cams(self.cams_np)
         self._sub = _lib.make_sub_range(sub_range)
+        self._tables_resident = False          # the schedule tables change with the ranges
         self.max_chunk = int(max_chunk)
         self.bin_factor = float(bin_factor)
         self.solver = int(solver)
         # soft background coverage (NEXT-1, Eq.10-15): delta > 0 enables it
         self.delta, self.soft_cut, self.soft_exact = float(delta), float(soft_cut), bool(soft_exact)
         self.soft_bin_factor = float(soft_bin_factor)
-        # K4 leaves the per-(pixel, sub-frame) winner slot for K6 (BLUR_CACHE_VISIBILITY)
+        # K4 leaves the per-(pixel, sub-frame) winner slot for K6 (BLUR_CACHE_VISIBILITY): None = on iff
+        # its size (2 B, + 4 B with soft coverage, per pixel of a 16-pixel-padded image and sub-frame)
+        # fits CACHE_BUDGET_BYTES; without it K6 recomputes the visibility (k6_raster_bwd_fx)
+        if cache_visibility is None:
+            px = ((self.H + 15) // 16 * 16) * ((self.W + 15) // 16 * 16)
+            need = int(self.N.sum()) * px * (6 if self.delta > 0 else 2)
+            cache_visibility = need <= self.CACHE_BUDGET_BYTES
         self.cache_flags = _lib.BLUR_CACHE_VISIBILITY if (cache_visibility and self.solver == 0) else 0
         self.auto_bins = bin_factor == 0.0 or (self.delta > 0 and soft_bin_factor == 0.0)
+        self.n_forward = 0
         self._alloc(self.bin_factor, self.soft_bin_factor)
 
     def _cfg(self, flags=0, census=None, events=None, soft_events=None):
+        # the host tables (schedule, poses, chunks) stay in this renderer's own workspace between calls
+        # with the same arguments: after the first upload every call skips the host->device copy
+        if self._tables_resident:
+            flags |= _lib.BLUR_TABLES_RESIDENT
         return _lib.make_config(self.max_chunk, flags | self.cache_flags, self.bin_factor, census, events, self.solver,
                                 self.delta,
                                 self.soft_cut, self.soft_exact, self.soft_bin_factor, soft_events)
@@ -58,12 +74,14 @@ class BlurRenderer:
     def _alloc(self, factor: float, soft_factor: float = 0.0):
         self.bin_factor = float(factor)
         self.soft_bin_factor = float(soft_factor)
+        self._tables_resident = False
         cfg = self._cfg()
         self.ws_bytes = _lib.blur_workspace_bytes(self.V, self.F, self.B, self.H, self.W, self._motions,
                                                   self._cams, self._sub, cfg)
         self.ws = None
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.ws[:256].zero_()
+        self._tables_resident = False
 
     def _autosize(self, verts, colors, out, ids, ids_subframe, census, stream, events, soft_events):
         """First forward: if a binning needed more entries than the default capacity, grow the
@@ -86,17 +104,20 @@ class BlurRenderer:
         workspace was sized for the ranges given at construction; narrower ranges (e.g. [0, 0) for the
         views outside an optimisation batch) fit in it."""
         self._sub = _lib.make_sub_range(sub_range)
+        self._tables_resident = False          # the schedule tables change with the ranges
 
     # -- forward / backward -------------------------------------------------------------
     def forward(self, verts: torch.Tensor, colors: torch.Tensor, out: Optional[torch.Tensor] = None,
                 ids: Optional[torch.Tensor] = None, ids_subframe: int = -1, census: Optional[torch.Tensor] = None,
                 stream=None, events=None, soft_events=None) -> torch.Tensor:
+        self.n_forward += 1     # the workspace now holds this call's setup (see _BlurFn.backward)
         if out is None:
             out = torch.empty((self.B, self.H, self.W, 4), dtype=torch.float32, device=self.device)
         cfg = self._cfg(0, census, events, soft_events)
         _lib.blur_render_fwd(verts, self.faces, colors, self._motions, self._cams, self.B, self.H, self.W, out,
                              self.ws, sub_range=self._sub, ids=ids, ids_subframe=ids_subframe, cfg=cfg,
                              stream=stream)
+        self._tables_resident = True
         if self.auto_bins:
             return self._autosize(verts, colors, out, ids, ids_subframe, census, stream, events, soft_events)
         return out
@@ -112,6 +133,7 @@ class BlurRenderer:
         _lib.blur_render_bwd(verts, self.faces, colors, self._motions, self._cams, self.B, self.H, self.W,
                              grad_rgba.contiguous(), grad_verts, grad_colors, self.ws, sub_range=self._sub, cfg=cfg,
                              stream=stream)
+        self._tables_resident = True
         return grad_verts, grad_colors
 
     def l2_loss_grad(self, out: torch.Tensor, target: torch.Tensor, n_norm: int = 0, loss=None, grad=None,
@@ -173,14 +195,18 @@ class _BlurFn(torch.autograd.Function):
     def forward(ctx, verts, colors, renderer: BlurRenderer):
         out = renderer.forward(verts.contiguous(), colors.contiguous())
         ctx.renderer = renderer
+        ctx.stamp = renderer.n_forward     # the forward whose setup (and visibility cache) the workspace holds
         ctx.save_for_backward(verts, colors)
         return out
 
     @staticmethod
     def backward(ctx, grad_out):
         verts, colors = ctx.saved_tensors
+        # reuse the workspace's keyframes / coefficients / bins (and visibility cache) only if no other
+        # forward ran on this renderer since this one; otherwise the backward rebuilds its own setup
+        reuse = ctx.renderer.n_forward == ctx.stamp
         dv, dc = ctx.renderer.backward(verts.contiguous(), colors.contiguous(), grad_out.contiguous(),
-                                       reuse_setup=True)
+                                       reuse_setup=reuse)
         return dv, dc, None
 
 

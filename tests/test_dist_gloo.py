@@ -99,13 +99,35 @@ def test_partition_rules():
     assert all(len(rs) == 2 for _, rs in split_groups(parts))
 
 
-@pytest.mark.parametrize("B,split", [(4, 0), (1, 0), (3, 2)])
+@pytest.mark.parametrize("B,split", [(4, 0), (1, 0), (3, 2), (2, 4)])
 def test_sharded_step_equals_single_process(B, split):
+    """world 2; split 4 > world is clamped to 2 (one sub-frame range per image and rank)."""
     ref_loss, ref_dv, ref_dc = [t.numpy() for t in _reference(_scene(B))]
     res = _run(B, split)
     for rank, loss, dv, dc, ngroups in res:
         assert np.allclose(loss, ref_loss, rtol=1e-12, atol=1e-15)
         assert np.allclose(dv, ref_dv, rtol=1e-10, atol=1e-13)
         assert np.allclose(dc, ref_dc, rtol=1e-10, atol=1e-13)
-    if B == 1:
-        assert all(r[4] == 1 for r in res)               # the image is split across both ranks
+    if B == 1 or split >= 2:
+        # every split image is shared by ranks {0, 1}: one group, all its images in one all-reduce
+        assert all(r[4] == 1 for r in res)
+
+
+def test_split_at_world_one_is_the_unsplit_step():
+    """world 1 with split 2: clamped to one range per image, equal to the plain step."""
+    sc = _scene(2)
+    ref = [t.numpy() for t in _reference(sc)]
+    step = ShardedStep(sc.motion["n_sub"], torch.tensor(sc.target, dtype=torch.float64),
+                       lambda im, sr: OracleRenderer(sc, im, sr), 0, 1, split=2)
+    assert [(u.k0, u.k1) for u in step.mine] == [(0, 6), (0, 6)] and not step.groups
+    got = [t.numpy() for t in step(torch.tensor(sc.verts, dtype=torch.float64),
+                                   torch.tensor(sc.colors, dtype=torch.float64))]
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
+
+
+def test_partition_split_clamped_and_groups_per_rank_set():
+    parts = partition([6] * 4, 2, split=4)
+    assert all(len({u.image for u in p}) == len(p) for p in parts)      # one range per image and rank
+    assert [(u.k0, u.k1) for u in parts[0]] == [(0, 3)] * 4 and [(u.k0, u.k1) for u in parts[1]] == [(3, 6)] * 4
+    assert {tuple(rs) for _, rs in split_groups(parts)} == {(0, 1)}

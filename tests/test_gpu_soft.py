@@ -216,3 +216,16 @@ def test_soft_c4_full_size_sampled_fwd_and_grad():
           rel_l2(got["dv"], rdv), "dC rel", rel_l2(got["dc"], rdc))
     assert (~ref["amb_win"]).sum() > 0.5 * len(pick) and np.linalg.norm(rdv) > 0
     assert rel_l2(got["dv"], rdv) < TOL_GRAD and rel_l2(got["dc"], rdc) < TOL_GRAD
+
+
+def test_soft_c4_two_full_views_subframe_window():
+    """Soft coverage (delta = 1e-4) on two complete C4 views (one translational, one rotational; every
+    pixel of 512^2) against the oracle, over a window of 8 of the 100 sub-frames (mid exposure, k = 46..53): the oracle
+    sums every face for every uncovered (pixel, sub-frame) (no cut-off, ~1e9 soft terms per view and
+    sub-frame window), so all 100 sub-frames of both views (~5 CPU-minutes on the box) would dominate
+    the suite; the window keeps the comparison complete in space.  The GPU renders in the bench's
+    per-image configuration (same bins, chunking and soft splits)."""
+    sc = scenes.make_c4().subset([2, 11])
+    r = check_soft(sc, 1e-4, sub_range=[[46, 54], [46, 54]], ids_k=50)
+    print(r)
+    assert r["soft_pixels"] > 1000

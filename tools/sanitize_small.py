@@ -1,5 +1,6 @@
 """Small fwd+bwd runs for compute-sanitizer (C1, a C2 view, a ragged random scene, the fallback path)."""
 import sys
+import os
 sys.path.insert(0, "."); sys.path.insert(0, "tests")
 import numpy as np
 import scenes
@@ -32,3 +33,12 @@ rec = Recovery(tv.astype(np.float32), f, np.full((len(tv), 3), 0.5, np.float32),
 for _ in range(3):
     rec.step()
 print("recovery", rec.loss_values(), flush=True)
+# the span raster kernels (k_span.cu, BLURRAST_RASTER=span: read per call by the library)
+os.environ["BLURRAST_RASTER"] = "span"
+for sc in [scenes.make_c1(), scenes.make_c2().subset([1]),
+           scenes.random_mesh_scene(40, 5, H=37, W=53, motion=scenes.rotate((0.2, 1, 0.3), 1.2, N=9, S=4))]:
+    G = np.random.default_rng(0).normal(size=(sc.B, sc.H, sc.W, 4)) * 1e-3
+    r = gpu_render(sc, ids_k=1, G=G)
+    print("span", sc.name, "status", r["status"], "sum", float(r["rgba"].sum()), flush=True)
+r = gpu_render(scenes.make_c2().subset([2]), ids_k=1, G=np.ones((1, 256, 256, 4)) * 1e-4, bin_factor=1e-9)
+print("span fallback status", r["status"], flush=True)
