@@ -47,7 +47,7 @@ __device__ __forceinline__ void load_rec(const float4 *__restrict__ r, FaceRec &
 
 // Fallback batch builder: faces whose per-tau box overlaps the tile, in index order, from fpos on.
 // Block-uniform.  Returns the batch size (0 when all faces are consumed).
-static __device__ __noinline__ int fallback_fill(const float4 *__restrict__ rseg, int F, float tau, const TileCtx &tc, int W, int H,
+static __device__ int fallback_fill(const float4 *__restrict__ rseg, int F, float tau, const TileCtx &tc, int W, int H,
                              int cap, int &fpos, int *sid, int *swsum)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -153,13 +153,14 @@ def test_soft_backward_without_reuse_and_delta_zero():
 @pytest.mark.parametrize("cfg", ["C2", "C3"])
 def test_soft_product_cache_equals_recompute(cfg):
     """BLUR_CACHE_VISIBILITY with delta > 0: K9 reads the products K8 left per (sub-frame, pixel)
-    instead of recomputing them; same gradients as the recomputing backward."""
+    instead of recomputing them; same gradients as the recomputing backward (the hard part of which takes
+    the fixed-point moments of k6_raster_bwd_fx: ~1e-5 relative, see test_visibility_cache_equals_recompute)."""
     sc = scenes.make(cfg).subset([0, 1])
     G = np.random.default_rng(5).normal(size=(sc.B, sc.H, sc.W, 4)).astype(np.float32) * 1e-4
     a = gpu_soft(sc, 1e-4, G=G, cache=True)
     b = gpu_soft(sc, 1e-4, G=G, cache=False)
     assert np.array_equal(a["rgba"], b["rgba"])
-    assert rel_l2(a["dv"], b["dv"]) < 1e-6 and rel_l2(a["dc"], b["dc"]) < 1e-6
+    assert rel_l2(a["dv"], b["dv"]) < 3e-4 and rel_l2(a["dc"], b["dc"]) < 3e-4
 
 
 def test_soft_forward_is_deterministic():
