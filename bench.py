@@ -269,6 +269,7 @@ def main():
 
     import scenes
     from paper_2602_07860_b200 import BlurRenderer, _lib
+    from paper_2602_07860_b200.renderer import cache_bytes_per_image
     from paper_2602_07860_b200.dist import ShardedStep
 
     assert torch.cuda.is_available(), "bench.py needs CUDA"
@@ -288,13 +289,16 @@ def main():
     verts = torch.tensor(sc.verts, device=dev)
     colors = torch.tensor(sc.colors, device=dev)
 
-    def make_renderer(images, sub_range):
+    def make_renderer(images, sub_range, workspace=None):
         s = sc.subset(images)
         return BlurRenderer(s.faces, s.motion, s.cams, s.H, s.W, s.V, device=dev, sub_range=sub_range,
-                            max_chunk=args.max_chunk, delta=args.delta)
+                            max_chunk=args.max_chunk, delta=args.delta, workspace=workspace)
 
+    # whole images in passes whose backward winner index fits the cache budget (C5: 2 images per pass)
+    per_image = cache_bytes_per_image(sc.H, sc.W, int(max(sc.motion["n_sub"])), args.delta)
+    pass_images = max(1, BlurRenderer.CACHE_BUDGET_BYTES // per_image) if not args.graph else 0
     step = ShardedStep(sc.motion["n_sub"], target, make_renderer, rank, world, split=args.split, device=dev,
-                       reduce=True)
+                       reduce=True, pass_images=pass_images)
     rend = step.renderer
     stream = torch.cuda.current_stream()
 
@@ -302,7 +306,7 @@ def main():
     census = torch.zeros(8, dtype=torch.int64, device=dev)
     units = np.zeros(8)
     if rend is not None:
-        rend.forward(verts, colors, census=census)
+        step.census(verts, colors, census)
         units = census.cpu().numpy().astype(np.float64)
     n_fsub = float(sum(u.k1 - u.k0 for u in step.mine)) * sc.F      # (face, sub-frame) evaluations
 
@@ -316,13 +320,14 @@ def main():
     flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
 
     def one_step(ev_f=None, ev_b=None, ev_sf=None, ev_sb=None):
+        # events: lists of CUDA event pairs, one per pass
         ev = {"fwd": ev_f, "bwd": ev_b, "soft_fwd": ev_sf, "soft_bwd": ev_sb} if ev_f is not None else None
         loss, dv, dc = step(verts, colors, events=ev)
         return loss
 
     graph = None
     if args.graph:
-        if rend is None or step.groups or world > 1:
+        if rend is None or step.groups or world > 1 or step.n_passes > 1:
             raise SystemExit("--graph needs 1 GPU and no sub-frame split")
         graph = rend.capture_step(verts, colors, step.targets, n_norm=step.n_norm)
 
@@ -343,11 +348,12 @@ def main():
     K = args.steps
     ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    evf = [evpair() for _ in range(K)]
-    evb = [evpair() for _ in range(K)]
+    npass = step.n_passes
+    evf = [[evpair() for _ in range(npass)] for _ in range(K)]
+    evb = [[evpair() for _ in range(npass)] for _ in range(K)]
     soft = args.delta > 0
-    evsf = [evpair() if soft else None for _ in range(K)]
-    evsb = [evpair() if soft else None for _ in range(K)]
+    evsf = [[evpair() for _ in range(npass)] if soft else None for _ in range(K)]
+    evsb = [[evpair() for _ in range(npass)] if soft else None for _ in range(K)]
     clocks = ClockSampler(local)
     dist.barrier()
     torch.cuda.synchronize()
@@ -368,10 +374,12 @@ def main():
             flush_buf.zero_()
             one_step(evf[i], evb[i], evsf[i], evsb[i])
         torch.cuda.synchronize()
-    fwd_ms = [evf[i][0].elapsed_time(evf[i][1]) for i in range(K)] if rend is not None else [0.0]
-    bwd_ms = [evb[i][0].elapsed_time(evb[i][1]) for i in range(K)] if rend is not None else [0.0]
-    sf_ms = [evsf[i][0].elapsed_time(evsf[i][1]) for i in range(K)] if soft and rend is not None else [0.0]
-    sb_ms = [evsb[i][0].elapsed_time(evsb[i][1]) for i in range(K)] if soft and rend is not None else [0.0]
+    def span(pairs):   # summed over the passes of a step
+        return sum(a.elapsed_time(b) for a, b in pairs)
+    fwd_ms = [span(evf[i]) for i in range(K)] if rend is not None else [0.0]
+    bwd_ms = [span(evb[i]) for i in range(K)] if rend is not None else [0.0]
+    sf_ms = [span(evsf[i]) for i in range(K)] if soft and rend is not None else [0.0]
+    sb_ms = [span(evsb[i]) for i in range(K)] if soft and rend is not None else [0.0]
     t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot_max = float(t.item())
@@ -508,7 +516,10 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": workload_config(sc, args, world, bool(step.groups), graph is not None),
+                "config": {**workload_config(sc, args, world, bool(step.groups), graph is not None),
+                           **({"passes_per_rank": step.n_passes,
+                               "visibility_cache": "per pass, <= %d MiB" % (BlurRenderer.CACHE_BUDGET_BYTES >> 20)}
+                              if step.n_passes > 1 else {})},
                 "barycentric_evals_per_s": {"executed": cand * world / (ms_per_step / 1000.0),
                                             "necessary": nec * world / (ms_per_step / 1000.0),
                                             "note": "per-rank census x ranks (rank 0's counts)"},

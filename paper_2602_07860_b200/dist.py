@@ -74,10 +74,15 @@ class ShardedStep:
     l2_loss_grad(out, target, n_norm) -> (loss[1], grad) and
     backward(verts, colors, grad, reuse_setup=True) -> (dV, dC), all on `device`.
     reduce: run the collectives even at world size 1 (the bench does, so that NCCL is exercised).
+    pass_images: when > 0 and smaller than this rank's image count (and no image is split), the rank
+    runs its images in passes of that many -- fwd -> loss -> bwd per pass, gradients summed -- with
+    renderers made as make_renderer(images, sub_range, workspace=arena) that share one workspace, so
+    that the backward's per-(pixel, sub-frame) winner index of a pass fits a memory budget
+    (BlurRenderer.CACHE_BUDGET_BYTES; cache_bytes_per_image).
     """
 
     def __init__(self, n_sub: Sequence[int], targets: torch.Tensor, make_renderer: Callable, rank: int,
-                 world: int, split: int = 0, device="cpu", reduce: bool = None):
+                 world: int, split: int = 0, device="cpu", reduce: bool = None, pass_images: int = 0):
         self.rank, self.world = rank, world
         self.reduce = (world > 1) if reduce is None else reduce
         self.parts = partition(n_sub, world, split)
@@ -87,7 +92,17 @@ class ShardedStep:
         B = len(n_sub)
         self.n_norm = int(B * int(np.prod(targets.shape[1:])))        # mean over the whole batch
         self.targets = targets[self.images].contiguous() if self.images else targets[:0]
-        self.renderer = make_renderer(self.images, [[u.k0, u.k1] for u in self.mine]) if self.images else None
+        whole = all(u.k0 == 0 and u.k1 == int(n_sub[u.image]) for u in self.mine)
+        npass = len(self.images) if not (0 < pass_images < len(self.images) and whole) else pass_images
+        self.passes = [list(range(i, min(i + npass, len(self.images)))) for i in range(0, len(self.images), max(npass, 1))]
+        if len(self.passes) > 1:
+            from .renderer import WorkspaceArena
+            arena = WorkspaceArena(device)
+            self.renderers = [make_renderer([self.images[i] for i in p], [[self.mine[i].k0, self.mine[i].k1] for i in p],
+                                            workspace=arena) for p in self.passes]
+        else:
+            self.renderers = [make_renderer(self.images, [[u.k0, u.k1] for u in self.mine])] if self.images else []
+        self.renderer = self.renderers[0] if self.renderers else None
         # loss is counted once per image: by the co-owner holding k0 == 0
         self.loss_mask = torch.tensor([1.0 if u.k0 == 0 else 0.0 for u in self.mine], dtype=targets.dtype,
                                       device=device)
@@ -105,6 +120,45 @@ class ShardedStep:
                     slots = torch.tensor([self.images.index(b) for b in imgs], dtype=torch.long, device=device)
                     self.groups.append((slots, g))
 
+    @staticmethod
+    def _pick(ev, key, p):
+        """events[key] is a list of CUDA event pairs, one per pass (or None)."""
+        e = ev.get(key)
+        return e[p] if e else None
+
+    @property
+    def n_passes(self) -> int:
+        return len(self.passes)
+
+    def census(self, verts: torch.Tensor, colors: torch.Tensor, census: torch.Tensor) -> None:
+        """Algorithmic unit counts of this rank's forward (summed over the passes) into `census`."""
+        for r in self.renderers:
+            r.forward(verts, colors, census=census)
+
+    def _passes(self, verts, colors, targets_ready, ev):
+        """Whole images in passes sharing one workspace: fwd -> loss -> bwd per pass, sums accumulated."""
+        V = verts.shape[0]
+        dv = torch.zeros(V, 3, dtype=verts.dtype, device=self.device)
+        dc = torch.zeros(V, 3, dtype=verts.dtype, device=self.device)
+        loss = torch.zeros(1, dtype=verts.dtype, device=self.device)
+
+        pick = self._pick
+        for p, (slots, r) in enumerate(zip(self.passes, self.renderers)):
+            out = r.forward(verts, colors, events=pick(ev, "fwd", p), soft_events=pick(ev, "soft_fwd", p))
+            if p == 0 and targets_ready is not None:
+                torch.cuda.current_stream().wait_event(targets_ready)
+            tg = self.targets[slots[0]:slots[-1] + 1]
+            lp, g = r.l2_loss_grad(out, tg, n_norm=self.n_norm)
+            dvp, dcp = r.backward(verts, colors, g, reuse_setup=True, events=pick(ev, "bwd", p),
+                                  soft_events=pick(ev, "soft_bwd", p))
+            dv += dvp
+            dc += dcp
+            loss += lp
+        flat = torch.cat([dv.reshape(-1), dc.reshape(-1), loss])
+        if self.reduce:
+            dist.all_reduce(flat)
+        return flat[-1:], flat[:3 * V].reshape(V, 3), flat[3 * V:6 * V].reshape(V, 3)
+
     def reduce_partials(self, out: torch.Tensor) -> None:
         """Sum the partial images of the split images over their co-owners: one all-reduce per group
         of ranks, all of the group's images at once."""
@@ -116,15 +170,15 @@ class ShardedStep:
     def __call__(self, verts: torch.Tensor, colors: torch.Tensor, targets_ready=None, events=None):
         """targets_ready: optional CUDA event after which self.targets is valid (a loader copying the
         next observed images on another stream overlaps that copy with the forward pass).
-        events: optional dict of CUDA event pairs recorded around the raster kernels ("fwd", "bwd",
-        "soft_fwd", "soft_bwd"; see BlurRenderer.forward / backward)."""
+        events: optional dict ("fwd", "bwd", "soft_fwd", "soft_bwd") of lists of CUDA event pairs, one
+        pair per pass, recorded around the raster kernels (see BlurRenderer.forward / backward)."""
         ev = events or {}
         V = verts.shape[0]
+        if len(self.passes) > 1:
+            return self._passes(verts, colors, targets_ready, ev)
         if self.renderer is not None:
-            if ev:
-                out = self.renderer.forward(verts, colors, events=ev.get("fwd"), soft_events=ev.get("soft_fwd"))
-            else:
-                out = self.renderer.forward(verts, colors)
+            out = self.renderer.forward(verts, colors, events=self._pick(ev, "fwd", 0),
+                                        soft_events=self._pick(ev, "soft_fwd", 0))
             if targets_ready is not None:
                 torch.cuda.current_stream().wait_event(targets_ready)
             self.reduce_partials(out)
@@ -138,11 +192,8 @@ class ShardedStep:
                                                         self.targets[i:i + 1].contiguous(), n_norm=self.n_norm)
                     loss_all += li * self.loss_mask[i]
                     grads[i].copy_(gi[0])
-            if ev:
-                dv, dc = self.renderer.backward(verts, colors, grads, reuse_setup=True, events=ev.get("bwd"),
-                                                soft_events=ev.get("soft_bwd"))
-            else:
-                dv, dc = self.renderer.backward(verts, colors, grads, reuse_setup=True)
+            dv, dc = self.renderer.backward(verts, colors, grads, reuse_setup=True, events=self._pick(ev, "bwd", 0),
+                                            soft_events=self._pick(ev, "soft_bwd", 0))
             flat = torch.cat([dv.reshape(-1), dc.reshape(-1), loss_all])
         else:
             flat = torch.zeros(6 * V + 1, dtype=verts.dtype, device=self.device)

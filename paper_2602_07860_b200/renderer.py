@@ -14,6 +14,32 @@ import torch
 from . import _lib
 
 
+class WorkspaceArena:
+    """One device workspace shared by renderers that run one after another (ShardedStep's passes): it
+    grows to the largest request, and a renderer re-uploads its host tables whenever the previous call
+    on the arena came from another renderer."""
+
+    def __init__(self, device="cuda"):
+        self.device = torch.device(device)
+        self.buf = None
+        self.owner = None
+
+    def view(self, nbytes: int) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = None
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self.buf[:256].zero_()
+            self.owner = None
+        return self.buf[:nbytes]
+
+
+def cache_bytes_per_image(H: int, W: int, n_sub: int, delta: float = 0.0) -> int:
+    """Size of BLUR_CACHE_VISIBILITY for one image: 2 B (+4 B of soft products) per pixel of the
+    16-pixel-padded image and sub-frame."""
+    px = ((H + 15) // 16 * 16) * ((W + 15) // 16 * 16)
+    return int(n_sub) * px * (6 if delta > 0 else 2)
+
+
 class BlurRenderer:
     """Motion-blurred rendering of one mesh topology for a batch of B observed images.
 
@@ -29,8 +55,10 @@ class BlurRenderer:
     def __init__(self, faces, motion: dict, cams, H: int, W: int, V: int, device="cuda",
                  sub_range=None, max_chunk: int = 0, bin_factor: float = 0.0, solver: int = 0,
                  delta: float = 0.0, soft_cut: float = 0.0, soft_exact: bool = False,
-                 soft_bin_factor: float = 0.0, cache_visibility: Optional[bool] = None):
+                 soft_bin_factor: float = 0.0, cache_visibility: Optional[bool] = None,
+                 workspace: Optional[WorkspaceArena] = None):
         _lib.load()
+        self.arena = workspace
         self.device = torch.device(device)
         self.faces = torch.as_tensor(np.asarray(faces.cpu() if torch.is_tensor(faces) else faces),
                                      dtype=torch.int32).contiguous().to(self.device)
@@ -54,8 +82,7 @@ class BlurRenderer:
         # its size (2 B, + 4 B with soft coverage, per pixel of a 16-pixel-padded image and sub-frame)
         # fits CACHE_BUDGET_BYTES; without it K6 recomputes the visibility (k6_raster_bwd_fx)
         if cache_visibility is None:
-            px = ((self.H + 15) // 16 * 16) * ((self.W + 15) // 16 * 16)
-            need = int(self.N.sum()) * px * (6 if self.delta > 0 else 2)
+            need = sum(cache_bytes_per_image(self.H, self.W, n, self.delta) for n in self.N)
             cache_visibility = need <= self.CACHE_BUDGET_BYTES
         self.cache_flags = _lib.BLUR_CACHE_VISIBILITY if (cache_visibility and self.solver == 0) else 0
         self.auto_bins = bin_factor == 0.0 or (self.delta > 0 and soft_bin_factor == 0.0)
@@ -65,7 +92,7 @@ class BlurRenderer:
     def _cfg(self, flags=0, census=None, events=None, soft_events=None):
         # the host tables (schedule, poses, chunks) stay in this renderer's own workspace between calls
         # with the same arguments: after the first upload every call skips the host->device copy
-        if self._tables_resident:
+        if self._tables_resident and (self.arena is None or self.arena.owner is self):
             flags |= _lib.BLUR_TABLES_RESIDENT
         return _lib.make_config(self.max_chunk, flags | self.cache_flags, self.bin_factor, census, events, self.solver,
                                 self.delta,
@@ -78,10 +105,23 @@ class BlurRenderer:
         cfg = self._cfg()
         self.ws_bytes = _lib.blur_workspace_bytes(self.V, self.F, self.B, self.H, self.W, self._motions,
                                                   self._cams, self._sub, cfg)
-        self.ws = None
-        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
-        self.ws[:256].zero_()
+        self._ws = None
+        if self.arena is None:
+            self._ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+            self._ws[:256].zero_()
+        else:
+            self.arena.view(self.ws_bytes)
         self._tables_resident = False
+
+    @property
+    def ws(self) -> torch.Tensor:
+        """The workspace (own, or this renderer's view of a shared arena)."""
+        return self._ws if self.arena is None else self.arena.view(self.ws_bytes)
+
+    def _mark(self):
+        self._tables_resident = True
+        if self.arena is not None:
+            self.arena.owner = self
 
     def _autosize(self, verts, colors, out, ids, ids_subframe, census, stream, events, soft_events):
         """First forward: if a binning needed more entries than the default capacity, grow the
@@ -117,7 +157,7 @@ class BlurRenderer:
         _lib.blur_render_fwd(verts, self.faces, colors, self._motions, self._cams, self.B, self.H, self.W, out,
                              self.ws, sub_range=self._sub, ids=ids, ids_subframe=ids_subframe, cfg=cfg,
                              stream=stream)
-        self._tables_resident = True
+        self._mark()
         if self.auto_bins:
             return self._autosize(verts, colors, out, ids, ids_subframe, census, stream, events, soft_events)
         return out
@@ -133,7 +173,7 @@ class BlurRenderer:
         _lib.blur_render_bwd(verts, self.faces, colors, self._motions, self._cams, self.B, self.H, self.W,
                              grad_rgba.contiguous(), grad_verts, grad_colors, self.ws, sub_range=self._sub, cfg=cfg,
                              stream=stream)
-        self._tables_resident = True
+        self._mark()
         return grad_verts, grad_colors
 
     def l2_loss_grad(self, out: torch.Tensor, target: torch.Tensor, n_norm: int = 0, loss=None, grad=None,

@@ -25,7 +25,7 @@ class OracleRenderer:
         self.sc = sc.subset(images)
         self.sub = np.asarray(sub_range, np.int32)
 
-    def forward(self, verts, colors):
+    def forward(self, verts, colors, **kw):
         r = oracle.render_fwd(self.sc, sub_range=self.sub, threads=1, verts=verts.numpy(), colors=colors.numpy())
         return torch.from_numpy(r["rgba"])
 
@@ -34,7 +34,7 @@ class OracleRenderer:
         d = out - target
         return (d * d).sum().reshape(1) / n, 2.0 * d / n
 
-    def backward(self, verts, colors, grad, reuse_setup=True):
+    def backward(self, verts, colors, grad, reuse_setup=True, **kw):
         dv, dc = oracle.render_bwd(self.sc, grad.numpy(), sub_range=self.sub, threads=1, verts=verts.numpy(),
                                    colors=colors.numpy())
         return torch.from_numpy(dv), torch.from_numpy(dc)

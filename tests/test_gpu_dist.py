@@ -120,3 +120,30 @@ def test_nccl_two_ranks_equal_one_gpu(split):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs (gpurun leases one)")
     _check(_run(2, split), _single_step())
+
+
+def test_passes_share_a_workspace_and_equal_one_pass():
+    """ShardedStep in passes (whole images, one shared workspace, the visibility cache sized per pass):
+    the same loss and gradients as one pass over all images."""
+    import torch
+    from paper_2602_07860_b200 import BlurRenderer
+    from paper_2602_07860_b200.dist import ShardedStep
+    sc = scenes.make_c3().subset([0, 1, 2, 3, 4])
+    dev = torch.device("cuda:0")
+    tgt = torch.tensor(sc.target, device=dev)
+
+    def mk(images, sub_range, workspace=None):
+        s = sc.subset(images)
+        return BlurRenderer(s.faces, s.motion, s.cams, s.H, s.W, s.V, device=dev, sub_range=sub_range,
+                            workspace=workspace)
+
+    v, c = torch.tensor(sc.verts, device=dev), torch.tensor(sc.colors, device=dev)
+    one = ShardedStep(sc.motion["n_sub"], tgt, mk, 0, 1, device=dev)
+    many = ShardedStep(sc.motion["n_sub"], tgt, mk, 0, 1, device=dev, pass_images=2)
+    assert many.n_passes == 3 and len({id(r.arena) for r in many.renderers}) == 1
+    for _ in range(2):   # the second call re-uploads the tables of each pass (shared arena)
+        a, b = one(v, c), many(v, c)
+    torch.cuda.synchronize()
+    assert abs(float(a[0]) - float(b[0])) <= 1e-6 * abs(float(a[0]))
+    assert rel_l2(b[1].cpu().numpy(), a[1].cpu().numpy()) < 1e-5
+    assert rel_l2(b[2].cpu().numpy(), a[2].cpu().numpy()) < 1e-5

@@ -13,6 +13,7 @@ import pytest
 
 import oracle
 import scenes
+from test_gpu_parity import mask_fractions   # the same caps on the excluded fractions (Q16/Q20)
 
 pytestmark = pytest.mark.gpu
 
@@ -50,6 +51,7 @@ def rel_l2(a, b):
 def check_soft(sc, delta, mode="binned", sub_range=None, soft_exact=False, grad=True, ids_k=0, **kw):
     ref = oracle.render_fwd(sc, mode=mode, eps_amb=1e-6, sub_range=sub_range, delta=delta, soft_exact=soft_exact,
                             ids_k=ids_k)
+    fr = mask_fractions(ref, int(max(sc.motion["n_sub"])))
     G = None
     if grad:
         G = 2.0 * (ref["rgba"] - sc.target) / ref["rgba"].size * (~ref["amb_win"])[..., None]
@@ -62,7 +64,7 @@ def check_soft(sc, delta, mode="binned", sub_range=None, soft_exact=False, grad=
     assert not mism.any(), "id mismatch at %d pixels" % mism.sum()
     soft_px = int(((ref["rgba"][..., 3] > 1e-6) & (ref["rgba"][..., 3] < 1 - 1e-6)).sum())
     out = dict(img_err=float(err[ok].max()), alpha_err=float(err[..., 3][ok].max()), amb=int((~ok).sum()),
-               soft_pixels=soft_px)
+               soft_pixels=soft_px, **fr)
     if grad:
         rdv, rdc = oracle.render_bwd(sc, G, mode=mode, sub_range=sub_range, delta=delta, soft_exact=soft_exact)
         hdv, _ = oracle.render_bwd(sc, G, mode=mode, sub_range=sub_range)
