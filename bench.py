@@ -423,7 +423,14 @@ def main():
            "peak_source": hbm_src,
            "achieved_gbs": (traffic / (dur / 1000.0) / 1e9) if (traffic and dur > 0) else None}
     hbm["frac"] = hbm["achieved_gbs"] / hbm_peak if hbm["achieved_gbs"] else None
-    weff = prof.get("warp_efficiency", {}).get(kname)
+    wp = prof.get("warp_efficiency", {}).get(kname) or {}
+    # the coverage loop walks a warp-uniform face mask, so its lanes are all active (ncu); the share of
+    # them whose test covers its pixel is the useful-lane efficiency (census, this run)
+    weff = {"kernel": wp.get("kernel"), "coverage_loop_active_lanes":
+            None if wp.get("coverage_loop") is None else min(1.0, wp["coverage_loop"]),
+            "coverage_loop_useful_lanes": (nec / cand) if cand else None,
+            "source": "ncu --set full (profiles/traffic.json) for the active lanes; census covered / executed "
+                      "tests for the useful ones"}
     roofline = {"bound": "alu", "kernel": kname, "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
                 "hbm_frac": hbm["frac"], "hbm": hbm,

@@ -1226,9 +1226,10 @@ static cudaError_t launch_bwd_t(const Tables &t, const float *grad, float *dC, c
 {
     dim3 grid(t.T, t.B, t.splits);
 #ifdef BR_K6_SORT
-    if (!t.vis) {   // round 1's counting-sort gather for the cached path (A/B builds)
+    if (!t.vis) {   // round 1's float counting-sort gather for the cached path (A/B: 6.86 vs 6.92 ms on C4)
 #else
-    if (true) {     // fixed-point moments (k6_raster_bwd_fx), visibility cached or recomputed
+    if (true) {     // fixed-point moments (k6_raster_bwd_fx), visibility cached or recomputed: both paths
+                    // reduce the same integer moments
 #endif
         const int smem = (int)sizeof(BwdFxSmem<MODE>);
         cudaError_t e = cudaFuncSetAttribute(k6_raster_bwd_fx<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

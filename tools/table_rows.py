@@ -8,7 +8,7 @@ def fmt(x, f="%.3g"):
 
 
 print("| Config | GPUs | blurred images/s (fwd+bwd) | e2e images/s | ms/step | barycentric evals/s (executed / necessary) "
-      "| % FP32 peak (kernel) | % HBM peak | warp eff. (kernel / coverage loop) | CPU oracle images/s (cores) |")
+      "| % FP32 peak (kernel) | % HBM peak | warp eff. (kernel lanes active / coverage-test lanes useful) | CPU oracle images/s (cores) |")
 print("|---|---|---|---|---|---|---|---|---|---|")
 for path in sys.argv[1:]:
     try:
@@ -27,4 +27,4 @@ for path in sys.argv[1:]:
         name, d["n_gpus"], fmt(d["value"], "%.1f"), fmt(e2e, "%.1f"), fmt(d["ms_per_step"], "%.3f"),
         fmt(ev.get("executed")), fmt(ev.get("necessary")), fmt(100 * r["frac"], "%.2f"), r["kernel"],
         fmt(None if r.get("hbm_frac") is None else 100 * r["hbm_frac"], "%.2f"), fmt(we.get("kernel"), "%.2f"),
-        fmt(we.get("coverage_loop"), "%.2f"), fmt(cb.get("value"), "%.3g"), cb.get("cores", "-")))
+        fmt(we.get("coverage_loop_useful_lanes"), "%.3f"), fmt(cb.get("value"), "%.3g"), cb.get("cores", "-")))
