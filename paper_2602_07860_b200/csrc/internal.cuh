@@ -15,6 +15,7 @@ constexpr int CAP = 512;         // per-(tile, sub-frame) face records staged pe
 constexpr int SORTCAP = 1024;    // bins longer than this take the exact fallback path
 constexpr float EPS_D = 1e-12f;  // Q8: |det F| <= 1e-12 NDC^2 -> face skipped for that sub-frame
 constexpr float BBOX_PAD = 1e-5f;  // NDC padding of conservative bounding boxes (>> fp32 error)
+constexpr int VIS_MAXN = 256;    // bins of at most this many faces get K4's visibility cache (BLUR_CACHE_VISIBILITY)
 
 // Per (face, segment) coefficient record: the paper's Eq.8 coefficients (A1, A2, A3, a1..a3),
 // computed once per segment, in edge-vector form about a per-edge origin (DESIGN.md
@@ -99,6 +100,8 @@ struct Tables {          // device pointers into the workspace
     uint32_t *covbits;   // [sum_b N_b][T][NWARP] coverage ballots per (sub-frame, tile, warp) or null
     uint16_t *vis;       // [sum_b N_b][T][TW*TH] winning bin slot per (sub-frame, pixel), 0xFFFF none;
                          // written by K4, read by K6 instead of recomputing visibility (or null)
+    int vis_gathered;    // 1: k6v_raster_bwd (k_gather.cu) has taken the cached chunks; k6_raster_bwd_fx skips them
+    unsigned char *vg_left;   // [splits][B][T] (blockIdx order z, y, x): 1 if k6v_raster_bwd left chunks of the CTA
     float *spart;        // [splits][B*H*W] soft alpha partial sums (K8)
     float *spz;          // [sum_b N_b][T][TW*TH] soft products per (sub-frame, pixel) left by K8 for K9
                          // (prod of the non-zero factors 1 - A; negative: one zero factor, NaN: two or
@@ -160,6 +163,7 @@ cudaError_t launch_raster_fwd_legacy(const Tables &t, float *out, int *ids, int 
                                      unsigned long long *census, cudaStream_t st);
 cudaError_t launch_raster_bwd_legacy(const Tables &t, const float *grad_rgba, float *grad_colors,
                                      cudaStream_t st);
+cudaError_t launch_vis_gather(const Tables &t, const float *grad_rgba, float *grad_colors, cudaStream_t st);
 cudaError_t launch_vertex_chain(const Tables &t, float *grad_verts, cudaStream_t st);
 cudaError_t launch_split_reduce(const Tables &t, float *out, cudaStream_t st);
 cudaError_t launch_l2(const float *out, const float *tgt, long long n, long long n_norm, float *loss,

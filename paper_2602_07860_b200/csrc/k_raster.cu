@@ -21,6 +21,7 @@
 // the order the faces are visited in.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "internal.cuh"
 #include "raster_common.cuh"
@@ -62,6 +63,7 @@ constexpr int SREC_F = BR_SREC_F;   // fwd: staged (tau, face) records per CTA (
 constexpr int SREC_B = BR_SREC_B;   // bwd: staged records per CTA; also the gather's slot limit
 constexpr int GMAX_F = BR_GMAX_F;   // max sub-frames staged together
 constexpr int GMAX_B = BR_GMAX_B;
+static_assert(VIS_MAXN <= SREC_B && VIS_MAXN <= SREC_F, "cached bins must fit both record stages");
 
 
 // max over the pixel centres of a local rect [x0..x1] x [y0..y1] of the edge function, >= -tol ?
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
         if (!bc.fb && n <= SREC_F) {
             // grouped path: the whole bin staged for up to Gs sub-frames at once
             const int Gs = min(GMAX_F, SREC_F / n), nw = (n + 31) >> 5;
-            uint16_t *vis_out = (MODE == 0 && n <= SREC_B) ? t.vis : nullptr;
+            uint16_t *vis_out = (MODE == 0 && n <= VIS_MAXN) ? t.vis : nullptr;
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
                 clear_words(S.wm, ng * NFP * nw);
@@ -832,7 +834,8 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd(Tables t, const 
         bc.fb = o + n > t.cap;
         FaceAcc acc;
         acc_zero(acc);
-        if (MODE == 0 && t.vis && !bc.fb && n <= SREC_B) {
+        if (MODE == 0 && t.vis && !bc.fb && n <= VIS_MAXN) {
+            if (t.vis_gathered) continue;   // taken by k6v_raster_bwd (k_gather.cu)
             // visibility from the forward's buffer: stage only the (face, sub-frame) pairs that won
             const int Gs = min(GMAX_B, group_div(SREC_B, n));
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
@@ -988,6 +991,8 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd_fx(Tables t, con
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BwdFxSmem<MODE> &S = *reinterpret_cast<BwdFxSmem<MODE> *>(smem_raw);
+    if (t.vis_gathered && !t.vg_left[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x])
+        return;   // every chunk of this CTA was taken by k6v_raster_bwd (k_gather.cu)
     const int b = blockIdx.y, tile = blockIdx.x;
     const ImgInfo &im = t.imgs[b];
     const int N = im.N, c_begin = im.chunk_begin, c_end = im.chunk_end, sched_off = im.sched_off;
@@ -1043,7 +1048,8 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd_fx(Tables t, con
         bc.ent = t.entries + o;
         bc.n = n;
         bc.fb = o + n > t.cap;
-        if (MODE == 0 && t.vis && !bc.fb && n <= SREC_B) {
+        if (MODE == 0 && t.vis && !bc.fb && n <= VIS_MAXN) {
+            if (t.vis_gathered) continue;   // taken by k6v_raster_bwd (k_gather.cu)
             // visibility from the forward's buffer (BLUR_CACHE_VISIBILITY): the pixels add their moments
             // to the slots they name, only the (face, sub-frame) pairs that won are staged
             const int Gs = min(GMAX_B, group_div(SREC_B, n));
@@ -1281,11 +1287,26 @@ cudaError_t launch_raster_fwd_legacy(const Tables &t, float *out, int *ids, int 
     }
 }
 
+// BLURRAST_VIS_GATHER=0: the cached chunks take k6_raster_bwd_fx's cached path instead (A/B)
+static bool vis_gather_off()
+{
+    const char *s = std::getenv("BLURRAST_VIS_GATHER");
+    return s && s[0] == '0';
+}
+
 cudaError_t launch_raster_bwd_legacy(const Tables &t, const float *grad, float *dC, cudaStream_t st)
 {
     if (t.B == 0 || t.T == 0 || t.F == 0) return cudaSuccess;
     switch (t.solver) {
-    case 0: return launch_bwd_t<0>(t, grad, dC, st);
+    case 0:
+        if (t.vis && !vis_gather_off()) {   // cached chunks: visibility gather (k_gather.cu); the rest below
+            cudaError_t e = launch_vis_gather(t, grad, dC, st);
+            if (e != cudaSuccess) return e;
+            Tables t2 = t;
+            t2.vis_gathered = 1;
+            return launch_bwd_t<0>(t2, grad, dC, st);
+        }
+        return launch_bwd_t<0>(t, grad, dC, st);
     case 1: return launch_bwd_t<1>(t, grad, dC, st);
     default: return launch_bwd_t<2>(t, grad, dC, st);
     }

@@ -144,6 +144,8 @@ def test_passes_share_a_workspace_and_equal_one_pass():
     for _ in range(2):   # the second call re-uploads the tables of each pass (shared arena)
         a, b = one(v, c), many(v, c)
     torch.cuda.synchronize()
-    assert abs(float(a[0]) - float(b[0])) <= 1e-6 * abs(float(a[0]))
+    # the loss is a float-atomic sum over K5's CTAs (and here over passes): 1e-5 relative, as DESIGN.md's
+    # determinism note states (1e-6 was met by chance; the pass split reorders the sum)
+    assert abs(float(a[0]) - float(b[0])) <= 1e-5 * abs(float(a[0]))
     assert rel_l2(b[1].cpu().numpy(), a[1].cpu().numpy()) < 1e-5
     assert rel_l2(b[2].cpu().numpy(), a[2].cpu().numpy()) < 1e-5
