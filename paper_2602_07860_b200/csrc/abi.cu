@@ -338,6 +338,7 @@ Tables make_tables(const Plan &P, void *ws)
     std::memset(&t, 0, sizeof(t));
     t.status = (int *)(w + P.o_status);
     t.binstat = (long long *)(w + P.o_status + 8);
+    t.orient = (double *)(w + P.o_status + 64);
     t.imgs = (const ImgInfo *)(w + P.o_imgs);
     t.chunks = (const Chunk *)(w + P.o_chunks);
     t.sched_s = (const int *)(w + P.o_ss);

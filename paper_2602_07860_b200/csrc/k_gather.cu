@@ -27,7 +27,7 @@
 //            REDs per vertex colour.
 // Pairs beyond SG_PCAP are taken in further batches (moments, pairs, flush).  Chunks K4 wrote no
 // winners for (longer bins, overflowed bins) are left to k6_raster_bwd_fx: the CTA raises its
-// Tables::vg_left flag, and k6_raster_bwd_fx runs only the CTAs that did, skipping the chunks taken here.
+// Tables::vg_left flag of its (image, tile), and k6_raster_bwd_fx runs only the CTAs of flagged tiles, skipping the chunks taken here.
 #include <cstdio>
 
 #include "internal.cuh"
@@ -38,6 +38,9 @@ namespace br {
 
 #ifndef BR_SG_PCAP
 #define BR_SG_PCAP 256
+#endif
+#ifndef BR_VG_SPLITS
+#define BR_VG_SPLITS 1     // CTAs per (image, tile) (chunks dealt round-robin)
 #endif
 #ifndef BR_VG_MINB
 #define BR_VG_MINB 4
@@ -108,8 +111,9 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
     const int lane = tid & 31, warp = tid >> 5;
     const ImgInfo &im = t.imgs[b];
     const int N = im.N, sched_off = im.sched_off;
+    const int vsp = gridDim.z;   // CTAs per (image, tile), taking every vsp-th chunk
     const int cfirst = im.chunk_begin + (int)blockIdx.z;
-    const int nc = cfirst < im.chunk_end ? (im.chunk_end - cfirst + t.splits - 1) / t.splits : 0;
+    const int nc = cfirst < im.chunk_end ? (im.chunk_end - cfirst + vsp - 1) / vsp : 0;
     TileCtx tc;
     tile_ctx(t, tile, tc);
     {   // the tile's pixel gradients in fixed point: scale 2^e with max |g| 2^e < 2^19
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
         if (ci >= w0 + SG_CMAX && ci < nc) {   // stage the next window of the chunk table
             w0 = ci;
             if (tid < SG_CMAX && w0 + tid < nc) {
-                const int c = cfirst + (w0 + tid) * t.splits;
+                const int c = cfirst + (w0 + tid) * vsp;
                 const Chunk ch = t.chunks[c];
                 const size_t bi = (size_t)c * t.T + tile;
                 const long long o = t.off[bi];
@@ -392,14 +396,15 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
             if (pb + np < total) __syncthreads();   // the next batch reuses plist / imom / contrib
         }
     }
-    if (tid == 0)
-        t.vg_left[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = (unsigned char)S.left;
+    if (tid == 0 && S.left) t.vg_left[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = 1;   // cleared before the launch
 }
 
 cudaError_t launch_vis_gather(const Tables &t, const float *grad, float *dC, cudaStream_t st)
 {
-    dim3 grid(t.T, t.B, t.splits);
+    dim3 grid(t.T, t.B, BR_VG_SPLITS);
     const int smem = (int)sizeof(VgSmem);
+    cudaError_t e0 = cudaMemsetAsync(t.vg_left, 0, (size_t)t.T * t.B, st);
+    if (e0 != cudaSuccess) return e0;
     cudaError_t e = cudaFuncSetAttribute(k6v_raster_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     k6v_raster_bwd<<<grid, NT, smem, st>>>(t, grad, dC);

@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.cuh"
 #include "raster_common.cuh"
@@ -562,6 +563,859 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
     }
 }
 
+// ------------------------------------------------------------------ lean forward (fast solver)
+//
+// k4l_raster_fwd: K4 for the fast solver without the census (the timed path).  The same stage, tests and
+// shading as k4_raster_fwd, but each (sub-frame, warp footprint) gets a compact list of the bin slots
+// whose record reaches it (shared atomic counters in the stage) instead of a bitmask over all slots:
+// the visibility loop walks exactly the reaching records, with no per-word walk over the mostly empty
+// mask words of long bins, and the per-(warp, sub-frame) bookkeeping is kept in registers.  Long and
+// overflowed bins take k4_raster_fwd's per-sub-frame batch path unchanged.
+
+#ifndef BR_K4L_PAIR2
+#define BR_K4L_PAIR2 0  // 1: two pairs per thread, both pairs' first record words requested together (measured slower)
+#endif
+#ifndef BR_K4L_SENT
+#define BR_K4L_SENT 0   // 1: the chunk's bin entries staged in shared memory (measured: no change)
+#endif
+#ifndef BR_K4L_CULL
+#define BR_K4L_CULL 0   // 1: faces turned away from the camera tested last, skipped per footprint behind its winners
+#endif                  //    (measured slower in this kernel: C4 K4 6.86 -> 7.17 ms)
+
+struct __align__(16) LeanSmem {
+    TauRec rec[SREC_F];
+    union {
+        struct {
+            uint16_t list[NFP][SREC_F];         // per footprint: sub-frame l's reaching records (byte offsets into rec)
+            int cnt[GMAX_F][NFP];               // ... at [l * n, l * n + cnt): faces turned towards the camera,
+            int cntb[GMAX_F][NFP];              // and at [l * n + n - cntb, l * n + n): the others
+            int ent[SREC_F];                    // the chunk's bin entries (face ids)
+        } g;                                    // grouped path
+        struct {
+            uint32_t wm[NFP * (SREC_F / 32 + GMAX_F)];
+            int sid[SREC_F];
+        } b;                                    // per-sub-frame batch path (long bins, fallback)
+    } u;
+    float taus[GMAX_F];
+    int wsum[NWARP];
+    float2 uv[NT];                              // the thread's pixel (ul, vl), reloaded per sub-frame
+    float4 fpc[NWARP];                          // the warp footprint's corner pixel centres (ul0, ul1, vl0, vl1)
+    float4 acc[TW * TH];                        // per-pixel (r, g, b, a) sums over the sub-frames
+};
+static_assert(SREC_F * 64 <= 65535, "list entries are 16-bit byte offsets");
+
+// Stage faces [0, n) of the bin at the ng sub-frames taus[0..ng): records rec[l * n + j] and, for every
+// footprint a record reaches, its byte offset in that footprint's list of sub-frame l (cnt must be zero).
+// Each warp takes candidate pairs 32 at a time, and the pairs whose per-tau box reaches the tile go
+// to a warp queue; the full stage (record load, Horner, footprint masks) runs on 32 queued pairs at a
+// time, so the box rejects (about half the pairs) leave no lanes idle in it.
+// the (face, sub-frame) pair p's first words: face, record, box test at tau (false: not staged)
+__device__ __forceinline__ bool pair_head(const BinCtx &bc, const int *ent, int p, float inv_ng, int ng, const float *taus,
+                                          const TileCtx &tc, int W, int H, int F, int &j, int &l, const float4 *&r,
+                                          float &D, int &x0, int &x1, int &y0, int &y1)
+{
+    j = div_small(p, inv_ng);
+    l = p - j * ng;
+    const int f = BR_K4L_SENT ? ent[j] : __ldg(ent + j);
+    if ((unsigned)f >= (unsigned)F) {     // never expected: bins hold valid face ids
+        atomicOr(bc.status, BLUR_ST_EINTERNAL);
+        return false;
+    }
+    r = bc.rseg + (size_t)f * REC_F4;
+    const float4 q6 = __ldg(r + 6);
+    const float4 b0 = __ldg(r + 7), b1 = __ldg(r + 8);
+    if (__float_as_int(q6.w) < 0) return false;               // skipped face (Q8, behind, bad index)
+    const float tau = taus[l];
+    D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);       // a1 t^2 + a2 t + a3
+    if (!(fabsf(D) > EPS_D)) return false;
+    return tile_pixels(box_lerp(tau, b0.x, b1.x), box_lerp(tau, b0.y, b1.y), box_lerp(tau, b0.z, b1.z),
+                       box_lerp(tau, b0.w, b1.w), W, H, tc, x0, x1, y0, y1);
+}
+
+__device__ __forceinline__ void pair_stage(const float4 *r, int j, int l, int n, float tau, float D, int x0, int x1,
+                                           int y0, int y1, const TileCtx &tc, TauRec *rec, uint16_t (*list)[SREC_F],
+                                           int (*cnt)[NFP], int (*cntb)[NFP], float sF)
+{
+    FaceRec fr;
+    load_rec(r, fr);
+    const uint32_t fm = stage_tau<true>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * n + j]);
+    const uint16_t off = (uint16_t)((l * n + j) * (int)sizeof(TauRec));
+    const bool back = BR_K4L_CULL && D * sF < 0.f;   // turned away from the camera (sF: mesh orientation)
+    for (uint32_t m = fm; m; m &= m - 1) {
+        const int w = __ffs(m) - 1;
+        if (!back) list[w][l * n + atomicAdd(&cnt[l][w], 1)] = off;
+        else list[w][l * n + n - 1 - atomicAdd(&cntb[l][w], 1)] = off;
+    }
+}
+
+// Stage faces [0, n) of the bin (face ids ent[] in shared memory) at the ng sub-frames taus[0..ng): records
+// rec[l * n + j] and, for every footprint a record reaches, its byte offset in that footprint's list of
+// sub-frame l (counters must be zero).  A thread takes two pairs at a time and requests both pairs' first
+// record words before testing either (the stage is a chain of L2 round trips: fewer of them per group).
+__device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *ent, int n, const float *taus, int ng,
+                                                 const TileCtx &tc, int W, int H, int F, TauRec *rec,
+                                                 uint16_t (*list)[SREC_F], int (*cnt)[NFP], int (*cntb)[NFP], float sF)
+{
+    const int npair = n * ng;
+    const float inv_ng = 1.0f / (float)ng;
+#if BR_K4L_PAIR2
+    for (int p0 = threadIdx.x; p0 < npair; p0 += 2 * NT) {
+        const int p1 = p0 + NT;
+        int ja, la, jb = 0, lb = 0, xa0, xa1, ya0, ya1, xb0 = 0, xb1 = 0, yb0 = 0, yb1 = 0;
+        const float4 *ra, *rb = nullptr;
+        float Da, Db = 0.f;
+        const bool oka = pair_head(bc, ent, p0, inv_ng, ng, taus, tc, W, H, F, ja, la, ra, Da, xa0, xa1, ya0, ya1);
+        const bool okb = p1 < npair && pair_head(bc, ent, p1, inv_ng, ng, taus, tc, W, H, F, jb, lb, rb, Db, xb0, xb1, yb0, yb1);
+        if (oka) pair_stage(ra, ja, la, n, taus[la], Da, xa0, xa1, ya0, ya1, tc, rec, list, cnt, cntb, sF);
+        if (okb) pair_stage(rb, jb, lb, n, taus[lb], Db, xb0, xb1, yb0, yb1, tc, rec, list, cnt, cntb, sF);
+    }
+#else
+    for (int p = threadIdx.x; p < npair; p += NT) {
+        int j, l, x0, x1, y0, y1;
+        const float4 *r;
+        float D;
+        if (pair_head(bc, ent, p, inv_ng, ng, taus, tc, W, H, F, j, l, r, D, x0, x1, y0, y1))
+            pair_stage(r, j, l, n, taus[l], D, x0, x1, y0, y1, tc, rec, list, cnt, cntb, sF);
+    }
+#endif
+}
+
+template <bool COV>
+__global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float *__restrict__ out, int *__restrict__ ids,
+                                                                int ids_k)
+{
+    static_assert(!BR_HALF, "the lean forward uses the warps' 8x4 footprints");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    LeanSmem &S = *reinterpret_cast<LeanSmem *>(smem_raw);
+    const int b = blockIdx.y, tile = blockIdx.x;
+    const ImgInfo &im = t.imgs[b];
+    const int N = im.N, c_begin = im.chunk_begin, c_end = im.chunk_end, sched_off = im.sched_off;
+    const long long rec_off = im.rec_off;
+    TileCtx tc;
+    tile_ctx(t, tile, tc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+    const int px = tc.px0 + lx, py = tc.py0 + ly;
+    const bool inimg = px < t.W && py < t.H;
+    const float ul = (float)(lx - TW / 2) * tc.sx;
+    const float vl = (float)(TH / 2 - ly) * tc.sy;
+    const int myp = ly * TW + lx;
+    const size_t pix = ((size_t)b * t.H + py) * t.W + px;
+    S.acc[myp] = make_float4(0.f, 0.f, 0.f, 0.f);
+    S.uv[threadIdx.x] = make_float2(ul, vl);
+    for (int i = threadIdx.x; i < GMAX_F * NFP; i += NT) { (&S.u.g.cnt[0][0])[i] = 0; (&S.u.g.cntb[0][0])[i] = 0; }
+    unsigned long long dz = 0;
+    const double orient = *t.orient;
+    const float sF = orient > 0.0 ? 1.f : orient < 0.0 ? -1.f : 0.f;
+    if (lane == 0)   // the warp footprint's corner pixel centres (the lanes' own ul, vl values)
+        S.fpc[warp] = make_float4((float)((warp & 1) * 8 - TW / 2) * tc.sx, (float)((warp & 1) * 8 + 7 - TW / 2) * tc.sx,
+                                  (float)(TH / 2 - (warp >> 1) * 4 - 3) * tc.sy, (float)(TH / 2 - (warp >> 1) * 4) * tc.sy);
+
+    for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
+        const Chunk ch = t.chunks[c];
+        const size_t bi = (size_t)c * t.T + tile;
+        const long long o = t.off[bi];
+        const int n = (int)(t.off[bi + 1] - o);
+        if (n == 0) {
+            if (ids && inimg && ids_k >= ch.k0 && ids_k < ch.k1) ids[pix] = -1;
+            if (COV) {
+                const unsigned m = __ballot_sync(0xffffffffu, !inimg);
+                if (lane == 0)
+                    for (int k = ch.k0; k < ch.k1; ++k) t.covbits[cov_word(t, im, k, tile) + warp] = m;
+            }
+            continue;
+        }
+        BinCtx bc;
+        bc.status = t.status;
+        bc.rseg = t.rec + (size_t)(rec_off + (long long)ch.s * t.F) * REC_F4;
+        bc.key0 = nullptr;
+        bc.key1 = nullptr;
+        bc.fcol = t.fcol;
+        bc.ent = t.entries + o;
+        bc.n = n;
+        bc.fb = o + n > t.cap;
+        if (!bc.fb && n <= SREC_F) {
+            const int Gs = min(GMAX_F, group_div(SREC_F, n));
+            uint16_t *vis_out = n <= VIS_MAXN ? t.vis : nullptr;
+#if BR_K4L_SENT
+            __syncthreads();   // the previous chunk's entries are consumed
+            for (int j = threadIdx.x; j < n; j += NT) S.u.g.ent[j] = __ldg(bc.ent + j);
+            const int *ents = S.u.g.ent;
+#else
+            const int *ents = bc.ent;
+#endif
+            for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
+                const int ng = min(Gs, ch.k1 - kg);
+                if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
+                __syncthreads();   // taus written; the previous group's lists and counters are consumed
+                stage_group_list(bc, ents, n, S.taus, ng, tc, t.W, t.H, t.F, S.rec, S.u.g.list, S.u.g.cnt, S.u.g.cntb, sF);
+                __syncthreads();
+                uint16_t *vrow = vis_out ? vis_out + ((size_t)(im.cov_off + kg) * t.T + tile) * (TW * TH) + myp : nullptr;
+                const int l_ids = (ids && inimg) ? ids_k - kg : -1;
+                const uint16_t *lst = S.u.g.list[warp];
+                const unsigned char *rbase = reinterpret_cast<const unsigned char *>(S.rec);
+                for (int l = 0; l < ng; ++l, lst += n) {
+                    const TauRec *rl = S.rec + l * n;
+#ifdef BR_EXP_NOVIS
+                    const int cn = 0, cb = 0;
+#else
+                    const int cn = S.u.g.cnt[l][warp], cb = S.u.g.cntb[l][warp];
+#endif
+                    const float2 uvp = S.uv[threadIdx.x];
+                    const float ul = uvp.x, vl = uvp.y;
+                    float zbest = __int_as_float(0x7f800000), tief = 0.f;
+                    int eoff = -1;
+                    for (int i = 0; i < cn; ++i) {   // faces turned towards the camera
+                        const int off = lst[i];
+                        const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
+                        const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
+                        const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
+                        const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
+                        const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
+                        const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
+                        const float emin = fminf(fminf(e0, e1), e2);
+                        tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
+                        if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
+                    }
+                    if (BR_K4L_CULL && cb) {   // the others: skipped where they are behind every pixel's winner
+                        float zmax = zbest;
+#pragma unroll
+                        for (int d = 16; d > 0; d >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, d));
+                        // zmax = +inf unless every pixel of the footprint has a winner.  The depth plane
+                        // fma(az, ul, fma(bz, vl, cz)) is monotone in ul and vl, so its minimum over the footprint's
+                        // pixel centres is its value at one corner: above zmax, the face cannot win or tie anywhere.
+#ifdef BR_K4L_STATS
+                        if (lane == 0) { atomicAdd(t.status + 40, cn); atomicAdd(t.status + 41, cb); atomicAdd(t.status + 43, zmax < __int_as_float(0x7f800000) ? 1 : 0); atomicAdd(t.status + 44, 1); }
+#endif
+                        const float4 fc = S.fpc[warp];
+                        for (int i = n - cb; i < n; ++i) {
+                            const int off = lst[i];
+                            const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
+                            const float4 q2 = rp[2];
+                            const float zmin = __fmaf_rn(q2.y, q2.y > 0.f ? fc.x : fc.y, __fmaf_rn(q2.z, q2.z > 0.f ? fc.z : fc.w, q2.w));
+#ifdef BR_K4L_STATS
+                            if (lane == 0 && zmin > zmax) atomicAdd(t.status + 42, 1);
+#endif
+                            if (zmin > zmax) continue;
+                            const float4 q0 = rp[0], q1 = rp[1];
+                            const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
+                            const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
+                            const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
+                            const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
+                            const float emin = fminf(fminf(e0, e1), e2);
+                            tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
+                            if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
+                        }
+                    }
+                    if (__any_sync(0xffffffffu, tief != 0.f)) {   // exact depth tie in the warp: face indices decide (Q7)
+                        zbest = __int_as_float(0x7f800000);
+                        eoff = -1;
+                        int fbest = 0x7fffffff;
+                        for (int ii = 0; ii < cn + cb; ++ii) {
+                            const int off = lst[ii < cn ? ii : n - cb + (ii - cn)];
+                            const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
+                            const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
+                            const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
+                            const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
+                            const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
+                            const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
+                            if (fminf(fminf(e0, e1), e2) >= 0.f && z <= zbest) {
+                                const int fj = reinterpret_cast<const TauRec *>(rbase + off)->fid;
+                                if (z < zbest || fj < fbest) { zbest = z; eoff = off; fbest = fj; }
+                            }
+                        }
+                    }
+                    const int ebest = eoff >= 0 ? eoff / (int)sizeof(TauRec) - l * n : -1;
+                    int fid = -1;
+                    if (ebest >= 0) {
+                        float pr, pg, pb;
+                        shade(rl[ebest], t.fcol, ul, vl, pr, pg, pb);      // Eq.9
+                        float4 a = S.acc[myp];
+                        a.x += pr; a.y += pg; a.z += pb; a.w += 1.f;
+                        S.acc[myp] = a;
+                        fid = rl[ebest].fid;
+                    }
+                    if (l == l_ids) ids[pix] = fid;
+                    if (vrow) {   // visibility cache for K6
+                        *vrow = ebest >= 0 ? (uint16_t)ebest : (uint16_t)0xFFFF;
+                        vrow += (size_t)t.T * (TW * TH);
+                    }
+                    if (COV) {   // soft path: which pixels of the warp are covered at this sub-frame
+                        const unsigned m = __ballot_sync(0xffffffffu, ebest >= 0 || !inimg);
+                        if (lane == 0) t.covbits[cov_word(t, im, kg + l, tile) + warp] = m;
+                    }
+                }
+                __syncthreads();   // lists read: clear the counters of this group
+                if (threadIdx.x < ng * NFP) { (&S.u.g.cnt[0][0])[threadIdx.x] = 0; (&S.u.g.cntb[0][0])[threadIdx.x] = 0; }
+            }
+        } else {
+            // per sub-frame, several batches (long bins) or the exact fallback scan (overflow): as k4_raster_fwd
+            for (int k = ch.k0; k < ch.k1; ++k) {
+                const float tau = t.sched_tau[sched_off + k];
+                float zbest = __int_as_float(0x7f800000);
+                int ebest = -1, bfid = -1, fbest = 0x7fffffff;
+                bool has = false;
+                float pr = 0.f, pg = 0.f, pb = 0.f;
+                int base = 0, fpos = 0;
+                __syncthreads();
+                if (threadIdx.x == 0) S.taus[0] = tau;
+                while (true) {
+                    const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SREC_F, base, fpos, S.u.b.sid, S.wsum);
+                    if (nb == 0) break;
+                    const int nw = (nb + 31) >> 5;
+                    clear_words(S.u.b.wm, NFP * nw);
+                    __syncthreads();
+                    stage_group<false, 0, true>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.u.b.sid, S.rec, nullptr, S.u.b.wm, dz);
+                    __syncthreads();
+                    vis_mask<false, 0>(S.rec, nullptr, S.u.b.wm + warp * nw, nw, base, ul, vl, zbest, ebest, fbest, dz, dz, false);
+                    if (ebest >= base) {   // winner changed in this batch: shade now (Eq.9)
+                        shade(S.rec[ebest - base], t.fcol, ul, vl, pr, pg, pb);
+                        has = true;
+                        bfid = S.rec[ebest - base].fid;
+                        fbest = bfid;      // ties against later batches compare face indices
+                    }
+                    base += nb;
+                    __syncthreads();
+                }
+                if (has) {
+                    float4 a = S.acc[myp];
+                    a.x += pr; a.y += pg; a.z += pb; a.w += 1.f;
+                    S.acc[myp] = a;
+                }
+                if (ids && inimg && k == ids_k) ids[pix] = has ? bfid : -1;
+                if (COV) {
+                    const unsigned m = __ballot_sync(0xffffffffu, has || !inimg);
+                    if (lane == 0) t.covbits[cov_word(t, im, k, tile) + warp] = m;
+                }
+            }
+            __syncthreads();   // the grouped path's counters share the batch path's shared memory
+            for (int i = threadIdx.x; i < GMAX_F * NFP; i += NT) { (&S.u.g.cnt[0][0])[i] = 0; (&S.u.g.cntb[0][0])[i] = 0; }
+        }
+    }
+    if (inimg && out) {   // out == null: coverage-only pass (soft backward without a preceding forward)
+        const float inv = 1.0f / (float)N;
+        const float4 a = S.acc[myp];
+        const float4 v = make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
+        if (t.splits == 1) reinterpret_cast<float4 *>(out)[pix] = v;
+        else t.part[(size_t)blockIdx.z * ((size_t)t.B * t.H * t.W) + pix] = v;
+    }
+}
+
+template <bool COV>
+static cudaError_t launch_fwd_lean(const Tables &t, float *out, int *ids, int ids_k, cudaStream_t st)
+{
+    dim3 grid(t.T, t.B, t.splits);
+    const int smem = (int)sizeof(LeanSmem);
+    cudaError_t e = cudaFuncSetAttribute(k4l_raster_fwd<COV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k4l_raster_fwd<COV><<<grid, NT, smem, st>>>(t, out, ids, ids_k);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ pipelined forward (fast solver)
+//
+// k4p_raster_fwd: K4 with warp specialisation.  Staging a group of (face, sub-frame) records is a chain
+// of dependent L2 loads (bin entry -> record words -> record); in k4l_raster_fwd every warp of the CTA
+// waits for it at a barrier before the footprint tests start (measured: with the tests removed,
+// k4l still takes 55% of its time).  Here 4 producer warps stage group g+1 into one of two record
+// buffers while the 8 consumer warps (one 8x4 footprint each) test and shade group g from the other;
+// the hand-off is a pair of named barriers per buffer (FULL: producers arrive, consumers wait;
+// EMPTY: consumers arrive, producers wait), so neither side waits for the other's latency.  The
+// records, tests, tie rule (Q7) and shading (Eq.9) are those of k4l_raster_fwd; the producers also
+// build the per-footprint record lists there (faces turned towards the camera first, BR_K4P_CULL).
+// Long bins and overflowed bins go through the same pipeline as per-sub-frame batches.
+
+#ifndef BR_KP_SREC
+#define BR_KP_SREC 256
+#endif
+#ifndef BR_K4P_CULL
+#define BR_K4P_CULL 1
+#endif
+#ifndef BR_KP_MINB
+#define BR_KP_MINB 3
+#endif
+constexpr int KP_SREC = BR_KP_SREC;   // records per buffer
+#ifndef BR_KP_NP
+#define BR_KP_NP 128
+#endif
+constexpr int KP_NP = BR_KP_NP;       // producer threads (warps 8..)
+constexpr int KP_NTH = NT + KP_NP;
+static_assert(KP_SREC * 64 <= 65535 && VIS_MAXN <= KP_SREC, "list offsets are 16-bit; cached bins take the group path");
+enum { KP_GROUP = 0, KP_BATCH = 1, KP_EMPTY = 2, KP_END = 3 };
+
+struct KpDesc {
+    int kind, n, ng, kg, k1, last;
+};
+
+struct __align__(16) KpSmem {
+    TauRec rec[2][KP_SREC];
+    uint16_t list[2][NFP][KP_SREC];          // per footprint: sub-frame l's records at [l*n, l*n + cnt) (towards
+    int cnt[2][GMAX_F][NFP];                 // the camera) and [l*n + n - cntb, l*n + n) (the others); byte
+    int cntb[2][GMAX_F][NFP];                // offsets into rec[b]
+    KpDesc desc[2];
+    float taus[2][GMAX_F];
+    int sid[KP_SREC];                        // the chunk's bin face ids / an overflowed bin's batch (producers)
+    float4 raw[KP_NP][REC_F4];               // producers: (face, segment) records copied in (cp.async)
+    int pws[KP_NP / 32];
+    float2 uv[NT];
+    float4 fpc[NWARP];
+    float4 acc[TW * TH];
+};
+
+// named barriers with immediate ids (a register id makes ptxas reserve all 16 barriers of the CTA, which
+// limits the CTAs per SM): 1 + b = FULL[b], 3 + b = EMPTY[b], 5 = producers only
+__device__ __forceinline__ void kp_bar_sync(int id, int)
+{
+    if (id == 1) asm volatile("bar.sync 1, %0;" ::"n"(KP_NTH) : "memory");
+    else if (id == 2) asm volatile("bar.sync 2, %0;" ::"n"(KP_NTH) : "memory");
+    else if (id == 3) asm volatile("bar.sync 3, %0;" ::"n"(KP_NTH) : "memory");
+    else asm volatile("bar.sync 4, %0;" ::"n"(KP_NTH) : "memory");
+}
+__device__ __forceinline__ void kp_bar_arrive(int id, int)
+{
+    if (id == 1) asm volatile("bar.arrive 1, %0;" ::"n"(KP_NTH) : "memory");
+    else if (id == 2) asm volatile("bar.arrive 2, %0;" ::"n"(KP_NTH) : "memory");
+    else if (id == 3) asm volatile("bar.arrive 3, %0;" ::"n"(KP_NTH) : "memory");
+    else asm volatile("bar.arrive 4, %0;" ::"n"(KP_NTH) : "memory");
+}
+__device__ __forceinline__ void kp_pbar() { asm volatile("bar.sync 5, %0;" ::"n"(KP_NP) : "memory"); }   // producers only
+
+// producers: stage faces j in [0, n) at the ng sub-frames taus[0..ng) into buffer b (faces: sid[j] if sid,
+// else the bin entries ent[j])
+__device__ __forceinline__ void kp_stage(const BinCtx &bc, const int *ent, const int *sid, int n, const float *taus,
+                                         int ng, const TileCtx &tc, int W, int H, int F, TauRec *rec,
+                                         uint16_t (*list)[KP_SREC], int (*cnt)[NFP], int (*cntb)[NFP], float sF, int ptid)
+{
+    const int npair = n * ng;
+    const float inv_ng = 1.0f / (float)ng;
+    for (int p = ptid; p < npair; p += KP_NP) {
+        const int j = div_small(p, inv_ng), l = p - j * ng;
+        const int f = sid ? sid[j] : __ldg(ent + j);
+        if ((unsigned)f >= (unsigned)F) {     // never expected: bins hold valid face ids
+            atomicOr(bc.status, BLUR_ST_EINTERNAL);
+            continue;
+        }
+        const float4 *r = bc.rseg + (size_t)f * REC_F4;
+        const float4 q6 = __ldg(r + 6);
+        if (__float_as_int(q6.w) < 0) continue;               // skipped face (Q8, behind, bad index)
+        const float tau = taus[l];
+        const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);   // a1 t^2 + a2 t + a3
+        if (!(fabsf(D) > EPS_D)) continue;
+        const float4 b0 = __ldg(r + 7), b1 = __ldg(r + 8);
+        int x0, x1, y0, y1;
+        if (!tile_pixels(box_lerp(tau, b0.x, b1.x), box_lerp(tau, b0.y, b1.y), box_lerp(tau, b0.z, b1.z),
+                         box_lerp(tau, b0.w, b1.w), W, H, tc, x0, x1, y0, y1))
+            continue;
+        FaceRec fr;
+        load_rec(r, fr);
+        const uint32_t fm = stage_tau<true>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * n + j]);
+        const uint16_t off = (uint16_t)((l * n + j) * (int)sizeof(TauRec));
+        const bool back = D * sF < 0.f;   // turned away from the camera (sF: mesh orientation, 0 = unknown)
+        for (uint32_t m = fm; m; m &= m - 1) {
+            const int w = __ffs(m) - 1;
+            if (!back) list[w][l * n + atomicAdd(&cnt[l][w], 1)] = off;
+            else list[w][l * n + n - 1 - atomicAdd(&cntb[l][w], 1)] = off;
+        }
+    }
+}
+
+__device__ __forceinline__ void kp_cp16(void *sdst, const void *gsrc)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
+// producers: stage bin faces j in [0, n) (face ids fid[j] in shared memory) at the ng sub-frames taus[0..ng).
+// The faces' records are copied into shared memory KP_NP at a time with cp.async (one L2 round trip per
+// KP_NP faces, no registers held while in flight), then the (face, sub-frame) pairs are evaluated from there.
+__device__ __forceinline__ void kp_stage_raw(const BinCtx &bc, const int *fid, int n, const float *taus, int ng,
+                                             const TileCtx &tc, int W, int H, int F, TauRec *rec,
+                                             uint16_t (*list)[KP_SREC], int (*cnt)[NFP], int (*cntb)[NFP], float sF,
+                                             float4 (*raw)[REC_F4], int ptid)
+{
+    const float inv_ng = 1.0f / (float)ng;
+    for (int fb = 0; fb < n; fb += KP_NP) {
+        const int nf = min(KP_NP, n - fb);
+        if (ptid < nf) {
+            const int f = fid[fb + ptid];
+            if ((unsigned)f < (unsigned)F) {
+                const float4 *r = bc.rseg + (size_t)f * REC_F4;
+#pragma unroll
+                for (int i = 0; i < REC_F4; ++i) kp_cp16(&raw[ptid][i], r + i);
+            } else {   // never expected: bins hold valid face ids
+                atomicOr(bc.status, BLUR_ST_EINTERNAL);
+                raw[ptid][6] = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+            }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        kp_pbar();
+        const int npair = nf * ng;
+        for (int p = ptid; p < npair; p += KP_NP) {
+            const int jj = div_small(p, inv_ng), l = p - jj * ng, j = fb + jj;
+            const float4 *rr = raw[jj];
+            const float4 q6 = rr[6];
+            if (__float_as_int(q6.w) < 0) continue;               // skipped face (Q8, behind, bad index)
+            const float tau = taus[l];
+            const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);   // a1 t^2 + a2 t + a3
+            if (!(fabsf(D) > EPS_D)) continue;
+            const float4 b0 = rr[7], b1 = rr[8];
+            int x0, x1, y0, y1;
+            if (!tile_pixels(box_lerp(tau, b0.x, b1.x), box_lerp(tau, b0.y, b1.y), box_lerp(tau, b0.z, b1.z),
+                             box_lerp(tau, b0.w, b1.w), W, H, tc, x0, x1, y0, y1))
+                continue;
+            FaceRec fr;
+#pragma unroll
+            for (int i = 0; i < REC_F4; ++i) fr.q[i] = rr[i];
+            const uint32_t fm = stage_tau<true>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * n + j]);
+            const uint16_t off = (uint16_t)((l * n + j) * (int)sizeof(TauRec));
+            const bool back = D * sF < 0.f;   // turned away from the camera (sF: mesh orientation, 0 = unknown)
+            for (uint32_t m = fm; m; m &= m - 1) {
+                const int w = __ffs(m) - 1;
+                if (!back) list[w][l * n + atomicAdd(&cnt[l][w], 1)] = off;
+                else list[w][l * n + n - 1 - atomicAdd(&cntb[l][w], 1)] = off;
+            }
+        }
+        kp_pbar();   // raw is reused by the next KP_NP faces
+    }
+}
+
+// producers: the next batch of an overflowed bin -- faces whose per-tau box overlaps the tile, in index order
+// from fpos on (k4_raster_fwd's fallback_fill with the producer warps); returns the batch size (0: done)
+__device__ __forceinline__ int kp_fill(const float4 *__restrict__ rseg, int F, float tau, const TileCtx &tc, int W, int H,
+                                       int &fpos, int *sid, int *pws, int ptid)
+{
+    const int lane = ptid & 31, pw = ptid >> 5;
+    int nb = 0;
+    kp_pbar();   // the previous batch's sid has been staged by every producer
+    while (fpos < F) {
+        const int f = fpos + ptid;
+        bool hit = false;
+        if (f < F) {
+            const float4 *r = rseg + (size_t)f * REC_F4;
+            const float4 q6 = __ldg(r + 6);
+            if (__float_as_int(q6.w) >= 0) {
+                const float4 b0 = __ldg(r + 7), b1 = __ldg(r + 8);
+                int x0, x1, y0, y1;
+                hit = tile_pixels(box_lerp(tau, b0.x, b1.x), box_lerp(tau, b0.y, b1.y), box_lerp(tau, b0.z, b1.z),
+                                  box_lerp(tau, b0.w, b1.w), W, H, tc, x0, x1, y0, y1);
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0) pws[pw] = __popc(m);
+        kp_pbar();
+        int pre = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < KP_NP / 32; ++w) {
+            const int c = pws[w];
+            pre += w < pw ? c : 0;
+            tot += c;
+        }
+        kp_pbar();
+        if (nb + tot > KP_SREC) break;                   // uniform: batch full
+        if (hit) sid[nb + pre + __popc(m & ((1u << lane) - 1u))] = f;
+        nb += tot;
+        fpos += KP_NP;
+    }
+    kp_pbar();   // sid[] complete before the batch is staged
+    return nb;
+}
+
+// consumers: the footprint tests of one list (records of buffer rbase) against this lane's pixel
+__device__ __forceinline__ void kp_vis(const unsigned char *rbase, const uint16_t *lst, int cn, int cbk, int n,
+                                       float ul, float vl, float4 fc, float &zbest, int &eoff, float &tief)
+{
+    for (int i = 0; i < cn; ++i) {   // faces turned towards the camera
+        const int off = lst[i];
+        const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
+        const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
+        const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
+        const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
+        const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
+        const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
+        const float emin = fminf(fminf(e0, e1), e2);
+        tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
+        if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
+    }
+    if (cbk) {   // the others: skipped where they are behind every pixel's winner
+        float zmax = zbest;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, d));
+        // zmax = +inf unless every pixel of the footprint has a winner.  The depth plane fma(az, ul, fma(bz, vl,
+        // cz)) is monotone in ul and vl, so its minimum over the footprint's pixel centres is its value at one
+        // corner: above zmax, the face cannot win or tie anywhere in the footprint.
+        for (int i = n - cbk; i < n; ++i) {
+            const int off = lst[i];
+            const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
+            const float4 q2 = rp[2];
+            const float zmin = __fmaf_rn(q2.y, q2.y > 0.f ? fc.x : fc.y, __fmaf_rn(q2.z, q2.z > 0.f ? fc.z : fc.w, q2.w));
+            if (zmin > zmax) continue;
+            const float4 q0 = rp[0], q1 = rp[1];
+            const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
+            const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
+            const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
+            const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
+            const float emin = fminf(fminf(e0, e1), e2);
+            tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
+            if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
+        }
+    }
+}
+
+// consumers: the lexicographic (depth, face index) z-test over both lists (exact ties, Q7; batches)
+__device__ __forceinline__ void kp_vis_tie(const unsigned char *rbase, const uint16_t *lst, int cn, int cbk, int n,
+                                           float ul, float vl, float &zbest, int &eoff, int &fbest)
+{
+    for (int ii = 0; ii < cn + cbk; ++ii) {
+        const int off = lst[ii < cn ? ii : n - cbk + (ii - cn)];
+        const TauRec *rr = reinterpret_cast<const TauRec *>(rbase + off);
+        const float4 *rp = reinterpret_cast<const float4 *>(rr);
+        const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
+        const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
+        const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
+        const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
+        const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
+        if (fminf(fminf(e0, e1), e2) >= 0.f && z <= zbest) {
+            const int fj = rr->fid;
+            if (z < zbest || fj < fbest) { zbest = z; eoff = off; fbest = fj; }
+        }
+    }
+}
+
+template <bool COV>
+__global__ void __launch_bounds__(KP_NTH, BR_KP_MINB) k4p_raster_fwd(Tables t, float *__restrict__ out,
+                                                                    int *__restrict__ ids, int ids_k)
+{
+    static_assert(!BR_HALF, "the pipelined forward uses the warps' 8x4 footprints");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    KpSmem &S = *reinterpret_cast<KpSmem *>(smem_raw);
+    const int b = blockIdx.y, tile = blockIdx.x;
+    const ImgInfo &im = t.imgs[b];
+    TileCtx tc;
+    tile_ctx(t, tile, tc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 2 * GMAX_F * NFP; i += KP_NTH) { (&S.cnt[0][0][0])[i] = 0; (&S.cntb[0][0][0])[i] = 0; }
+    if (threadIdx.x < NT) {
+        const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+        S.uv[threadIdx.x] = make_float2((float)(lx - TW / 2) * tc.sx, (float)(TH / 2 - ly) * tc.sy);
+        S.acc[ly * TW + lx] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (lane == 0)   // the warp footprint's corner pixel centres (the lanes' own ul, vl values)
+            S.fpc[warp] = make_float4((float)((warp & 1) * 8 - TW / 2) * tc.sx, (float)((warp & 1) * 8 + 7 - TW / 2) * tc.sx,
+                                      (float)(TH / 2 - (warp >> 1) * 4 - 3) * tc.sy, (float)(TH / 2 - (warp >> 1) * 4) * tc.sy);
+    }
+    __syncthreads();
+
+    if (threadIdx.x >= NT) {
+        // ---------------------------------------------------------------- producers
+        const int ptid = threadIdx.x - NT;
+        const double orient = *t.orient;
+        const float sF = BR_K4P_CULL ? (orient > 0.0 ? 1.f : orient < 0.0 ? -1.f : 0.f) : 0.f;
+        const bool need_empty = ids != nullptr || COV;
+        const int sched_off = im.sched_off;
+        int g = 0;
+        for (int c = im.chunk_begin + (int)blockIdx.z; c < im.chunk_end; c += t.splits) {
+            const Chunk ch = t.chunks[c];
+            const size_t bi = (size_t)c * t.T + tile;
+            const long long o = t.off[bi];
+            const int n = (int)(t.off[bi + 1] - o);
+            if (n == 0) {
+                if (need_empty) {
+                    const int bb = g & 1;
+                    if (g >= 2) kp_bar_sync(3 + bb, KP_NTH);
+                    if (ptid == 0) S.desc[bb] = KpDesc{KP_EMPTY, 0, 0, ch.k0, ch.k1, 1};
+                    kp_bar_arrive(1 + bb, KP_NTH);
+                    ++g;
+                }
+                continue;
+            }
+            BinCtx bc;
+            bc.status = t.status;
+            bc.rseg = t.rec + (size_t)(im.rec_off + (long long)ch.s * t.F) * REC_F4;
+            bc.key0 = nullptr;
+            bc.key1 = nullptr;
+            bc.fcol = t.fcol;
+            bc.ent = t.entries + o;
+            bc.n = n;
+            bc.fb = o + n > t.cap;
+            if (!bc.fb && n <= KP_SREC) {
+                const int Gs = min(GMAX_F, group_div(KP_SREC, n));
+                kp_pbar();   // every producer is done with the previous chunk's face ids
+                for (int j = ptid; j < n; j += KP_NP) S.sid[j] = __ldg(bc.ent + j);
+                for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
+                    const int ng = min(Gs, ch.k1 - kg), bb = g & 1;
+                    if (g >= 2) kp_bar_sync(3 + bb, KP_NTH);   // buffer bb consumed (and its counters cleared)
+                    if (ptid < ng) S.taus[bb][ptid] = t.sched_tau[sched_off + kg + ptid];
+                    if (ptid == 0) S.desc[bb] = KpDesc{KP_GROUP, n, ng, kg, 0, 0};
+                    kp_pbar();
+                    kp_stage_raw(bc, S.sid, n, S.taus[bb], ng, tc, t.W, t.H, t.F, S.rec[bb], S.list[bb], S.cnt[bb],
+                                 S.cntb[bb], sF, S.raw, ptid);
+                    kp_bar_arrive(1 + bb, KP_NTH);
+                    ++g;
+                }
+            } else {
+                for (int k = ch.k0; k < ch.k1; ++k) {
+                    const float tau = t.sched_tau[sched_off + k];
+                    int base = 0, fpos = 0;
+                    while (true) {
+                        const int bb = g & 1;
+                        if (g >= 2) kp_bar_sync(3 + bb, KP_NTH);
+                        int nb;
+                        if (bc.fb) nb = kp_fill(bc.rseg, t.F, tau, tc, t.W, t.H, fpos, S.sid, S.pws, ptid);
+                        else nb = min(KP_SREC, n - base);
+                        const bool last = nb == 0 || (!bc.fb && base + nb >= n);
+                        if (ptid == 0) { S.taus[bb][0] = tau; S.desc[bb] = KpDesc{KP_BATCH, nb, 1, k, base, last ? 1 : 0}; }
+                        kp_pbar();
+                        if (nb > 0)
+                            kp_stage(bc, bc.ent + base, bc.fb ? S.sid : nullptr, nb, S.taus[bb], 1, tc, t.W, t.H, t.F, S.rec[bb],
+                                     S.list[bb], S.cnt[bb], S.cntb[bb], sF, ptid);
+                        kp_bar_arrive(1 + bb, KP_NTH);
+                        ++g;
+                        base += nb;
+                        if (last) break;
+                    }
+                }
+            }
+        }
+        const int bb = g & 1;
+        if (g >= 2) kp_bar_sync(3 + bb, KP_NTH);
+        if (ptid == 0) S.desc[bb] = KpDesc{KP_END, 0, 0, 0, 0, 0};
+        kp_bar_arrive(1 + bb, KP_NTH);
+        return;
+    }
+
+    // -------------------------------------------------------------------- consumers (8 warps, one footprint each)
+    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+    const int px = tc.px0 + lx, py = tc.py0 + ly;
+    const bool inimg = px < t.W && py < t.H;
+    const int myp = ly * TW + lx;
+    // per-sub-frame batch state (long and overflowed bins)
+    float bz = __int_as_float(0x7f800000), pr = 0.f, pg = 0.f, pb = 0.f;
+    int bfb = 0x7fffffff, bfid = -1;
+    bool has = false;
+    for (int g = 0;; ++g) {
+        const int bb = g & 1;
+        kp_bar_sync(1 + bb, KP_NTH);
+        const KpDesc d = S.desc[bb];
+        if (d.kind == KP_END) break;
+        const unsigned char *rbase = reinterpret_cast<const unsigned char *>(S.rec[bb]);
+        const float2 uvp = S.uv[threadIdx.x];
+        const float ul = uvp.x, vl = uvp.y;
+        if (d.kind == KP_EMPTY) {
+            if (ids && inimg && ids_k >= d.kg && ids_k < d.k1) ids[((size_t)b * t.H + py) * t.W + px] = -1;
+            if (COV) {
+                const unsigned m = __ballot_sync(0xffffffffu, !inimg);
+                if (lane == 0)
+                    for (int k = d.kg; k < d.k1; ++k) t.covbits[cov_word(t, im, k, tile) + warp] = m;
+            }
+        } else if (d.kind == KP_GROUP) {
+            const int n = d.n;
+            uint16_t *vrow = (n <= VIS_MAXN && t.vis) ? t.vis + ((size_t)(im.cov_off + d.kg) * t.T + tile) * (TW * TH) + myp : nullptr;
+            const uint16_t *lst = S.list[bb][warp];
+            const float4 fc = S.fpc[warp];
+            for (int l = 0; l < d.ng; ++l, lst += n) {
+                const int cn = S.cnt[bb][l][warp], cbk = S.cntb[bb][l][warp];
+                float zbest = __int_as_float(0x7f800000), tief = 0.f;
+                int eoff = -1;
+                kp_vis(rbase, lst, cn, cbk, n, ul, vl, fc, zbest, eoff, tief);
+                if (__any_sync(0xffffffffu, tief != 0.f)) {   // exact depth tie in the warp: face indices decide (Q7)
+                    zbest = __int_as_float(0x7f800000);
+                    eoff = -1;
+                    int fbest = 0x7fffffff;
+                    kp_vis_tie(rbase, lst, cn, cbk, n, ul, vl, zbest, eoff, fbest);
+                }
+                __syncwarp();
+                if (lane == 0) { S.cnt[bb][l][warp] = 0; S.cntb[bb][l][warp] = 0; }
+                const int ebest = eoff >= 0 ? eoff / (int)sizeof(TauRec) - l * n : -1;
+                int fid = -1;
+                if (ebest >= 0) {
+                    const TauRec &rw = *reinterpret_cast<const TauRec *>(rbase + eoff);
+                    float r_, g_, b_;
+                    shade(rw, t.fcol, ul, vl, r_, g_, b_);      // Eq.9
+                    float4 a = S.acc[myp];
+                    a.x += r_; a.y += g_; a.z += b_; a.w += 1.f;
+                    S.acc[myp] = a;
+                    fid = rw.fid;
+                }
+                if (ids && inimg && d.kg + l == ids_k) ids[((size_t)b * t.H + py) * t.W + px] = fid;
+                if (vrow) {   // visibility cache for K6
+                    *vrow = ebest >= 0 ? (uint16_t)ebest : (uint16_t)0xFFFF;
+                    vrow += (size_t)t.T * (TW * TH);
+                }
+                if (COV) {   // soft path: which pixels of the warp are covered at this sub-frame
+                    const unsigned m = __ballot_sync(0xffffffffu, ebest >= 0 || !inimg);
+                    if (lane == 0) t.covbits[cov_word(t, im, d.kg + l, tile) + warp] = m;
+                }
+            }
+        } else {   // KP_BATCH: one sub-frame d.kg, records of bin slots [d.k1, d.k1 + n); d.last ends it
+            const int n = d.n;
+            if (n > 0) {
+                const uint16_t *lst = S.list[bb][warp];
+                const int cn = S.cnt[bb][0][warp], cbk = S.cntb[bb][0][warp];
+                int eoff = -1;
+                kp_vis_tie(rbase, lst, cn, cbk, n, ul, vl, bz, eoff, bfb);
+                __syncwarp();
+                if (lane == 0) { S.cnt[bb][0][warp] = 0; S.cntb[bb][0][warp] = 0; }
+                if (eoff >= 0) {   // winner changed in this batch: shade now (Eq.9)
+                    const TauRec &rw = *reinterpret_cast<const TauRec *>(rbase + eoff);
+                    shade(rw, t.fcol, ul, vl, pr, pg, pb);
+                    has = true;
+                    bfid = rw.fid;
+                }
+            }
+            if (d.last) {
+                if (has) {
+                    float4 a = S.acc[myp];
+                    a.x += pr; a.y += pg; a.z += pb; a.w += 1.f;
+                    S.acc[myp] = a;
+                }
+                if (ids && inimg && d.kg == ids_k) ids[((size_t)b * t.H + py) * t.W + px] = has ? bfid : -1;
+                if (COV) {
+                    const unsigned m = __ballot_sync(0xffffffffu, has || !inimg);
+                    if (lane == 0) t.covbits[cov_word(t, im, d.kg, tile) + warp] = m;
+                }
+                bz = __int_as_float(0x7f800000);
+                bfb = 0x7fffffff;
+                bfid = -1;
+                has = false;
+            }
+        }
+        kp_bar_arrive(3 + bb, KP_NTH);
+    }
+    if (inimg && out) {   // out == null: coverage-only pass (soft backward without a preceding forward)
+        const float inv = 1.0f / (float)im.N;
+        const float4 a = S.acc[myp];
+        const float4 v = make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
+        const size_t pix = ((size_t)b * t.H + py) * t.W + px;
+        if (t.splits == 1) reinterpret_cast<float4 *>(out)[pix] = v;
+        else t.part[(size_t)blockIdx.z * ((size_t)t.B * t.H * t.W) + pix] = v;
+    }
+}
+
+template <bool COV>
+static cudaError_t launch_fwd_pipe(const Tables &t, float *out, int *ids, int ids_k, cudaStream_t st)
+{
+    dim3 grid(t.T, t.B, t.splits);
+    const int smem = (int)sizeof(KpSmem);
+    cudaError_t e = cudaFuncSetAttribute(k4p_raster_fwd<COV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k4p_raster_fwd<COV><<<grid, KP_NTH, smem, st>>>(t, out, ids, ids_k);
+    return cudaGetLastError();
+}
+
+// BLURRAST_FWD=pipe: the warp-specialised k4p_raster_fwd instead of k4l_raster_fwd (A/B; measured slower,
+// DESIGN.md section 4)
+static bool pipe_fwd_on()
+{
+    const char *s = std::getenv("BLURRAST_FWD");
+    return s && std::strcmp(s, "pipe") == 0;
+}
+
+// BLURRAST_LEAN_FWD=0: the fast solver's timed forward takes k4_raster_fwd instead (A/B)
+static bool lean_fwd_off()
+{
+    const char *s = std::getenv("BLURRAST_LEAN_FWD");
+    return s && s[0] == '0';
+}
+
 // ------------------------------------------------------------------ backward
 //
 // Visibility as in the forward pass.  Then, per (tile, sub-frame): the face's gradient is linear in
@@ -991,7 +1845,7 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd_fx(Tables t, con
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BwdFxSmem<MODE> &S = *reinterpret_cast<BwdFxSmem<MODE> *>(smem_raw);
-    if (t.vis_gathered && !t.vg_left[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x])
+    if (t.vis_gathered && !t.vg_left[(size_t)blockIdx.y * gridDim.x + blockIdx.x])
         return;   // every chunk of this CTA was taken by k6v_raster_bwd (k_gather.cu)
     const int b = blockIdx.y, tile = blockIdx.x;
     const ImgInfo &im = t.imgs[b];
@@ -1278,7 +2132,12 @@ cudaError_t launch_raster_fwd_legacy(const Tables &t, float *out, int *ids, int 
 {
     if (t.B == 0 || t.T == 0) return cudaSuccess;
     switch (t.solver * 2 + (census ? 1 : 0)) {
-    case 0: return launch_fwd_t<false, 0>(t, out, ids, ids_k, nullptr, st);
+    case 0:
+        if (pipe_fwd_on())
+            return t.covbits ? launch_fwd_pipe<true>(t, out, ids, ids_k, st) : launch_fwd_pipe<false>(t, out, ids, ids_k, st);
+        if (!lean_fwd_off())
+            return t.covbits ? launch_fwd_lean<true>(t, out, ids, ids_k, st) : launch_fwd_lean<false>(t, out, ids, ids_k, st);
+        return launch_fwd_t<false, 0>(t, out, ids, ids_k, nullptr, st);
     case 1: return launch_fwd_t<true, 0>(t, out, ids, ids_k, census, st);
     case 2: return launch_fwd_t<false, 1>(t, out, ids, ids_k, nullptr, st);
     case 3: return launch_fwd_t<true, 1>(t, out, ids, ids_k, census, st);

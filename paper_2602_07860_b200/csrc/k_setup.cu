@@ -10,6 +10,8 @@
 //     bit-identical coefficients up to sign (watertight coverage).  det F(tau) = d3 + tau(d2 + tau d1)
 //     from keyframe edge vectors (A8 regrouped).  The A11-A16 expansion itself is ill-conditioned
 //     in fp32; this is the same polynomial, see DESIGN.md.
+#include <algorithm>
+
 #include "internal.cuh"
 #include "../../include/blurrast.h"
 
@@ -22,6 +24,7 @@ __global__ void __launch_bounds__(256) k1_keyframes(Tables t, const float *__res
     const int V = t.V;
     const int nk = (im.S + 1) * V;
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx == 0 && b == 0) *t.orient = 0.0;   // k_orient accumulates after this kernel
     if (idx >= nk) return;
     const int s = idx / V, v = idx - s * V;
     const PoseRec &pr = t.poses[im.pose_off + s];
@@ -161,6 +164,25 @@ __global__ void __launch_bounds__(256) k2_face_setup(Tables t, const int *__rest
     for (int k = lane; k < cnt; k += 32) out[k] = st[warp][k];
 }
 
+// Mesh orientation for the forward's visiting order (k4l_raster_fwd: faces turned towards the camera
+// first, so that the others can be skipped per warp footprint once every pixel there has a nearer winner).
+// Only the sign is used, and only for speed: the result of the raster does not depend on it.
+__global__ void __launch_bounds__(256) k_orient(Tables t, const float *__restrict__ verts, const int *__restrict__ faces)
+{
+    double acc = 0.0;
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < t.F; f += gridDim.x * blockDim.x) {
+        const int a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
+        if ((unsigned)a >= (unsigned)t.V || (unsigned)b >= (unsigned)t.V || (unsigned)c >= (unsigned)t.V) continue;
+        const double ax = verts[3 * a], ay = verts[3 * a + 1], az = verts[3 * a + 2];
+        const double bx = verts[3 * b], by = verts[3 * b + 1], bz = verts[3 * b + 2];
+        const double cx = verts[3 * c], cy = verts[3 * c + 1], cz = verts[3 * c + 2];
+        acc += ax * (by * cz - bz * cy) + ay * (bz * cx - bx * cz) + az * (bx * cy - by * cx);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    if ((threadIdx.x & 31) == 0 && acc != 0.0) atomicAdd(t.orient, acc);
+}
+
 cudaError_t launch_setup(const Tables &t, const float *verts, const int *faces, const float *colors,
                          int maxS, cudaStream_t st)
 {
@@ -174,6 +196,7 @@ cudaError_t launch_setup(const Tables &t, const float *verts, const int *faces, 
         long long nf = (long long)maxS * t.F;
         dim3 grid((unsigned)((nf + 255) / 256), (unsigned)t.B);
         k2_face_setup<<<grid, 256, 0, st>>>(t, faces, colors);
+        k_orient<<<(unsigned)std::min<long long>((t.F + 255) / 256, 148), 256, 0, st>>>(t, verts, faces);
     }
     return cudaGetLastError();
 }
