@@ -575,6 +575,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
 #ifndef BR_K4L_PAIR2
 #define BR_K4L_PAIR2 0  // 1: two pairs per thread, both pairs' first record words requested together (measured slower)
 #endif
+#ifndef BR_K4L_TWOPASS
+#define BR_K4L_TWOPASS 0   // 1: box tests first, then the full stage over the compacted accepted pairs (C4 6.88 -> 7.51 ms)
+#endif
 #ifndef BR_K4L_SENT
 #define BR_K4L_SENT 0   // 1: the chunk's bin entries staged in shared memory (measured: no change)
 #endif
@@ -589,7 +592,9 @@ struct __align__(16) LeanSmem {
             uint16_t list[NFP][SREC_F];         // per footprint: sub-frame l's reaching records (byte offsets into rec)
             int cnt[GMAX_F][NFP];               // ... at [l * n, l * n + cnt): faces turned towards the camera,
             int cntb[GMAX_F][NFP];              // and at [l * n + n - cntb, l * n + n): the others
-            int ent[SREC_F];                    // the chunk's bin entries (face ids)
+            int ent[BR_K4L_SENT ? SREC_F : 1];  // the chunk's bin entries (face ids)
+            int acc_pairs[BR_K4L_TWOPASS ? SREC_F : 1];   // box-accepted pairs: j | l << 9 | box << 13
+            int nacc;
         } g;                                    // grouped path
         struct {
             uint32_t wm[NFP * (SREC_F / 32 + GMAX_F)];
@@ -680,6 +685,43 @@ __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *en
 #endif
 }
 
+// Two passes: the box tests of all the group's pairs, the accepted ones compacted into apairs (warp-aggregated
+// slots), a barrier, then the full stage over the accepted pairs -- every lane of the stage has a pair (about
+// half the pairs miss the tile at their sub-frame).  nacc must be zero on entry; it is left nonzero.
+__device__ __forceinline__ void stage_group_2pass(const BinCtx &bc, const int *ent, int n, const float *taus, int ng,
+                                                  const TileCtx &tc, int W, int H, int F, TauRec *rec,
+                                                  uint16_t (*list)[SREC_F], int (*cnt)[NFP], int (*cntb)[NFP], float sF,
+                                                  int *apairs, int *nacc)
+{
+    const int npair = n * ng, lane = threadIdx.x & 31;
+    const float inv_ng = 1.0f / (float)ng;
+    for (int p0 = threadIdx.x - lane; p0 < npair; p0 += NT) {   // warp-uniform trip count
+        const int p = p0 + lane;
+        int j = 0, l = 0, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+        const float4 *r;
+        float D;
+        const bool ok = p < npair && pair_head(bc, ent, p, inv_ng, ng, taus, tc, W, H, F, j, l, r, D, x0, x1, y0, y1);
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        int base = 0;
+        if (lane == 0 && m) base = atomicAdd(nacc, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (ok) apairs[base + __popc(m & ((1u << lane) - 1u))] = j | (l << 9) | (x0 << 13) | (x1 << 17) | (y0 << 21) | (y1 << 25);
+    }
+    __syncthreads();
+    const int na = *nacc;
+    for (int i = threadIdx.x; i < na; i += NT) {
+        const int code = apairs[i];
+        const int j = code & 0x1FF, l = (code >> 9) & 0xF;
+        const int f = BR_K4L_SENT ? ent[j] : __ldg(ent + j);
+        const float4 *r = bc.rseg + (size_t)f * REC_F4;
+        const float tau = taus[l];
+        const float4 q6 = __ldg(r + 6);
+        const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);
+        pair_stage(r, j, l, n, tau, D, (code >> 13) & 0xF, (code >> 17) & 0xF, (code >> 21) & 0xF, (code >> 25) & 0xF, tc,
+                   rec, list, cnt, cntb, sF);
+    }
+}
+
 template <bool COV>
 __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float *__restrict__ out, int *__restrict__ ids,
                                                                 int ids_k)
@@ -704,6 +746,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
     S.acc[myp] = make_float4(0.f, 0.f, 0.f, 0.f);
     S.uv[threadIdx.x] = make_float2(ul, vl);
     for (int i = threadIdx.x; i < GMAX_F * NFP; i += NT) { (&S.u.g.cnt[0][0])[i] = 0; (&S.u.g.cntb[0][0])[i] = 0; }
+    if (threadIdx.x == 0) S.u.g.nacc = 0;
     unsigned long long dz = 0;
     const double orient = *t.orient;
     const float sF = orient > 0.0 ? 1.f : orient < 0.0 ? -1.f : 0.f;
@@ -748,7 +791,12 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                 const int ng = min(Gs, ch.k1 - kg);
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
                 __syncthreads();   // taus written; the previous group's lists and counters are consumed
+#if BR_K4L_TWOPASS
+                stage_group_2pass(bc, ents, n, S.taus, ng, tc, t.W, t.H, t.F, S.rec, S.u.g.list, S.u.g.cnt, S.u.g.cntb, sF,
+                                  S.u.g.acc_pairs, &S.u.g.nacc);
+#elif !defined(BR_EXP_NOSTAGE)
                 stage_group_list(bc, ents, n, S.taus, ng, tc, t.W, t.H, t.F, S.rec, S.u.g.list, S.u.g.cnt, S.u.g.cntb, sF);
+#endif
                 __syncthreads();
                 uint16_t *vrow = vis_out ? vis_out + ((size_t)(im.cov_off + kg) * t.T + tile) * (TW * TH) + myp : nullptr;
                 const int l_ids = (ids && inimg) ? ids_k - kg : -1;
@@ -847,6 +895,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                 }
                 __syncthreads();   // lists read: clear the counters of this group
                 if (threadIdx.x < ng * NFP) { (&S.u.g.cnt[0][0])[threadIdx.x] = 0; (&S.u.g.cntb[0][0])[threadIdx.x] = 0; }
+                if (threadIdx.x == 0) S.u.g.nacc = 0;
             }
         } else {
             // per sub-frame, several batches (long bins) or the exact fallback scan (overflow): as k4_raster_fwd
@@ -890,6 +939,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
             }
             __syncthreads();   // the grouped path's counters share the batch path's shared memory
             for (int i = threadIdx.x; i < GMAX_F * NFP; i += NT) { (&S.u.g.cnt[0][0])[i] = 0; (&S.u.g.cntb[0][0])[i] = 0; }
+            if (threadIdx.x == 0) S.u.g.nacc = 0;
         }
     }
     if (inimg && out) {   // out == null: coverage-only pass (soft backward without a preceding forward)
