@@ -37,7 +37,7 @@
 namespace br {
 
 #ifndef BR_SG_PCAP
-#define BR_SG_PCAP 256
+#define BR_SG_PCAP 224
 #endif
 #ifndef BR_VG_SPLITS
 #define BR_VG_SPLITS 1     // CTAs per (image, tile) (chunks dealt round-robin)
@@ -46,7 +46,7 @@ namespace br {
 #define BR_VG_PREFETCH 0   // 1: L1 prefetch of the won faces' records in the list phase (C4 K6 +1%, C3 -2%)
 #endif
 #ifndef BR_VG_MINB
-#define BR_VG_MINB 4
+#define BR_VG_MINB 5
 #endif
 constexpr int SG_T = 16;                 // sub-frames per super-group (16-bit won masks)
 constexpr int SG_SLOTS = 4 * NT;         // bin slots per super-group (4 per thread in the list phase)
@@ -61,10 +61,9 @@ struct __align__(16) VgSmem {
     uint4 vis[SG_T][SG_SEG];             // winner slot per (group sub-frame, pixel), 0xFFFF none
     uint32_t wmask[SG_SLOTS / 2];        // won masks being built, two 16-bit slots per word
     uint32_t sbm[SG_SLOTS];              // per group slot: first pair index << 16 | won mask (bit l: won at sub-frame l)
-    int sface[SG_SLOTS];                 // face id of each won group slot
     int imom[SG_PCAP][9];                // fixed-point moments M0 (rgb), Mu (rgb), Mv (rgb) per pair
-    float contrib[SG_PCAP][16];          // per pair: dv (6, screen space), dc (9)
-    uint16_t plist[SG_PCAP];             // pairs of the batch: group slot | l << 10
+    float contrib[SG_PCAP][15];          // per pair: dv (6, screen space), dc (9)
+    int plist[SG_PCAP];                  // pairs of the batch: group slot | l << 10 | face id << 14 (-1 << 14: bad id)
     // chunk-table window of this CTA (chunks c_begin + z + i * splits)
     int ci_n[SG_CMAX], ci_k0[SG_CMAX], ci_ng[SG_CMAX], ci_s[SG_CMAX];
     long long ci_o[SG_CMAX];
@@ -91,17 +90,31 @@ __device__ __forceinline__ uint16_t u4_get(const uint4 &w, int k)
     return (uint16_t)((k & 1) ? x >> 16 : x & 0xFFFFu);
 }
 
+// the face id of group slot gs (won at group sub-frame l0), -1 if out of range (never expected)
+__device__ __forceinline__ int slot_face(const Tables &t, const VgSmem &S, int gs, int l0)
+{
+    const int f = __ldg(t.entries + S.t_o[l0] + (gs - S.t_soff[l0]));
+    if ((unsigned)f >= (unsigned)t.F) {
+        atomicOr(t.status, BLUR_ST_EINTERNAL);
+        return -1;
+    }
+    return f;
+}
+
 // write the batch's pair codes (pairs [pb, pb + np)) of this thread's four group slots
-__device__ __forceinline__ void write_plist(VgSmem &S, int pb, int np)
+__device__ __forceinline__ void write_plist(const Tables &t, VgSmem &S, int pb, int np)
 {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int gs = 4 * threadIdx.x + q;
         const uint32_t w = S.sbm[gs];
         unsigned mk = w & 0xFFFFu;
+        if (!mk) continue;
         int i = (int)(w >> 16) - pb;
+        if (i >= np || i + __popc(mk) <= 0) continue;
+        const int f = slot_face(t, S, gs, __ffs(mk) - 1);
         for (; mk; mk &= mk - 1, ++i)
-            if ((unsigned)i < (unsigned)np) S.plist[i] = (uint16_t)(gs | ((__ffs(mk) - 1) << 10));
+            if ((unsigned)i < (unsigned)np) S.plist[i] = gs | ((__ffs(mk) - 1) << 10) | (f << 14);
     }
 }
 
@@ -261,15 +274,10 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
             for (int q = 0; q < 4; ++q) {
                 const int gs = 4 * tid + q;
                 S.sbm[gs] = ((uint32_t)base << 16) | mk[q];
-                if (mk[q]) {
+                if (mk[q] && base < SG_PCAP) {
                     // the slot's chunk: that of its first won sub-frame
                     const int l0 = __ffs(mk[q]) - 1;
-                    int f = __ldg(t.entries + S.t_o[l0] + (gs - S.t_soff[l0]));
-                    if ((unsigned)f >= (unsigned)t.F) {
-                        atomicOr(t.status, BLUR_ST_EINTERNAL);
-                        f = -1;
-                    }
-                    S.sface[gs] = f;
+                    const int f = slot_face(t, S, gs, l0);
 #if BR_VG_PREFETCH
                     if (f >= 0) {   // the pair phase reads the face's segment record and colours: start them now
                         const float4 *rr = t.rec + ((size_t)(im.rec_off + (long long)S.t_seg[l0] * t.F) + f) * REC_F4;
@@ -280,7 +288,7 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
 #endif
                     int i = base;
                     for (unsigned m = mk[q]; m; m &= m - 1, ++i)
-                        if (i < SG_PCAP) S.plist[i] = (uint16_t)(gs | ((__ffs(m) - 1) << 10));
+                        if (i < SG_PCAP) S.plist[i] = gs | ((__ffs(m) - 1) << 10) | (f << 14);
                 }
                 base += __popc(mk[q]);
             }
@@ -290,7 +298,7 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
         for (int pb = 0; pb < total; pb += SG_PCAP) {
             const int np = min(SG_PCAP, total - pb);
             if (pb > 0) {
-                write_plist(S, pb, np);
+                write_plist(t, S, pb, np);
                 __syncthreads();
             }
             // moments (imom is zero on entry: cleared at start and by every pair that read it)
@@ -336,8 +344,7 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
             // pairs: thread per pair
             for (int i = tid; i < np; i += NT) {
                 const int code = S.plist[i];
-                const int gs = code & 0x3FF, l = code >> 10;
-                const int fj = S.sface[gs];
+                const int l = (code >> 10) & 0xF, fj = code >> 14;
                 int *mi = S.imom[i];
                 float m[9];
 #pragma unroll
@@ -403,7 +410,8 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
 #pragma unroll
                     for (int e = 0; e < 9; ++e) acc.c[e] += cb[6 + e];
                 }
-                if (S.sface[gs] >= 0) flush(t, im, S.t_seg[l0], S.sface[gs], acc.k0, acc.k1, acc.c, dC);
+                const int fj = S.plist[max(base, pb) - pb] >> 14;
+                if (fj >= 0) flush(t, im, S.t_seg[l0], fj, acc.k0, acc.k1, acc.c, dC);
             }
             if (pb + np < total) __syncthreads();   // the next batch reuses plist / imom / contrib
         }
