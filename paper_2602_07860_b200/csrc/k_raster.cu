@@ -581,8 +581,18 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
 #ifndef BR_K4L_SENT
 #define BR_K4L_SENT 0   // 1: the chunk's bin entries staged in shared memory (measured: no change)
 #endif
+#ifndef BR_K4L_UNROLL
+#define BR_K4L_UNROLL 0
+#endif
+#if BR_K4L_UNROLL
+#define BR_UNROLL4 _Pragma("unroll 4")
+#else
+#define BR_UNROLL4
+#endif
 #ifndef BR_K4L_CULL
-#define BR_K4L_CULL 0   // 1: faces turned away from the camera tested last, skipped per footprint behind its winners
+#define BR_K4L_CULL 2   // faces turned away from the camera in a second list per footprint, tested last; 2: the whole
+                        // list skipped when every pixel's winner is nearer than the list's lowest depth; 1: each face
+                        // skipped behind the winners (per-face test; measured slower)
 #endif                  //    (measured slower in this kernel: C4 K4 6.86 -> 7.17 ms)
 
 struct __align__(16) LeanSmem {
@@ -592,6 +602,7 @@ struct __align__(16) LeanSmem {
             uint16_t list[NFP][SREC_F];         // per footprint: sub-frame l's reaching records (byte offsets into rec)
             int cnt[GMAX_F][NFP];               // ... at [l * n, l * n + cnt): faces turned towards the camera,
             int cntb[GMAX_F][NFP];              // and at [l * n + n - cntb, l * n + n): the others
+            int minz[GMAX_F][NFP];              // lowest depth of the others over the footprint (float bits, >= 0)
             int ent[BR_K4L_SENT ? SREC_F : 1];  // the chunk's bin entries (face ids)
             int acc_pairs[BR_K4L_TWOPASS ? SREC_F : 1];   // box-accepted pairs: j | l << 9 | box << 13
             int nacc;
@@ -639,17 +650,34 @@ __device__ __forceinline__ bool pair_head(const BinCtx &bc, const int *ent, int 
 
 __device__ __forceinline__ void pair_stage(const float4 *r, int j, int l, int n, float tau, float D, int x0, int x1,
                                            int y0, int y1, const TileCtx &tc, TauRec *rec, uint16_t (*list)[SREC_F],
-                                           int (*cnt)[NFP], int (*cntb)[NFP], float sF)
+                                           int (*cnt)[NFP], int (*cntb)[NFP], float sF, int (*minz)[NFP])
 {
     FaceRec fr;
     load_rec(r, fr);
     const uint32_t fm = stage_tau<true>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * n + j]);
     const uint16_t off = (uint16_t)((l * n + j) * (int)sizeof(TauRec));
     const bool back = BR_K4L_CULL && D * sF < 0.f;   // turned away from the camera (sF: mesh orientation)
+    if (!back) {
+        for (uint32_t m = fm; m; m &= m - 1) {
+            const int w = __ffs(m) - 1;
+            list[w][l * n + atomicAdd(&cnt[l][w], 1)] = off;
+        }
+        return;
+    }
+    const TauRec &R = rec[l * n + j];
+    const float az = R.az, bz = R.bz, cz = R.cz;
     for (uint32_t m = fm; m; m &= m - 1) {
         const int w = __ffs(m) - 1;
-        if (!back) list[w][l * n + atomicAdd(&cnt[l][w], 1)] = off;
-        else list[w][l * n + n - 1 - atomicAdd(&cntb[l][w], 1)] = off;
+        list[w][l * n + n - 1 - atomicAdd(&cntb[l][w], 1)] = off;
+        if (BR_K4L_CULL == 2) {
+            // the depth plane fma(az, ul, fma(bz, vl, cz)) is monotone in ul and vl: its minimum over the
+            // footprint's pixel centres is its value at one corner (the lanes' own ul, vl values)
+            const int wx = w & 1, wy = w >> 1;
+            const float u = (float)((az > 0.f ? 0 : 7) + wx * FPW - TW / 2) * tc.sx;
+            const float v = (float)(TH / 2 - wy * 4 - (bz > 0.f ? 3 : 0)) * tc.sy;
+            const float zm = fmaxf(__fmaf_rn(az, u, __fmaf_rn(bz, v, cz)), 0.f);   // NaN -> 0 (no skip)
+            atomicMin(&minz[l][w], __float_as_int(zm));
+        }
     }
 }
 
@@ -659,7 +687,8 @@ __device__ __forceinline__ void pair_stage(const float4 *r, int j, int l, int n,
 // record words before testing either (the stage is a chain of L2 round trips: fewer of them per group).
 __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *ent, int n, const float *taus, int ng,
                                                  const TileCtx &tc, int W, int H, int F, TauRec *rec,
-                                                 uint16_t (*list)[SREC_F], int (*cnt)[NFP], int (*cntb)[NFP], float sF)
+                                                 uint16_t (*list)[SREC_F], int (*cnt)[NFP], int (*cntb)[NFP], float sF,
+                                                 int (*minz)[NFP])
 {
     const int npair = n * ng;
     const float inv_ng = 1.0f / (float)ng;
@@ -671,8 +700,8 @@ __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *en
         float Da, Db = 0.f;
         const bool oka = pair_head(bc, ent, p0, inv_ng, ng, taus, tc, W, H, F, ja, la, ra, Da, xa0, xa1, ya0, ya1);
         const bool okb = p1 < npair && pair_head(bc, ent, p1, inv_ng, ng, taus, tc, W, H, F, jb, lb, rb, Db, xb0, xb1, yb0, yb1);
-        if (oka) pair_stage(ra, ja, la, n, taus[la], Da, xa0, xa1, ya0, ya1, tc, rec, list, cnt, cntb, sF);
-        if (okb) pair_stage(rb, jb, lb, n, taus[lb], Db, xb0, xb1, yb0, yb1, tc, rec, list, cnt, cntb, sF);
+        if (oka) pair_stage(ra, ja, la, n, taus[la], Da, xa0, xa1, ya0, ya1, tc, rec, list, cnt, cntb, sF, minz);
+        if (okb) pair_stage(rb, jb, lb, n, taus[lb], Db, xb0, xb1, yb0, yb1, tc, rec, list, cnt, cntb, sF, minz);
     }
 #else
     for (int p = threadIdx.x; p < npair; p += NT) {
@@ -680,7 +709,7 @@ __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *en
         const float4 *r;
         float D;
         if (pair_head(bc, ent, p, inv_ng, ng, taus, tc, W, H, F, j, l, r, D, x0, x1, y0, y1))
-            pair_stage(r, j, l, n, taus[l], D, x0, x1, y0, y1, tc, rec, list, cnt, cntb, sF);
+            pair_stage(r, j, l, n, taus[l], D, x0, x1, y0, y1, tc, rec, list, cnt, cntb, sF, minz);
     }
 #endif
 }
@@ -691,7 +720,7 @@ __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *en
 __device__ __forceinline__ void stage_group_2pass(const BinCtx &bc, const int *ent, int n, const float *taus, int ng,
                                                   const TileCtx &tc, int W, int H, int F, TauRec *rec,
                                                   uint16_t (*list)[SREC_F], int (*cnt)[NFP], int (*cntb)[NFP], float sF,
-                                                  int *apairs, int *nacc)
+                                                  int (*minz)[NFP], int *apairs, int *nacc)
 {
     const int npair = n * ng, lane = threadIdx.x & 31;
     const float inv_ng = 1.0f / (float)ng;
@@ -718,7 +747,7 @@ __device__ __forceinline__ void stage_group_2pass(const BinCtx &bc, const int *e
         const float4 q6 = __ldg(r + 6);
         const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);
         pair_stage(r, j, l, n, tau, D, (code >> 13) & 0xF, (code >> 17) & 0xF, (code >> 21) & 0xF, (code >> 25) & 0xF, tc,
-                   rec, list, cnt, cntb, sF);
+                   rec, list, cnt, cntb, sF, minz);
     }
 }
 
@@ -745,7 +774,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
     const size_t pix = ((size_t)b * t.H + py) * t.W + px;
     S.acc[myp] = make_float4(0.f, 0.f, 0.f, 0.f);
     S.uv[threadIdx.x] = make_float2(ul, vl);
-    for (int i = threadIdx.x; i < GMAX_F * NFP; i += NT) { (&S.u.g.cnt[0][0])[i] = 0; (&S.u.g.cntb[0][0])[i] = 0; }
+    for (int i = threadIdx.x; i < GMAX_F * NFP; i += NT) {
+        (&S.u.g.cnt[0][0])[i] = 0; (&S.u.g.cntb[0][0])[i] = 0; (&S.u.g.minz[0][0])[i] = 0x7f800000;
+    }
     if (threadIdx.x == 0) S.u.g.nacc = 0;
     unsigned long long dz = 0;
     const double orient = *t.orient;
@@ -793,9 +824,10 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                 __syncthreads();   // taus written; the previous group's lists and counters are consumed
 #if BR_K4L_TWOPASS
                 stage_group_2pass(bc, ents, n, S.taus, ng, tc, t.W, t.H, t.F, S.rec, S.u.g.list, S.u.g.cnt, S.u.g.cntb, sF,
-                                  S.u.g.acc_pairs, &S.u.g.nacc);
+                                  S.u.g.minz, S.u.g.acc_pairs, &S.u.g.nacc);
 #elif !defined(BR_EXP_NOSTAGE)
-                stage_group_list(bc, ents, n, S.taus, ng, tc, t.W, t.H, t.F, S.rec, S.u.g.list, S.u.g.cnt, S.u.g.cntb, sF);
+                stage_group_list(bc, ents, n, S.taus, ng, tc, t.W, t.H, t.F, S.rec, S.u.g.list, S.u.g.cnt, S.u.g.cntb, sF,
+                                 S.u.g.minz);
 #endif
                 __syncthreads();
                 uint16_t *vrow = vis_out ? vis_out + ((size_t)(im.cov_off + kg) * t.T + tile) * (TW * TH) + myp : nullptr;
@@ -813,7 +845,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                     const float ul = uvp.x, vl = uvp.y;
                     float zbest = __int_as_float(0x7f800000), tief = 0.f;
                     int eoff = -1;
-                    for (int i = 0; i < cn; ++i) {   // faces turned towards the camera
+                    BR_UNROLL4 for (int i = 0; i < cn; ++i) {   // faces turned towards the camera
                         const int off = lst[i];
                         const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
                         const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
@@ -825,7 +857,28 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                         tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
                         if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
                     }
-                    if (BR_K4L_CULL && cb) {   // the others: skipped where they are behind every pixel's winner
+                    if (BR_K4L_CULL == 2 && cb) {   // the others, unless all of them are behind every pixel's winner
+                        float zmax = zbest;
+#pragma unroll
+                        for (int d = 16; d > 0; d >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, d));
+                        // zmax = +inf unless every pixel of the footprint has a winner; each face of the list has
+                        // its depth >= minz at every pixel of the footprint (staging, corner of the plane)
+                        if (!(zmax < __int_as_float(S.u.g.minz[l][warp]))) {
+                            BR_UNROLL4 for (int i = n - cb; i < n; ++i) {
+                                const int off = lst[i];
+                                const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
+                                const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
+                                const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
+                                const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
+                                const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
+                                const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
+                                const float emin = fminf(fminf(e0, e1), e2);
+                                tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
+                                if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
+                            }
+                        }
+                    }
+                    if (BR_K4L_CULL == 1 && cb) {   // the others: skipped where they are behind every pixel's winner
                         float zmax = zbest;
 #pragma unroll
                         for (int d = 16; d > 0; d >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, d));
@@ -836,7 +889,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                         if (lane == 0) { atomicAdd(t.status + 40, cn); atomicAdd(t.status + 41, cb); atomicAdd(t.status + 43, zmax < __int_as_float(0x7f800000) ? 1 : 0); atomicAdd(t.status + 44, 1); }
 #endif
                         const float4 fc = S.fpc[warp];
-                        for (int i = n - cb; i < n; ++i) {
+                        BR_UNROLL4 for (int i = n - cb; i < n; ++i) {
                             const int off = lst[i];
                             const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
                             const float4 q2 = rp[2];
@@ -894,7 +947,10 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                     }
                 }
                 __syncthreads();   // lists read: clear the counters of this group
-                if (threadIdx.x < ng * NFP) { (&S.u.g.cnt[0][0])[threadIdx.x] = 0; (&S.u.g.cntb[0][0])[threadIdx.x] = 0; }
+                if (threadIdx.x < ng * NFP) {
+                    (&S.u.g.cnt[0][0])[threadIdx.x] = 0; (&S.u.g.cntb[0][0])[threadIdx.x] = 0;
+                    (&S.u.g.minz[0][0])[threadIdx.x] = 0x7f800000;
+                }
                 if (threadIdx.x == 0) S.u.g.nacc = 0;
             }
         } else {
@@ -938,7 +994,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                 }
             }
             __syncthreads();   // the grouped path's counters share the batch path's shared memory
-            for (int i = threadIdx.x; i < GMAX_F * NFP; i += NT) { (&S.u.g.cnt[0][0])[i] = 0; (&S.u.g.cntb[0][0])[i] = 0; }
+            for (int i = threadIdx.x; i < GMAX_F * NFP; i += NT) {
+                (&S.u.g.cnt[0][0])[i] = 0; (&S.u.g.cntb[0][0])[i] = 0; (&S.u.g.minz[0][0])[i] = 0x7f800000;
+            }
             if (threadIdx.x == 0) S.u.g.nacc = 0;
         }
     }
