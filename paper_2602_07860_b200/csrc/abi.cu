@@ -100,7 +100,7 @@ struct Plan {
     size_t o_cov = 0, o_spart = 0, o_scnt = 0, o_soff = 0, o_sbsum = 0, o_sent = 0;
     bool vis = false;      // BLUR_CACHE_VISIBILITY: K4 leaves the winning bin slot per (pixel, sub-frame)
     size_t o_vis = 0;
-    size_t o_vgl = 0;      // visibility gather: per raster CTA, 1 if it left chunks to k6_raster_bwd_fx
+    size_t o_vgl = 0;      // visibility gather: count + list of the (image, tile)s it left to k6_raster_bwd_fx
     size_t o_spz = 0;      // soft products K8 -> K9 (BLUR_CACHE_VISIBILITY with delta > 0)
     bool spz_on = false;
     size_t total = 0;
@@ -325,7 +325,7 @@ int make_plan(int V, int F, int B, int H, int W, const blur_motion *m, const blu
     P.vis = cache && legacy_env();
     P.spz_on = cache && P.soft;
     if (P.vis) { P.o_vis = o; o = align256(o + 2 * (size_t)P.n_sub * P.T * TW * TH); }
-    if (P.vis) { P.o_vgl = o; o = align256(o + (size_t)P.T * B * P.splits); }
+    if (P.vis) { P.o_vgl = o; o = align256(o + 16 + 4 * (size_t)P.T * B); }
     if (P.spz_on) { P.o_spz = o; o = align256(o + 4 * (size_t)P.n_sub * P.T * TW * TH); }
     P.total = o;
     return BLUR_OK;
@@ -374,7 +374,7 @@ Tables make_tables(const Plan &P, void *ws)
         t.sb.sortcap = 4096;
     }
     if (P.vis) t.vis = (uint16_t *)(w + P.o_vis);
-    if (P.vis) t.vg_left = (unsigned char *)(w + P.o_vgl);
+    if (P.vis) { t.vg_count = (int *)(w + P.o_vgl); t.vg_list = (int *)(w + P.o_vgl + 16); }
     if (P.spz_on) t.spz = (float *)(w + P.o_spz);
     t.legacy = legacy_env() ? 1 : 0;
     return t;

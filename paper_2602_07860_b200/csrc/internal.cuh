@@ -103,7 +103,8 @@ struct Tables {          // device pointers into the workspace
     double *orient;      // mesh orientation: sum over faces of det(P0[v0], P0[v1], P0[v2]) (6 x signed volume;
                          // > 0: outward counter-clockwise faces), written by the setup (k_orient)
     int vis_gathered;    // 1: k6v_raster_bwd (k_gather.cu) has taken the cached chunks; k6_raster_bwd_fx skips them
-    unsigned char *vg_left;   // [B][T]: 1 if k6v_raster_bwd left chunks of the (image, tile) to k6_raster_bwd_fx
+    int *vg_count;       // k6v_raster_bwd: number of (image, tile)s with chunks left to k6_raster_bwd_fx,
+    int *vg_list;        // ... and their b * T + tile ([B * T])
     float *spart;        // [splits][B*H*W] soft alpha partial sums (K8)
     float *spz;          // [sum_b N_b][T][TW*TH] soft products per (sub-frame, pixel) left by K8 for K9
                          // (prod of the non-zero factors 1 - A; negative: one zero factor, NaN: two or

@@ -27,7 +27,7 @@
 //            REDs per vertex colour.
 // Pairs beyond SG_PCAP are taken in further batches (moments, pairs, flush).  Chunks K4 wrote no
 // winners for (longer bins, overflowed bins) are left to k6_raster_bwd_fx: the CTA raises its
-// Tables::vg_left flag of its (image, tile), and k6_raster_bwd_fx runs only the CTAs of flagged tiles, skipping the chunks taken here.
+// (image, tile) in Tables::vg_list, and k6_raster_bwd_fx runs only the listed tiles, skipping the chunks taken here.
 #include <cstdio>
 
 #include "internal.cuh"
@@ -42,6 +42,7 @@ namespace br {
 #ifndef BR_VG_SPLITS
 #define BR_VG_SPLITS 1     // CTAs per (image, tile) (chunks dealt round-robin)
 #endif
+static_assert(BR_VG_SPLITS == 1, "the leftover list names whole (image, tile)s: one CTA must see all their chunks");
 #ifndef BR_VG_PREFETCH
 #define BR_VG_PREFETCH 0   // 1: L1 prefetch of the won faces' records in the list phase (C4 K6 +1%, C3 -2%)
 #endif
@@ -416,14 +417,15 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
             if (pb + np < total) __syncthreads();   // the next batch reuses plist / imom / contrib
         }
     }
-    if (tid == 0 && S.left) t.vg_left[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = 1;   // cleared before the launch
+    if (tid == 0 && S.left)   // list the (image, tile) for k6_raster_bwd_fx (count cleared before the launch)
+        t.vg_list[atomicAdd(t.vg_count, 1)] = blockIdx.y * t.T + blockIdx.x;
 }
 
 cudaError_t launch_vis_gather(const Tables &t, const float *grad, float *dC, cudaStream_t st)
 {
     dim3 grid(t.T, t.B, BR_VG_SPLITS);
     const int smem = (int)sizeof(VgSmem);
-    cudaError_t e0 = cudaMemsetAsync(t.vg_left, 0, (size_t)t.T * t.B, st);
+    cudaError_t e0 = cudaMemsetAsync(t.vg_count, 0, sizeof(int), st);
     if (e0 != cudaSuccess) return e0;
     cudaError_t e = cudaFuncSetAttribute(k6v_raster_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;

@@ -100,7 +100,7 @@ __device__ __forceinline__ bool rect_reaches(const float A[3], const float B[3],
 // Evaluate a record at tau for this tile -> TauRec + the mask of warp footprints it can reach
 // (bit w = culling footprint w, see FPW; 0 = the face cannot cover any pixel of the tile at tau).
 // D = det F(tau) (|D| > EPS_D) and the face's pixel box in the tile come from the caller's rejects.
-template <bool GRID>
+template <bool GRID, bool BOXONLY = false>
 __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, float D, int x0, int x1, int y0, int y1,
                                               const TileCtx &tc, TauRec &out)
 {
@@ -131,7 +131,10 @@ __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, floa
     // column term A_i u per footprint column of the box, a row term G_i + B_i v + tol_i per row, and the
     // footprint is reached iff every edge has column + row term >= 0
     uint32_t fm = 0u;
-    if (!GRID) {   // per footprint (K6's copy: keeps that kernel's register allocation)
+    if (BOXONLY) {   // the footprints the box reaches (a superset: more footprint tests, a cheaper stage)
+        for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
+            for (int wx = x0 >> FPW_SH; wx <= (x1 >> FPW_SH); ++wx) fm |= 1u << (wy * (TW / FPW) + wx);
+    } else if (!GRID) {   // per footprint (K6's copy: keeps that kernel's register allocation)
         for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
             for (int wx = x0 >> FPW_SH; wx <= (x1 >> FPW_SH); ++wx) {
                 const int rx0 = max(x0, wx * FPW), rx1 = min(x1, wx * FPW + FPW - 1);
@@ -581,6 +584,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
 #ifndef BR_K4L_SENT
 #define BR_K4L_SENT 0   // 1: the chunk's bin entries staged in shared memory (measured: no change)
 #endif
+#ifndef BR_K4L_BACKBOX
+#define BR_K4L_BACKBOX 0   // 1: faces turned away from the camera get footprints from the box only (C4 K4 6.14 -> 6.38 ms)
+#endif
 #ifndef BR_K4L_UNROLL
 #define BR_K4L_UNROLL 0
 #endif
@@ -654,9 +660,11 @@ __device__ __forceinline__ void pair_stage(const float4 *r, int j, int l, int n,
 {
     FaceRec fr;
     load_rec(r, fr);
-    const uint32_t fm = stage_tau<true>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * n + j]);
-    const uint16_t off = (uint16_t)((l * n + j) * (int)sizeof(TauRec));
     const bool back = BR_K4L_CULL && D * sF < 0.f;   // turned away from the camera (sF: mesh orientation)
+    // the faces turned away are mostly skipped with their whole list: their footprints from the box alone
+    const uint32_t fm = (BR_K4L_BACKBOX && back) ? stage_tau<true, true>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * n + j])
+                                                 : stage_tau<true>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * n + j]);
+    const uint16_t off = (uint16_t)((l * n + j) * (int)sizeof(TauRec));
     if (!back) {
         for (uint32_t m = fm; m; m &= m - 1) {
             const int w = __ffs(m) - 1;
@@ -1948,14 +1956,32 @@ __device__ __forceinline__ int take_moments(int *m, float inv, float sx, float s
 }
 
 template <int MODE>
+__device__ __forceinline__ void k6_fx_tile(const Tables &t, const float *__restrict__ grad, float *__restrict__ dC,
+                                           int b, int tile, int z, BwdFxSmem<MODE> &S);
+
+template <int MODE>
 __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd_fx(Tables t, const float *__restrict__ grad,
                                                                   float *__restrict__ dC)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BwdFxSmem<MODE> &S = *reinterpret_cast<BwdFxSmem<MODE> *>(smem_raw);
-    if (t.vis_gathered && !t.vg_left[(size_t)blockIdx.y * gridDim.x + blockIdx.x])
-        return;   // every chunk of this CTA was taken by k6v_raster_bwd (k_gather.cu)
-    const int b = blockIdx.y, tile = blockIdx.x;
+    if (!t.vis_gathered) {   // grid: tiles x images x splits
+        k6_fx_tile<MODE>(t, grad, dC, blockIdx.y, blockIdx.x, blockIdx.z, S);
+        return;
+    }
+    // after k6v_raster_bwd (k_gather.cu): only the (image, tile)s it listed as having chunks left, grid-stride
+    const int nl = *t.vg_count;
+    for (int i = blockIdx.x; i < nl; i += gridDim.x) {
+        const int item = t.vg_list[i];
+        __syncthreads();   // the previous item's shared memory is no longer read
+        k6_fx_tile<MODE>(t, grad, dC, item / t.T, item % t.T, blockIdx.z, S);
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void k6_fx_tile(const Tables &t, const float *__restrict__ grad, float *__restrict__ dC,
+                                           int b, int tile, int z, BwdFxSmem<MODE> &S)
+{
     const ImgInfo &im = t.imgs[b];
     const int N = im.N, c_begin = im.chunk_begin, c_end = im.chunk_end, sched_off = im.sched_off;
     const long long rec_off = im.rec_off;
@@ -1995,7 +2021,7 @@ __global__ void __launch_bounds__(NT, BR_K6_MINB) k6_raster_bwd_fx(Tables t, con
     unsigned int stamp = 0;   // group counter of the cached path (won flags)
     __syncthreads();
 
-    for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
+    for (int c = c_begin + z; c < c_end; c += t.splits) {
         const Chunk ch = t.chunks[c];
         const size_t bi = (size_t)c * t.T + tile;
         const long long o = t.off[bi];
@@ -2202,6 +2228,8 @@ static cudaError_t launch_bwd_t(const Tables &t, const float *grad, float *dC, c
         const int smem = (int)sizeof(BwdFxSmem<MODE>);
         cudaError_t e = cudaFuncSetAttribute(k6_raster_bwd_fx<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
+        if (t.vis_gathered)   // grid-stride over the listed (image, tile)s
+            grid = dim3((unsigned)std::min<long long>((long long)t.T * t.B, 148LL * BR_K6_MINB), 1, t.splits);
         k6_raster_bwd_fx<MODE><<<grid, NT, smem, st>>>(t, grad, dC);
         return cudaGetLastError();
     }
