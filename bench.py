@@ -393,7 +393,10 @@ def main():
     bw_flop = (FLOP_BWD * cov + FLOP_SETUP * n_fsub) if (rend is not None and rend.cache_flags) else \
         fw_flop + FLOP_BWD * cov
     f_avg, b_avg = float(np.mean(fwd_ms)), float(np.mean(bwd_ms))
-    kernels = [("k4_raster_fwd", fw_flop, f_avg), ("k6_raster_bwd", bw_flop, b_avg)]
+    # the timed kernels: K4 = k4l_raster_fwd (lean forward); K6 = k6v_raster_bwd (visibility gather) with the
+    # cache, k6_raster_bwd_fx (recomputed visibility) without
+    cached = rend is not None and bool(rend.cache_flags)
+    kernels = [("k4l_raster_fwd", fw_flop, f_avg), ("k6v_raster_bwd" if cached else "k6_raster_bwd_fx", bw_flop, b_avg)]
     if soft:
         kernels += [("k8_soft_fwd", FLOP_SOFT_FWD * soft_terms, float(np.mean(sf_ms))),
                     ("k9_soft_bwd", (FLOP_SOFT_BWD_CACHED if (rend is not None and rend.cache_flags) else FLOP_SOFT_BWD) * soft_terms,

@@ -596,9 +596,8 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
 #define BR_UNROLL4
 #endif
 #ifndef BR_K4L_CULL
-#define BR_K4L_CULL 2   // faces turned away from the camera in a second list per footprint, tested last; 2: the whole
-                        // list skipped when every pixel's winner is nearer than the list's lowest depth; 1: each face
-                        // skipped behind the winners (per-face test; measured slower)
+#define BR_K4L_CULL 2   // 2: faces turned away from the camera in a second list per footprint, tested last, the whole
+                        // list skipped when every pixel's winner is nearer than the list's lowest depth; 0: one list
 #endif                  //    (measured slower in this kernel: C4 K4 6.86 -> 7.17 ms)
 
 struct __align__(16) LeanSmem {
@@ -621,7 +620,6 @@ struct __align__(16) LeanSmem {
     float taus[GMAX_F];
     int wsum[NWARP];
     float2 uv[NT];                              // the thread's pixel (ul, vl), reloaded per sub-frame
-    float4 fpc[NWARP];                          // the warp footprint's corner pixel centres (ul0, ul1, vl0, vl1)
     float4 acc[TW * TH];                        // per-pixel (r, g, b, a) sums over the sub-frames
 };
 static_assert(SREC_F * 64 <= 65535, "list entries are 16-bit byte offsets");
@@ -789,9 +787,6 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
     unsigned long long dz = 0;
     const double orient = *t.orient;
     const float sF = orient > 0.0 ? 1.f : orient < 0.0 ? -1.f : 0.f;
-    if (lane == 0)   // the warp footprint's corner pixel centres (the lanes' own ul, vl values)
-        S.fpc[warp] = make_float4((float)((warp & 1) * 8 - TW / 2) * tc.sx, (float)((warp & 1) * 8 + 7 - TW / 2) * tc.sx,
-                                  (float)(TH / 2 - (warp >> 1) * 4 - 3) * tc.sy, (float)(TH / 2 - (warp >> 1) * 4) * tc.sy);
 
     for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
         const Chunk ch = t.chunks[c];
@@ -853,6 +848,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                     const float ul = uvp.x, vl = uvp.y;
                     float zbest = __int_as_float(0x7f800000), tief = 0.f;
                     int eoff = -1;
+                    // coverage loop: begin (tools/update_traffic.py)
                     BR_UNROLL4 for (int i = 0; i < cn; ++i) {   // faces turned towards the camera
                         const int off = lst[i];
                         const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
@@ -886,36 +882,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                             }
                         }
                     }
-                    if (BR_K4L_CULL == 1 && cb) {   // the others: skipped where they are behind every pixel's winner
-                        float zmax = zbest;
-#pragma unroll
-                        for (int d = 16; d > 0; d >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, d));
-                        // zmax = +inf unless every pixel of the footprint has a winner.  The depth plane
-                        // fma(az, ul, fma(bz, vl, cz)) is monotone in ul and vl, so its minimum over the footprint's
-                        // pixel centres is its value at one corner: above zmax, the face cannot win or tie anywhere.
-#ifdef BR_K4L_STATS
-                        if (lane == 0) { atomicAdd(t.status + 40, cn); atomicAdd(t.status + 41, cb); atomicAdd(t.status + 43, zmax < __int_as_float(0x7f800000) ? 1 : 0); atomicAdd(t.status + 44, 1); }
-#endif
-                        const float4 fc = S.fpc[warp];
-                        BR_UNROLL4 for (int i = n - cb; i < n; ++i) {
-                            const int off = lst[i];
-                            const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
-                            const float4 q2 = rp[2];
-                            const float zmin = __fmaf_rn(q2.y, q2.y > 0.f ? fc.x : fc.y, __fmaf_rn(q2.z, q2.z > 0.f ? fc.z : fc.w, q2.w));
-#ifdef BR_K4L_STATS
-                            if (lane == 0 && zmin > zmax) atomicAdd(t.status + 42, 1);
-#endif
-                            if (zmin > zmax) continue;
-                            const float4 q0 = rp[0], q1 = rp[1];
-                            const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
-                            const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
-                            const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
-                            const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
-                            const float emin = fminf(fminf(e0, e1), e2);
-                            tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
-                            if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
-                        }
-                    }
+                    // coverage loop: end
                     if (__any_sync(0xffffffffu, tief != 0.f)) {   // exact depth tie in the warp: face indices decide (Q7)
                         zbest = __int_as_float(0x7f800000);
                         eoff = -1;

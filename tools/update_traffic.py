@@ -5,8 +5,8 @@ the warp efficiency (active lanes per executed warp instruction / 32) of the who
 coverage-test loop (the source lines of vis_mask_fast / vis_mask in k_raster.cu) -> roofline.warp_efficiency.
 
 usage: python tools/update_traffic.py REPORT.ncu-rep CONFIG [kernel_regex=name ...]
-e.g.   python tools/update_traffic.py gpurun_out/prof_c4.ncu-rep C4 'k4_raster_fwd<0, 0>=k4_raster_fwd' \
-           'k6_raster_bwd<0>=k6_raster_bwd'
+e.g.   python tools/update_traffic.py gpurun_out/prof_c4.ncu-rep C4 'k4l_raster_fwd<0>=k4l_raster_fwd' \
+           'k6v_raster_bwd=k6v_raster_bwd'
 """
 import csv
 import io
@@ -42,13 +42,19 @@ def raw_rows(rep):
 
 
 def coverage_loop_efficiency(rep, func_sub):
-    """threads / warp instruction over the source lines of the coverage loops (k_raster.cu)."""
+    """threads / warp instruction over the source lines of the coverage loops (k_raster.cu): k4l_raster_fwd's
+    lines between its `coverage loop: begin` / `end` markers, else vis_mask_fast / vis_mask."""
     src = open(os.path.join(ROOT, "paper_2602_07860_b200", "csrc", "k_raster.cu")).read().split("\n")
     lines = set()
-    for name in ("vis_mask_fast", "vis_mask"):
-        start = next(i for i, l in enumerate(src) if re.match(r"__device__ __forceinline__ (bool|void) %s\(" % name, l))
-        end = next(i for i in range(start + 1, len(src)) if src[i].startswith("}"))
-        lines.update(range(start + 1, end + 2))
+    if func_sub.startswith("k4l"):
+        b = next(i for i, l in enumerate(src) if "coverage loop: begin" in l)
+        e = next(i for i in range(b, len(src)) if "coverage loop: end" in src[i])
+        lines.update(range(b + 1, e + 2))
+    else:
+        for name in ("vis_mask_fast", "vis_mask"):
+            start = next(i for i, l in enumerate(src) if re.match(r"__device__ __forceinline__ (bool|void) %s\(" % name, l))
+            end = next(i for i in range(start + 1, len(src)) if src[i].startswith("}"))
+            lines.update(range(start + 1, end + 2))
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     fname = func = None
