@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
             if (pb + np < total) __syncthreads();   // the next batch reuses plist / imom / contrib
         }
     }
-    if (tid == 0 && S.left)   // list the (image, tile) for k6_raster_bwd_fx (count cleared before the launch)
+    if (tid == 0 && S.left)   // list the (image, tile) for k6_raster_bwd_fx (count zeroed by K1 and by K7 of the previous backward)
         t.vg_list[atomicAdd(t.vg_count, 1)] = blockIdx.y * t.T + blockIdx.x;
 }
 
@@ -425,8 +425,7 @@ cudaError_t launch_vis_gather(const Tables &t, const float *grad, float *dC, cud
 {
     dim3 grid(t.T, t.B, BR_VG_SPLITS);
     const int smem = (int)sizeof(VgSmem);
-    cudaError_t e0 = cudaMemsetAsync(t.vg_count, 0, sizeof(int), st);
-    if (e0 != cudaSuccess) return e0;
+
     cudaError_t e = cudaFuncSetAttribute(k6v_raster_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     k6v_raster_bwd<<<grid, NT, smem, st>>>(t, grad, dC);

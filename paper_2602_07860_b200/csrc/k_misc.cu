@@ -18,6 +18,7 @@ __global__ void __launch_bounds__(256) k7_vertex_chain(Tables t, float *__restri
     __shared__ double part[8][3][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int v = blockIdx.x * 32 + lane;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && t.vg_count) *t.vg_count = 0;   // the gather's list, for the next backward
     double acc[3] = {0.0, 0.0, 0.0};
     if (v < t.V) {
         int q = 0;   // running index of the (image, keyframe) term

@@ -24,7 +24,10 @@ __global__ void __launch_bounds__(256) k1_keyframes(Tables t, const float *__res
     const int V = t.V;
     const int nk = (im.S + 1) * V;
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx == 0 && b == 0) *t.orient = 0.0;   // k_orient accumulates after this kernel
+    if (idx == 0 && b == 0) {
+        *t.orient = 0.0;                  // K2 accumulates the mesh orientation after this kernel
+        if (t.vg_count) *t.vg_count = 0;  // the visibility gather's leftover list (k_gather.cu) starts empty
+    }
     if (idx >= nk) return;
     const int s = idx / V, v = idx - s * V;
     const PoseRec &pr = t.poses[im.pose_off + s];
@@ -140,7 +143,7 @@ __device__ __forceinline__ void face_setup(const Tables &t, const ImgInfo &im, i
 // K2: thread per (segment, face) of image blockIdx.y; each warp stages its 32 consecutive records in
 // shared memory and stores them as one contiguous run (coalesced, instead of 176-B strided stores)
 __global__ void __launch_bounds__(256) k2_face_setup(Tables t, const int *__restrict__ faces,
-                                                     const float *__restrict__ colors)
+                                                     const float *__restrict__ colors, const float *__restrict__ verts)
 {
     __shared__ float4 st[8][32 * REC_F4];
     const int b = blockIdx.y;
@@ -149,6 +152,25 @@ __global__ void __launch_bounds__(256) k2_face_setup(Tables t, const int *__rest
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int base = blockIdx.x * blockDim.x + warp * 32, idx = base + lane;
     if (base >= n) return;   // warp-uniform
+    if (b == 0 && base < F) {
+        // mesh orientation for the forward's visiting order (k4l_raster_fwd: faces turned towards the camera
+        // first, so that the others can be skipped per warp footprint once every pixel there has a nearer
+        // winner): sum over faces of det(P0[v0], P0[v1], P0[v2]) = 6 x the signed volume.  Only its sign is
+        // used, and only for speed: the raster's result does not depend on it.
+        double d = 0.0;
+        if (idx < F) {
+            const int a = faces[3 * idx], c1 = faces[3 * idx + 1], c2 = faces[3 * idx + 2];
+            if ((unsigned)a < (unsigned)t.V && (unsigned)c1 < (unsigned)t.V && (unsigned)c2 < (unsigned)t.V) {
+                const double ax = verts[3 * a], ay = verts[3 * a + 1], az = verts[3 * a + 2];
+                const double bx = verts[3 * c1], by = verts[3 * c1 + 1], bz = verts[3 * c1 + 2];
+                const double cx = verts[3 * c2], cy = verts[3 * c2 + 1], cz = verts[3 * c2 + 2];
+                d = ax * (by * cz - bz * cy) + ay * (bz * cx - bx * cz) + az * (bx * cy - by * cx);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        if (lane == 0 && d != 0.0) atomicAdd(t.orient, d);
+    }
     float4 r[REC_F4];
 #pragma unroll
     for (int q = 0; q < REC_F4; ++q) r[q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -164,25 +186,6 @@ __global__ void __launch_bounds__(256) k2_face_setup(Tables t, const int *__rest
     for (int k = lane; k < cnt; k += 32) out[k] = st[warp][k];
 }
 
-// Mesh orientation for the forward's visiting order (k4l_raster_fwd: faces turned towards the camera
-// first, so that the others can be skipped per warp footprint once every pixel there has a nearer winner).
-// Only the sign is used, and only for speed: the result of the raster does not depend on it.
-__global__ void __launch_bounds__(256) k_orient(Tables t, const float *__restrict__ verts, const int *__restrict__ faces)
-{
-    double acc = 0.0;
-    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < t.F; f += gridDim.x * blockDim.x) {
-        const int a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
-        if ((unsigned)a >= (unsigned)t.V || (unsigned)b >= (unsigned)t.V || (unsigned)c >= (unsigned)t.V) continue;
-        const double ax = verts[3 * a], ay = verts[3 * a + 1], az = verts[3 * a + 2];
-        const double bx = verts[3 * b], by = verts[3 * b + 1], bz = verts[3 * b + 2];
-        const double cx = verts[3 * c], cy = verts[3 * c + 1], cz = verts[3 * c + 2];
-        acc += ax * (by * cz - bz * cy) + ay * (bz * cx - bx * cz) + az * (bx * cy - by * cx);
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
-    if ((threadIdx.x & 31) == 0 && acc != 0.0) atomicAdd(t.orient, acc);
-}
-
 cudaError_t launch_setup(const Tables &t, const float *verts, const int *faces, const float *colors,
                          int maxS, cudaStream_t st)
 {
@@ -195,8 +198,7 @@ cudaError_t launch_setup(const Tables &t, const float *verts, const int *faces, 
     if (t.F > 0) {
         long long nf = (long long)maxS * t.F;
         dim3 grid((unsigned)((nf + 255) / 256), (unsigned)t.B);
-        k2_face_setup<<<grid, 256, 0, st>>>(t, faces, colors);
-        k_orient<<<(unsigned)std::min<long long>((t.F + 255) / 256, 148), 256, 0, st>>>(t, verts, faces);
+        k2_face_setup<<<grid, 256, 0, st>>>(t, faces, colors, verts);
     }
     return cudaGetLastError();
 }
