@@ -303,8 +303,8 @@ def main():
     stream = torch.cuda.current_stream()
 
     # census (outside timing): algorithmic unit counts of this rank's forward
-    census = torch.zeros(8, dtype=torch.int64, device=dev)
-    units = np.zeros(8)
+    census = torch.zeros(12, dtype=torch.int64, device=dev)
+    units = np.zeros(12)
     if rend is not None:
         step.census(verts, colors, census)
         units = census.cpu().numpy().astype(np.float64)
@@ -387,7 +387,11 @@ def main():
     value = sc.B / (ms_per_step / 1000.0)
 
     # roofline of the dominant kernel (raster fwd K4 or raster bwd K6), this rank's launches
-    nec, cov, cand, staged, soft_terms, soft_staged, soft_items, soft_iters = units
+    nec, cov, cand_all, staged_all, soft_terms, soft_staged, soft_items, soft_iters = units[:8]
+    # the timed forward's own counts (census [8..11], same order as [0..3]): it skips the lists of faces turned
+    # away from the camera where every pixel already has a nearer winner, so it executes fewer tests than every
+    # bin face at its footprints (cand_all); round 1's kernel (no skip) leaves them 0 -> the full counts
+    cand, cov_exec, staged = (units[10], units[8], units[11]) if units[10] > 0 else (cand_all, nec, staged_all)
     fw_flop = FLOP_PAIR * nec + FLOP_SHADE * cov + FLOP_SETUP * n_fsub
     # K6 with the visibility buffer (BlurRenderer default) does not recompute the forward's tests
     bw_flop = (FLOP_BWD * cov + FLOP_SETUP * n_fsub) if (rend is not None and rend.cache_flags) else \
@@ -431,7 +435,7 @@ def main():
     # them whose test covers its pixel is the useful-lane efficiency (census, this run)
     weff = {"kernel": wp.get("kernel"), "coverage_loop_active_lanes":
             None if wp.get("coverage_loop") is None else min(1.0, wp["coverage_loop"]),
-            "coverage_loop_useful_lanes": (nec / cand) if cand else None,
+            "coverage_loop_useful_lanes": (cov_exec / cand) if cand else None,
             "source": "ncu --set full (profiles/traffic.json) for the active lanes; census covered / executed "
                       "tests for the useful ones"}
     roofline = {"bound": "alu", "kernel": kname, "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
@@ -444,7 +448,8 @@ def main():
                                "SM count and clocks.max.sm)",
                 "fwd_raster_ms": f_avg, "bwd_raster_ms": b_avg,
                 **({"soft_fwd_ms": float(np.mean(sf_ms)), "soft_bwd_ms": float(np.mean(sb_ms))} if soft else {}),
-                "executed_pair_tests_per_launch": cand, "necessary_pairs_per_launch": nec,
+                "executed_pair_tests_per_launch": cand, "all_faces_pair_tests_per_launch": cand_all,
+                "covered_among_executed_per_launch": cov_exec, "necessary_pairs_per_launch": nec,
                 "covered_pixel_subframes_per_launch": cov, "staged_records_per_launch": staged,
                 # every timed kernel: algorithmic TFLOP/s (same per-unit figures) and fraction of the peak
                 "kernels_frac": {k[0]: (k[1] / (k[2] / 1000.0) / 1e12 / FP32_PEAK_TFLOPS if k[2] > 0 else 0.0)

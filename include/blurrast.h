@@ -121,11 +121,15 @@ typedef struct {
     int32_t flags;                 /* BLUR_REUSE_SETUP */
     float bin_factor;              /* bin-entry capacity per (chunk, face) (0 = default 3.0); see
                                       blur_read_bins for sizing it to the geometry */
-    unsigned long long *census;    /* device u64[8] or NULL: fwd adds [covered (pixel,face,subframe)
+    unsigned long long *census;    /* device u64[12] or NULL: fwd adds [covered (pixel,face,subframe)
                                       pairs, covered (pixel,subframe), candidate pair tests,
-                                      staged (face,subframe,tile) records, soft (pixel,face,subframe)
-                                      terms evaluated, staged soft records, soft work items (sub-frame,
-                                      8x4 footprint), soft face iterations of those items] */
+                                      staged (face,subframe,tile) records (these four: every bin face
+                                      tested at its footprints, the algorithmic counts), soft
+                                      (pixel,face,subframe) terms evaluated, staged soft records, soft
+                                      work items (sub-frame, 8x4 footprint), soft face iterations of
+                                      those items, then the same first four counts for the timed
+                                      fast-solver forward, which skips faces hidden behind nearer
+                                      winners] (a census call renders the batch twice) */
     void *raster_events[2];        /* host cudaEvent_t pair or NULLs: recorded on `stream` right
                                       before / after the raster kernel (K4 in fwd, K6 in bwd), for
                                       timing the dominant kernel inside a step */

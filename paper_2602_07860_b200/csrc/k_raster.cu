@@ -654,7 +654,8 @@ __device__ __forceinline__ bool pair_head(const BinCtx &bc, const int *ent, int 
 
 __device__ __forceinline__ void pair_stage(const float4 *r, int j, int l, int n, float tau, float D, int x0, int x1,
                                            int y0, int y1, const TileCtx &tc, TauRec *rec, uint16_t (*list)[SREC_F],
-                                           int (*cnt)[NFP], int (*cntb)[NFP], float sF, int (*minz)[NFP])
+                                           int (*cnt)[NFP], int (*cntb)[NFP], float sF, int (*minz)[NFP],
+                                           unsigned long long *nstage = nullptr)
 {
     FaceRec fr;
     load_rec(r, fr);
@@ -663,6 +664,7 @@ __device__ __forceinline__ void pair_stage(const float4 *r, int j, int l, int n,
     const uint32_t fm = (BR_K4L_BACKBOX && back) ? stage_tau<true, true>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * n + j])
                                                  : stage_tau<true>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * n + j]);
     const uint16_t off = (uint16_t)((l * n + j) * (int)sizeof(TauRec));
+    if (nstage) *nstage += fm != 0u;
     if (!back) {
         for (uint32_t m = fm; m; m &= m - 1) {
             const int w = __ffs(m) - 1;
@@ -694,7 +696,7 @@ __device__ __forceinline__ void pair_stage(const float4 *r, int j, int l, int n,
 __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *ent, int n, const float *taus, int ng,
                                                  const TileCtx &tc, int W, int H, int F, TauRec *rec,
                                                  uint16_t (*list)[SREC_F], int (*cnt)[NFP], int (*cntb)[NFP], float sF,
-                                                 int (*minz)[NFP])
+                                                 int (*minz)[NFP], unsigned long long *nstage = nullptr)
 {
     const int npair = n * ng;
     const float inv_ng = 1.0f / (float)ng;
@@ -715,7 +717,7 @@ __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *en
         const float4 *r;
         float D;
         if (pair_head(bc, ent, p, inv_ng, ng, taus, tc, W, H, F, j, l, r, D, x0, x1, y0, y1))
-            pair_stage(r, j, l, n, taus[l], D, x0, x1, y0, y1, tc, rec, list, cnt, cntb, sF, minz);
+            pair_stage(r, j, l, n, taus[l], D, x0, x1, y0, y1, tc, rec, list, cnt, cntb, sF, minz, nstage);
     }
 #endif
 }
@@ -757,9 +759,9 @@ __device__ __forceinline__ void stage_group_2pass(const BinCtx &bc, const int *e
     }
 }
 
-template <bool COV>
+template <bool COV, bool CENSUS = false>
 __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float *__restrict__ out, int *__restrict__ ids,
-                                                                int ids_k)
+                                                                int ids_k, unsigned long long *census = nullptr)
 {
     static_assert(!BR_HALF, "the lean forward uses the warps' 8x4 footprints");
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -784,7 +786,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
         (&S.u.g.cnt[0][0])[i] = 0; (&S.u.g.cntb[0][0])[i] = 0; (&S.u.g.minz[0][0])[i] = 0x7f800000;
     }
     if (threadIdx.x == 0) S.u.g.nacc = 0;
-    unsigned long long dz = 0;
+    unsigned long long dz = 0, c_cov = 0, c_test = 0, c_shade = 0, c_stage = 0;   // census (CENSUS builds)
     const double orient = *t.orient;
     const float sF = orient > 0.0 ? 1.f : orient < 0.0 ? -1.f : 0.f;
 
@@ -830,7 +832,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                                   S.u.g.minz, S.u.g.acc_pairs, &S.u.g.nacc);
 #elif !defined(BR_EXP_NOSTAGE)
                 stage_group_list(bc, ents, n, S.taus, ng, tc, t.W, t.H, t.F, S.rec, S.u.g.list, S.u.g.cnt, S.u.g.cntb, sF,
-                                 S.u.g.minz);
+                                 S.u.g.minz, CENSUS ? &c_stage : nullptr);
 #endif
                 __syncthreads();
                 uint16_t *vrow = vis_out ? vis_out + ((size_t)(im.cov_off + kg) * t.T + tile) * (TW * TH) + myp : nullptr;
@@ -858,6 +860,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                         const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
                         const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
                         const float emin = fminf(fminf(e0, e1), e2);
+                        if (CENSUS && inimg) { c_test++; c_cov += emin >= 0.f; }
                         tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
                         if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
                     }
@@ -877,6 +880,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                                 const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
                                 const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
                                 const float emin = fminf(fminf(e0, e1), e2);
+                                if (CENSUS && inimg) { c_test++; c_cov += emin >= 0.f; }
                                 tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
                                 if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
                             }
@@ -910,6 +914,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                         a.x += pr; a.y += pg; a.z += pb; a.w += 1.f;
                         S.acc[myp] = a;
                         fid = rl[ebest].fid;
+                        if (CENSUS && inimg) c_shade++;
                     }
                     if (l == l_ids) ids[pix] = fid;
                     if (vrow) {   // visibility cache for K6
@@ -945,9 +950,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                     const int nw = (nb + 31) >> 5;
                     clear_words(S.u.b.wm, NFP * nw);
                     __syncthreads();
-                    stage_group<false, 0, true>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.u.b.sid, S.rec, nullptr, S.u.b.wm, dz);
+                    stage_group<CENSUS, 0, true>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.u.b.sid, S.rec, nullptr, S.u.b.wm, c_stage);
                     __syncthreads();
-                    vis_mask<false, 0>(S.rec, nullptr, S.u.b.wm + warp * nw, nw, base, ul, vl, zbest, ebest, fbest, dz, dz, false);
+                    vis_mask<CENSUS, 0>(S.rec, nullptr, S.u.b.wm + warp * nw, nw, base, ul, vl, zbest, ebest, fbest, c_cov, c_test, inimg);
                     if (ebest >= base) {   // winner changed in this batch: shade now (Eq.9)
                         shade(S.rec[ebest - base], t.fcol, ul, vl, pr, pg, pb);
                         has = true;
@@ -957,6 +962,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                     base += nb;
                     __syncthreads();
                 }
+                if (CENSUS && has && inimg) c_shade++;
                 if (has) {
                     float4 a = S.acc[myp];
                     a.x += pr; a.y += pg; a.z += pb; a.w += 1.f;
@@ -982,16 +988,23 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
         if (t.splits == 1) reinterpret_cast<float4 *>(out)[pix] = v;
         else t.part[(size_t)blockIdx.z * ((size_t)t.B * t.H * t.W) + pix] = v;
     }
+    if (CENSUS) {
+        atomicAdd(census + 0, c_cov);
+        atomicAdd(census + 1, c_shade);
+        atomicAdd(census + 2, c_test);
+        atomicAdd(census + 3, c_stage);
+    }
 }
 
-template <bool COV>
-static cudaError_t launch_fwd_lean(const Tables &t, float *out, int *ids, int ids_k, cudaStream_t st)
+template <bool COV, bool CENSUS = false>
+static cudaError_t launch_fwd_lean(const Tables &t, float *out, int *ids, int ids_k, cudaStream_t st,
+                                   unsigned long long *census = nullptr)
 {
     dim3 grid(t.T, t.B, t.splits);
     const int smem = (int)sizeof(LeanSmem);
-    cudaError_t e = cudaFuncSetAttribute(k4l_raster_fwd<COV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(k4l_raster_fwd<COV, CENSUS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    k4l_raster_fwd<COV><<<grid, NT, smem, st>>>(t, out, ids, ids_k);
+    k4l_raster_fwd<COV, CENSUS><<<grid, NT, smem, st>>>(t, out, ids, ids_k, census);
     return cudaGetLastError();
 }
 
@@ -2241,7 +2254,12 @@ cudaError_t launch_raster_fwd_legacy(const Tables &t, float *out, int *ids, int 
         if (!lean_fwd_off())
             return t.covbits ? launch_fwd_lean<true>(t, out, ids, ids_k, st) : launch_fwd_lean<false>(t, out, ids, ids_k, st);
         return launch_fwd_t<false, 0>(t, out, ids, ids_k, nullptr, st);
-    case 1: return launch_fwd_t<true, 0>(t, out, ids, ids_k, census, st);
+    case 1: {   // census: the algorithmic counts (every bin face tested), then the timed kernel's own counts
+        cudaError_t e = launch_fwd_t<true, 0>(t, out, ids, ids_k, census, st);
+        if (e != cudaSuccess || lean_fwd_off() || pipe_fwd_on()) return e;
+        return t.covbits ? launch_fwd_lean<true, true>(t, out, ids, ids_k, st, census + 8)
+                         : launch_fwd_lean<false, true>(t, out, ids, ids_k, st, census + 8);
+    }
     case 2: return launch_fwd_t<false, 1>(t, out, ids, ids_k, nullptr, st);
     case 3: return launch_fwd_t<true, 1>(t, out, ids, ids_k, census, st);
     case 4: return launch_fwd_t<false, 2>(t, out, ids, ids_k, nullptr, st);

@@ -11,7 +11,7 @@ dev = torch.device("cuda:0")
 r = BlurRenderer(sc.faces, sc.motion, sc.cams, sc.H, sc.W, sc.V, device=dev)
 v, c = torch.tensor(sc.verts, device=dev), torch.tensor(sc.colors, device=dev)
 r.forward(v, c)
-cen = torch.zeros(8, dtype=torch.int64, device=dev)
+cen = torch.zeros(12, dtype=torch.int64, device=dev)
 r.forward(v, c, census=cen)
 x = cen.cpu().numpy().astype(float)
 T = (sc.H // 16) * (sc.W // 16)
