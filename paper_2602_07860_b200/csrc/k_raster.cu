@@ -575,6 +575,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
 // mask words of long bins, and the per-(warp, sub-frame) bookkeeping is kept in registers.  Long and
 // overflowed bins take k4_raster_fwd's per-sub-frame batch path unchanged.
 
+#ifndef BR_K4L_UNIT
+#define BR_K4L_UNIT 0   // 1: staging units of (face, block of sub-frames), one record load per unit (C4 K4 6.14 -> 8.09 ms)
+#endif
 #ifndef BR_K4L_PAIR2
 #define BR_K4L_PAIR2 0  // 1: two pairs per thread, both pairs' first record words requested together (measured slower)
 #endif
@@ -652,6 +655,11 @@ __device__ __forceinline__ bool pair_head(const BinCtx &bc, const int *ent, int 
                        box_lerp(tau, b0.w, b1.w), W, H, tc, x0, x1, y0, y1);
 }
 
+__device__ __forceinline__ void pair_stage_fr(const FaceRec &fr, int j, int l, int n, float tau, float D, int x0, int x1,
+                                              int y0, int y1, const TileCtx &tc, TauRec *rec, uint16_t (*list)[SREC_F],
+                                              int (*cnt)[NFP], int (*cntb)[NFP], float sF, int (*minz)[NFP],
+                                              unsigned long long *nstage);
+
 __device__ __forceinline__ void pair_stage(const float4 *r, int j, int l, int n, float tau, float D, int x0, int x1,
                                            int y0, int y1, const TileCtx &tc, TauRec *rec, uint16_t (*list)[SREC_F],
                                            int (*cnt)[NFP], int (*cntb)[NFP], float sF, int (*minz)[NFP],
@@ -659,6 +667,14 @@ __device__ __forceinline__ void pair_stage(const float4 *r, int j, int l, int n,
 {
     FaceRec fr;
     load_rec(r, fr);
+    pair_stage_fr(fr, j, l, n, tau, D, x0, x1, y0, y1, tc, rec, list, cnt, cntb, sF, minz, nstage);
+}
+
+__device__ __forceinline__ void pair_stage_fr(const FaceRec &fr, int j, int l, int n, float tau, float D, int x0, int x1,
+                                              int y0, int y1, const TileCtx &tc, TauRec *rec, uint16_t (*list)[SREC_F],
+                                              int (*cnt)[NFP], int (*cntb)[NFP], float sF, int (*minz)[NFP],
+                                              unsigned long long *nstage)
+{
     const bool back = BR_K4L_CULL && D * sF < 0.f;   // turned away from the camera (sF: mesh orientation)
     // the faces turned away are mostly skipped with their whole list: their footprints from the box alone
     const uint32_t fm = (BR_K4L_BACKBOX && back) ? stage_tau<true, true>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * n + j])
@@ -700,7 +716,36 @@ __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *en
 {
     const int npair = n * ng;
     const float inv_ng = 1.0f / (float)ng;
-#if BR_K4L_PAIR2
+#if BR_K4L_UNIT
+    // units of (face j, block of kb consecutive sub-frames), at most one per thread: the face's whole record is
+    // requested at once and evaluated at each sub-frame of the block (one L2 round trip per unit instead of two
+    // per pair)
+    const int kb = (npair + NT - 1) / NT, nb = (ng + kb - 1) / kb, nunit = n * nb;
+    const float inv_nb = 1.0f / (float)nb;
+    for (int u = threadIdx.x; u < nunit; u += NT) {
+        const int j = div_small(u, inv_nb), lb = u - j * nb;
+        const int f = BR_K4L_SENT ? ent[j] : __ldg(ent + j);
+        if ((unsigned)f >= (unsigned)F) {     // never expected: bins hold valid face ids
+            atomicOr(bc.status, BLUR_ST_EINTERNAL);
+            continue;
+        }
+        FaceRec fr;
+        load_rec(bc.rseg + (size_t)f * REC_F4, fr);
+        if (__float_as_int(fr.q[6].w) < 0) continue;          // skipped face (Q8, behind, bad index)
+        const int l1 = min(ng, lb * kb + kb);
+        for (int l = lb * kb; l < l1; ++l) {
+            const float tau = taus[l];
+            const float D = __fmaf_rn(tau, __fmaf_rn(tau, fr.q[6].x, fr.q[6].y), fr.q[6].z);   // a1 t^2 + a2 t + a3
+            if (!(fabsf(D) > EPS_D)) continue;
+            int x0, x1, y0, y1;
+            if (!tile_pixels(box_lerp(tau, fr.q[7].x, fr.q[8].x), box_lerp(tau, fr.q[7].y, fr.q[8].y),
+                             box_lerp(tau, fr.q[7].z, fr.q[8].z), box_lerp(tau, fr.q[7].w, fr.q[8].w), W, H, tc, x0, x1, y0,
+                             y1))
+                continue;
+            pair_stage_fr(fr, j, l, n, tau, D, x0, x1, y0, y1, tc, rec, list, cnt, cntb, sF, minz, nstage);
+        }
+    }
+#elif BR_K4L_PAIR2
     for (int p0 = threadIdx.x; p0 < npair; p0 += 2 * NT) {
         const int p1 = p0 + NT;
         int ja, la, jb = 0, lb = 0, xa0, xa1, ya0, ya1, xb0 = 0, xb1 = 0, yb0 = 0, yb1 = 0;
