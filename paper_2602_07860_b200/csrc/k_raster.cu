@@ -603,6 +603,12 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                         // list skipped when every pixel's winner is nearer than the list's lowest depth; 0: one list
 #endif                  //    (measured slower in this kernel: C4 K4 6.86 -> 7.17 ms)
 
+#ifdef BR_K4L_STATS   // diagnostics build (tools/k4l_stats.py): counters in the workspace's status block
+#define K4L_STAT(t_, i_, v_) atomicAdd(reinterpret_cast<unsigned long long *>((t_).status) + (i_), (unsigned long long)(v_))
+#else
+#define K4L_STAT(t_, i_, v_) ((void)0)
+#endif
+
 struct __align__(16) LeanSmem {
     TauRec rec[SREC_F];
     union {
@@ -761,8 +767,20 @@ __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *en
         int j, l, x0, x1, y0, y1;
         const float4 *r;
         float D;
-        if (pair_head(bc, ent, p, inv_ng, ng, taus, tc, W, H, F, j, l, r, D, x0, x1, y0, y1))
+        if (pair_head(bc, ent, p, inv_ng, ng, taus, tc, W, H, F, j, l, r, D, x0, x1, y0, y1)
+#ifdef BR_EXP_NOBACK
+            && !(D * sF < 0.f)   // timing experiment only: faces turned away are never staged (not exact)
+#endif
+            ) {
+#ifdef BR_K4L_STATS
+            unsigned long long ns = 0;
+            pair_stage(r, j, l, n, taus[l], D, x0, x1, y0, y1, tc, rec, list, cnt, cntb, sF, minz, &ns);
+            atomicAdd(reinterpret_cast<unsigned long long *>(bc.status) + 21, 1ull);
+            if (ns) atomicAdd(reinterpret_cast<unsigned long long *>(bc.status) + (D * sF < 0.f ? 23 : 22), 1ull);
+#else
             pair_stage(r, j, l, n, taus[l], D, x0, x1, y0, y1, tc, rec, list, cnt, cntb, sF, minz, nstage);
+#endif
+        }
     }
 #endif
 }
@@ -880,6 +898,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                                  S.u.g.minz, CENSUS ? &c_stage : nullptr);
 #endif
                 __syncthreads();
+                if (threadIdx.x == 0) { K4L_STAT(t, 20, n * ng); K4L_STAT(t, 29, 1); }
                 uint16_t *vrow = vis_out ? vis_out + ((size_t)(im.cov_off + kg) * t.T + tile) * (TW * TH) + myp : nullptr;
                 const int l_ids = (ids && inimg) ? ids_k - kg : -1;
                 const uint16_t *lst = S.u.g.list[warp];
@@ -895,6 +914,11 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                     const float ul = uvp.x, vl = uvp.y;
                     float zbest = __int_as_float(0x7f800000), tief = 0.f;
                     int eoff = -1;
+#ifdef BR_K4L_STATS
+                    if (lane == 0) {
+                        K4L_STAT(t, 24, 1); K4L_STAT(t, 25, cn + cb > 0); K4L_STAT(t, 26, cn); K4L_STAT(t, 28, cb);
+                    }
+#endif
                     // coverage loop: begin (tools/update_traffic.py)
                     BR_UNROLL4 for (int i = 0; i < cn; ++i) {   // faces turned towards the camera
                         const int off = lst[i];
@@ -916,6 +940,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                         // zmax = +inf unless every pixel of the footprint has a winner; each face of the list has
                         // its depth >= minz at every pixel of the footprint (staging, corner of the plane)
                         if (!(zmax < __int_as_float(S.u.g.minz[l][warp]))) {
+#ifdef BR_K4L_STATS
+                            if (lane == 0) K4L_STAT(t, 27, cb);
+#endif
                             BR_UNROLL4 for (int i = n - cb; i < n; ++i) {
                                 const int off = lst[i];
                                 const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
