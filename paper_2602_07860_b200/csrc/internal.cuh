@@ -166,6 +166,9 @@ cudaError_t launch_raster_fwd_legacy(const Tables &t, float *out, int *ids, int 
                                      unsigned long long *census, cudaStream_t st);
 cudaError_t launch_raster_bwd_legacy(const Tables &t, const float *grad_rgba, float *grad_colors,
                                      cudaStream_t st);
+// K4 in the pixel-major evaluation order (k_pixmajor.cu; BLURRAST_FWD=pixmajor, A/B only)
+bool pixmajor_fwd_on();
+cudaError_t launch_raster_fwd_pixmajor(const Tables &t, float *out, int *ids, int ids_k, cudaStream_t st);
 cudaError_t launch_vis_gather(const Tables &t, const float *grad_rgba, float *grad_colors, cudaStream_t st);
 cudaError_t launch_vertex_chain(const Tables &t, float *grad_verts, cudaStream_t st);
 cudaError_t launch_split_reduce(const Tables &t, float *out, cudaStream_t st);

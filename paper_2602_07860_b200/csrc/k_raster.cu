@@ -2321,6 +2321,7 @@ cudaError_t launch_raster_fwd_legacy(const Tables &t, float *out, int *ids, int 
     if (t.B == 0 || t.T == 0) return cudaSuccess;
     switch (t.solver * 2 + (census ? 1 : 0)) {
     case 0:
+        if (pixmajor_fwd_on()) return launch_raster_fwd_pixmajor(t, out, ids, ids_k, st);
         if (pipe_fwd_on())
             return t.covbits ? launch_fwd_pipe<true>(t, out, ids, ids_k, st) : launch_fwd_pipe<false>(t, out, ids, ids_k, st);
         if (!lean_fwd_off())

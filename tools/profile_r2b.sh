@@ -7,9 +7,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 echo launches=$?
 CMD1="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD1 > gpurun_out/plain1_r2b.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k4l_raster_fwd|k6v_raster_bwd" -s 2 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:"k4l_raster_fwd|k6v_raster_bwd" -s 2 -c 4 \
     -o gpurun_out/prof_r2b_c4 $CMD1 > gpurun_out/ncu_full_r2b.log 2>&1
 echo full=$?
-python tools/update_traffic.py gpurun_out/prof_r2b_c4.ncu-rep C4 'k4l_raster_fwd<0>=k4l_raster_fwd' 'k6v_raster_bwd=k6v_raster_bwd'
+python tools/update_traffic.py gpurun_out/prof_r2b_c4.ncu-rep C4 'k4l_raster_fwd<0, 0>=k4l_raster_fwd' 'k6v_raster_bwd=k6v_raster_bwd'
 python tools/ncu_stalls.py gpurun_out/prof_r2b_c4.ncu-rep k4l_raster k4l 14 > gpurun_out/r2b_stalls.txt 2>&1
 python tools/ncu_stalls.py gpurun_out/prof_r2b_c4.ncu-rep k6v_raster k6v 14 >> gpurun_out/r2b_stalls.txt 2>&1
