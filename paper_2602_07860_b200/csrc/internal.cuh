@@ -21,9 +21,14 @@ constexpr int VIS_MAXN = 256;    // bins of at most this many faces get K4's vis
 // computed once per segment, in edge-vector form about a per-edge origin (DESIGN.md
 // "edge-vector form"), plus the depth keyframes and conservative keyframe bounding boxes.
 // 44 floats = 11 x float4 = 176 B.
-//   [8i+0..8i+7]  numerator of w_i (edge opposite corner i): ox, oy, a0, a1, b0, b1, g1, g2
-//                 N_i(tau; p) = (a0 + a1 tau)(u - ox) + (b0 + b1 tau)(v - oy) + tau (g1 + g2 tau)
-//                 i.e. A1_i = g2, A2_i(p) = a1 (u-ox) + b1 (v-oy) + g1, A3_i(p) = a0 (u-ox) + b0 (v-oy)
+//   [8i+0..8i+7]  numerator of w_i (edge opposite corner i): ox, oy, a0, a1, b0, b1, dax, day
+//                 N_i(tau; p) = (a0 + a1 tau)(u - ax(tau)) + (b0 + b1 tau)(v - ay(tau)),
+//                 a(tau) = (ox + tau dax, oy + tau day) the edge's canonical start vertex at tau (Eq.5-6):
+//                 the Eq.8 polynomial A1 tau^2 + A2(p) tau + A3(p) in factored form, with
+//                 A1_i = -(a1 dax + b1 day), A2_i(p) = a1 (u-ox) + b1 (v-oy) - (a0 dax + b0 day),
+//                 A3_i(p) = a0 (u-ox) + b0 (v-oy).  Evaluated about the moving vertex, the pixel offsets
+//                 stay of the size of the triangle however far it travels in the segment (the expanded
+//                 form cancels terms of the size of the travel: 20x the fp32 error of a limb sliver on C4)
 //   [24..26]      d1, d2, d3: det F(tau) = d3 + tau (d2 + tau d1)  (a1, a2, a3 of Eq.8)
 //   [27]          face id (int bits), -1 = skipped face
 //   [28..31]      bbox at keyframe s (xmin, xmax, ymin, ymax), [32..35] at keyframe s+1 (padded)
@@ -139,6 +144,18 @@ __device__ __forceinline__ void ndc_to_index(float lo, float hi, int n, bool fli
 __device__ __forceinline__ size_t cov_word(const Tables &t, const ImgInfo &im, int k, int tile)
 {
     return ((size_t)(im.cov_off + k) * t.T + tile) * (NT / 32);
+}
+
+// Edge i of a K2 record at tau (qa = record float4 2i, qb = 2i+1): d/du and d/dv of N_i and its value at
+// (uc, vc), N_i = al (uc - ax(tau)) + be (vc - ay(tau)).  Every kernel evaluates records through this one
+// helper, so the two faces of an edge (same canonical data, sign flipped) get exact negations: watertight.
+__device__ __forceinline__ void rec_edge_at(const float4 qa, const float4 qb, float tau, float uc, float vc, float &al,
+                                            float &be, float &gp)
+{
+    al = __fmaf_rn(tau, qa.w, qa.z);
+    be = __fmaf_rn(tau, qb.y, qb.x);
+    const float ax = __fmaf_rn(tau, qb.z, qa.x), ay = __fmaf_rn(tau, qb.w, qa.y);
+    gp = __fmaf_rn(al, __fsub_rn(uc, ax), __fmul_rn(be, __fsub_rn(vc, ay)));
 }
 
 // conservative keyframe box lerped to tau (monotone in tau for fixed endpoints)

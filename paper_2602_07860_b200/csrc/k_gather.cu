@@ -369,12 +369,9 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
                     pr.fid = fj;
 #pragma unroll
                     for (int e = 0; e < 3; ++e) {
-                        const float4 qa = __ldg(rr + 2 * e), qb = __ldg(rr + 2 * e + 1);   // ox oy a0 a1 | b0 b1 g1 g2
-                        const float al = __fmaf_rn(tau, qa.w, qa.z);
-                        const float be = __fmaf_rn(tau, qb.y, qb.x);
-                        const float ga = __fmul_rn(tau, __fmaf_rn(tau, qb.w, qb.z));
-                        const float ddx = __fsub_rn(tc.uc, qa.x), ddy = __fsub_rn(tc.vc, qa.y);
-                        const float gp = __fmaf_rn(al, ddx, __fmaf_rn(be, ddy, ga));
+                        const float4 qa = __ldg(rr + 2 * e), qb = __ldg(rr + 2 * e + 1);   // ox oy a0 a1 | b0 b1 dax day
+                        float al, be, gp;
+                        rec_edge_at(qa, qb, tau, tc.uc, tc.vc, al, be, gp);
                         pr.a[e] = al * sgn;
                         pr.b[e] = be * sgn;
                         pr.g[e] = gp * sgn;

@@ -65,11 +65,12 @@ __device__ __forceinline__ void pm_edge(const float *ef, int i, const TileCtx &t
     const float ox = ef[8 * i], oy = ef[8 * i + 1];
     a0 = ef[8 * i + 2]; a1 = ef[8 * i + 3];
     b0 = ef[8 * i + 4]; b1 = ef[8 * i + 5];
-    const float g1 = ef[8 * i + 6];
-    R = ef[8 * i + 7];
+    const float dax = ef[8 * i + 6], day = ef[8 * i + 7];
     const float dx = __fsub_rn(tc.uc, ox), dy = __fsub_rn(tc.vc, oy);
-    // N_i = (a0 + a1 tau)(ul + dx) + (b0 + b1 tau)(vl + dy) + tau (g1 + R tau)
+    // N_i = (a0 + a1 tau)(ul + dx - tau dax) + (b0 + b1 tau)(vl + dy - tau day), expanded in tau (order (i))
     P = __fmaf_rn(a0, dx, __fmul_rn(b0, dy));
+    const float g1 = -__fmaf_rn(a0, dax, __fmul_rn(b0, day));
+    R = -__fmaf_rn(a1, dax, __fmul_rn(b1, day));
     Q = __fmaf_rn(a1, dx, __fmaf_rn(b1, dy, g1));
 }
 

@@ -36,6 +36,9 @@ namespace br {
 #ifndef BR_HALF
 #define BR_HALF 0
 #endif
+#ifndef BR_K4L_MASKBF
+#define BR_K4L_MASKBF 0   // 1: the staging's footprint mask without data-dependent loops (all 8 footprints, box bits)
+#endif
 // Culling footprints: BR_HALF = 1 -> 4x4 pixel blocks (16 per tile, two per warp: the left and right
 // halves of its 8x4 pixels iterate their own face masks), 0 -> the warps' 8x4 blocks.
 constexpr int FPW_SH = BR_HALF ? 2 : 3, FPW = 1 << FPW_SH;   // footprint width (pixels); height 4
@@ -111,12 +114,8 @@ __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, floa
     const float *ef = reinterpret_cast<const float *>(fr.q);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        const float ox = ef[8 * i], oy = ef[8 * i + 1];
-        const float al = __fmaf_rn(tau, ef[8 * i + 3], ef[8 * i + 2]);
-        const float be = __fmaf_rn(tau, ef[8 * i + 5], ef[8 * i + 4]);
-        const float ga = __fmul_rn(tau, __fmaf_rn(tau, ef[8 * i + 7], ef[8 * i + 6]));
-        const float dx = __fsub_rn(tc.uc, ox), dy = __fsub_rn(tc.vc, oy);
-        const float gp = __fmaf_rn(al, dx, __fmaf_rn(be, dy, ga));
+        float al, be, gp;
+        rec_edge_at(fr.q[2 * i], fr.q[2 * i + 1], tau, tc.uc, tc.vc, al, be, gp);
         A[i] = al * sg;
         B[i] = be * sg;
         G[i] = gp * sg;
@@ -141,6 +140,33 @@ __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, floa
                 const int ry0 = max(y0, wy * 4), ry1 = min(y1, wy * 4 + 3);
                 if (rect_reaches_t(A, B, G, tol, rx0, rx1, ry0, ry1, tc)) fm |= 1u << (wy * (TW / FPW) + wx);
             }
+    } else if (BR_K4L_MASKBF && !BR_HALF) {
+        // branch-free: all 2 x 4 footprints of the tile, each rect clipped to the box (empty rows / columns
+        // give a rect outside the box and are masked off by the box bits); the same max-corner test
+    const int wx0 = x0 >> 3, wx1 = x1 >> 3, wy0 = y0 >> 2, wy1 = y1 >> 2;
+    float cu0[3], cu1[3];
+    {
+        const float ul00 = (float)(max(x0, 0) - TW / 2) * tc.sx, ul01 = (float)(min(x1, 7) - TW / 2) * tc.sx;
+        const float ul10 = (float)(max(x0, 8) - TW / 2) * tc.sx, ul11 = (float)(min(x1, 15) - TW / 2) * tc.sx;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            cu0[i] = A[i] * (A[i] > 0.f ? ul01 : ul00);
+            cu1[i] = A[i] * (A[i] > 0.f ? ul11 : ul10);
+        }
+    }
+    const uint32_t colm = (wx0 == 0 ? 1u : 0u) | (wx1 == 1 ? 2u : 0u);
+#pragma unroll
+    for (int wy = 0; wy < 4; ++wy) {
+        const float vlmin = (float)(TH / 2 - min(y1, wy * 4 + 3)) * tc.sy;
+        const float vlmax = (float)(TH / 2 - max(y0, wy * 4)) * tc.sy;
+        float rv[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) rv[i] = G[i] + B[i] * (B[i] > 0.f ? vlmax : vlmin) + tol[i];
+        const bool c0 = rv[0] + cu0[0] >= 0.f && rv[1] + cu0[1] >= 0.f && rv[2] + cu0[2] >= 0.f;
+        const bool c1 = rv[0] + cu1[0] >= 0.f && rv[1] + cu1[1] >= 0.f && rv[2] + cu1[2] >= 0.f;
+        const uint32_t rowm = (wy >= wy0 && wy <= wy1) ? colm : 0u;
+        fm |= (((c0 ? 1u : 0u) | (c1 ? 2u : 0u)) & rowm) << (2 * wy);
+    }
     } else {
     const int wx0 = x0 >> FPW_SH, ncol = (x1 >> FPW_SH) - wx0 + 1;
     float cu[TW / FPW][3];
@@ -721,7 +747,7 @@ __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *en
                                                  int (*minz)[NFP], unsigned long long *nstage = nullptr)
 {
     const int npair = n * ng;
-    const float inv_ng = 1.0f / (float)ng;
+    const float inv_ng = BR_K4L_MASKBF ? __frcp_rn((float)ng) : 1.0f / (float)ng;
 #if BR_K4L_UNIT
     // units of (face j, block of kb consecutive sub-frames), at most one per thread: the face's whole record is
     // requested at once and evaluated at each sub-frame of the block (one L2 round trip per unit instead of two
@@ -1612,12 +1638,8 @@ __device__ __forceinline__ void stage_rec(const FaceRec &fr, float tau, const Ti
     const float *ef = reinterpret_cast<const float *>(fr.q);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        const float ox = ef[8 * i], oy = ef[8 * i + 1];
-        const float al = __fmaf_rn(tau, ef[8 * i + 3], ef[8 * i + 2]);
-        const float be = __fmaf_rn(tau, ef[8 * i + 5], ef[8 * i + 4]);
-        const float ga = __fmul_rn(tau, __fmaf_rn(tau, ef[8 * i + 7], ef[8 * i + 6]));
-        const float dx = __fsub_rn(tc.uc, ox), dy = __fsub_rn(tc.vc, oy);
-        const float gp = __fmaf_rn(al, dx, __fmaf_rn(be, dy, ga));
+        float al, be, gp;
+        rec_edge_at(fr.q[2 * i], fr.q[2 * i + 1], tau, tc.uc, tc.vc, al, be, gp);
         A[i] = al * sg;
         B[i] = be * sg;
         G[i] = gp * sg;

@@ -115,8 +115,8 @@ __device__ __forceinline__ void face_setup(const Tables &t, const ImgInfo &im, i
         e[8 * i + 3] = sg * (float)(-dey);                   // a1
         e[8 * i + 4] = sg * (float)e0x;                      // b0 = d N / d v at tau = 0
         e[8 * i + 5] = sg * (float)dex;                      // b1
-        e[8 * i + 6] = sg * (float)xcross(dax, day, e0x, e0y);   // g1 = cross(da, e0)
-        e[8 * i + 7] = sg * (float)xcross(dax, day, dex, dey);   // g2 = cross(da, de) = A1_i
+        e[8 * i + 6] = (float)dax;                          // motion of the canonical vertex over the segment
+        e[8 * i + 7] = (float)day;                          // (a position: not sign-flipped)
     }
     // det F(tau) = cross(E1(tau), E2(tau)), E1 = v1 - v0, E2 = v2 - v0 (A8)
     const double E1x = X0[1] - X0[0], E1y = Y0[1] - Y0[0], E2x = X0[2] - X0[0], E2y = Y0[2] - Y0[0];

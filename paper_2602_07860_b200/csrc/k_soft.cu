@@ -211,12 +211,9 @@ __device__ __forceinline__ uint32_t soft_stage(const Tables &t, const float4 *__
     float A[3], B[3], G[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {   // Eq.8 numerators at tau, re-centred at the tile centre
-        const float4 e0 = __ldg(r + 2 * i), e1 = __ldg(r + 2 * i + 1);   // ox oy a0 a1 | b0 b1 g1 g2
-        const float al = __fmaf_rn(tau, e0.w, e0.z);
-        const float be = __fmaf_rn(tau, e1.y, e1.x);
-        const float ga = __fmul_rn(tau, __fmaf_rn(tau, e1.w, e1.z));
-        const float dx = __fsub_rn(tc.uc, e0.x), dy = __fsub_rn(tc.vc, e0.y);
-        const float gp = __fmaf_rn(al, dx, __fmaf_rn(be, dy, ga));
+        const float4 e0 = __ldg(r + 2 * i), e1 = __ldg(r + 2 * i + 1);   // ox oy a0 a1 | b0 b1 dax day
+        float al, be, gp;
+        rec_edge_at(e0, e1, tau, tc.uc, tc.vc, al, be, gp);
         A[i] = al * sg;
         B[i] = be * sg;
         G[i] = gp * sg;

@@ -147,12 +147,8 @@ __device__ __forceinline__ void eval_tau(const FaceRec &fr, float tau, float D, 
     const float *ef = reinterpret_cast<const float *>(fr.q);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        const float ox = ef[8 * i], oy = ef[8 * i + 1];
-        const float al = __fmaf_rn(tau, ef[8 * i + 3], ef[8 * i + 2]);
-        const float be = __fmaf_rn(tau, ef[8 * i + 5], ef[8 * i + 4]);
-        const float ga = __fmul_rn(tau, __fmaf_rn(tau, ef[8 * i + 7], ef[8 * i + 6]));
-        const float dx = __fsub_rn(tc.uc, ox), dy = __fsub_rn(tc.vc, oy);
-        const float gp = __fmaf_rn(al, dx, __fmaf_rn(be, dy, ga));
+        float al, be, gp;
+        rec_edge_at(fr.q[2 * i], fr.q[2 * i + 1], tau, tc.uc, tc.vc, al, be, gp);
         A[i] = al * sg;
         B[i] = be * sg;
         G[i] = gp * sg;

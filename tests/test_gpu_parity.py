@@ -75,7 +75,7 @@ def mask_fractions(ref, N, min_touched=2000):
 
 
 def check_parity(sc, ids_k=0, mode="binned", max_chunk=0, sub_range=None, grad=True, all_pixel_grad=True,
-                 gpu_sc=None, views=None):
+                 gpu_sc=None, views=None, cache=False):
     """Oracle vs GPU on sc.  gpu_sc/views: the GPU renders gpu_sc (e.g. the whole batch in the bench's
     launch configuration) and its images `views` are compared with sc (= gpu_sc.subset(views))."""
     ref = oracle.render_fwd(sc, mode=mode, ids_k=ids_k, eps_amb=1e-6, sub_range=sub_range)
@@ -92,7 +92,7 @@ def check_parity(sc, ids_k=0, mode="binned", max_chunk=0, sub_range=None, grad=T
         Gb[views] = Gs
         return Gb
 
-    got = gpu_render(gpu_sc or sc, ids_k=ids_k, sub_range=sub_range, max_chunk=max_chunk, G=embed(G))
+    got = gpu_render(gpu_sc or sc, ids_k=ids_k, sub_range=sub_range, max_chunk=max_chunk, G=embed(G), cache=cache)
     if gpu_sc is not None:
         got["rgba"], got["ids"] = got["rgba"][views], got["ids"][views]
     assert not (got["status"] & 8), "internal consistency check failed"
@@ -112,7 +112,7 @@ def check_parity(sc, ids_k=0, mode="binned", max_chunk=0, sub_range=None, grad=T
         out.update(dv=ev, dc=ec)
         if all_pixel_grad:   # reported beside the excluded one: the same comparison with G unmasked
             adv, adc = oracle.render_bwd(sc, G_all, mode=mode, sub_range=sub_range)
-            ga = gpu_render(gpu_sc or sc, sub_range=sub_range, max_chunk=max_chunk, G=embed(G_all))
+            ga = gpu_render(gpu_sc or sc, sub_range=sub_range, max_chunk=max_chunk, G=embed(G_all), cache=cache)
             out.update(dv_all_pixels=rel_l2(ga["dv"], adv), dc_all_pixels=rel_l2(ga["dc"], adc))
     return out
 
@@ -137,6 +137,19 @@ def test_c2_full():
 
 def test_c3_subset():
     r = check_parity(scenes.make_c3().subset([0, 3, 6]), ids_k=25)
+    print(r)
+
+
+def test_c3_full_batch():
+    """C3 (BASELINE configs[2]): all 8 views, the rotating top, compared completely."""
+    r = check_parity(scenes.make_c3(), ids_k=25)
+    print(r)
+
+
+def test_c4_full_batch_bench_path():
+    """C4 (BASELINE configs[3], the bench workload): all 16 views in one launch with the visibility cache and
+    the K6 gather, as bench.py times them, compared completely with the binned oracle."""
+    r = check_parity(scenes.make_c4(), ids_k=40, cache=True)
     print(r)
 
 
