@@ -533,7 +533,9 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {**workload_config(sc, args, world, bool(step.groups), graph is not None),
                            **({"passes_per_rank": step.n_passes,
-                               "visibility_cache": "per pass, <= %d MiB" % (BlurRenderer.CACHE_BUDGET_BYTES >> 20)}
+                               "visibility_cache": "per pass, <= %d MiB (a one-image pass: <= %d MiB)"
+                                                   % (BlurRenderer.CACHE_BUDGET_BYTES >> 20,
+                                                      BlurRenderer.CACHE_IMAGE_BYTES >> 20)}
                               if step.n_passes > 1 else {})},
                 "barycentric_evals_per_s": {"executed": cand * world / (ms_per_step / 1000.0),
                                             "necessary": nec * world / (ms_per_step / 1000.0),

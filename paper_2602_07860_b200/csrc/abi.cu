@@ -371,7 +371,7 @@ Tables make_tables(const Plan &P, void *ws)
         t.sb.entries = (int *)(w + P.o_sent);
         t.sb.cap = P.scap;
         t.sb.binstat = (long long *)(w + P.o_status + 24);
-        t.sb.sortcap = 4096;
+        t.sb.sortcap = 16384;   // k_bin.cu SORTCAP_BIG
     }
     if (P.vis) t.vis = (uint16_t *)(w + P.o_vis);
     if (P.vis) { t.vg_count = (int *)(w + P.o_vgl); t.vg_list = (int *)(w + P.o_vgl + 16); }

@@ -315,11 +315,14 @@ __global__ void __launch_bounds__(256) k3_sort(Tables t, BinSet bs, int nbins)
     }
 }
 
-// ---- CTA-per-bin bitonic sort of the bins longer than SORTCAP (soft bins, up to bs.sortcap)
-constexpr int SORTCAP_BIG = 4096;
+// ---- CTA-per-bin bitonic sort of the bins longer than SORTCAP (soft bins, up to bs.sortcap <= SORTCAP_BIG):
+// the bin in dynamic shared memory (64 KB at 16384 entries).  Longer soft bins take the raster kernels' exact
+// fallback, a scan of every face of the segment per (sub-frame, tile): on C5 (1024^2, 81,920 faces, rcut = 21
+// px) the silhouette tiles' soft bins exceed 4,096 entries, and that scan was most of K8/K9's time.
+constexpr int SORTCAP_BIG = 16384;
 __global__ void __launch_bounds__(512) k3_sort_big(Tables t, BinSet bs, int nbins)
 {
-    __shared__ int s[SORTCAP_BIG];
+    extern __shared__ int s[];   // [SORTCAP_BIG]
     __shared__ int bad;
     for (int bi = blockIdx.x; bi < nbins; bi += gridDim.x) {
         const long long o = bs.off[bi];
@@ -399,7 +402,12 @@ cudaError_t launch_binning(const Tables &t, const BinSet &bs, float dil, cudaStr
         int sb = (nbins + 7) / 8;
         if (sb > 148 * 16) sb = 148 * 16;
         if (bs.sortcap > 0) k3_sort<<<sb, 256, 0, st>>>(t, bs, nbins);
-        if (bs.sortcap > SORTCAP) k3_sort_big<<<std::min(nbins, 148 * 4), 512, 0, st>>>(t, bs, nbins);
+        if (bs.sortcap > SORTCAP) {
+            const int smem = (int)sizeof(int) * SORTCAP_BIG;
+            e = cudaFuncSetAttribute(k3_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+            k3_sort_big<<<std::min(nbins, 148 * 2), 512, smem, st>>>(t, bs, nbins);
+        }
     }
     return cudaGetLastError();
 }

@@ -51,6 +51,9 @@ class BlurRenderer:
     # BLUR_CACHE_VISIBILITY budget: the per-(pixel, sub-frame) winner index (2 B, +4 B of soft products)
     # is kept between the forward and the backward only when it fits (C4: 0.84 GB; C5: 34 GB -> off)
     CACHE_BUDGET_BYTES = 1 << 30
+    # ... except that a single image always keeps it up to CACHE_IMAGE_BYTES (C5 with soft coverage: 1.6 GB
+    # per image; without it K9 runs its two-pass product recompute: 3.5x slower on C5)
+    CACHE_IMAGE_BYTES = 2 << 30
 
     def __init__(self, faces, motion: dict, cams, H: int, W: int, V: int, device="cuda",
                  sub_range=None, max_chunk: int = 0, bin_factor: float = 0.0, solver: int = 0,
@@ -83,7 +86,7 @@ class BlurRenderer:
         # fits CACHE_BUDGET_BYTES; without it K6 recomputes the visibility (k6_raster_bwd_fx)
         if cache_visibility is None:
             need = sum(cache_bytes_per_image(self.H, self.W, n, self.delta) for n in self.N)
-            cache_visibility = need <= self.CACHE_BUDGET_BYTES
+            cache_visibility = need <= (self.CACHE_IMAGE_BYTES if self.B == 1 else self.CACHE_BUDGET_BYTES)
         self.cache_flags = _lib.BLUR_CACHE_VISIBILITY if (cache_visibility and self.solver == 0) else 0
         self.auto_bins = bin_factor == 0.0 or (self.delta > 0 and soft_bin_factor == 0.0)
         self.n_forward = 0
