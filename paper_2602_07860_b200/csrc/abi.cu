@@ -108,6 +108,9 @@ struct Plan {
 
 bool legacy_env();
 
+#ifndef BR_CHUNK2_TILES
+#define BR_CHUNK2_TILES 3.5   // 2-sub-frame chunks up to 3.5 tiles of motion per sub-frame (C3 2.80 -> 2.56 ms/step
+#endif                        // with the lean K4; 1.5 was fitted to round 1's kernel; C2, C4, C5 unchanged)
 int auto_chunk(const blur_motion &m, const blur_camera &c, int H, int W)
 {
     const double dx = c.eye[0] - c.target[0], dy = c.eye[1] - c.target[1], dz = c.eye[2] - c.target[2];
@@ -125,10 +128,10 @@ int auto_chunk(const blur_motion &m, const blur_camera &c, int H, int W)
         world = std::fabs((double)m.angle) + 2.0;
     const double disp = world * ndc_per_world * px_per_ndc / (N - 1);
     if (disp <= 1e-6) return 16;
-    // chunk ~ one tile of motion; at least 2 sub-frames unless the motion exceeds 1.5 tiles per
-    // sub-frame (then per-sub-frame bins); at most 8 (rule fitted on C2-C5, profiles/r1_summary.md)
+    // chunk ~ one tile of motion; at least 2 sub-frames unless the motion exceeds BR_CHUNK2_TILES tiles per
+    // sub-frame (then per-sub-frame bins); at most 8 (rule fitted on C2-C5: tools/chunk_sweep.sh)
     int g = (int)std::floor(TW / disp);
-    if (disp <= 1.5 * TW && g < 2) g = 2;
+    if (disp <= BR_CHUNK2_TILES * TW && g < 2) g = 2;
     if (g < 1) g = 1;
     if (g > 8) g = 8;
     return g;
