@@ -36,8 +36,11 @@ namespace br {
 #ifndef BR_HALF
 #define BR_HALF 0
 #endif
+#ifndef BR_K4L_MICRO
+#define BR_K4L_MICRO 1   // 1: one-instruction warp max of the winners' depths, __frcp_rn for 1/|D|
+#endif
 #ifndef BR_K4L_MASKBF
-#define BR_K4L_MASKBF 0   // 1: the staging's footprint mask without data-dependent loops (all 8 footprints, box bits)
+#define BR_K4L_MASKBF 1   // 1: the staging's footprint mask without data-dependent loops (all 8 footprints, box bits)
 #endif
 // Culling footprints: BR_HALF = 1 -> 4x4 pixel blocks (16 per tile, two per warp: the left and right
 // halves of its 8x4 pixels iterate their own face masks), 0 -> the warps' 8x4 blocks.
@@ -109,7 +112,7 @@ __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, floa
 {
     const float4 q6 = fr.q[6];
     const float sg = D < 0.f ? -1.f : 1.f;
-    const float invD = 1.0f / fabsf(D);
+    const float invD = BR_K4L_MICRO ? __frcp_rn(fabsf(D)) : 1.0f / fabsf(D);   // the same correctly rounded value
     float A[3], B[3], G[3];
     const float *ef = reinterpret_cast<const float *>(fr.q);
 #pragma unroll
@@ -960,9 +963,15 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                         if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
                     }
                     if (BR_K4L_CULL == 2 && cb) {   // the others, unless all of them are behind every pixel's winner
+#if BR_K4L_MICRO
+                        // depths are positive: the integer order of their bits is the float order (one REDUX; a NaN
+                        // gives a NaN maximum, which never skips)
+                        const float zmax = __int_as_float(__reduce_max_sync(0xffffffffu, __float_as_int(zbest)));
+#else
                         float zmax = zbest;
 #pragma unroll
                         for (int d = 16; d > 0; d >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, d));
+#endif
                         // zmax = +inf unless every pixel of the footprint has a winner; each face of the list has
                         // its depth >= minz at every pixel of the footprint (staging, corner of the plane)
                         if (!(zmax < __int_as_float(S.u.g.minz[l][warp]))) {
@@ -1104,6 +1113,354 @@ static cudaError_t launch_fwd_lean(const Tables &t, float *out, int *ids, int id
     if (e != cudaSuccess) return e;
     k4l_raster_fwd<COV, CENSUS><<<grid, NT, smem, st>>>(t, out, ids, ids_k, census);
     return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ super-grouped lean forward (measured A/B)
+//
+// k4s_raster_fwd: k4l_raster_fwd with super-groups.  The automatic chunks of fast motions hold 2-3 sub-frames, so
+// a k4l group is one chunk: ~200 (face, sub-frame) pairs staged between two barriers, ~20 (sub-frame, footprint)
+// visits, and a third barrier to clear the counters (C4: 4.4e5 groups per launch, barrier waits the top stall).
+// Here a group takes consecutive chunks of this CTA's share of the tile, sub-frame slot by slot, while the
+// records fit (SREC_F) and the slots GMAX_F: each slot L has its own record range [rb_L, rb_L + n_L) -- its
+// chunk's bin at its sub-frame -- and its own footprint lists in the same index range (faces turned towards the
+// camera from the start, the others from the end), so the stage, the tests, the tie rule (Q7), the list-level
+// skip of the faces turned away and the shading (Eq.9) are exactly k4l's; only the grouping differs.  Long and
+// overflowed bins flush the group and take k4l's per-sub-frame batch path.
+
+struct SGSeg {             // one chunk's part of a super-group (block-uniform, shared memory)
+    const int *ent;        // bin entries (face ids)
+    const float4 *rseg;    // records of the chunk's (image, segment)
+    int n, ng;             // bin length, sub-frame slots taken
+    int pbase, lbase;      // first pair, first slot of this part
+    int rbase;             // first record
+};
+constexpr int SG_MAXC = GMAX_F;
+
+struct __align__(16) SGSmem {
+    LeanSmem L;
+    SGSeg seg[SG_MAXC];
+    int slot_rb[GMAX_F];   // per slot: first record, bin length, absolute sub-frame, visibility cache on
+    int slot_n[GMAX_F];
+    int slot_k[GMAX_F];
+    int slot_vis[GMAX_F];
+};
+
+static_assert(sizeof(SGSmem) + 1024 <= 228 * 1024 / BR_K4_MINB, "k4s_raster_fwd: BR_K4_MINB CTAs per SM");
+
+__device__ __forceinline__ void pair_stage_sg(const FaceRec &fr, int ri, int rb, int n, int L, float tau, float D, int x0,
+                                              int x1, int y0, int y1, const TileCtx &tc, TauRec *rec,
+                                              uint16_t (*list)[SREC_F], int (*cnt)[NFP], int (*cntb)[NFP], float sF,
+                                              int (*minz)[NFP])
+{
+    const bool back = BR_K4L_CULL && D * sF < 0.f;
+    const uint32_t fm = stage_tau<true>(fr, tau, D, x0, x1, y0, y1, tc, rec[ri]);
+    const uint16_t off = (uint16_t)(ri * (int)sizeof(TauRec));
+    if (!back) {
+        for (uint32_t m = fm; m; m &= m - 1) {
+            const int w = __ffs(m) - 1;
+            list[w][rb + atomicAdd(&cnt[L][w], 1)] = off;
+        }
+        return;
+    }
+    const TauRec &R = rec[ri];
+    const float az = R.az, bz = R.bz, cz = R.cz;
+    for (uint32_t m = fm; m; m &= m - 1) {
+        const int w = __ffs(m) - 1;
+        list[w][rb + n - 1 - atomicAdd(&cntb[L][w], 1)] = off;
+        if (BR_K4L_CULL == 2) {   // lowest depth of the plane over the footprint's pixel centres (k4l)
+            const int wx = w & 1, wy = w >> 1;
+            const float u = (float)((az > 0.f ? 0 : 7) + wx * FPW - TW / 2) * tc.sx;
+            const float v = (float)(TH / 2 - wy * 4 - (bz > 0.f ? 3 : 0)) * tc.sy;
+            const float zm = fmaxf(__fmaf_rn(az, u, __fmaf_rn(bz, v, cz)), 0.f);
+            atomicMin(&minz[L][w], __float_as_int(zm));
+        }
+    }
+}
+
+template <bool COV>
+__global__ void __launch_bounds__(NT, BR_K4_MINB) k4s_raster_fwd(Tables t, float *__restrict__ out, int *__restrict__ ids,
+                                                                int ids_k)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SGSmem &SG = *reinterpret_cast<SGSmem *>(smem_raw);
+    LeanSmem &S = SG.L;
+    const int b = blockIdx.y, tile = blockIdx.x;
+    const ImgInfo &im = t.imgs[b];
+    const int N = im.N, c_end = im.chunk_end, sched_off = im.sched_off;
+    const long long rec_off = im.rec_off;
+    TileCtx tc;
+    tile_ctx(t, tile, tc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+    const int px = tc.px0 + lx, py = tc.py0 + ly;
+    const bool inimg = px < t.W && py < t.H;
+    const float ul0 = (float)(lx - TW / 2) * tc.sx;
+    const float vl0 = (float)(TH / 2 - ly) * tc.sy;
+    const int myp = ly * TW + lx;
+    const size_t pix = ((size_t)b * t.H + py) * t.W + px;
+    S.acc[myp] = make_float4(0.f, 0.f, 0.f, 0.f);
+    S.uv[threadIdx.x] = make_float2(ul0, vl0);
+    for (int i = threadIdx.x; i < GMAX_F * NFP; i += NT) {
+        (&S.u.g.cnt[0][0])[i] = 0; (&S.u.g.cntb[0][0])[i] = 0; (&S.u.g.minz[0][0])[i] = 0x7f800000;
+    }
+    unsigned long long c_stage = 0;
+    const double orient = *t.orient;
+    const float sF = orient > 0.0 ? 1.f : orient < 0.0 ? -1.f : 0.f;
+
+    int c = im.chunk_begin + (int)blockIdx.z;   // next chunk of this CTA's share, and its next sub-frame
+    int kc = c < c_end ? t.chunks[c].k0 : 0;
+    while (c < c_end) {
+        // ---- compose a super-group (every thread computes the same composition from the same words)
+        int nseg = 0, P = 0, R = 0, NL = 0;
+        bool batch_chunk = false;
+        while (c < c_end) {
+            const Chunk ch = t.chunks[c];
+            const size_t bi = (size_t)c * t.T + tile;
+            const long long o = t.off[bi];
+            const int n = (int)(t.off[bi + 1] - o);
+            if (n == 0) {   // nothing covers the tile: background at every sub-frame of the chunk
+                if (ids && inimg && ids_k >= ch.k0 && ids_k < ch.k1) ids[pix] = -1;
+                if (COV) {
+                    const unsigned m = __ballot_sync(0xffffffffu, !inimg);
+                    if (lane == 0)
+                        for (int k = ch.k0; k < ch.k1; ++k) t.covbits[cov_word(t, im, k, tile) + warp] = m;
+                }
+                c += t.splits;
+                kc = c < c_end ? t.chunks[c].k0 : 0;
+                continue;
+            }
+            if (o + n > t.cap || n > SREC_F) {   // long or overflowed bin: after the pending group, alone
+                batch_chunk = nseg == 0;
+                break;
+            }
+            const int ng = min(min(ch.k1 - kc, GMAX_F - NL), (SREC_F - R) / n);
+            if (ng <= 0) break;   // group full
+            if (threadIdx.x == 0) {
+                SGSeg &sg = SG.seg[nseg];
+                sg.ent = t.entries + o;
+                sg.rseg = t.rec + (size_t)(rec_off + (long long)ch.s * t.F) * REC_F4;
+                sg.n = n; sg.ng = ng; sg.pbase = P; sg.lbase = NL; sg.rbase = R;
+            }
+            if (threadIdx.x < ng) {
+                const int L = NL + threadIdx.x;
+                S.taus[L] = t.sched_tau[sched_off + kc + threadIdx.x];
+                SG.slot_rb[L] = R + threadIdx.x * n;
+                SG.slot_n[L] = n;
+                SG.slot_k[L] = kc + threadIdx.x;
+                SG.slot_vis[L] = n <= VIS_MAXN;
+            }
+            ++nseg; P += n * ng; R += n * ng; NL += ng;
+            kc += ng;
+            if (kc >= ch.k1) {
+                c += t.splits;
+                kc = c < c_end ? t.chunks[c].k0 : 0;
+            }
+            if (NL >= GMAX_F) break;
+        }
+        if (nseg > 0) {
+            __syncthreads();   // composition written; the previous group's lists and counters are consumed
+            // ---- stage: pairs over the parts, part by part
+            for (int p = threadIdx.x; p < P; p += NT) {
+                int s = 0;
+                while (s + 1 < nseg && SG.seg[s + 1].pbase <= p) ++s;
+                const SGSeg &sg = SG.seg[s];
+                const int pl = p - sg.pbase, ng = sg.ng, n = sg.n;
+                const int j = div_small(pl, __frcp_rn((float)ng));
+                const int l = pl - j * ng, L = sg.lbase + l;
+                const int f = __ldg(sg.ent + j);
+                if ((unsigned)f >= (unsigned)t.F) { atomicOr(t.status, BLUR_ST_EINTERNAL); continue; }
+                const float4 *r = sg.rseg + (size_t)f * REC_F4;
+                const float4 q6 = __ldg(r + 6);
+                const float4 b0 = __ldg(r + 7), b1 = __ldg(r + 8);
+                if (__float_as_int(q6.w) < 0) continue;   // skipped face (Q8, behind, bad index)
+                const float tau = S.taus[L];
+                const float D = __fmaf_rn(tau, __fmaf_rn(tau, q6.x, q6.y), q6.z);
+                if (!(fabsf(D) > EPS_D)) continue;
+                int x0, x1, y0, y1;
+                if (!tile_pixels(box_lerp(tau, b0.x, b1.x), box_lerp(tau, b0.y, b1.y), box_lerp(tau, b0.z, b1.z),
+                                 box_lerp(tau, b0.w, b1.w), t.W, t.H, tc, x0, x1, y0, y1))
+                    continue;
+                FaceRec fr;
+                load_rec(r, fr);
+                const int rb = sg.rbase + l * n;
+                pair_stage_sg(fr, rb + j, rb, n, L, tau, D, x0, x1, y0, y1, tc, S.rec, S.u.g.list, S.u.g.cnt,
+                              S.u.g.cntb, sF, S.u.g.minz);
+            }
+            __syncthreads();
+            // ---- visibility and shading per slot (k4l's loop body)
+            const unsigned char *rbase = reinterpret_cast<const unsigned char *>(S.rec);
+            for (int L = 0; L < NL; ++L) {
+                const int rb = SG.slot_rb[L], n = SG.slot_n[L], k = SG.slot_k[L];
+                const uint16_t *lst = S.u.g.list[warp] + rb;
+                const int cn = S.u.g.cnt[L][warp], cb = S.u.g.cntb[L][warp];
+                const float2 uvp = S.uv[threadIdx.x];
+                const float ul = uvp.x, vl = uvp.y;
+                float zbest = __int_as_float(0x7f800000), tief = 0.f;
+                int eoff = -1;
+                for (int i = 0; i < cn; ++i) {   // faces turned towards the camera
+                    const int off = lst[i];
+                    const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
+                    const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
+                    const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
+                    const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
+                    const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
+                    const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
+                    const float emin = fminf(fminf(e0, e1), e2);
+                    tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
+                    if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
+                }
+                if (BR_K4L_CULL == 2 && cb) {   // the others, unless all of them are behind every pixel's winner
+                    const float zmax = __int_as_float(__reduce_max_sync(0xffffffffu, __float_as_int(zbest)));
+                    if (!(zmax < __int_as_float(S.u.g.minz[L][warp]))) {
+                        for (int i = n - cb; i < n; ++i) {
+                            const int off = lst[i];
+                            const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
+                            const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
+                            const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
+                            const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
+                            const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
+                            const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
+                            const float emin = fminf(fminf(e0, e1), e2);
+                            tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
+                            if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
+                        }
+                    }
+                }
+                if (__any_sync(0xffffffffu, tief != 0.f)) {   // exact depth tie in the warp: face indices decide (Q7)
+                    zbest = __int_as_float(0x7f800000);
+                    eoff = -1;
+                    int fbest = 0x7fffffff;
+                    for (int ii = 0; ii < cn + cb; ++ii) {
+                        const int off = lst[ii < cn ? ii : n - cb + (ii - cn)];
+                        const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
+                        const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
+                        const float e0 = edge_eval(q0.x, q0.w, q1.z, ul, vl);
+                        const float e1 = edge_eval(q0.y, q1.x, q1.w, ul, vl);
+                        const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
+                        const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
+                        if (fminf(fminf(e0, e1), e2) >= 0.f && z <= zbest) {
+                            const int fj = reinterpret_cast<const TauRec *>(rbase + off)->fid;
+                            if (z < zbest || fj < fbest) { zbest = z; eoff = off; fbest = fj; }
+                        }
+                    }
+                }
+                const int eb = eoff >= 0 ? eoff / (int)sizeof(TauRec) : -1;   // record index
+                int fid = -1;
+                if (eb >= 0) {
+                    float pr, pg, pbb;
+                    shade(S.rec[eb], t.fcol, ul, vl, pr, pg, pbb);      // Eq.9
+                    float4 a = S.acc[myp];
+                    a.x += pr; a.y += pg; a.z += pbb; a.w += 1.f;
+                    S.acc[myp] = a;
+                    fid = S.rec[eb].fid;
+                }
+                if (ids && inimg && k == ids_k) ids[pix] = fid;
+                if (t.vis && SG.slot_vis[L])   // visibility cache for K6: the winner's slot in its bin
+                    t.vis[((size_t)(im.cov_off + k) * t.T + tile) * (TW * TH) + myp] =
+                        eb >= 0 ? (uint16_t)(eb - rb) : (uint16_t)0xFFFF;
+                if (COV) {
+                    const unsigned m = __ballot_sync(0xffffffffu, eb >= 0 || !inimg);
+                    if (lane == 0) t.covbits[cov_word(t, im, k, tile) + warp] = m;
+                }
+            }
+            __syncthreads();   // lists read: clear the counters of this group
+            if (threadIdx.x < NL * NFP) {
+                (&S.u.g.cnt[0][0])[threadIdx.x] = 0; (&S.u.g.cntb[0][0])[threadIdx.x] = 0;
+                (&S.u.g.minz[0][0])[threadIdx.x] = 0x7f800000;
+            }
+            continue;
+        }
+        if (!batch_chunk) continue;
+        // ---- a long or overflowed bin: per sub-frame, several batches or the exact fallback scan (as k4l)
+        {
+            const Chunk ch = t.chunks[c];
+            const size_t bi = (size_t)c * t.T + tile;
+            const long long o = t.off[bi];
+            BinCtx bc;
+            bc.status = t.status;
+            bc.rseg = t.rec + (size_t)(rec_off + (long long)ch.s * t.F) * REC_F4;
+            bc.key0 = nullptr;
+            bc.key1 = nullptr;
+            bc.fcol = t.fcol;
+            bc.ent = t.entries + o;
+            bc.n = (int)(t.off[bi + 1] - o);
+            bc.fb = o + bc.n > t.cap;
+            const float ul = ul0, vl = vl0;
+            unsigned long long c_cov = 0, c_test = 0;
+            for (int k = ch.k0; k < ch.k1; ++k) {
+                const float tau = t.sched_tau[sched_off + k];
+                float zbest = __int_as_float(0x7f800000);
+                int ebest = -1, bfid = -1, fbest = 0x7fffffff;
+                bool has = false;
+                float pr = 0.f, pg = 0.f, pbb = 0.f;
+                int base = 0, fpos = 0;
+                __syncthreads();
+                if (threadIdx.x == 0) S.taus[0] = tau;
+                while (true) {
+                    const int nb = next_batch(bc, t.F, tau, tc, t.W, t.H, SREC_F, base, fpos, S.u.b.sid, S.wsum);
+                    if (nb == 0) break;
+                    const int nw = (nb + 31) >> 5;
+                    clear_words(S.u.b.wm, NFP * nw);
+                    __syncthreads();
+                    stage_group<false, 0, true>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.u.b.sid, S.rec, nullptr,
+                                                S.u.b.wm, c_stage);
+                    __syncthreads();
+                    vis_mask<false, 0>(S.rec, nullptr, S.u.b.wm + warp * nw, nw, base, ul, vl, zbest, ebest, fbest, c_cov,
+                                       c_test, inimg);
+                    if (ebest >= base) {   // winner changed in this batch: shade now (Eq.9)
+                        shade(S.rec[ebest - base], t.fcol, ul, vl, pr, pg, pbb);
+                        has = true;
+                        bfid = S.rec[ebest - base].fid;
+                        fbest = bfid;
+                    }
+                    base += nb;
+                    __syncthreads();
+                }
+                if (has) {
+                    float4 a = S.acc[myp];
+                    a.x += pr; a.y += pg; a.z += pbb; a.w += 1.f;
+                    S.acc[myp] = a;
+                }
+                if (ids && inimg && k == ids_k) ids[pix] = has ? bfid : -1;
+                if (COV) {
+                    const unsigned m = __ballot_sync(0xffffffffu, has || !inimg);
+                    if (lane == 0) t.covbits[cov_word(t, im, k, tile) + warp] = m;
+                }
+            }
+            __syncthreads();   // the grouped path's counters share the batch path's shared memory
+            for (int i = threadIdx.x; i < GMAX_F * NFP; i += NT) {
+                (&S.u.g.cnt[0][0])[i] = 0; (&S.u.g.cntb[0][0])[i] = 0; (&S.u.g.minz[0][0])[i] = 0x7f800000;
+            }
+            c += t.splits;
+            kc = c < c_end ? t.chunks[c].k0 : 0;
+        }
+    }
+    if (inimg && out) {   // out == null: coverage-only pass (soft backward without a preceding forward)
+        const float inv = 1.0f / (float)N;
+        const float4 a = S.acc[myp];
+        const float4 v = make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
+        if (t.splits == 1) reinterpret_cast<float4 *>(out)[pix] = v;
+        else t.part[(size_t)blockIdx.z * ((size_t)t.B * t.H * t.W) + pix] = v;
+    }
+}
+
+template <bool COV>
+static cudaError_t launch_fwd_sg(const Tables &t, float *out, int *ids, int ids_k, cudaStream_t st)
+{
+    dim3 grid(t.T, t.B, t.splits);
+    const int smem = (int)sizeof(SGSmem);
+    cudaError_t e = cudaFuncSetAttribute(k4s_raster_fwd<COV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k4s_raster_fwd<COV><<<grid, NT, smem, st>>>(t, out, ids, ids_k);
+    return cudaGetLastError();
+}
+
+// BLURRAST_FWD=sg: the super-grouped k4s_raster_fwd instead of k4l_raster_fwd (A/B; measured slower: C4 K4 5.92 ->
+// 6.34 ms, C3 1.26 -> 1.39 ms, parity-green)
+static bool sg_fwd_on()
+{
+    const char *s = std::getenv("BLURRAST_FWD");
+    return s && std::strcmp(s, "sg") == 0;
 }
 
 // ------------------------------------------------------------------ pipelined forward (fast solver)
@@ -2346,6 +2703,8 @@ cudaError_t launch_raster_fwd_legacy(const Tables &t, float *out, int *ids, int 
         if (pixmajor_fwd_on()) return launch_raster_fwd_pixmajor(t, out, ids, ids_k, st);
         if (pipe_fwd_on())
             return t.covbits ? launch_fwd_pipe<true>(t, out, ids, ids_k, st) : launch_fwd_pipe<false>(t, out, ids, ids_k, st);
+        if (sg_fwd_on())
+            return t.covbits ? launch_fwd_sg<true>(t, out, ids, ids_k, st) : launch_fwd_sg<false>(t, out, ids, ids_k, st);
         if (!lean_fwd_off())
             return t.covbits ? launch_fwd_lean<true>(t, out, ids, ids_k, st) : launch_fwd_lean<false>(t, out, ids, ids_k, st);
         return launch_fwd_t<false, 0>(t, out, ids, ids_k, nullptr, st);
