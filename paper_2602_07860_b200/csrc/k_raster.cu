@@ -36,6 +36,9 @@ namespace br {
 #ifndef BR_HALF
 #define BR_HALF 0
 #endif
+#ifndef BR_K4L_GRP
+#define BR_K4L_GRP BR_SREC_F   // (face, sub-frame) pairs per k4l group at most (one sub-frame at least)
+#endif
 #ifndef BR_K4L_MICRO
 #define BR_K4L_MICRO 1   // 1: one-instruction warp max of the winners' depths, __frcp_rn for 1/|D|
 #endif
@@ -906,7 +909,8 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
         bc.n = n;
         bc.fb = o + n > t.cap;
         if (!bc.fb && n <= SREC_F) {
-            const int Gs = min(GMAX_F, group_div(SREC_F, n));
+            const int Gs = BR_K4L_GRP >= SREC_F ? min(GMAX_F, group_div(SREC_F, n))
+                                                : max(1, min(GMAX_F, group_div(BR_K4L_GRP, n)));
             uint16_t *vis_out = n <= VIS_MAXN ? t.vis : nullptr;
 #if BR_K4L_SENT
             __syncthreads();   // the previous chunk's entries are consumed
