@@ -158,6 +158,15 @@ __device__ __forceinline__ void rec_edge_at(const float4 qa, const float4 qb, fl
     gp = __fmaf_rn(al, __fsub_rn(uc, ax), __fmul_rn(be, __fsub_rn(vc, ay)));
 }
 
+// Checked build (-DBR_CHECKED, tools/checked_build.sh): shared-memory index invariants of the raster kernels
+// are tested at run time and a violation raises BLUR_ST_EINTERNAL (surfaced by blur_read_status /
+// BLURRAST_CHECK=1) -- the memory-safety evidence this pool allows in place of compute-sanitizer.
+#ifdef BR_CHECKED
+#define BR_CHECK(cond, status_ptr) do { if (!(cond)) atomicOr((status_ptr), 8); } while (0)
+#else
+#define BR_CHECK(cond, status_ptr) ((void)0)
+#endif
+
 // conservative keyframe box lerped to tau (monotone in tau for fixed endpoints)
 __device__ __forceinline__ float box_lerp(float tau, float a, float b) { return __fmaf_rn(tau, __fsub_rn(b, a), a); }
 

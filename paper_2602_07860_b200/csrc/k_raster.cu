@@ -641,6 +641,10 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
 #define K4L_STAT(t_, i_, v_) ((void)0)
 #endif
 
+#ifdef BR_CHECKED
+__device__ int *g_status_dbg;   // the launch's status word, for the checks inside the staging helpers
+#endif
+
 struct __align__(16) LeanSmem {
     TauRec rec[SREC_F];
     union {
@@ -722,7 +726,9 @@ __device__ __forceinline__ void pair_stage_fr(const FaceRec &fr, int j, int l, i
     if (!back) {
         for (uint32_t m = fm; m; m &= m - 1) {
             const int w = __ffs(m) - 1;
-            list[w][l * n + atomicAdd(&cnt[l][w], 1)] = off;
+            const int q = atomicAdd(&cnt[l][w], 1);
+            BR_CHECK(q < n && l * n + q < SREC_F && w < NFP, g_status_dbg);
+            list[w][l * n + q] = off;
         }
         return;
     }
@@ -730,7 +736,9 @@ __device__ __forceinline__ void pair_stage_fr(const FaceRec &fr, int j, int l, i
     const float az = R.az, bz = R.bz, cz = R.cz;
     for (uint32_t m = fm; m; m &= m - 1) {
         const int w = __ffs(m) - 1;
-        list[w][l * n + n - 1 - atomicAdd(&cntb[l][w], 1)] = off;
+        const int q = atomicAdd(&cntb[l][w], 1);
+        BR_CHECK(q < n && l * n + n - 1 - q >= l * n && l * n + n - 1 < SREC_F && w < NFP, g_status_dbg);
+        list[w][l * n + n - 1 - q] = off;
         if (BR_K4L_CULL == 2) {
             // the depth plane fma(az, ul, fma(bz, vl, cz)) is monotone in ul and vl: its minimum over the
             // footprint's pixel centres is its value at one corner (the lanes' own ul, vl values)
@@ -943,6 +951,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
 #else
                     const int cn = S.u.g.cnt[l][warp], cb = S.u.g.cntb[l][warp];
 #endif
+                    BR_CHECK(cn + cb <= n && (l + 1) * n <= SREC_F, t.status);
                     const float2 uvp = S.uv[threadIdx.x];
                     const float ul = uvp.x, vl = uvp.y;
                     float zbest = __int_as_float(0x7f800000), tief = 0.f;
@@ -1115,6 +1124,10 @@ static cudaError_t launch_fwd_lean(const Tables &t, float *out, int *ids, int id
     const int smem = (int)sizeof(LeanSmem);
     cudaError_t e = cudaFuncSetAttribute(k4l_raster_fwd<COV, CENSUS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
+#ifdef BR_CHECKED
+    e = cudaMemcpyToSymbolAsync(g_status_dbg, &t.status, sizeof(int *), 0, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+#endif
     k4l_raster_fwd<COV, CENSUS><<<grid, NT, smem, st>>>(t, out, ids, ids_k, census);
     return cudaGetLastError();
 }
@@ -1162,7 +1175,9 @@ __device__ __forceinline__ void pair_stage_sg(const FaceRec &fr, int ri, int rb,
     if (!back) {
         for (uint32_t m = fm; m; m &= m - 1) {
             const int w = __ffs(m) - 1;
-            list[w][rb + atomicAdd(&cnt[L][w], 1)] = off;
+            const int q = atomicAdd(&cnt[L][w], 1);
+            BR_CHECK(q < n && rb + q < SREC_F && L < GMAX_F, g_status_dbg);
+            list[w][rb + q] = off;
         }
         return;
     }
@@ -1170,7 +1185,9 @@ __device__ __forceinline__ void pair_stage_sg(const FaceRec &fr, int ri, int rb,
     const float az = R.az, bz = R.bz, cz = R.cz;
     for (uint32_t m = fm; m; m &= m - 1) {
         const int w = __ffs(m) - 1;
-        list[w][rb + n - 1 - atomicAdd(&cntb[L][w], 1)] = off;
+        const int q = atomicAdd(&cntb[L][w], 1);
+        BR_CHECK(q < n && rb + n - 1 < SREC_F && L < GMAX_F, g_status_dbg);
+        list[w][rb + n - 1 - q] = off;
         if (BR_K4L_CULL == 2) {   // lowest depth of the plane over the footprint's pixel centres (k4l)
             const int wx = w & 1, wy = w >> 1;
             const float u = (float)((az > 0.f ? 0 : 7) + wx * FPW - TW / 2) * tc.sx;
@@ -1297,6 +1314,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4s_raster_fwd(Tables t, float
                 const int rb = SG.slot_rb[L], n = SG.slot_n[L], k = SG.slot_k[L];
                 const uint16_t *lst = S.u.g.list[warp] + rb;
                 const int cn = S.u.g.cnt[L][warp], cb = S.u.g.cntb[L][warp];
+                BR_CHECK(cn + cb <= n && rb + n <= SREC_F, t.status);
                 const float2 uvp = S.uv[threadIdx.x];
                 const float ul = uvp.x, vl = uvp.y;
                 float zbest = __int_as_float(0x7f800000), tief = 0.f;
@@ -1455,6 +1473,10 @@ static cudaError_t launch_fwd_sg(const Tables &t, float *out, int *ids, int ids_
     const int smem = (int)sizeof(SGSmem);
     cudaError_t e = cudaFuncSetAttribute(k4s_raster_fwd<COV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
+#ifdef BR_CHECKED
+    e = cudaMemcpyToSymbolAsync(g_status_dbg, &t.status, sizeof(int *), 0, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+#endif
     k4s_raster_fwd<COV><<<grid, NT, smem, st>>>(t, out, ids, ids_k);
     return cudaGetLastError();
 }
