@@ -24,6 +24,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cuda_pipeline.h>
+
 #include "internal.cuh"
 #include "raster_common.cuh"
 #include "../../include/blurrast.h"
@@ -35,6 +37,9 @@ namespace br {
 #endif
 #ifndef BR_HALF
 #define BR_HALF 0
+#endif
+#ifndef BR_K4L_PREF
+#define BR_K4L_PREF 0   // 1: the next chunk's bin entries are copied to shared memory (cp.async) during the tests
 #endif
 #ifndef BR_K4L_GRP
 #define BR_K4L_GRP BR_SREC_F   // (face, sub-frame) pairs per k4l group at most (one sub-frame at least)
@@ -666,6 +671,7 @@ struct __align__(16) LeanSmem {
     int wsum[NWARP];
     float2 uv[NT];                              // the thread's pixel (ul, vl), reloaded per sub-frame
     float4 acc[TW * TH];                        // per-pixel (r, g, b, a) sums over the sub-frames
+    int pent[BR_K4L_PREF ? SREC_F : 1];         // the next chunk's bin entries, prefetched by cp.async
 };
 static_assert(SREC_F * 64 <= 65535, "list entries are 16-bit byte offsets");
 
@@ -681,7 +687,7 @@ __device__ __forceinline__ bool pair_head(const BinCtx &bc, const int *ent, int 
 {
     j = div_small(p, inv_ng);
     l = p - j * ng;
-    const int f = BR_K4L_SENT ? ent[j] : __ldg(ent + j);
+    const int f = (BR_K4L_SENT || BR_K4L_PREF) ? ent[j] : __ldg(ent + j);   // generic load: ent may be in shared memory
     if ((unsigned)f >= (unsigned)F) {     // never expected: bins hold valid face ids
         atomicOr(bc.status, BLUR_ST_EINTERNAL);
         return false;
@@ -770,7 +776,7 @@ __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *en
     const float inv_nb = 1.0f / (float)nb;
     for (int u = threadIdx.x; u < nunit; u += NT) {
         const int j = div_small(u, inv_nb), lb = u - j * nb;
-        const int f = BR_K4L_SENT ? ent[j] : __ldg(ent + j);
+        const int f = (BR_K4L_SENT || BR_K4L_PREF) ? ent[j] : __ldg(ent + j);   // generic load: ent may be in shared memory
         if ((unsigned)f >= (unsigned)F) {     // never expected: bins hold valid face ids
             atomicOr(bc.status, BLUR_ST_EINTERNAL);
             continue;
@@ -852,7 +858,7 @@ __device__ __forceinline__ void stage_group_2pass(const BinCtx &bc, const int *e
     for (int i = threadIdx.x; i < na; i += NT) {
         const int code = apairs[i];
         const int j = code & 0x1FF, l = (code >> 9) & 0xF;
-        const int f = BR_K4L_SENT ? ent[j] : __ldg(ent + j);
+        const int f = (BR_K4L_SENT || BR_K4L_PREF) ? ent[j] : __ldg(ent + j);   // generic load: ent may be in shared memory
         const float4 *r = bc.rseg + (size_t)f * REC_F4;
         const float tau = taus[l];
         const float4 q6 = __ldg(r + 6);
@@ -892,6 +898,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
     unsigned long long dz = 0, c_cov = 0, c_test = 0, c_shade = 0, c_stage = 0;   // census (CENSUS builds)
     const double orient = *t.orient;
     const float sF = orient > 0.0 ? 1.f : orient < 0.0 ? -1.f : 0.f;
+    int pref_c = -1;   // chunk whose bin entries were prefetched into S.pent (BR_K4L_PREF)
 
     for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
         const Chunk ch = t.chunks[c];
@@ -925,11 +932,14 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
             for (int j = threadIdx.x; j < n; j += NT) S.u.g.ent[j] = __ldg(bc.ent + j);
             const int *ents = S.u.g.ent;
 #else
-            const int *ents = bc.ent;
+            const int *ents = (BR_K4L_PREF && pref_c == c) ? S.pent : bc.ent;
 #endif
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
+#if BR_K4L_PREF
+                __pipeline_wait_prior(0);   // this thread's prefetched entries have landed
+#endif
                 __syncthreads();   // taus written; the previous group's lists and counters are consumed
 #if BR_K4L_TWOPASS
                 stage_group_2pass(bc, ents, n, S.taus, ng, tc, t.W, t.H, t.F, S.rec, S.u.g.list, S.u.g.cnt, S.u.g.cntb, sF,
@@ -940,6 +950,22 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
 #endif
                 __syncthreads();
                 if (threadIdx.x == 0) { K4L_STAT(t, 20, n * ng); K4L_STAT(t, 29, 1); }
+#if BR_K4L_PREF
+                if (kg + Gs >= ch.k1) {   // last group of the chunk: bring the next chunk's bin entries in during the tests
+                    pref_c = -1;
+                    const int c2 = c + t.splits;
+                    if (c2 < c_end) {
+                        const size_t bi2 = (size_t)c2 * t.T + tile;
+                        const long long o2 = t.off[bi2];
+                        const int n2 = (int)(t.off[bi2 + 1] - o2);
+                        if (n2 > 0 && n2 <= SREC_F && o2 + n2 <= t.cap) {
+                            for (int j = threadIdx.x; j < n2; j += NT) __pipeline_memcpy_async(S.pent + j, t.entries + o2 + j, 4);
+                            __pipeline_commit();
+                            pref_c = c2;
+                        }
+                    }
+                }
+#endif
                 uint16_t *vrow = vis_out ? vis_out + ((size_t)(im.cov_off + kg) * t.T + tile) * (TW * TH) + myp : nullptr;
                 const int l_ids = (ids && inimg) ? ids_k - kg : -1;
                 const uint16_t *lst = S.u.g.list[warp];
@@ -1162,7 +1188,7 @@ struct __align__(16) SGSmem {
     int slot_vis[GMAX_F];
 };
 
-static_assert(sizeof(SGSmem) + 1024 <= 228 * 1024 / BR_K4_MINB, "k4s_raster_fwd: BR_K4_MINB CTAs per SM");
+static_assert(BR_K4L_PREF || sizeof(SGSmem) + 1024 <= 228 * 1024 / BR_K4_MINB, "k4s_raster_fwd: BR_K4_MINB CTAs per SM");
 
 __device__ __forceinline__ void pair_stage_sg(const FaceRec &fr, int ri, int rb, int n, int L, float tau, float D, int x0,
                                               int x1, int y0, int y1, const TileCtx &tc, TauRec *rec,
