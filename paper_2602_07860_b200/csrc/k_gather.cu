@@ -15,10 +15,11 @@
 //            memory; each run of equal winners sets its bit in the slot's 16-bit won mask (atomicOr).
 //   list     thread = 4 consecutive group slots: a block scan of the won masks' popcounts lays out the
 //            group's won pairs slot-major (pair index = slot base + rank of the sub-frame in the mask).
-//   moments  thread = (sub-frame, segment): the pixels of a run of equal winners sum q = round(g 2^e),
-//            q (x - 8), q (8 - y) in registers, and the run adds them to its pair with native 32-bit
-//            shared atomics (integer sums: exact and order-independent, deterministic; 2^e per tile with
-//            max |q| < 2^19, as k6_raster_bwd_fx).
+//   moments  thread = (sub-frame, segment): a run of equal winners takes its sums of q = round(g 2^e) and
+//            q (x - 8) as two lookups in per-row prefix sums built once per CTA (q (8 - y) = dy x the first),
+//            and adds them to its pair with native 32-bit shared atomics (integer sums: exact and
+//            order-independent, deterministic, identical to summing the pixels; 2^e per tile with max |q| <
+//            2^19, as k6_raster_bwd_fx).  (Summing the run's pixels one by one instead: C4 K6 3.36 ms vs 2.90.)
 //   pairs    thread = won pair (face f at sub-frame tau): the face's segment record is evaluated at tau
 //            (Eq.8 numerators and denominator by Horner, "computed only once" per segment) and
 //            face_grad turns the moments into dL/dv (screen space) and dL/dc of the pair.
@@ -46,6 +47,9 @@ static_assert(BR_VG_SPLITS == 1, "the leftover list names whole (image, tile)s: 
 #ifndef BR_VG_PREFETCH
 #define BR_VG_PREFETCH 0   // 1: L1 prefetch of the won faces' records in the list phase (C4 K6 +1%, C3 -2%)
 #endif
+#ifndef BR_VG_PREFIX
+#define BR_VG_PREFIX 1     // 1: per-row prefix sums of the fixed-point pixel gradients; a run's moments are two lookups
+#endif
 #ifndef BR_VG_MINB
 #define BR_VG_MINB 5
 #endif
@@ -58,7 +62,12 @@ static_assert(VIS_MAXN <= SG_SLOTS, "a cached bin must fit a super-group");
 static_assert(SG_T * SG_SEG == 2 * NT, "two (sub-frame, segment) items per thread");
 
 struct __align__(16) VgSmem {
+#if BR_VG_PREFIX
+    int2 pq[TH][TW + 1][3];              // per row, prefix sums over x < k of q (rgb) and q (x - 8) (rgb), packed
+                                         // (q.x, q.y) (q.z, u.x) (u.y, u.z): a run's moments are two lookups
+#else
     int4 qg[TW * TH];                    // dL/dI / N of the tile (rgb) in fixed point, q = round(g 2^e)
+#endif
     uint4 vis[SG_T][SG_SEG];             // winner slot per (group sub-frame, pixel), 0xFFFF none
     uint32_t wmask[SG_SLOTS / 2];        // won masks being built, two 16-bit slots per word
     uint32_t sbm[SG_SLOTS];              // per group slot: first pair index << 16 | won mask (bit l: won at sub-frame l)
@@ -156,7 +165,29 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
         if (gm > 0.f) frexpf(gm, &ex);
         ex = min(max(ex, -100), 100);
         const float scale = ldexpf(1.0f, 19 - ex);
+#if BR_VG_PREFIX
+        {   // inclusive scans of q and q (x - 8) along the row (16 lanes of a half warp), exact in 32-bit integers
+            int v[6];
+            v[0] = __float2int_rn(g.x * scale); v[1] = __float2int_rn(g.y * scale); v[2] = __float2int_rn(g.z * scale);
+            const int dx = lx - TW / 2;
+            v[3] = v[0] * dx; v[4] = v[1] * dx; v[5] = v[2] * dx;
+#pragma unroll
+            for (int d = 1; d < TW; d <<= 1)
+#pragma unroll
+                for (int q = 0; q < 6; ++q) {
+                    const int y = __shfl_up_sync(0xffffffffu, v[q], d, TW);
+                    if (lx >= d) v[q] += y;
+                }
+            S.pq[ly][lx + 1][0] = make_int2(v[0], v[1]);
+            S.pq[ly][lx + 1][1] = make_int2(v[2], v[3]);
+            S.pq[ly][lx + 1][2] = make_int2(v[4], v[5]);
+            if (lx == 0) {
+                S.pq[ly][0][0] = make_int2(0, 0); S.pq[ly][0][1] = make_int2(0, 0); S.pq[ly][0][2] = make_int2(0, 0);
+            }
+        }
+#else
         S.qg[tid] = make_int4(__float2int_rn(g.x * scale), __float2int_rn(g.y * scale), __float2int_rn(g.z * scale), 0);
+#endif
     }
     float inv_scale;
     {
@@ -313,10 +344,22 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
                 const unsigned low = (1u << l) - 1u;   // (< 2^15: selects mask bits only)
                 int cur = -1, prev = -1;
                 int m0 = 0, m1 = 0, m2 = 0, u0 = 0, u1 = 0, u2 = 0;
+#if BR_VG_PREFIX
+                int ka = 0;   // first pixel of the current run
+#endif
 #pragma unroll
                 for (int k = 0; k <= 8; ++k) {
                     const int e = k < 8 ? (int)u4_get(w, k) : 0xFFFF;
                     if (e != prev) {   // run boundary: add the finished run, start the next
+#if BR_VG_PREFIX
+                        if (cur >= 0) {   // the run [ka, k) of this segment: prefix differences
+                            const int2 *pa = S.pq[row][x0 + ka], *pb = S.pq[row][x0 + k];
+                            const int2 a0 = pa[0], a1 = pa[1], a2 = pa[2], b0 = pb[0], b1 = pb[1], b2 = pb[2];
+                            m0 = b0.x - a0.x; m1 = b0.y - a0.y; m2 = b1.x - a1.x;
+                            u0 = b1.y - a1.y; u1 = b2.x - a2.x; u2 = b2.y - a2.y;
+                        }
+                        ka = k;
+#endif
                         if (cur >= 0) {
                             int *m = S.imom[cur];
                             atomicAdd(m + 0, m0); atomicAdd(m + 1, m1); atomicAdd(m + 2, m2);
@@ -333,12 +376,14 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
                         m0 = m1 = m2 = u0 = u1 = u2 = 0;
                         prev = e;
                     }
+#if !BR_VG_PREFIX
                     if (k < 8 && cur >= 0) {
                         const int4 q = S.qg[row * TW + x0 + k];
                         const int dx = x0 + k - TW / 2;
                         m0 += q.x; m1 += q.y; m2 += q.z;
                         u0 += q.x * dx; u1 += q.y * dx; u2 += q.z * dx;
                     }
+#endif
                 }
             }
             __syncthreads();
