@@ -47,6 +47,9 @@ static_assert(BR_VG_SPLITS == 1, "the leftover list names whole (image, tile)s: 
 #ifndef BR_VG_PREFETCH
 #define BR_VG_PREFETCH 0   // 1: L1 prefetch of the won faces' records in the list phase (C4 K6 +1%, C3 -2%)
 #endif
+#ifndef BR_VIS_STREAM
+#define BR_VIS_STREAM 1   // streaming (evict-first) reads of the visibility cache (k_raster.cu: C4 step -0.4%)
+#endif
 #ifndef BR_VG_PREFIX
 #define BR_VG_PREFIX 1     // 1: per-row prefix sums of the fixed-point pixel gradients; a run's moments are two lookups
 #endif
@@ -253,7 +256,11 @@ __global__ void __launch_bounds__(NT, BR_VG_MINB) k6v_raster_bwd(Tables t, const
             const int it = tid + h * NT, l = it / SG_SEG, sg = it % SG_SEG;
             if (l >= L) continue;
             const int row = sg >> 1, x0 = (sg & 1) * 8;
+#if BR_VIS_STREAM
+            uint4 w = __ldcs(reinterpret_cast<const uint4 *>(t.vis + ((size_t)(im.cov_off + S.t_k[l]) * t.T + tile) * (TW * TH)) + sg);
+#else
             uint4 w = reinterpret_cast<const uint4 *>(t.vis + ((size_t)(im.cov_off + S.t_k[l]) * t.T + tile) * (TW * TH))[sg];
+#endif
             const int n = S.t_n[l], soff = S.t_soff[l];
             const bool rowin = tc.py0 + row < t.H;
             unsigned ow[4] = {0u, 0u, 0u, 0u};

@@ -41,6 +41,9 @@ namespace br {
 #ifndef BR_K4L_PREF
 #define BR_K4L_PREF 0   // 1: the next chunk's bin entries are copied to shared memory (cp.async) during the tests
 #endif
+#ifndef BR_VIS_STREAM
+#define BR_VIS_STREAM 1   // 1: the visibility cache is written / read with evict-first (streaming) accesses
+#endif
 #ifndef BR_K4L_GRP
 #define BR_K4L_GRP BR_SREC_F   // (face, sub-frame) pairs per k4l group at most (one sub-frame at least)
 #endif
@@ -1064,7 +1067,11 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                     }
                     if (l == l_ids) ids[pix] = fid;
                     if (vrow) {   // visibility cache for K6
+#if BR_VIS_STREAM
+                        __stcs(vrow, ebest >= 0 ? (unsigned short)ebest : (unsigned short)0xFFFF);   // evict-first: keep L2 for the records
+#else
                         *vrow = ebest >= 0 ? (uint16_t)ebest : (uint16_t)0xFFFF;
+#endif
                         vrow += (size_t)t.T * (TW * TH);
                     }
                     if (COV) {   // soft path: which pixels of the warp are covered at this sub-frame
