@@ -41,7 +41,10 @@ HISTORY = """| change (round 2) | fwd ms | bwd ms | step ms | images/s |
 | third session: records evaluated about the moving vertex a(tau) (numerics; no time change) | 6.15 | 3.36 | 10.16 | 1574 |
 | (tried) K4 order (i), pixel-major (`BLURRAST_FWD=pixmajor`, `r2c_order_i_vs_ii.md`) | 20.1-24.0 | - | - | - |
 | K4 REDUX warp max for the list skip, `__frcp_rn`, branch-free footprint masks | 5.92 | 3.36 | 9.95 | 1608 |
-| (tried) K4 super-groups of consecutive chunks (`BLURRAST_FWD=sg`); group caps 192/256/320 pairs | 6.13-6.68 | - | - | - |"""
+| (tried) K4 super-groups of consecutive chunks (`BLURRAST_FWD=sg`); group caps 192/256/320 pairs | 6.13-6.68 | - | - | - |
+| (tried) K4 next chunk's bin entries prefetched by `cp.async` (`BR_K4L_PREF`) | 6.03 | - | - | - |
+| K6 run moments from per-row prefix sums (two lookups per run) | 5.92 | 2.90 | 9.50 | 1685 |
+| visibility cache written / read evict-first (streaming) | 5.90 | 2.91 | 9.46 | 1691 |"""
 
 
 def row(label, d):
