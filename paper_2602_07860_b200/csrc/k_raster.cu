@@ -44,6 +44,9 @@ namespace br {
 #ifndef BR_VIS_STREAM
 #define BR_VIS_STREAM 1   // 1: the visibility cache is written / read with evict-first (streaming) accesses
 #endif
+#ifndef BR_K4L_LAZY
+#define BR_K4L_LAZY 0   // 1: faces turned away are staged by a warp only where its footprint's back list is tested
+#endif
 #ifndef BR_K4L_GRP
 #define BR_K4L_GRP BR_SREC_F   // (face, sub-frame) pairs per k4l group at most (one sub-frame at least)
 #endif
@@ -222,6 +225,37 @@ __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, floa
     out.invD = invD;
     out.fid = __float_as_int(q6.w);
     return fm;
+}
+
+// The record of a (face, sub-frame) for this tile without its footprint mask: the same arithmetic as stage_tau
+// (bit-identical TauRec), for the lazily staged faces turned away from the camera (BR_K4L_LAZY).
+__device__ __forceinline__ void rec_at(const FaceRec &fr, float tau, float D, const TileCtx &tc, TauRec &out)
+{
+    const float4 q6 = fr.q[6];
+    const float sg = D < 0.f ? -1.f : 1.f;
+    const float invD = BR_K4L_MICRO ? __frcp_rn(fabsf(D)) : 1.0f / fabsf(D);
+    float A[3], B[3], G[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        float al, be, gp;
+        rec_edge_at(fr.q[2 * i], fr.q[2 * i + 1], tau, tc.uc, tc.vc, al, be, gp);
+        A[i] = al * sg;
+        B[i] = be * sg;
+        G[i] = gp * sg;
+    }
+    const float4 z0 = fr.q[9], z1 = fr.q[10];
+    const float za = __fmaf_rn(tau, z1.x - z0.x, z0.x);
+    const float zb = __fmaf_rn(tau, z1.y - z0.y, z0.y);
+    const float zc = __fmaf_rn(tau, z1.z - z0.z, z0.z);
+    out.a[0] = A[0]; out.a[1] = A[1]; out.a[2] = A[2];
+    out.b[0] = B[0]; out.b[1] = B[1]; out.b[2] = B[2];
+    out.g[0] = G[0]; out.g[1] = G[1]; out.g[2] = G[2];
+    const float dzb = zb - za, dzc = zc - za;
+    out.az = __fmaf_rn(A[1], dzb, A[2] * dzc) * invD;
+    out.bz = __fmaf_rn(B[1], dzb, B[2] * dzc) * invD;
+    out.cz = __fmaf_rn(__fmaf_rn(G[1], dzb, G[2] * dzc), invD, za);
+    out.invD = invD;
+    out.fid = __float_as_int(q6.w);
 }
 
 // NEXT-2 ablation (the paper's per-frame baseline): instead of evaluating
@@ -821,6 +855,25 @@ __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *en
             && !(D * sF < 0.f)   // timing experiment only: faces turned away are never staged (not exact)
 #endif
             ) {
+#if BR_K4L_LAZY
+            if (D * sF < 0.f) {   // turned away: only its depth bound and box footprints now (staged if needed)
+                const float4 z0 = __ldg(r + 9), z1 = __ldg(r + 10);
+                const float tau = taus[l];
+                const float zlo = fminf(fminf(__fmaf_rn(tau, z1.x - z0.x, z0.x), __fmaf_rn(tau, z1.y - z0.y, z0.y)),
+                                        __fmaf_rn(tau, z1.z - z0.z, z0.z));
+                // the face's depth at any of its points is a convex combination of its corners' (Q6): >= zlo
+                const int zb = __float_as_int(fmaxf(zlo, 0.f));   // NaN -> 0: never skips
+                for (int wy = y0 >> 2; wy <= (y1 >> 2); ++wy)
+                    for (int wx = x0 >> 3; wx <= (x1 >> 3); ++wx) {
+                        const int w = wy * 2 + wx;
+                        const int q = atomicAdd(&cntb[l][w], 1);
+                        BR_CHECK(q < n && l * n + n - 1 < SREC_F, g_status_dbg);
+                        list[w][l * n + n - 1 - q] = (uint16_t)j;   // the bin slot (not a record offset)
+                        atomicMin(&minz[l][w], zb);
+                    }
+                continue;
+            }
+#endif
 #ifdef BR_K4L_STATS
             unsigned long long ns = 0;
             pair_stage(r, j, l, n, taus[l], D, x0, x1, y0, y1, tc, rec, list, cnt, cntb, sF, minz, &ns);
@@ -870,6 +923,64 @@ __device__ __forceinline__ void stage_group_2pass(const BinCtx &bc, const int *e
                    rec, list, cnt, cntb, sF, minz);
     }
 }
+
+#if BR_K4L_LAZY
+// Lazily staged faces turned away from the camera: the warp stages the back list entries [i0, i1) of its
+// footprint itself, 32 at a time (lane i: the face's record at tau for this tile, rec_at), and every lane tests
+// them against its pixel with the values broadcast by shuffles -- the same TauRec, the same tests as the staged
+// path (bit-identical), without a CTA barrier.  TIE: the Q7 re-run, comparing (depth, face index).
+template <bool TIE, bool CENSUS>
+__device__ __forceinline__ void lazy_back(const uint16_t *lst, int i0, int i1, const int *ent, const float4 *rseg, int F,
+                                          int *status, float tau, const TileCtx &tc, float ul, float vl, int lane,
+                                          float &zbest, int &eoff, float &tief, int &fbest, bool inimg,
+                                          unsigned long long &c_cov, unsigned long long &c_test)
+{
+    for (int b0 = i0; b0 < i1; b0 += 32) {
+        const int i = b0 + lane;
+        TauRec R;
+        R.a[0] = R.a[1] = R.a[2] = 0.f; R.b[0] = R.b[1] = R.b[2] = 0.f;
+        R.g[0] = R.g[1] = R.g[2] = -1.f;   // no record: never covers
+        R.az = R.bz = R.cz = 0.f;
+        R.fid = 0x7fffffff;
+        int jj = 0;
+        if (i < i1) {
+            jj = lst[i];
+            const int f = (BR_K4L_SENT || BR_K4L_PREF) ? ent[jj] : __ldg(ent + jj);
+            if ((unsigned)f < (unsigned)F) {
+                FaceRec fr;
+                load_rec(rseg + (size_t)f * REC_F4, fr);
+                const float D = __fmaf_rn(tau, __fmaf_rn(tau, fr.q[6].x, fr.q[6].y), fr.q[6].z);
+                if (__float_as_int(fr.q[6].w) >= 0 && fabsf(D) > EPS_D) rec_at(fr, tau, D, tc, R);
+            } else {
+                atomicOr(status, BLUR_ST_EINTERNAL);
+            }
+        }
+        const int cnt = min(32, i1 - b0);
+        for (int sl = 0; sl < cnt; ++sl) {
+            const float a0 = __shfl_sync(0xffffffffu, R.a[0], sl), a1 = __shfl_sync(0xffffffffu, R.a[1], sl);
+            const float a2 = __shfl_sync(0xffffffffu, R.a[2], sl), b0v = __shfl_sync(0xffffffffu, R.b[0], sl);
+            const float b1 = __shfl_sync(0xffffffffu, R.b[1], sl), b2 = __shfl_sync(0xffffffffu, R.b[2], sl);
+            const float g0 = __shfl_sync(0xffffffffu, R.g[0], sl), g1 = __shfl_sync(0xffffffffu, R.g[1], sl);
+            const float g2 = __shfl_sync(0xffffffffu, R.g[2], sl), az = __shfl_sync(0xffffffffu, R.az, sl);
+            const float bz = __shfl_sync(0xffffffffu, R.bz, sl), cz = __shfl_sync(0xffffffffu, R.cz, sl);
+            const int js = __shfl_sync(0xffffffffu, jj, sl);
+            const float e0 = edge_eval(a0, b0v, g0, ul, vl);
+            const float e1 = edge_eval(a1, b1, g1, ul, vl);
+            const float e2 = edge_eval(a2, b2, g2, ul, vl);
+            const float z = __fmaf_rn(az, ul, __fmaf_rn(bz, vl, cz));
+            const float emin = fminf(fminf(e0, e1), e2);
+            if (CENSUS && inimg) { c_test++; c_cov += emin >= 0.f; }
+            if (!TIE) {
+                tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
+                if (emin >= 0.f && z < zbest) { zbest = z; eoff = 0x10000 | js; }
+            } else {
+                const int fs = __shfl_sync(0xffffffffu, R.fid, sl);
+                if (emin >= 0.f && z <= zbest && (z < zbest || fs < fbest)) { zbest = z; eoff = 0x10000 | js; fbest = fs; }
+            }
+        }
+    }
+}
+#endif
 
 template <bool COV, bool CENSUS = false>
 __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float *__restrict__ out, int *__restrict__ ids,
@@ -985,6 +1096,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                     const float ul = uvp.x, vl = uvp.y;
                     float zbest = __int_as_float(0x7f800000), tief = 0.f;
                     int eoff = -1;
+                    bool backs = false;   // BR_K4L_LAZY: the back list was tested (staged by this warp)
 #ifdef BR_K4L_STATS
                     if (lane == 0) {
                         K4L_STAT(t, 24, 1); K4L_STAT(t, 25, cn + cb > 0); K4L_STAT(t, 26, cn); K4L_STAT(t, 28, cb);
@@ -1020,6 +1132,12 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
 #ifdef BR_K4L_STATS
                             if (lane == 0) K4L_STAT(t, 27, cb);
 #endif
+#if BR_K4L_LAZY
+                            backs = true;
+                            int fdum = 0;
+                            lazy_back<false, CENSUS>(lst, n - cb, n, ents, bc.rseg, t.F, t.status, S.taus[l], tc, ul, vl, lane,
+                                                     zbest, eoff, tief, fdum, inimg, c_cov, c_test);
+#else
                             BR_UNROLL4 for (int i = n - cb; i < n; ++i) {
                                 const int off = lst[i];
                                 const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
@@ -1033,6 +1151,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                                 tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
                                 if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
                             }
+#endif
                         }
                     }
                     // coverage loop: end
@@ -1040,7 +1159,14 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                         zbest = __int_as_float(0x7f800000);
                         eoff = -1;
                         int fbest = 0x7fffffff;
+#if BR_K4L_LAZY
+                        // faces turned away tie only if their list was tested (a skipped list is strictly behind)
+                        if (backs) lazy_back<true, false>(lst, n - cb, n, ents, bc.rseg, t.F, t.status, S.taus[l], tc, ul, vl,
+                                                          lane, zbest, eoff, tief, fbest, inimg, c_cov, c_test);
+                        for (int ii = 0; ii < cn; ++ii) {
+#else
                         for (int ii = 0; ii < cn + cb; ++ii) {
+#endif
                             const int off = lst[ii < cn ? ii : n - cb + (ii - cn)];
                             const float4 *rp = reinterpret_cast<const float4 *>(rbase + off);
                             const float4 q0 = rp[0], q1 = rp[1], q2 = rp[2];
@@ -1054,15 +1180,33 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                             }
                         }
                     }
+#if BR_K4L_LAZY
+                    const int ebest = eoff >= 0x10000 ? (eoff & 0xFFFF) : eoff >= 0 ? eoff / (int)sizeof(TauRec) - l * n : -1;
+#else
                     const int ebest = eoff >= 0 ? eoff / (int)sizeof(TauRec) - l * n : -1;
+#endif
                     int fid = -1;
                     if (ebest >= 0) {
                         float pr, pg, pb;
-                        shade(rl[ebest], t.fcol, ul, vl, pr, pg, pb);      // Eq.9
+#if BR_K4L_LAZY
+                        if (eoff >= 0x10000) {   // a face turned away won: its record again (rare)
+                            const int f = (BR_K4L_SENT || BR_K4L_PREF) ? ents[ebest] : __ldg(ents + ebest);
+                            FaceRec fr;
+                            load_rec(bc.rseg + (size_t)f * REC_F4, fr);
+                            const float tau = S.taus[l];
+                            TauRec R;
+                            rec_at(fr, tau, __fmaf_rn(tau, __fmaf_rn(tau, fr.q[6].x, fr.q[6].y), fr.q[6].z), tc, R);
+                            shade(R, t.fcol, ul, vl, pr, pg, pb);      // Eq.9
+                            fid = R.fid;
+                        } else
+#endif
+                        {
+                            shade(rl[ebest], t.fcol, ul, vl, pr, pg, pb);      // Eq.9
+                            fid = rl[ebest].fid;
+                        }
                         float4 a = S.acc[myp];
                         a.x += pr; a.y += pg; a.z += pb; a.w += 1.f;
                         S.acc[myp] = a;
-                        fid = rl[ebest].fid;
                         if (CENSUS && inimg) c_shade++;
                     }
                     if (l == l_ids) ids[pix] = fid;
