@@ -47,6 +47,9 @@ namespace br {
 namespace {
 
 constexpr int SNW = NT / 32;     // warps per CTA
+#ifndef BR_SOFT_CART
+#define BR_SOFT_CART 1   // 1: closest points measured in Cartesian coordinates of F(X) (soft_eval)
+#endif
 #ifndef BR_SREC_F8
 #define BR_SREC_F8 224
 #endif
@@ -255,11 +258,24 @@ __device__ __forceinline__ uint32_t soft_stage(const Tables &t, const float4 *__
     const float r20 = g22 > 0.f ? g12 / g22 : __int_as_float(0x7fffffff);
     const float c1 = l12 > 0.f ? (e1x * e3x + e1y * e3y) / l12 : 0.f;
     const float c2 = l12 > 0.f ? (e2x * e3x + e2y * e3y) / l12 : 0.f;
+#if BR_SOFT_CART
+    // Cartesian form: p' - v0(X) = (p - v0(tau)) + w1 M1 + w2 M2 with M_i = E_i(X) - E_i(tau) (= 0 when tau is the
+    // keyframe X), the closest point of each edge of F(X) by its projection parameter (A17), distances in F(X)
+    (void)r01; (void)r20; (void)c1; (void)c2;
+    const float f1x = xT[1] - xT[0], f1y = yT[1] - yT[0], f2x = xT[2] - xT[0], f2y = yT[2] - yT[0];   // F(tau)
+    out.q[0] = make_float4(A[1] * invD, B[1] * invD, G[1] * invD, A[2] * invD);
+    out.q[1] = make_float4(B[2] * invD, G[2] * invD, __fsub_rn(xT[0], tc.uc), __fsub_rn(yT[0], tc.vc));
+    out.q[2] = make_float4(e1x, e1y, e2x, e2y);
+    out.q[3] = make_float4(e1x - f1x, e1y - f1y, e2x - f2x, e2y - f2y);
+    out.q[4] = make_float4(g11 > 0.f ? 1.0f / g11 : __int_as_float(0x7fffffff), g22 > 0.f ? 1.0f / g22 : __int_as_float(0x7fffffff),
+                           l12 > 0.f ? 1.0f / l12 : __int_as_float(0x7fffffff), 0.f);
+#else
     out.q[0] = make_float4(A[1] * invD, B[1] * invD, G[1] * invD, A[2] * invD);
     out.q[1] = make_float4(B[2] * invD, G[2] * invD, __fsub_rn(xT[0], tc.uc), r01);
     out.q[2] = make_float4(c1, c2, __fsub_rn(yT[0], tc.vc), r20);
     out.q[3] = make_float4(e1x, e1y, e2x, e2y);
     out.q[4] = make_float4(xT[1] - xT[0], yT[1] - yT[0], xT[2] - xT[0], yT[2] - yT[0]);   // F(tau)
+#endif
     return fm;
 }
 
@@ -287,6 +303,49 @@ __device__ __forceinline__ float resid2(float d1, float d2, const float4 &E)
     return __fmaf_rn(rx, rx, ry * ry);
 }
 
+#if BR_SOFT_CART
+// Cartesian closest point (A17-A18) of p' on F(X): p' is formed about v0 as (p - v0(tau)) + w1 M1 + w2 M2, so it
+// is p itself when tau is the keyframe X, and each edge candidate's squared distance is measured directly.  (The
+// barycentric form below measures them through w = F(tau)^-1 p; for a limb sliver -- det F ~ 5e-8 NDC^2 on C5 --
+// w reaches ~1e4, the three edges' candidates lie within 1e-5 NDC of each other and their distances differ by
+// ~5e-4 relative, below that form's fp32 resolution: a C5 view chose another edge than the oracle at tau = 0.)
+__device__ __forceinline__ SoftHit soft_eval(const SoftRec &r, float ul, float vl)
+{
+    const float4 q0 = r.q[0], q1 = r.q[1], q2 = r.q[2], q3 = r.q[3], q4 = r.q[4];
+    const float w1 = __fmaf_rn(q0.x, ul, __fmaf_rn(q0.y, vl, q0.z));   // w(tau), Eq.8
+    const float w2 = __fmaf_rn(q0.w, ul, __fmaf_rn(q1.x, vl, q1.y));
+    const float px = __fsub_rn(ul, q1.z), py = __fsub_rn(vl, q1.w);     // p - v0(tau)
+    const float sx = __fmaf_rn(w1, q3.x, __fmaf_rn(w2, q3.z, px));     // p' - v0(X)
+    const float sy = __fmaf_rn(w1, q3.y, __fmaf_rn(w2, q3.w, py));
+    SoftHit h;
+    // edge v0v1: w^* = (1 - t, t, 0), point t E1
+    float tt = __saturatef(__fmaf_rn(sx, q2.x, sy * q2.y) * q4.x);
+    float dx = __fmaf_rn(-tt, q2.x, sx), dy = __fmaf_rn(-tt, q2.y, sy);
+    float best = __fmaf_rn(dx, dx, dy * dy);
+    h.t = tt; h.e = 0;
+    // edge v1v2: w^* = (0, 1 - t, t), point E1 + t (E2 - E1)
+    const float e3x = q2.z - q2.x, e3y = q2.w - q2.y;
+    const float ox = sx - q2.x, oy = sy - q2.y;
+    tt = __saturatef(__fmaf_rn(ox, e3x, oy * e3y) * q4.z);
+    dx = __fmaf_rn(-tt, e3x, ox); dy = __fmaf_rn(-tt, e3y, oy);
+    float qq = __fmaf_rn(dx, dx, dy * dy);
+    if (qq < best) { best = qq; h.t = tt; h.e = 1; }
+    // edge v2v0: w^* = (t, 0, 1 - t), point E2 - t E2 (parameter from v2, as A17: a zero-length edge is v2, Q19)
+    const float o2x = sx - q2.z, o2y = sy - q2.w;
+    tt = __saturatef(-__fmaf_rn(o2x, q2.z, o2y * q2.w) * q4.y);
+    dx = __fmaf_rn(tt, q2.z, o2x); dy = __fmaf_rn(tt, q2.w, o2y);
+    qq = __fmaf_rn(dx, dx, dy * dy);
+    if (qq < best) { h.t = tt; h.e = 2; }
+    // Eq.14: d = || p - F(tau) w^* ||^2 with F(tau) = F(X) - M
+    const float ws1 = h.e == 0 ? h.t : (h.e == 1 ? 1.f - h.t : 0.f);
+    const float ws2 = h.e == 0 ? 0.f : (h.e == 1 ? h.t : 1.f - h.t);
+    const float f1x = q2.x - q3.x, f1y = q2.y - q3.y, f2x = q2.z - q3.z, f2y = q2.w - q3.w;
+    h.rx = px - __fmaf_rn(ws1, f1x, ws2 * f2x);
+    h.ry = py - __fmaf_rn(ws1, f1y, ws2 * f2y);
+    h.d = __fmaf_rn(h.rx, h.rx, h.ry * h.ry);
+    return h;
+}
+#else
 __device__ __forceinline__ SoftHit soft_eval(const SoftRec &r, float ul, float vl)
 {
     const float4 q0 = r.q[0], q1 = r.q[1], q2 = r.q[2], q3 = r.q[3];
@@ -318,6 +377,7 @@ __device__ __forceinline__ SoftHit soft_eval(const SoftRec &r, float ul, float v
     h.d = __fmaf_rn(h.rx, h.rx, h.ry * h.ry);
     return h;
 }
+#endif
 
 // Stage faces [base, base + nb) of the bin (or sid[] in fallback mode) at the ng sub-frames taus:
 // records rec[l * nb + j], masks wm[(l * SNW + w) * nw + j / 32] (cleared by the caller).
