@@ -44,7 +44,9 @@ HISTORY = """| change (round 2) | fwd ms | bwd ms | step ms | images/s |
 | (tried) K4 super-groups of consecutive chunks (`BLURRAST_FWD=sg`); group caps 192/256/320 pairs | 6.13-6.68 | - | - | - |
 | (tried) K4 next chunk's bin entries prefetched by `cp.async` (`BR_K4L_PREF`) | 6.03 | - | - | - |
 | K6 run moments from per-row prefix sums (two lookups per run) | 5.92 | 2.90 | 9.50 | 1685 |
-| visibility cache written / read evict-first (streaming) | 5.90 | 2.91 | 9.46 | 1691 |"""
+| visibility cache written / read evict-first (streaming) | 5.90 | 2.91 | 9.46 | 1691 |
+| (tried) K4 lazy staging of the faces turned away (`BR_K4L_LAZY`) | 6.44 | - | - | - |
+| soft: Cartesian closest points (C5 sliver parity fix; soft C4 +2%) | 5.90 | 2.91 | 9.42 | 1699 |"""
 
 
 def row(label, d):
@@ -95,7 +97,7 @@ gpurun call on one box) and `tools/profile_r2b.sh` (ncu launch list + `ncu --set
 and K6 = `k6v_raster_bwd` on C4).  Raw files: `r2c_launches_C4.csv` (ncu launch list), `r2c_ncu_details_raster_C4.csv`
 (ncu details of K4 and K6), `traffic.json` (DRAM bytes per launch and warp efficiencies -> `roofline.traffic`,
 `roofline.hbm`, `roofline.warp_efficiency`), `r2c_checked_build.log` (the checked build over the GPU tests),
-`r2c_order_i_vs_ii.md` (K4 evaluation orders).  Earlier sessions: `r2b_summary.md`, `r2_summary.md`; round 1: `r1_summary.md`.
+`r2c_order_i_vs_ii.md` (K4 evaluation orders), `r2c_variants_parity.log` (the A/B forwards over the parity tests).  Earlier sessions: `r2b_summary.md`, `r2_summary.md`; round 1: `r1_summary.md`.
 
 ## Bench lines (1 B200)
 
