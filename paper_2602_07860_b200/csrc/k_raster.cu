@@ -1339,7 +1339,7 @@ struct __align__(16) SGSmem {
     int slot_vis[GMAX_F];
 };
 
-static_assert(BR_K4L_PREF || sizeof(SGSmem) + 1024 <= 228 * 1024 / BR_K4_MINB, "k4s_raster_fwd: BR_K4_MINB CTAs per SM");
+static_assert(BR_K4L_PREF || BR_K4_MINB > 5 || sizeof(SGSmem) + 1024 <= 228 * 1024 / BR_K4_MINB, "k4s_raster_fwd: BR_K4_MINB CTAs per SM");
 
 __device__ __forceinline__ void pair_stage_sg(const FaceRec &fr, int ri, int rb, int n, int L, float tau, float D, int x0,
                                               int x1, int y0, int y1, const TileCtx &tc, TauRec *rec,
