@@ -44,6 +44,9 @@ namespace br {
 #ifndef BR_VIS_STREAM
 #define BR_VIS_STREAM 1   // 1: the visibility cache is written / read with evict-first (streaming) accesses
 #endif
+#ifndef BR_K4L_ONELOAD
+#define BR_K4L_ONELOAD 0   // 1: each staged pair requests its whole record at once
+#endif
 #ifndef BR_K4L_LAZY
 #define BR_K4L_LAZY 0   // 1: faces turned away are staged by a warp only where its footprint's back list is tested
 #endif
@@ -844,6 +847,28 @@ __device__ __forceinline__ void stage_group_list(const BinCtx &bc, const int *en
         const bool okb = p1 < npair && pair_head(bc, ent, p1, inv_ng, ng, taus, tc, W, H, F, jb, lb, rb, Db, xb0, xb1, yb0, yb1);
         if (oka) pair_stage(ra, ja, la, n, taus[la], Da, xa0, xa1, ya0, ya1, tc, rec, list, cnt, cntb, sF, minz);
         if (okb) pair_stage(rb, jb, lb, n, taus[lb], Db, xb0, xb1, yb0, yb1, tc, rec, list, cnt, cntb, sF, minz);
+    }
+#elif BR_K4L_ONELOAD
+    // the whole record requested at once (one L2 round trip after the bin entry instead of two), also for the
+    // pairs the box test then rejects
+    for (int p = threadIdx.x; p < npair; p += NT) {
+        const int j = div_small(p, inv_ng), l = p - j * ng;
+        const int f = (BR_K4L_SENT || BR_K4L_PREF) ? ent[j] : __ldg(ent + j);
+        if ((unsigned)f >= (unsigned)F) {
+            atomicOr(bc.status, BLUR_ST_EINTERNAL);
+            continue;
+        }
+        FaceRec fr;
+        load_rec(bc.rseg + (size_t)f * REC_F4, fr);
+        if (__float_as_int(fr.q[6].w) < 0) continue;                   // skipped face (Q8, behind, bad index)
+        const float tau = taus[l];
+        const float D = __fmaf_rn(tau, __fmaf_rn(tau, fr.q[6].x, fr.q[6].y), fr.q[6].z);
+        if (!(fabsf(D) > EPS_D)) continue;
+        int x0, x1, y0, y1;
+        if (!tile_pixels(box_lerp(tau, fr.q[7].x, fr.q[8].x), box_lerp(tau, fr.q[7].y, fr.q[8].y),
+                         box_lerp(tau, fr.q[7].z, fr.q[8].z), box_lerp(tau, fr.q[7].w, fr.q[8].w), W, H, tc, x0, x1, y0, y1))
+            continue;
+        pair_stage_fr(fr, j, l, n, tau, D, x0, x1, y0, y1, tc, rec, list, cnt, cntb, sF, minz, nstage);
     }
 #else
     for (int p = threadIdx.x; p < npair; p += NT) {
