@@ -6,6 +6,7 @@ All arithmetic runs in libblurrast's CUDA kernels; torch only provides device me
 """
 from __future__ import annotations
 
+import os
 from typing import Optional
 
 import numpy as np
@@ -50,7 +51,7 @@ class BlurRenderer:
 
     # BLUR_CACHE_VISIBILITY budget: the per-(pixel, sub-frame) winner index (2 B, +4 B of soft products)
     # is kept between the forward and the backward only when it fits (C4: 0.84 GB; C5: 34 GB -> off)
-    CACHE_BUDGET_BYTES = 1 << 30
+    CACHE_BUDGET_BYTES = int(os.environ.get("BLURRAST_CACHE_BUDGET_MB", "1024")) << 20
     # ... except that a single image always keeps it up to CACHE_IMAGE_BYTES (C5 with soft coverage: 1.6 GB
     # per image; without it K9 runs its two-pass product recompute: 3.5x slower on C5)
     CACHE_IMAGE_BYTES = 2 << 30
