@@ -2598,6 +2598,37 @@ __device__ __forceinline__ void add_moments(int *m, int4 q, int dx, int dy)
     atomicAdd(m + 9, 1);
 }
 
+#ifndef BR_FX_RUNS
+#define BR_FX_RUNS 1   // 1: a warp's 8-pixel row runs of equal winners add their moments once (prefix differences)
+#endif
+// Run-aggregated form of add_moments for a whole warp (8x4 footprint, lanes 8r..8r+7 = one 8-pixel row):
+// each run of equal keys (the winner's slot, -1 none) in a row adds its sums once, from the lanes' inclusive
+// row prefixes P of q and q dx (built once per tile); q dy = dy x sum q (one row).  The same integers as the
+// per-pixel atomics (exact, order-independent).  All 32 lanes must call it.
+__device__ __forceinline__ void run_moments(int *imom, int key, int lane, const int P[6], int dy)
+{
+    const int c = lane & 7;
+    const int kp = __shfl_up_sync(0xffffffffu, key, 1), kn = __shfl_down_sync(0xffffffffu, key, 1);
+    const bool st = c == 0 || kp != key, en = c == 7 || kn != key;
+    const unsigned sm = __ballot_sync(0xffffffffu, st);
+    const int s = 31 - __clz(sm & (0xffffffffu >> (31 - lane)));   // first lane of this lane's run
+    const int src = (s & 7) ? s - 1 : s;
+    int b[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        b[i] = __shfl_sync(0xffffffffu, P[i], src);
+        if ((s & 7) == 0) b[i] = 0;
+    }
+    if (en && key >= 0) {
+        int *m = imom + 10 * key;
+        const int m0 = P[0] - b[0], m1 = P[1] - b[1], m2 = P[2] - b[2];
+        atomicAdd(m + 0, m0); atomicAdd(m + 1, m1); atomicAdd(m + 2, m2);
+        atomicAdd(m + 3, P[3] - b[3]); atomicAdd(m + 4, P[4] - b[4]); atomicAdd(m + 5, P[5] - b[5]);
+        atomicAdd(m + 6, m0 * dy); atomicAdd(m + 7, m1 * dy); atomicAdd(m + 8, m2 * dy);
+        atomicAdd(m + 9, lane - s + 1);
+    }
+}
+
 // read, clear and convert the fixed-point moments of one record (returns the won count)
 __device__ __forceinline__ int take_moments(int *m, float inv, float sx, float sy, float f[9])
 {
@@ -2675,6 +2706,20 @@ __device__ __forceinline__ void k6_fx_tile(const Tables &t, const float *__restr
     const float scale = ldexpf(1.0f, 19 - ex), inv_scale = ldexpf(1.0f, ex - 19);
     S.qg[myp] = make_int4(__float2int_rn(g.x * scale), __float2int_rn(g.y * scale), __float2int_rn(g.z * scale), 0);
     const int dx = lx - TW / 2, dy = TH / 2 - ly;
+#if BR_FX_RUNS
+    int P[6];   // inclusive prefixes over this lane's 8-pixel row segment of q and q dx (run_moments)
+    {
+        const int4 q0 = S.qg[myp];
+        P[0] = q0.x; P[1] = q0.y; P[2] = q0.z; P[3] = q0.x * dx; P[4] = q0.y * dx; P[5] = q0.z * dx;
+#pragma unroll
+        for (int d = 1; d < 8; d <<= 1)
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                const int y = __shfl_up_sync(0xffffffffu, P[i], d, 8);
+                if ((lane & 7) >= d) P[i] += y;
+            }
+    }
+#endif
     unsigned long long d0 = 0, d1 = 0, d2 = 0;
     for (int j = threadIdx.x; j < SREC_B; j += NT) S.won[j] = 0xFFFFFFFFu;
     unsigned int stamp = 0;   // group counter of the cached path (won flags)
@@ -2775,7 +2820,11 @@ __device__ __forceinline__ void k6_fx_tile(const Tables &t, const float *__restr
                         vis_mask<false, MODE>(S.rec + l * n, S.vtx + 3 * l * n, wml, nw, 0, ul, vl, zbest, ebest, fbest,
                                               d0, d1, false);
                     }
+#if BR_FX_RUNS
+                    run_moments(&S.imom[0][0], (inimg && ebest >= 0) ? l * n + ebest : -1, lane, P, dy);
+#else
                     if (inimg && ebest >= 0) add_moments(S.imom[l * n + ebest], q, dx, dy);
+#endif
                 }
                 __syncthreads();
                 for (int j = threadIdx.x; j < n; j += NT) {   // one thread per bin slot
