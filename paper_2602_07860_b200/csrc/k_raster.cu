@@ -69,7 +69,7 @@ __device__ __forceinline__ int fp_of(int warp, int lane) { return BR_HALF ? warp
 #define BR_SREC_F 448
 #endif
 #ifndef BR_SREC_B
-#define BR_SREC_B 256
+#define BR_SREC_B 384   // (256 -> 384: C5 step 378.8 -> 375.1 ms, C4 K6 2.91 -> 2.88 ms)
 #endif
 #ifndef BR_GMAX_F
 #define BR_GMAX_F 16
@@ -2892,7 +2892,11 @@ __device__ __forceinline__ void k6_fx_tile(const Tables &t, const float *__restr
                     __syncthreads();
                     stage_group<false, MODE, true>(bc, nb, base, S.taus, 1, tc, t.W, t.H, t.F, S.sid, S.rec, S.vtx, S.wm, d2);
                     __syncthreads();
+#if BR_FX_RUNS
+                    run_moments(&S.imom[0][0], (ebest >= base && ebest < base + nb) ? ebest - base : -1, lane, P, dy);
+#else
                     if (ebest >= base && ebest < base + nb) add_moments(S.imom[ebest - base], S.qg[myp], dx, dy);
+#endif
                     __syncthreads();
                     for (int j = threadIdx.x; j < nb; j += NT) {
                         float m[9];
