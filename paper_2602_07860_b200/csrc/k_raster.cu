@@ -53,6 +53,9 @@ namespace br {
 #ifndef BR_K4L_GRP
 #define BR_K4L_GRP BR_SREC_F   // (face, sub-frame) pairs per k4l group at most (one sub-frame at least)
 #endif
+#ifndef BR_STAGE_EARLY
+#define BR_STAGE_EARLY 0   // 1: stage_tau writes the record before the footprint masks
+#endif
 #ifndef BR_K4L_MICRO
 #define BR_K4L_MICRO 1   // 1: one-instruction warp max of the winners' depths, __frcp_rn for 1/|D|
 #endif
@@ -140,6 +143,24 @@ __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, floa
         B[i] = be * sg;
         G[i] = gp * sg;
     }
+#if BR_STAGE_EARLY
+    {   // the record first (its slot is this pair's own; unused when no footprint is reached): the record's
+        // registers die before the footprint masks need theirs (fewer spills under the 48-register cap)
+        const float4 z0 = fr.q[9], z1 = fr.q[10];
+        const float za = __fmaf_rn(tau, z1.x - z0.x, z0.x);
+        const float zb = __fmaf_rn(tau, z1.y - z0.y, z0.y);
+        const float zc = __fmaf_rn(tau, z1.z - z0.z, z0.z);
+        out.a[0] = A[0]; out.a[1] = A[1]; out.a[2] = A[2];
+        out.b[0] = B[0]; out.b[1] = B[1]; out.b[2] = B[2];
+        out.g[0] = G[0]; out.g[1] = G[1]; out.g[2] = G[2];
+        const float dzb = zb - za, dzc = zc - za;
+        out.az = __fmaf_rn(A[1], dzb, A[2] * dzc) * invD;
+        out.bz = __fmaf_rn(B[1], dzb, B[2] * dzc) * invD;
+        out.cz = __fmaf_rn(__fmaf_rn(G[1], dzb, G[2] * dzc), invD, za);
+        out.invD = invD;
+        out.fid = __float_as_int(q6.w);
+    }
+#endif
     // culling footprints (FPW x 4) reached by the box and the three edge half-planes; the
     // rounding allowance is bounded once over the whole tile (|ul|, |vl| <= 8 pixels)
     float tol[3];
@@ -210,7 +231,7 @@ __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, floa
                 fm |= 1u << (wy * (TW / FPW) + wx0 + c);
     }
     }
-    if (!fm) return 0u;
+    if (!fm || BR_STAGE_EARLY) return fm;
     const float4 z0 = fr.q[9], z1 = fr.q[10];
     const float za = __fmaf_rn(tau, z1.x - z0.x, z0.x);
     const float zb = __fmaf_rn(tau, z1.y - z0.y, z0.y);
