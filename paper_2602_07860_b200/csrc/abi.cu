@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: ranges cost a branch unless a tool (nsys, ncu --nvtx) attaches
+
 #include "internal.cuh"
 #include "../../include/blurrast.h"
 
@@ -25,6 +27,15 @@ using namespace br;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range over a scope: the ABI calls and their phases (setup, binning, raster, soft, vertex chain) show up
+// by name on a profiler timeline (`ncu --nvtx --nvtx-include "blur_render_fwd/"`)
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx &) = delete;
+    Nvtx &operator=(const Nvtx &) = delete;
+};
 
 int fail(int code, const std::string &msg)
 {
@@ -476,9 +487,13 @@ int prepare(const float *verts, int V, const int32_t *faces, int F, const float 
         r = upload_tables(P, ws, st);
         if (r) return r;
     }
-    r = cuda_check(launch_setup(t, verts, faces, colors, P.maxS, st), "setup kernels");
-    if (r) return r;
+    {
+        Nvtx n("K1-K2 setup");
+        r = cuda_check(launch_setup(t, verts, faces, colors, P.maxS, st), "setup kernels");
+        if (r) return r;
+    }
     // (the soft bins are built after K4: their sort skips the tiles K4 found fully covered)
+    Nvtx n("K3 binning");
     return cuda_check(launch_binning(t, hard_bins(t), 0.f, st), "binning kernels");
 }
 
@@ -510,6 +525,7 @@ int blur_render_fwd(const float *verts, int V, const int32_t *faces, int F, cons
                     const int32_t *sub_range, float *out_rgba, int32_t *ids, int ids_subframe,
                     const blur_config *cfg, void *ws, size_t ws_bytes, blur_stream_t stream)
 {
+    Nvtx range("blur_render_fwd");
     g_err.clear();
     cudaStream_t st = (cudaStream_t)stream;
     if (B > 0 && !cams) return fail(BLUR_EINVAL, "cams is NULL");
@@ -519,14 +535,18 @@ int blur_render_fwd(const float *verts, int V, const int32_t *faces, int F, cons
     int r = prepare(verts, V, faces, F, colors, motions, cams, B, H, W, sub_range, cfg, ws, ws_bytes, st, true, P, t);
     if (r) return r;
     if (cfg && cfg->raster_events[0]) cudaEventRecord((cudaEvent_t)cfg->raster_events[0], st);
-    r = cuda_check(launch_raster_fwd(t, out_rgba, ids, ids_subframe, cfg ? cfg->census : nullptr, st), "raster fwd");
-    if (r) return r;
+    {
+        Nvtx n("K4 raster fwd");
+        r = cuda_check(launch_raster_fwd(t, out_rgba, ids, ids_subframe, cfg ? cfg->census : nullptr, st), "raster fwd");
+        if (r) return r;
+    }
     if (P.splits > 1) {
         r = cuda_check(launch_split_reduce(t, out_rgba, st), "split reduce");
         if (r) return r;
     }
     if (cfg && cfg->raster_events[1]) cudaEventRecord((cudaEvent_t)cfg->raster_events[1], st);
     if (P.soft) {   // NEXT-1: background alpha of the uncovered (pixel, sub-frame) pairs K4 recorded
+        Nvtx n("K8 soft fwd");
         r = cuda_check(launch_binning(t, t.sb, P.rcut, st), "soft binning kernels");
         if (r) return r;
         if (cfg->soft_events[0]) cudaEventRecord((cudaEvent_t)cfg->soft_events[0], st);
@@ -543,6 +563,7 @@ int blur_render_bwd(const float *verts, int V, const int32_t *faces, int F, cons
                     const int32_t *sub_range, const float *grad_rgba, float *grad_verts, float *grad_colors,
                     const blur_config *cfg, void *ws, size_t ws_bytes, blur_stream_t stream)
 {
+    Nvtx range("blur_render_bwd");
     g_err.clear();
     cudaStream_t st = (cudaStream_t)stream;
     if (B > 0 && !cams) return fail(BLUR_EINVAL, "cams is NULL");
@@ -572,15 +593,20 @@ int blur_render_bwd(const float *verts, int V, const int32_t *faces, int F, cons
         if (r) return r;
     }
     if (cfg && cfg->raster_events[0]) cudaEventRecord((cudaEvent_t)cfg->raster_events[0], st);
-    r = cuda_check(launch_raster_bwd(t, grad_rgba, grad_colors, st), "raster bwd");
-    if (r) return r;
+    {
+        Nvtx n("K6 raster bwd");
+        r = cuda_check(launch_raster_bwd(t, grad_rgba, grad_colors, st), "raster bwd");
+        if (r) return r;
+    }
     if (cfg && cfg->raster_events[1]) cudaEventRecord((cudaEvent_t)cfg->raster_events[1], st);
     if (P.soft) {
+        Nvtx n("K9 soft bwd");
         if (cfg->soft_events[0]) cudaEventRecord((cudaEvent_t)cfg->soft_events[0], st);
         r = cuda_check(launch_soft_bwd(t, grad_rgba, st), "soft bwd");
         if (r) return r;
         if (cfg->soft_events[1]) cudaEventRecord((cudaEvent_t)cfg->soft_events[1], st);
     }
+    Nvtx n("K7 vertex chain");
     r = cuda_check(launch_vertex_chain(t, grad_verts, st), "vertex chain");
     if (r) return r;
     if (check_env()) return sync_status(ws, P, st);
@@ -590,6 +616,7 @@ int blur_render_bwd(const float *verts, int V, const int32_t *faces, int F, cons
 int blur_l2_loss_grad(const float *out, const float *target, int64_t n, int64_t n_norm, float *loss, float *grad,
                       blur_stream_t stream)
 {
+    Nvtx range("blur_l2_loss_grad");
     g_err.clear();
     if (n < 0) return fail(BLUR_EINVAL, "n < 0");
     if (!loss || (n > 0 && (!out || !target || !grad))) return fail(BLUR_EINVAL, "NULL pointer");
