@@ -696,6 +696,11 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
 #else
 #define BR_UNROLL4
 #endif
+#ifndef BR_K4L_TPREF
+#define BR_K4L_TPREF 0   // 1: the next chunk's header / bin offsets and the next group's taus are requested one phase
+                         // ahead (registers), so that no global load sits between two barriers (measured: C4 K4
+                         // 5.86 -> 5.96 ms, 16 B more spill loads; parity-green)
+#endif
 #ifndef BR_K4L_CULL
 #define BR_K4L_CULL 2   // 2: faces turned away from the camera in a second list per footprint, tested last, the whole
                         // list skipped when every pixel's winner is nearer than the list's lowest depth; 0: one list
@@ -1060,11 +1065,37 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
     const float sF = orient > 0.0 ? 1.f : orient < 0.0 ? -1.f : 0.f;
     int pref_c = -1;   // chunk whose bin entries were prefetched into S.pent (BR_K4L_PREF)
 
+#if BR_K4L_TPREF
+    // software pipeline over the chunks: chunk c + splits's header and bin offsets are loaded at the top of
+    // chunk c; the taus of the next group are loaded after the stage and stored to S.taus after the tests
+    int tau_k = -1;   // S.taus holds the taus of sub-frames tau_k.. (when >= 0)
+    Chunk chn;
+    long long on = 0, on1 = 0;
+    if (c_begin + (int)blockIdx.z < c_end) {
+        const int c0 = c_begin + (int)blockIdx.z;
+        chn = t.chunks[c0];
+        on = t.off[(size_t)c0 * t.T + tile];
+        on1 = t.off[(size_t)c0 * t.T + tile + 1];
+    }
+#endif
     for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
+#if BR_K4L_TPREF
+        const Chunk ch = chn;
+        const long long o = on;
+        const int n = (int)(on1 - on);
+        const bool has_next = c + t.splits < c_end;
+        if (has_next) {
+            const size_t bi2 = (size_t)(c + t.splits) * t.T + tile;
+            chn = t.chunks[c + t.splits];
+            on = t.off[bi2];
+            on1 = t.off[bi2 + 1];
+        }
+#else
         const Chunk ch = t.chunks[c];
         const size_t bi = (size_t)c * t.T + tile;
         const long long o = t.off[bi];
         const int n = (int)(t.off[bi + 1] - o);
+#endif
         if (n == 0) {
             if (ids && inimg && ids_k >= ch.k0 && ids_k < ch.k1) ids[pix] = -1;
             if (COV) {
@@ -1096,7 +1127,11 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
 #endif
             for (int kg = ch.k0; kg < ch.k1; kg += Gs) {
                 const int ng = min(Gs, ch.k1 - kg);
+#if BR_K4L_TPREF
+                if (tau_k != kg && threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
+#else
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
+#endif
 #if BR_K4L_PREF
                 __pipeline_wait_prior(0);   // this thread's prefetched entries have landed
 #endif
@@ -1110,6 +1145,14 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
 #endif
                 __syncthreads();
                 if (threadIdx.x == 0) { K4L_STAT(t, 20, n * ng); K4L_STAT(t, 29, 1); }
+#if BR_K4L_TPREF && !BR_K4L_LAZY
+                // the next group's taus (this chunk's next group, else the next chunk's first), requested now and
+                // stored after the tests (the tests do not read S.taus); taus past the image's N are not read
+                const int k_nx = kg + Gs < ch.k1 ? kg + Gs : (has_next ? chn.k0 : -1);
+                float tau_nx = 0.f;
+                if (k_nx >= 0 && threadIdx.x < GMAX_F && k_nx + (int)threadIdx.x < N)
+                    tau_nx = t.sched_tau[sched_off + k_nx + threadIdx.x];
+#endif
 #if BR_K4L_PREF
                 if (kg + Gs >= ch.k1) {   // last group of the chunk: bring the next chunk's bin entries in during the tests
                     pref_c = -1;
@@ -1269,6 +1312,10 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                         if (lane == 0) t.covbits[cov_word(t, im, kg + l, tile) + warp] = m;
                     }
                 }
+#if BR_K4L_TPREF && !BR_K4L_LAZY
+                if (k_nx >= 0 && threadIdx.x < GMAX_F) S.taus[threadIdx.x] = tau_nx;
+                tau_k = k_nx;
+#endif
                 __syncthreads();   // lists read: clear the counters of this group
                 if (threadIdx.x < ng * NFP) {
                     (&S.u.g.cnt[0][0])[threadIdx.x] = 0; (&S.u.g.cntb[0][0])[threadIdx.x] = 0;
@@ -1278,6 +1325,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
             }
         } else {
             // per sub-frame, several batches (long bins) or the exact fallback scan (overflow): as k4_raster_fwd
+#if BR_K4L_TPREF
+            tau_k = -1;   // S.taus[0] is rewritten here
+#endif
             for (int k = ch.k0; k < ch.k1; ++k) {
                 const float tau = t.sched_tau[sched_off + k];
                 float zbest = __int_as_float(0x7f800000);
