@@ -80,6 +80,15 @@ def test_workspace_query_and_validation(lib):
     with pytest.raises(_lib.BlurError) as e:
         _lib.blur_workspace_bytes(sc.V, sc.F, sc.B, 64, 64, m, c, cfg=_lib.make_config(delta=1e-4, solver=2))
     assert "solver" in str(e.value)
+    # K3 launches one grid row per chunk (gridDim.y <= 65535): more chunks are refused up front
+    many = {k: v.copy() for k, v in sc.motion.items()}
+    many["n_sub"][0] = 65536
+    one = _lib.make_config(max_chunk=1)
+    with pytest.raises(_lib.BlurError) as e:
+        _lib.blur_workspace_bytes(sc.V, sc.F, 1, 64, 64, _lib.make_motions(many), c, cfg=one)
+    assert "65535" in str(e.value)
+    many["n_sub"][0] = 65535   # the largest batch of one-sub-frame chunks is accepted
+    assert _lib.blur_workspace_bytes(sc.V, sc.F, 1, 64, 64, _lib.make_motions(many), c, cfg=one) > 0
 
 
 def test_product_path_has_no_oracle_or_cpu_fallback():
