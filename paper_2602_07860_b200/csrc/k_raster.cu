@@ -701,6 +701,11 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                          // ahead (registers), so that no global load sits between two barriers (measured: C4 K4
                          // 5.86 -> 5.96 ms, 16 B more spill loads; parity-green)
 #endif
+#ifndef BR_K4L_NWIN
+#define BR_K4L_NWIN 0   // 1: the bin sizes of the CTA's next 32 chunks are loaded at once (lane j: chunk j), so that
+                        // empty bins cost no L2 round trip each (measured: C4 K4 5.86 -> 5.95 ms, C3 1.25 -> 1.26;
+                        // parity-green: the empty-bin round trips are hidden by the other CTAs of the SM)
+#endif
 #ifndef BR_K4L_CULL
 #define BR_K4L_CULL 2   // 2: faces turned away from the camera in a second list per footprint, tested last, the whole
                         // list skipped when every pixel's winner is nearer than the list's lowest depth; 0: one list
@@ -1078,8 +1083,27 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
         on1 = t.off[(size_t)c0 * t.T + tile + 1];
     }
 #endif
+#if BR_K4L_NWIN && !BR_K4L_TPREF
+    int nwin = 0;   // lane j: the bin size of the CTA's chunk (window start + j)
+    for (int c = c_begin + (int)blockIdx.z, jc = 0; c < c_end; c += t.splits, ++jc) {
+        if ((jc & 31) == 0) {
+            const int cc = c + lane * t.splits;
+            nwin = 0;
+            if (cc < c_end) {
+                const size_t b2 = (size_t)cc * t.T + tile;
+                nwin = (int)(t.off[b2 + 1] - t.off[b2]);
+            }
+        }
+        const int n = __shfl_sync(0xffffffffu, nwin, jc & 31);
+        if (n == 0 && !ids && !COV) continue;   // nothing to render or record for this chunk
+        const Chunk ch = t.chunks[c];
+        const size_t bi = (size_t)c * t.T + tile;
+        const long long o = t.off[bi];
+#else
     for (int c = c_begin + (int)blockIdx.z; c < c_end; c += t.splits) {
-#if BR_K4L_TPREF
+#endif
+#if BR_K4L_NWIN && !BR_K4L_TPREF
+#elif BR_K4L_TPREF
         const Chunk ch = chn;
         const long long o = on;
         const int n = (int)(on1 - on);
