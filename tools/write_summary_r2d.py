@@ -98,7 +98,7 @@ Generated by `tools/write_summary_r2d.py` from `tools/baseline_table.sh` (one be
 gpurun call on one box) and `tools/profile_tag.sh (TAG=r2d)` (ncu launch list + `ncu --set full` of K4 = `k4l_raster_fwd`
 and K6 = `k6v_raster_bwd` on C4).  Raw files: `r2d_launches_C4.csv` (ncu launch list), `r2d_ncu_details_raster_C4.csv`
 (ncu details of K4 and K6), `traffic.json` (DRAM bytes per launch and warp efficiencies -> `roofline.traffic`,
-`roofline.hbm`, `roofline.warp_efficiency`), `r2c_checked_build.log` (the checked build over the GPU tests),
+`roofline.hbm`, `roofline.warp_efficiency`), `r2d_checked_build.log` (the checked build over the GPU tests, final code; `r2c_checked_build.log` the third session's),
 `r2c_order_i_vs_ii.md` (K4 evaluation orders), `r2c_variants_parity.log` (the A/B forwards over the parity tests), `r2d_gpu_tests.log` (this session's `pytest -m gpu` + smoke on the final code).  Earlier sessions: `r2c_summary.md`, `r2b_summary.md`, `r2_summary.md`; round 1: `r1_summary.md`.
 
 ## Bench lines (1 B200)
