@@ -706,6 +706,11 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                         // empty bins cost no L2 round trip each (measured: C4 K4 5.86 -> 5.95 ms, C3 1.25 -> 1.26;
                         // parity-green: the empty-bin round trips are hidden by the other CTAs of the SM)
 #endif
+#ifndef BR_K4L_EKEEP
+#define BR_K4L_EKEEP 1   // 1: the coverage loop keeps the winner's three edge values, so that shading reads only its
+                         // invD and face id from shared memory (the a, b, g words were ~25% of K4's shared wavefronts,
+                         // half of them bank conflicts between the lanes' different winners)
+#endif
 #ifndef BR_K4L_CULL
 #define BR_K4L_CULL 2   // 2: faces turned away from the camera in a second list per footprint, tested last, the whole
                         // list skipped when every pixel's winner is nearer than the list's lowest depth; 0: one list
@@ -1210,6 +1215,12 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                     float zbest = __int_as_float(0x7f800000), tief = 0.f;
                     int eoff = -1;
                     bool backs = false;   // BR_K4L_LAZY: the back list was tested (staged by this warp)
+#if BR_K4L_EKEEP && !BR_K4L_LAZY
+                    float ew0 = 0.f, ew1 = 0.f, ew2 = 0.f;   // the winner's edge values at this pixel
+#define EKEEP_SET(a, b, c) (ew0 = (a), ew1 = (b), ew2 = (c))
+#else
+#define EKEEP_SET(a, b, c) ((void)0)
+#endif
 #ifdef BR_K4L_STATS
                     if (lane == 0) {
                         K4L_STAT(t, 24, 1); K4L_STAT(t, 25, cn + cb > 0); K4L_STAT(t, 26, cn); K4L_STAT(t, 28, cb);
@@ -1227,7 +1238,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                         const float emin = fminf(fminf(e0, e1), e2);
                         if (CENSUS && inimg) { c_test++; c_cov += emin >= 0.f; }
                         tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
-                        if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
+                        if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; EKEEP_SET(e0, e1, e2); }
                     }
                     if (BR_K4L_CULL == 2 && cb) {   // the others, unless all of them are behind every pixel's winner
 #if BR_K4L_MICRO
@@ -1262,7 +1273,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                                 const float emin = fminf(fminf(e0, e1), e2);
                                 if (CENSUS && inimg) { c_test++; c_cov += emin >= 0.f; }
                                 tief = (emin >= 0.f && z == zbest) ? 1.f : tief;
-                                if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; }
+                                if (emin >= 0.f && z < zbest) { zbest = z; eoff = off; EKEEP_SET(e0, e1, e2); }
                             }
 #endif
                         }
@@ -1289,7 +1300,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                             const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
                             if (fminf(fminf(e0, e1), e2) >= 0.f && z <= zbest) {
                                 const int fj = reinterpret_cast<const TauRec *>(rbase + off)->fid;
-                                if (z < zbest || fj < fbest) { zbest = z; eoff = off; fbest = fj; }
+                                if (z < zbest || fj < fbest) { zbest = z; eoff = off; fbest = fj; EKEEP_SET(e0, e1, e2); }
                             }
                         }
                     }
@@ -1314,8 +1325,21 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                         } else
 #endif
                         {
+#if BR_K4L_EKEEP && !BR_K4L_LAZY
+                            // Eq.9 with the winner's edge values from the tests: w_i = e_i / |D|, the same
+                            // arithmetic as shade() (edge_eval(a_i, b_i, g_i) * invD)
+                            const float2 idf = *reinterpret_cast<const float2 *>(&rl[ebest].invD);   // invD, fid
+                            fid = __float_as_int(idf.y);
+                            const float w0 = ew0 * idf.x, w1 = ew1 * idf.x, w2 = ew2 * idf.x;
+                            const float4 *fc = t.fcol + 3 * (size_t)fid;
+                            const float4 c0 = __ldg(fc), c1 = __ldg(fc + 1), c2 = __ldg(fc + 2);
+                            pr = __fmaf_rn(w0, c0.x, __fmaf_rn(w1, c0.w, w2 * c1.z));
+                            pg = __fmaf_rn(w0, c0.y, __fmaf_rn(w1, c1.x, w2 * c1.w));
+                            pb = __fmaf_rn(w0, c0.z, __fmaf_rn(w1, c1.y, w2 * c2.x));
+#else
                             shade(rl[ebest], t.fcol, ul, vl, pr, pg, pb);      // Eq.9
                             fid = rl[ebest].fid;
+#endif
                         }
                         float4 a = S.acc[myp];
                         a.x += pr; a.y += pg; a.z += pb; a.w += 1.f;
@@ -1347,6 +1371,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                 }
                 if (threadIdx.x == 0) S.u.g.nacc = 0;
             }
+#undef EKEEP_SET
         } else {
             // per sub-frame, several batches (long bins) or the exact fallback scan (overflow): as k4_raster_fwd
 #if BR_K4L_TPREF
