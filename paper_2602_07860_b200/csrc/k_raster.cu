@@ -126,10 +126,12 @@ __device__ __forceinline__ bool rect_reaches(const float A[3], const float B[3],
 // Evaluate a record at tau for this tile -> TauRec + the mask of warp footprints it can reach
 // (bit w = culling footprint w, see FPW; 0 = the face cannot cover any pixel of the tile at tau).
 // D = det F(tau) (|D| > EPS_D) and the face's pixel box in the tile come from the caller's rejects.
-template <bool GRID, bool BOXONLY = false>
+template <bool GRID, bool BOXONLY = false, bool R48 = false>
 __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, float D, int x0, int x1, int y0, int y1,
-                                              const TileCtx &tc, TauRec &out)
+                                              const TileCtx &tc, TauRec &out, float4 *d48 = nullptr,
+                                              float2 *x48 = nullptr)
 {
+    // R48: the record goes to d48[0..2] (TauRec's first 48 bytes, in its order) and (invD, face) to *x48; out unused
     const float4 q6 = fr.q[6];
     const float sg = D < 0.f ? -1.f : 1.f;
     const float invD = BR_K4L_MICRO ? __frcp_rn(fabsf(D)) : 1.0f / fabsf(D);   // the same correctly rounded value
@@ -236,13 +238,25 @@ __device__ __forceinline__ uint32_t stage_tau(const FaceRec &fr, float tau, floa
     const float za = __fmaf_rn(tau, z1.x - z0.x, z0.x);
     const float zb = __fmaf_rn(tau, z1.y - z0.y, z0.y);
     const float zc = __fmaf_rn(tau, z1.z - z0.z, z0.z);
-    out.a[0] = A[0]; out.a[1] = A[1]; out.a[2] = A[2];
-    out.b[0] = B[0]; out.b[1] = B[1]; out.b[2] = B[2];
-    out.g[0] = G[0]; out.g[1] = G[1]; out.g[2] = G[2];
+    if (!R48) {
+        out.a[0] = A[0]; out.a[1] = A[1]; out.a[2] = A[2];
+        out.b[0] = B[0]; out.b[1] = B[1]; out.b[2] = B[2];
+        out.g[0] = G[0]; out.g[1] = G[1]; out.g[2] = G[2];
+    }
     // depth interpolated with the screen-space weights (Q6): z(p) = sum_i w_i(p) z_i, written as
     // z0 + w1 (z1 - z0) + w2 (z2 - z0).  Same plane when sum_i w_i = 1; in fp32 the weights of a
     // sliver face sum to 1 +- 1e-4, and this form keeps that error off the absolute depth.
     const float dzb = zb - za, dzc = zc - za;
+    if (R48) {
+        const float az = __fmaf_rn(A[1], dzb, A[2] * dzc) * invD;
+        const float bz = __fmaf_rn(B[1], dzb, B[2] * dzc) * invD;
+        const float cz = __fmaf_rn(__fmaf_rn(G[1], dzb, G[2] * dzc), invD, za);
+        d48[0] = make_float4(A[0], A[1], A[2], B[0]);
+        d48[1] = make_float4(B[1], B[2], G[0], G[1]);
+        d48[2] = make_float4(G[2], az, bz, cz);
+        *x48 = make_float2(invD, q6.w);
+        return fm;
+    }
     out.az = __fmaf_rn(A[1], dzb, A[2] * dzc) * invD;
     out.bz = __fmaf_rn(B[1], dzb, B[2] * dzc) * invD;
     out.cz = __fmaf_rn(__fmaf_rn(G[1], dzb, G[2] * dzc), invD, za);
@@ -711,6 +725,11 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                          // invD and face id from shared memory (the a, b, g words were ~25% of K4's shared wavefronts,
                          // half of them bank conflicts between the lanes' different winners)
 #endif
+#ifndef BR_K4L_R48
+#define BR_K4L_R48 1   // 1: the grouped stage holds 48-B records (the 12 words the tests read) and a separate (invD, face)
+                       // pair per slot: a 48-B stride spreads 8 consecutive slots over all 32 banks, so the stage's
+                       // record stores are conflict-free (64-B records: 4-way conflicts, ~11% of K4's shared wavefronts)
+#endif
 #ifndef BR_K4L_CULL
 #define BR_K4L_CULL 2   // 2: faces turned away from the camera in a second list per footprint, tested last, the whole
                         // list skipped when every pixel's winner is nearer than the list's lowest depth; 0: one list
@@ -750,6 +769,17 @@ struct __align__(16) LeanSmem {
     int pent[BR_K4L_PREF ? SREC_F : 1];         // the next chunk's bin entries, prefetched by cp.async
 };
 static_assert(SREC_F * 64 <= 65535, "list entries are 16-bit byte offsets");
+// BR_K4L_R48 view of the grouped path's record stage (the batch path keeps TauRec[SREC_F] in the same bytes):
+// 48-B records [0, SREC_F) followed by the (invD, face id) pairs
+constexpr int R48_BYTES = 48;
+static_assert(SREC_F * (R48_BYTES + 8) <= SREC_F * (int)sizeof(TauRec), "the 48-B view fits the record stage");
+static_assert(!(BR_K4L_R48 && (BR_K4L_LAZY || !BR_K4L_EKEEP || BR_STAGE_EARLY)),
+              "the 48-B records need EKEEP shading, no lazy staging and the record written after the masks");
+__device__ __forceinline__ float2 *r48_x(TauRec *rec) { return reinterpret_cast<float2 *>(reinterpret_cast<float4 *>(rec) + 3 * SREC_F); }
+__device__ __forceinline__ const float2 *r48_x(const TauRec *rec)
+{
+    return reinterpret_cast<const float2 *>(reinterpret_cast<const float4 *>(rec) + 3 * SREC_F);
+}
 
 // Stage faces [0, n) of the bin at the ng sub-frames taus[0..ng): records rec[l * n + j] and, for every
 // footprint a record reaches, its byte offset in that footprint's list of sub-frame l (cnt must be zero).
@@ -800,10 +830,19 @@ __device__ __forceinline__ void pair_stage_fr(const FaceRec &fr, int j, int l, i
                                               unsigned long long *nstage)
 {
     const bool back = BR_K4L_CULL && D * sF < 0.f;   // turned away from the camera (sF: mesh orientation)
+#if BR_K4L_R48
+    const int slot = l * n + j;
+    float4 *d48 = reinterpret_cast<float4 *>(rec) + 3 * slot;   // the slot's 48-B record + (invD, face)
+    const uint32_t fm = (BR_K4L_BACKBOX && back)
+                            ? stage_tau<true, true, true>(fr, tau, D, x0, x1, y0, y1, tc, rec[0], d48, r48_x(rec) + slot)
+                            : stage_tau<true, false, true>(fr, tau, D, x0, x1, y0, y1, tc, rec[0], d48, r48_x(rec) + slot);
+    const uint16_t off = (uint16_t)(slot * R48_BYTES);
+#else
     // the faces turned away are mostly skipped with their whole list: their footprints from the box alone
     const uint32_t fm = (BR_K4L_BACKBOX && back) ? stage_tau<true, true>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * n + j])
                                                  : stage_tau<true>(fr, tau, D, x0, x1, y0, y1, tc, rec[l * n + j]);
     const uint16_t off = (uint16_t)((l * n + j) * (int)sizeof(TauRec));
+#endif
     if (nstage) *nstage += fm != 0u;
     if (!back) {
         for (uint32_t m = fm; m; m &= m - 1) {
@@ -814,8 +853,13 @@ __device__ __forceinline__ void pair_stage_fr(const FaceRec &fr, int j, int l, i
         }
         return;
     }
+#if BR_K4L_R48
+    const float4 z48 = d48[2];   // (g2, az, bz, cz)
+    const float az = z48.y, bz = z48.z, cz = z48.w;
+#else
     const TauRec &R = rec[l * n + j];
     const float az = R.az, bz = R.bz, cz = R.cz;
+#endif
     for (uint32_t m = fm; m; m &= m - 1) {
         const int w = __ffs(m) - 1;
         const int q = atomicAdd(&cntb[l][w], 1);
@@ -1299,13 +1343,19 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                             const float e2 = edge_eval(q0.z, q1.y, q2.x, ul, vl);
                             const float z = __fmaf_rn(q2.y, ul, __fmaf_rn(q2.z, vl, q2.w));
                             if (fminf(fminf(e0, e1), e2) >= 0.f && z <= zbest) {
+#if BR_K4L_R48
+                                const int fj = __float_as_int(r48_x(S.rec)[off / R48_BYTES].y);
+#else
                                 const int fj = reinterpret_cast<const TauRec *>(rbase + off)->fid;
+#endif
                                 if (z < zbest || fj < fbest) { zbest = z; eoff = off; fbest = fj; EKEEP_SET(e0, e1, e2); }
                             }
                         }
                     }
 #if BR_K4L_LAZY
                     const int ebest = eoff >= 0x10000 ? (eoff & 0xFFFF) : eoff >= 0 ? eoff / (int)sizeof(TauRec) - l * n : -1;
+#elif BR_K4L_R48
+                    const int ebest = eoff >= 0 ? eoff / R48_BYTES - l * n : -1;
 #else
                     const int ebest = eoff >= 0 ? eoff / (int)sizeof(TauRec) - l * n : -1;
 #endif
@@ -1328,7 +1378,11 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
 #if BR_K4L_EKEEP && !BR_K4L_LAZY
                             // Eq.9 with the winner's edge values from the tests: w_i = e_i / |D|, the same
                             // arithmetic as shade() (edge_eval(a_i, b_i, g_i) * invD)
+#if BR_K4L_R48
+                            const float2 idf = r48_x(S.rec)[l * n + ebest];   // invD, fid
+#else
                             const float2 idf = *reinterpret_cast<const float2 *>(&rl[ebest].invD);   // invD, fid
+#endif
                             fid = __float_as_int(idf.y);
                             const float w0 = ew0 * idf.x, w1 = ew1 * idf.x, w2 = ew2 * idf.x;
                             const float4 *fc = t.fcol + 3 * (size_t)fid;
