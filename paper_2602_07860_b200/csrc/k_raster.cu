@@ -730,6 +730,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                        // pair per slot: a 48-B stride spreads 8 consecutive slots over all 32 banks, so the stage's
                        // record stores are conflict-free (64-B records: 4-way conflicts, ~11% of K4's shared wavefronts)
 #endif
+#ifndef BR_K4L_WCLR
+#define BR_K4L_WCLR 0   // 1: every warp clears its own footprint's counters (cnt, cntb, minz) right after its tests of a
+#endif                  //    sub-frame -- NFP == NWARP, so warp w is their only reader -- and the group's third barrier goes
 #ifndef BR_K4L_CULL
 #define BR_K4L_CULL 2   // 2: faces turned away from the camera in a second list per footprint, tested last, the whole
                         // list skipped when every pixel's winner is nearer than the list's lowest depth; 0: one list
@@ -769,6 +772,8 @@ struct __align__(16) LeanSmem {
     int pent[BR_K4L_PREF ? SREC_F : 1];         // the next chunk's bin entries, prefetched by cp.async
 };
 static_assert(SREC_F * 64 <= 65535, "list entries are 16-bit byte offsets");
+static_assert(!BR_K4L_WCLR || (NFP == NWARP && !BR_K4L_LAZY && !BR_K4L_TWOPASS && !BR_K4L_TPREF),
+              "per-warp counter clears: one warp per footprint, S.taus and nacc untouched by the tests");
 // BR_K4L_R48 view of the grouped path's record stage (the batch path keeps TauRec[SREC_F] in the same bytes):
 // 48-B records [0, SREC_F) followed by the (invD, face id) pairs
 constexpr int R48_BYTES = 48;
@@ -1323,6 +1328,10 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                         }
                     }
                     // coverage loop: end
+#if BR_K4L_WCLR
+                    __syncwarp();   // every lane has read this footprint's counters
+                    if (lane == 0) { S.u.g.cnt[l][warp] = 0; S.u.g.cntb[l][warp] = 0; S.u.g.minz[l][warp] = 0x7f800000; }
+#endif
                     if (__any_sync(0xffffffffu, tief != 0.f)) {   // exact depth tie in the warp: face indices decide (Q7)
                         zbest = __int_as_float(0x7f800000);
                         eoff = -1;
@@ -1418,12 +1427,14 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                 if (k_nx >= 0 && threadIdx.x < GMAX_F) S.taus[threadIdx.x] = tau_nx;
                 tau_k = k_nx;
 #endif
+#if !BR_K4L_WCLR
                 __syncthreads();   // lists read: clear the counters of this group
                 if (threadIdx.x < ng * NFP) {
                     (&S.u.g.cnt[0][0])[threadIdx.x] = 0; (&S.u.g.cntb[0][0])[threadIdx.x] = 0;
                     (&S.u.g.minz[0][0])[threadIdx.x] = 0x7f800000;
                 }
                 if (threadIdx.x == 0) S.u.g.nacc = 0;
+#endif
             }
 #undef EKEEP_SET
         } else {
