@@ -731,8 +731,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
                        // record stores are conflict-free (64-B records: 4-way conflicts, ~11% of K4's shared wavefronts)
 #endif
 #ifndef BR_K4L_WCLR
-#define BR_K4L_WCLR 0   // 1: every warp clears its own footprint's counters (cnt, cntb, minz) right after its tests of a
+#define BR_K4L_WCLR 1   // 1: every warp clears its own footprint's counters (cnt, cntb, minz) right after its tests of a
 #endif                  //    sub-frame -- NFP == NWARP, so warp w is their only reader -- and the group's third barrier goes
+                        //    (C4 K4 5.634 -> 5.505 ms, C3 1.236 -> 1.203 ms, C5 217.8 -> 212.5 ms; parity green)
 #ifndef BR_K4L_CULL
 #define BR_K4L_CULL 2   // 2: faces turned away from the camera in a second list per footprint, tested last, the whole
                         // list skipped when every pixel's winner is nearer than the list's lowest depth; 0: one list
