@@ -734,6 +734,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
 #define BR_K4L_WCLR 1   // 1: every warp clears its own footprint's counters (cnt, cntb, minz) right after its tests of a
 #endif                  //    sub-frame -- NFP == NWARP, so warp w is their only reader -- and the group's third barrier goes
                         //    (C4 K4 5.634 -> 5.505 ms, C3 1.236 -> 1.203 ms, C5 217.8 -> 212.5 ms; parity green)
+#ifndef BR_K4L_GTAU
+#define BR_K4L_GTAU 0   // 1: the stage reads its sub-frame times from the schedule in global memory (in parallel with the
+#endif                  //    bin entries) instead of S.taus, so no load sits between the chunk header and the group's barrier
 #ifndef BR_K4L_CULL
 #define BR_K4L_CULL 2   // 2: faces turned away from the camera in a second list per footprint, tested last, the whole
                         // list skipped when every pixel's winner is nearer than the list's lowest depth; 0: one list
@@ -773,6 +776,7 @@ struct __align__(16) LeanSmem {
     int pent[BR_K4L_PREF ? SREC_F : 1];         // the next chunk's bin entries, prefetched by cp.async
 };
 static_assert(SREC_F * 64 <= 65535, "list entries are 16-bit byte offsets");
+static_assert(!BR_K4L_GTAU || (!BR_K4L_LAZY && !BR_K4L_TWOPASS && !BR_K4L_TPREF), "S.taus is not written with BR_K4L_GTAU");
 static_assert(!BR_K4L_WCLR || (NFP == NWARP && !BR_K4L_LAZY && !BR_K4L_TWOPASS && !BR_K4L_TPREF),
               "per-warp counter clears: one warp per footprint, S.taus and nacc untouched by the tests");
 // BR_K4L_R48 view of the grouped path's record stage (the batch path keeps TauRec[SREC_F] in the same bytes):
@@ -1208,7 +1212,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                 const int ng = min(Gs, ch.k1 - kg);
 #if BR_K4L_TPREF
                 if (tau_k != kg && threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
-#else
+#elif !BR_K4L_GTAU
                 if (threadIdx.x < ng) S.taus[threadIdx.x] = t.sched_tau[sched_off + kg + threadIdx.x];
 #endif
 #if BR_K4L_PREF
@@ -1219,8 +1223,8 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                 stage_group_2pass(bc, ents, n, S.taus, ng, tc, t.W, t.H, t.F, S.rec, S.u.g.list, S.u.g.cnt, S.u.g.cntb, sF,
                                   S.u.g.minz, S.u.g.acc_pairs, &S.u.g.nacc);
 #elif !defined(BR_EXP_NOSTAGE)
-                stage_group_list(bc, ents, n, S.taus, ng, tc, t.W, t.H, t.F, S.rec, S.u.g.list, S.u.g.cnt, S.u.g.cntb, sF,
-                                 S.u.g.minz, CENSUS ? &c_stage : nullptr);
+                stage_group_list(bc, ents, n, BR_K4L_GTAU ? t.sched_tau + sched_off + kg : S.taus, ng, tc, t.W, t.H, t.F, S.rec,
+                                 S.u.g.list, S.u.g.cnt, S.u.g.cntb, sF, S.u.g.minz, CENSUS ? &c_stage : nullptr);
 #endif
                 __syncthreads();
                 if (threadIdx.x == 0) { K4L_STAT(t, 20, n * ng); K4L_STAT(t, 29, 1); }

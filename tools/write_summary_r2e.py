@@ -51,7 +51,8 @@ HISTORY = """| change (round 2) | fwd ms | bwd ms | step ms | images/s |
 | (tried) K4 record written before the footprint masks (`BR_STAGE_EARLY`); whole record per pair in one request (`BR_K4L_ONELOAD`) | 5.88-5.90 | - | - | - |
 | (tried) K4 next chunk header / next taus one phase ahead (`BR_K4L_TPREF`); bin sizes of 32 chunks in one load (`BR_K4L_NWIN`) | 5.95-5.96 | - | - | - |
 | K4 coverage loop keeps the winner's edge values; shading reads only (invD, face) (`BR_K4L_EKEEP`) | 5.75 | 2.88 | 9.28 | 1724 |
-| K4 48-B stage records + separate (invD, face) pairs: conflict-free record stores (`BR_K4L_R48`) | 5.64 | 2.88 | 9.18 | 1743 |"""
+| K4 48-B stage records + separate (invD, face) pairs: conflict-free record stores (`BR_K4L_R48`) | 5.64 | 2.88 | 9.18 | 1743 |
+| K4 per-warp counter clears, two barriers per group instead of three (`BR_K4L_WCLR`) | 5.51 | 2.88 | 9.06 | 1765 |"""
 
 
 def row(label, d):
@@ -101,7 +102,7 @@ Generated by `tools/write_summary_r2e.py` from `tools/baseline_table.sh` (one be
 gpurun call on one box) and `tools/profile_tag.sh (TAG=r2e)` (ncu launch list + `ncu --set full` of K4 = `k4l_raster_fwd`
 and K6 = `k6v_raster_bwd` on C4).  Raw files: `r2e_launches_C4.csv` (ncu launch list), `r2e_ncu_details_raster_C4.csv`
 (ncu details of K4 and K6), `traffic.json` (DRAM bytes per launch and warp efficiencies -> `roofline.traffic`,
-`roofline.hbm`, `roofline.warp_efficiency`), `r2d_checked_build.log` (the checked build over the GPU tests, final code; `r2c_checked_build.log` the third session's),
+`roofline.hbm`, `roofline.warp_efficiency`), `r2e_checked_build.log` (the checked build over the GPU tests, final code; `r2d_checked_build.log` the fourth session's, `r2c_checked_build.log` the third session's),
 `r2c_order_i_vs_ii.md` (K4 evaluation orders), `r2c_variants_parity.log` (the A/B forwards over the parity tests), `r2e_gpu_tests.log` (this session's `pytest -m gpu` + smoke on the final code).  Earlier sessions: `r2d_summary.md` (the full C1-C5 table, before EKEEP / R48), `r2c_summary.md`, `r2b_summary.md`, `r2_summary.md`; round 1: `r1_summary.md`.
 
 ## Bench lines (1 B200)
