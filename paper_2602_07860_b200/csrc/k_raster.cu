@@ -737,6 +737,7 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
 #ifndef BR_K4L_GTAU
 #define BR_K4L_GTAU 0   // 1: the stage reads its sub-frame times from the schedule in global memory (in parallel with the
 #endif                  //    bin entries) instead of S.taus, so no load sits between the chunk header and the group's barrier
+                        //    (measured with WCLR on: C4 K4 5.50 -> 5.52 ms, C5 fwd 212.5 -> 213.8 ms, parity-green; kept off)
 #ifndef BR_K4L_CULL
 #define BR_K4L_CULL 2   // 2: faces turned away from the camera in a second list per footprint, tested last, the whole
                         // list skipped when every pixel's winner is nearer than the list's lowest depth; 0: one list

@@ -68,18 +68,18 @@ def row(label, d):
 
 
 def main():
-    lines = [("C1 (`--config C1 --graph --steps 50`)", "absent_table_C1"),
-             ("C2 (`--config C2 --graph --steps 50`)", "absent_table_C2"),
-             ("C2 eager", "absent_table_C2_eager"),
+    lines = [("C1 (`--config C1 --graph --steps 50`)", "table_C1"),
+             ("C2 (`--config C2 --graph --steps 50`)", "table_C2"),
+             ("C2 eager", "table_C2_eager"),
              ("C3 (`--config C3 --graph --steps 50`)", "r2e_bench_C3"),
-             ("C3 eager", "absent_table_C3_eager"),
+             ("C3 eager", "table_C3_eager"),
              ("C4 (`python bench.py`, the default)", "r2e_bench_C4"),
-             ("C4 soft coverage (`--delta 1e-4`)", "absent_table_C4_soft"),
+             ("C4 soft coverage (`--delta 1e-4`)", "table_C4_soft"),
              ("C5 (`--config C5 --steps 3`)", "r2e_bench_C5"),
-             ("C5 soft coverage (`--config C5 --delta 1e-4 --steps 1`)", "absent_table_C5_soft")]
+             ("C5 soft coverage (`--config C5 --delta 1e-4 --steps 1`)", "table_C5_soft")]
     rows_b = [row(lab, d) for lab, d in ((lab, load(n)) for lab, n in lines) if d is not None]
     c4 = load("r2e_bench_C4")
-    ref = None
+    ref = load("bench_ref")
     launches = os.path.join(OUT, "r2e_launches_C4.csv")
     rep = os.path.join(OUT, "prof_r2e_c4.ncu-rep")
     tab_l = sp.launches(launches)
