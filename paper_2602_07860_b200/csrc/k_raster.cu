@@ -738,6 +738,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
 #define BR_K4L_GTAU 0   // 1: the stage reads its sub-frame times from the schedule in global memory (in parallel with the
 #endif                  //    bin entries) instead of S.taus, so no load sits between the chunk header and the group's barrier
                         //    (measured with WCLR on: C4 K4 5.50 -> 5.52 ms, C5 fwd 212.5 -> 213.8 ms, parity-green; kept off)
+#ifndef BR_K4L_HPREF
+#define BR_K4L_HPREF 0  // 1: the next chunk's header and bin offsets are copied to shared memory by cp.async while this chunk
+#endif                  //    is staged (no registers held; made visible by the stage's barrier): one L2 round trip less per chunk
 #ifndef BR_K4L_CULL
 #define BR_K4L_CULL 2   // 2: faces turned away from the camera in a second list per footprint, tested last, the whole
                         // list skipped when every pixel's winner is nearer than the list's lowest depth; 0: one list
@@ -775,9 +778,11 @@ struct __align__(16) LeanSmem {
     float2 uv[NT];                              // the thread's pixel (ul, vl), reloaded per sub-frame
     float4 acc[TW * TH];                        // per-pixel (r, g, b, a) sums over the sub-frames
     int pent[BR_K4L_PREF ? SREC_F : 1];         // the next chunk's bin entries, prefetched by cp.async
+    struct __align__(8) NHdr { int b, s, k0, k1; long long o, o1; } nh[2];   // BR_K4L_HPREF: prefetched chunk headers
 };
 static_assert(SREC_F * 64 <= 65535, "list entries are 16-bit byte offsets");
 static_assert(!BR_K4L_GTAU || (!BR_K4L_LAZY && !BR_K4L_TWOPASS && !BR_K4L_TPREF), "S.taus is not written with BR_K4L_GTAU");
+static_assert(!BR_K4L_HPREF || (!BR_K4L_TPREF && !BR_K4L_NWIN && !BR_K4L_PREF), "one prefetch scheme at a time");
 static_assert(!BR_K4L_WCLR || (NFP == NWARP && !BR_K4L_LAZY && !BR_K4L_TWOPASS && !BR_K4L_TPREF),
               "per-warp counter clears: one warp per footprint, S.taus and nacc untouched by the tests");
 // BR_K4L_R48 view of the grouped path's record stage (the batch path keeps TauRec[SREC_F] in the same bytes):
@@ -1129,6 +1134,10 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
     const double orient = *t.orient;
     const float sF = orient > 0.0 ? 1.f : orient < 0.0 ? -1.f : 0.f;
     int pref_c = -1;   // chunk whose bin entries were prefetched into S.pent (BR_K4L_PREF)
+#if BR_K4L_HPREF
+    int hp_par = 0;        // S.nh[hp_par] holds this chunk's header when hp_ok (block-uniform)
+    bool hp_ok = false;
+#endif
 
 #if BR_K4L_TPREF
     // software pipeline over the chunks: chunk c + splits's header and bin offsets are loaded at the top of
@@ -1174,6 +1183,21 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
             on = t.off[bi2];
             on1 = t.off[bi2 + 1];
         }
+#elif BR_K4L_HPREF
+        Chunk ch;
+        long long o;
+        int n;
+        if (hp_ok) {   // copied to shared memory while the previous chunk was staged
+            const LeanSmem::NHdr &h = S.nh[hp_par];
+            ch.s = h.s; ch.k0 = h.k0; ch.k1 = h.k1;
+            o = h.o;
+            n = (int)(h.o1 - o);
+        } else {
+            ch = t.chunks[c];
+            const size_t bi = (size_t)c * t.T + tile;
+            o = t.off[bi];
+            n = (int)(t.off[bi + 1] - o);
+        }
 #else
         const Chunk ch = t.chunks[c];
         const size_t bi = (size_t)c * t.T + tile;
@@ -1187,8 +1211,28 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                 if (lane == 0)
                     for (int k = ch.k0; k < ch.k1; ++k) t.covbits[cov_word(t, im, k, tile) + warp] = m;
             }
+#if BR_K4L_HPREF
+            hp_ok = false;   // no barrier in this chunk: the next one reads its header from global memory
+#endif
             continue;
         }
+#if BR_K4L_HPREF
+        // the next chunk's header into the other buffer: its last readers were two barriers ago at least; the copies
+        // are waited for before this chunk's barriers (wait_prior below), which make them visible to the CTA
+        if (c + t.splits < c_end) {
+            if (threadIdx.x < 4) {
+                const int c2 = c + t.splits;
+                const long long *src = threadIdx.x < 2 ? reinterpret_cast<const long long *>(t.chunks + c2) + threadIdx.x
+                                                       : t.off + ((size_t)c2 * t.T + tile) + (threadIdx.x - 2);
+                __pipeline_memcpy_async(reinterpret_cast<long long *>(&S.nh[hp_par ^ 1]) + threadIdx.x, src, 8);
+            }
+            __pipeline_commit();
+            hp_par ^= 1;
+            hp_ok = true;
+        } else {
+            hp_ok = false;
+        }
+#endif
         BinCtx bc;
         bc.status = t.status;
         bc.rseg = t.rec + (size_t)(rec_off + (long long)ch.s * t.F) * REC_F4;
@@ -1226,6 +1270,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
 #elif !defined(BR_EXP_NOSTAGE)
                 stage_group_list(bc, ents, n, BR_K4L_GTAU ? t.sched_tau + sched_off + kg : S.taus, ng, tc, t.W, t.H, t.F, S.rec,
                                  S.u.g.list, S.u.g.cnt, S.u.g.cntb, sF, S.u.g.minz, CENSUS ? &c_stage : nullptr);
+#endif
+#if BR_K4L_HPREF
+                __pipeline_wait_prior(0);   // the next chunk's header has landed (threads 0-3; no-op otherwise)
 #endif
                 __syncthreads();
                 if (threadIdx.x == 0) { K4L_STAT(t, 20, n * ng); K4L_STAT(t, 29, 1); }
@@ -1487,6 +1534,9 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4l_raster_fwd(Tables t, float
                     if (lane == 0) t.covbits[cov_word(t, im, k, tile) + warp] = m;
                 }
             }
+#if BR_K4L_HPREF
+            __pipeline_wait_prior(0);
+#endif
             __syncthreads();   // the grouped path's counters share the batch path's shared memory
             for (int i = threadIdx.x; i < GMAX_F * NFP; i += NT) {
                 (&S.u.g.cnt[0][0])[i] = 0; (&S.u.g.cntb[0][0])[i] = 0; (&S.u.g.minz[0][0])[i] = 0x7f800000;
