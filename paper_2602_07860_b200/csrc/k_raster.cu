@@ -741,6 +741,8 @@ __global__ void __launch_bounds__(NT, BR_K4_MINB) k4_raster_fwd(Tables t, float 
 #ifndef BR_K4L_HPREF
 #define BR_K4L_HPREF 0  // 1: the next chunk's header and bin offsets are copied to shared memory by cp.async while this chunk
 #endif                  //    is staged (no registers held; made visible by the stage's barrier): one L2 round trip less per chunk
+                        //    (measured: C4 K4 5.51 -> 5.98 ms, C3 1.21 -> 1.32 ms, C5 fwd 212.5 -> 231.1 ms; 16 B more spills and a
+                        //    cp.async commit / wait per group; parity-green; kept off)
 #ifndef BR_K4L_CULL
 #define BR_K4L_CULL 2   // 2: faces turned away from the camera in a second list per footprint, tested last, the whole
                         // list skipped when every pixel's winner is nearer than the list's lowest depth; 0: one list

@@ -52,7 +52,9 @@ HISTORY = """| change (round 2) | fwd ms | bwd ms | step ms | images/s |
 | (tried) K4 next chunk header / next taus one phase ahead (`BR_K4L_TPREF`); bin sizes of 32 chunks in one load (`BR_K4L_NWIN`) | 5.95-5.96 | - | - | - |
 | K4 coverage loop keeps the winner's edge values; shading reads only (invD, face) (`BR_K4L_EKEEP`) | 5.75 | 2.88 | 9.28 | 1724 |
 | K4 48-B stage records + separate (invD, face) pairs: conflict-free record stores (`BR_K4L_R48`) | 5.64 | 2.88 | 9.18 | 1743 |
-| K4 per-warp counter clears, two barriers per group instead of three (`BR_K4L_WCLR`) | 5.51 | 2.88 | 9.06 | 1765 |"""
+| K4 per-warp counter clears, two barriers per group instead of three (`BR_K4L_WCLR`) | 5.51 | 2.88 | 9.06 | 1765 |
+| (tried) K4 stage reads its taus from the global schedule (`BR_K4L_GTAU`) | 5.52 | - | - | - |
+| (tried) K4 next chunk's header copied to shared memory by `cp.async` during the stage (`BR_K4L_HPREF`) | 5.98 | - | - | - |"""
 
 
 def row(label, d):
